@@ -1,0 +1,281 @@
+"""Benchmark: BO iterations/sec of the surrogate pass at (N, n=220) on B200.
+
+One step = one BO iteration at n = 220 observations:
+  mark the previous pick visited -> append its observation (single-CTA
+  bordered Cholesky row + one new row of V over all N candidates + posterior)
+  -> mean variance -> contextual-variance lambda -> acquisition -> masked
+  argmax, result back on the host.
+The model is rolled back to 219 observations before each append (prefix-
+stable state), so every timed step does the full work at exactly n = 220.
+
+Workload (default, config C4 of BASELINE.json): random-rough synthetic space,
+grid 10^6 (d = 6), invalid 0, base seed 20261017, strategy bo-ei with
+contextual variance (StrategyConfig defaults: Matern 3/2, l = 1.5).
+V (1.76 GB) >> L2 (126 MB), so every step streams from HBM (no L2 flush needed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c4|c3]
+Under torchrun (N > 1) every rank runs an independent replica of the workload
+(run-level sharding, no collective on the data path); value = total iter/s.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import shutil
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BASE_SEED = 20261017
+METRIC = "BO iterations/sec (full-space GP posterior+acquisition) at N, n=220"
+CONFIGS = {
+    "c4": dict(grid=[10] * 6, invalid=0.0, workload="C4 synthetic random-rough 1M candidates (10^6 grid, d=6), n=220, bo-ei, contextual variance"),
+    "c3": dict(grid=[10, 10, 10, 10, 5, 2], invalid=0.3, workload="C3 synthetic random-rough 100k candidates (d=6, ~30% invalid), n=220, bo-lcb, contextual variance"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=220)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        if shutil.which("nvidia-smi"):
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i] and "Not" not in s[2 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured"
+    return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def make_workload(cfg):
+    from paper_2111_14991_b200 import synthetic
+    coords, ids, values = synthetic.random_rough(cfg["grid"], BASE_SEED, cfg["invalid"])
+    return coords, ids, values
+
+
+def prefix_positions(values, n, seed):
+    """n distinct valid positions (a seeded run prefix)."""
+    rng = np.random.default_rng(seed)
+    valid = np.nonzero(~np.isnan(values))[0]
+    return rng.choice(valid, n, replace=False)
+
+
+def cpu_baseline(cfg, n, budget_s=30.0):
+    """Reference CPU path (oracle/_ref/ref_tool, the unmodified reference
+    compiled with the Eigen-API shim) on the host cores, bounded sample."""
+    tool = ROOT / "oracle" / "_ref" / "ref_tool"
+    if not tool.exists():
+        return None
+    cores = os.cpu_count() or 1
+    grid = "x".join(str(k) for k in cfg["grid"])
+    try:
+        out = subprocess.run([str(tool), "bench", grid, str(BASE_SEED), str(n), str(cores), "1", "ei"],
+                             capture_output=True, text=True, timeout=budget_s * 20)
+        rec = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001
+        return {"value": None, "unit": "iter/s", "cores": cores, "kind": "reference", "error": str(e)[:200]}
+    return {"value": rec["iters_per_sec"], "unit": "iter/s", "cores": rec["threads"], "kind": "reference",
+            "sample": f"1 BO iteration of the reference CPU path at N={rec['N']}, n={rec['n']}: GpModel::fit + "
+                      f"GpModel::predict over all unvisited candidates split across {rec['threads']} threads + "
+                      f"lambda + best_candidate (oracle/_ref/ref_tool bench)",
+            "seconds_per_iteration": rec["seconds_per_step"]}
+
+
+def run_reference_arm(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    tool = ROOT / "oracle" / "_ref" / "ref_tool"
+    base = {"impl": "reference", "metric": METRIC, "unit": "iter/s", "higher_is_better": True,
+            "n_gpus": args.gpus, "config": {"workload": cfg["workload"], "N": int(np.prod(cfg["grid"])), "n": args.n}}
+    if not tool.exists():
+        print(json.dumps({**base, "unavailable": "oracle/_ref/ref_tool not built"}))
+        return
+    cores = os.cpu_count() or 1
+    grid = "x".join(str(k) for k in cfg["grid"])
+    steps = max(1, min(args.steps, 3))
+    out = subprocess.run([str(tool), "bench", grid, str(BASE_SEED), str(args.n), str(cores), str(steps), "ei"],
+                         capture_output=True, text=True)
+    rec = json.loads(out.stdout.strip().splitlines()[-1])
+    v = rec["iters_per_sec"]
+    print(json.dumps({**base, "value": v, "steps": rec["steps"], "warmup": 0,
+                      "ms_per_step": 1e3 * rec["seconds_per_step"], "dtype": "f64", "data": "synthetic",
+                      "scaling": "weak", "vs_baseline": None,
+                      "cpu_baseline": {"value": v, "unit": "iter/s", "cores": rec["threads"], "kind": "reference",
+                                       "sample": f"{rec['steps']} full BO iterations at N={rec['N']}, n={rec['n']} "
+                                                 f"(reference GpModel::fit + predict over all unvisited, "
+                                                 f"{rec['threads']} threads)"},
+                      "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+        return
+    rank, world, local = dist_env()
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2111_14991_b200 as gt
+    from paper_2111_14991_b200 import AcquisitionId, ContextualVarianceState, ExplorationConfig, MaternKernel, MaternNu
+
+    coords, ids, values = make_workload(cfg)
+    N = len(values)
+    n = args.n
+    af = AcquisitionId.ei if args.config == "c4" else AcquisitionId.lcb
+    launches0 = gt.load().gtc_kernel_launches()
+    space = gt.Space(coords, device=local)
+    run = gt.SurrogateRun(space, MaternKernel(MaternNu.three_halves, 1.5, 1.0), n_max=n)
+    pos = prefix_positions(values, n - 1, BASE_SEED + rank)
+    y = values[pos]
+    run.fit(pos, y)
+    for p in pos:
+        run.mark_visited(int(p))
+    cv = ContextualVarianceState(float(np.mean(y[:20])), run.mean_variance())
+    expl = ExplorationConfig()
+    f_best = float(np.min(y))
+    sel = run.select([af], f_best, expl, cv)
+    pick = sel.pick(af)
+
+    stream = torch.cuda.ExternalStream(gt.load().gtc_run_stream(run.handle))
+
+    def step(pick, f_best):
+        run.truncate(n - 1)                  # model back to n-1 observations
+        run.mark_visited(pick)
+        yv = float(values[pick])
+        run.append(pick, yv)                 # GP update + predictive pass at n
+        fb = min(f_best, yv)
+        s = run.select([af], fb, expl, cv)   # lambda + acquisition + argmax
+        run.unmark_visited(pick)             # keep the candidate set size fixed
+        return s.pick(af), run.last_pass_ms()
+
+    for _ in range(args.warmup):
+        pick, _ = step(pick, f_best)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches_before = gt.load().gtc_kernel_launches()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    pass_ms = []
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pick, ms = step(pick, f_best)
+            pass_ms.append(ms)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    launches = gt.load().gtc_kernel_launches() - launches_before
+    dev_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([dev_ms, wall], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dev_ms, wall = float(t[0]), float(t[1])
+    value = world * args.steps / (dev_ms / 1e3)
+    e2e = world * args.steps / wall
+    peaks, peak_kind = measured_peaks()
+    avg_pass = float(np.mean(pass_ms))
+    alg_bytes = N * 8 * n  # n-1 rows of V read + 1 row written per candidate
+    achieved = alg_bytes / (avg_pass / 1e3) / 1e9
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "N": N, "n": n, "d": coords.shape[1],
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "V stream 1.76 GB/step > 126 MB L2 (no flush needed)" if N >= 1_000_000 else "inputs > L2 not guaranteed"},
+            "e2e": {"value": e2e, "unit": "iter/s", "h2d_bytes_per_step": 16 + 56,
+                    "d2h_bytes_per_step": 48 + 104},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                         "kernel": "k_extend<1,NU=3/2> (predictive pass)", "kernel_ms": avg_pass,
+                         "algorithmic_bytes": alg_bytes, "peak_kind": peak_kind},
+            "clocks": clocks.summary(),
+        }
+        if not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(cfg, n)
+        print(json.dumps(out))
+    run.close()
+    space.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,187 @@
+/*
+ * gridtune_cuda.h — C ABI of the B200-native BO surrogate pass.
+ *
+ * Drop-in boundary for the per-iteration surrogate pass of the reference
+ * `gridtune` BO tuner (/root/reference/proj/include/gridtune).  The reference
+ * binds this path as header-only C++ (no FFI); every entry point below replaces
+ * one reference call site, cited as file:line.  INTEGRATION.md shows the
+ * reference-side binding.  Plain pointers and sizes only; no torch / CUDA types.
+ *
+ * Conventions
+ *  - All arithmetic is IEEE FP64; positions are int64 indices into the
+ *    caller's enumerated candidate list (EnumeratedSpace::configs order,
+ *    search_space.hpp:216-245), ascending canonical index.
+ *  - Host buffers are caller-owned and only read/written during the call.
+ *    Device memory is owned by the handle.
+ *  - Status: 0 = OK, negative = error (mapped to gridtune exception types by
+ *    the C++ host layer, errors.hpp:55-108).  gtc_last_error() returns the
+ *    message of the last failing call on the calling thread.
+ *  - Re-entrant per handle: no global mutable state; each run owns one CUDA
+ *    stream; distinct handles may be used from different host threads and
+ *    devices concurrently (experiment.hpp:335-358 runs BO runs in a pool).
+ *  - There is no CPU fallback: every compute entry point runs sm_100a kernels
+ *    and fails with GTC_ERR_CUDA when no device is usable.
+ */
+#ifndef GRIDTUNE_CUDA_H_
+#define GRIDTUNE_CUDA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (C++ exception each maps to) --------------------------- */
+#define GTC_OK 0
+#define GTC_ERR_INVALID (-1)       /* gridtune::Error (bad argument, "GP fit: ...")   */
+#define GTC_ERR_CONDITIONING (-2)  /* gridtune::ModelConditioningError, gp.hpp:123-127 */
+#define GTC_ERR_NO_CANDIDATES (-3) /* Error("acquisition: no candidates remaining"),  portfolio.hpp:57-59 */
+#define GTC_ERR_CUDA (-4)          /* CUDA runtime failure / no device                */
+#define GTC_ERR_OOM (-5)           /* device allocation failed                         */
+#define GTC_ERR_CONFIG (-6)        /* gridtune::ConfigError                            */
+#define GTC_ERR_CAPACITY (-7)      /* more observations than the run's n_max          */
+
+/* ---- enums mirroring the reference ---------------------------------------- */
+/* MaternNu, gp.hpp:12 */
+#define GTC_NU_HALF 0
+#define GTC_NU_THREE_HALVES 1
+#define GTC_NU_FIVE_HALVES 2
+/* AcquisitionId order ei, poi, lcb (acquisition.hpp:44); bit k selects slot k */
+#define GTC_AF_EI 0
+#define GTC_AF_POI 1
+#define GTC_AF_LCB 2
+#define GTC_AF_MASK(af) (1u << (af))
+/* ExplorationConfig::Mode, acquisition.hpp:55-59 */
+#define GTC_LAMBDA_CONSTANT 0
+#define GTC_LAMBDA_CONTEXTUAL_VARIANCE 1
+
+typedef struct gtc_space gtc_space; /* resident normalised search space      */
+typedef struct gtc_run gtc_run;     /* one BO run's resident surrogate state */
+typedef struct gtc_gp gtc_gp;       /* stand-alone GpModel (arbitrary points) */
+
+/* MaternKernel, gp.hpp:27-56 */
+typedef struct {
+  int32_t nu;             /* GTC_NU_* */
+  double lengthscale;     /* > 0 */
+  double output_variance; /* > 0 */
+} gtc_kernel;
+
+/* GpModel::fit arguments (gp.hpp:81-83) plus the run's capacity. */
+typedef struct {
+  gtc_kernel kernel;
+  double noise;  /* >= 0, default 1e-10 */
+  double jitter; /* > 0,  default 1e-6  */
+  int32_t n_max; /* maximum GP training size for the run (budget)  */
+} gtc_model_config;
+
+/* Model scalars after a fit/append (GpModel accessors gp.hpp:137-142). */
+typedef struct {
+  int32_t n;      /* train_size()                           */
+  int32_t rebuilt;/* 1 if the call refactorised from scratch (jitter escalation) */
+  double y_mean;  /* y_mean()                               */
+  double y_std;   /* y_std()                                */
+  double jitter;  /* jitter() actually used                 */
+} gtc_fit_info;
+
+/* One iteration's selection request (strategies.hpp:404-436). */
+typedef struct {
+  uint32_t af_mask;              /* GTC_AF_MASK(GTC_AF_EI) | ...; every active AF of `multi` */
+  int32_t lambda_mode;           /* GTC_LAMBDA_*                                        */
+  double lambda_constant;        /* ExplorationConfig::constant (0.01)                   */
+  double cv_initial_sample_mean; /* ContextualVarianceState, acquisition.hpp:63-66       */
+  double cv_initial_mean_variance;
+  double f_best_raw;             /* run's best raw observation (strategies.hpp:409,424)  */
+  const int64_t* excluded;       /* optional positions to skip (portfolio pending set)  */
+  int32_t n_excluded;
+} gtc_select_args;
+
+typedef struct {
+  int64_t position[3];  /* argmax per AF slot (ei, poi, lcb); -1 when not requested  */
+  double score[3];      /* the winning score (LCB slot holds -lcb, portfolio.hpp:47) */
+  double lambda;        /* exploration factor used                                   */
+  double mean_variance; /* mean posterior variance over the candidates               */
+  double best_std;      /* GpModel::standardize(f_best_raw)                          */
+  int64_t n_candidates; /* unvisited, non-excluded candidates scored                 */
+  int32_t cv_fallback;  /* 1: contextual variance undefined, constant used          */
+} gtc_select_result;
+
+/* ---- library ---------------------------------------------------------------- */
+const char* gtc_last_error(void);
+const char* gtc_version(void);
+/* Number of kernels this library has launched in the calling process. */
+uint64_t gtc_kernel_launches(void);
+
+/* ---- resident search space (EnumeratedSpace, search_space.hpp:216-245) ------ */
+/* coords: n x d row-major, as EnumeratedSpace::coords[pos][j]
+ * (SearchSpace::normalize, search_space.hpp:158-166).  Stored on `device` as
+ * structure-of-arrays [d][n_pad]. */
+int gtc_space_create(int device, const double* coords, int64_t n, int32_t d, gtc_space** out);
+int gtc_space_destroy(gtc_space* space);
+int64_t gtc_space_size(const gtc_space* space);
+
+/* ---- BO run: resident GP + predictions over the whole space ----------------- */
+int gtc_run_create(gtc_space* space, const gtc_model_config* config, gtc_run** out);
+int gtc_run_destroy(gtc_run* run);
+
+/* GpModel::fit over candidates at `positions` (the fit_current lambda,
+ * strategies.hpp:298-307 -> gp.hpp:81-135) including jitter escalation, then
+ * the full predictive pass over every candidate (refresh_predictions,
+ * strategies.hpp:366-387).  n == 0 gives the prior. */
+int gtc_fit(gtc_run* run, const int64_t* positions, const double* y_raw, int32_t n,
+            gtc_fit_info* info);
+
+/* Appends one valid observation (strategies.hpp:444-449): incremental
+ * bordered-Cholesky row + one new row of V = L^-1 K* over all candidates, and
+ * the refreshed posterior.  Equivalent to a refit; escalates jitter and
+ * refactorises when the new pivot fails, exactly like gp.hpp:116-129. */
+int gtc_append(gtc_run* run, int64_t position, double y_raw, gtc_fit_info* info);
+
+/* Rolls the model back to its first n observations (prefix-stable state). */
+int gtc_truncate(gtc_run* run, int32_t n, gtc_fit_info* info);
+
+/* Visited bookkeeping (RunContext::evaluate, strategies.hpp:183-186). */
+int gtc_mark_visited(gtc_run* run, int64_t position);
+int gtc_unmark_visited(gtc_run* run, int64_t position);
+int64_t gtc_unvisited_count(const gtc_run* run);
+
+/* Fused mean-variance -> lambda -> EI/PI/LCB -> masked argmax for every AF in
+ * af_mask in one pass over the candidates (strategies.hpp:404-436,
+ * acquisition.hpp:12-83, portfolio.hpp:32-61). */
+int gtc_select(gtc_run* run, const gtc_select_args* args, gtc_select_result* out);
+
+/* Mean posterior variance over the unvisited candidates (the initial
+ * contextual-variance normaliser, strategies.hpp:392-397; 0 when empty). */
+int gtc_mean_variance(gtc_run* run, double* mean_variance, int64_t* count);
+
+/* Copies the current standardized posterior mean / variance of every
+ * candidate (GpPrediction.mean/.variance, gp.hpp:62-69) into host arrays of
+ * length gtc_space_size().  Visited candidates carry values too. */
+int gtc_read_predictions(gtc_run* run, double* mean, double* variance);
+
+/* Device-side timing helper for benchmarks: CUDA-event milliseconds of the
+ * last gtc_append's predictive-pass kernel (0 if none). */
+double gtc_last_pass_ms(const gtc_run* run);
+/* The CUDA stream the run launches on (as an opaque integer, for NCCL). */
+uint64_t gtc_run_stream(const gtc_run* run);
+
+/* ---- stand-alone GpModel over arbitrary points (gp.hpp:81-168) --------------- */
+/* X: n x d row-major, y: n raw observations. */
+int gtc_gp_fit(int device, const gtc_kernel* kernel, const double* X, const double* y_raw,
+               int32_t n, int32_t d, double noise, double jitter, gtc_gp** out,
+               gtc_fit_info* info);
+/* Posterior at m points (Xstar m x d row-major), standardized scale. */
+int gtc_gp_predict(gtc_gp* gp, const double* Xstar, int64_t m, double* mean, double* variance);
+int gtc_gp_info(const gtc_gp* gp, gtc_fit_info* info);
+int gtc_gp_destroy(gtc_gp* gp);
+
+/* ---- acquisition over caller spans (best_candidate, portfolio.hpp:32-61) ----- */
+/* means/stds: n candidates (CandidateScores spans); excluded: optional n bytes. */
+int gtc_best_candidate(int device, int32_t af, const double* means, const double* stds, int64_t n,
+                       double best_std, double lambda, const uint8_t* excluded,
+                       int64_t* position_out, double* score_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GRIDTUNE_CUDA_H_ */

@@ -1,0 +1,124 @@
+"""ctypes binding of the C ABI declared in include/gridtune_cuda.h.
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (nvcc,
+sm_100a).  There is deliberately no fallback: if the library is missing or
+no CUDA device is usable, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import pathlib
+
+HERE = pathlib.Path(__file__).resolve().parent
+LIB_PATH = HERE / "libgridtune_b200.so"
+
+# status codes (gridtune_cuda.h)
+GTC_OK = 0
+GTC_ERR_INVALID = -1
+GTC_ERR_CONDITIONING = -2
+GTC_ERR_NO_CANDIDATES = -3
+GTC_ERR_CUDA = -4
+GTC_ERR_OOM = -5
+GTC_ERR_CONFIG = -6
+GTC_ERR_CAPACITY = -7
+
+
+class gtc_kernel(C.Structure):
+    _fields_ = [("nu", C.c_int32), ("lengthscale", C.c_double), ("output_variance", C.c_double)]
+
+
+class gtc_model_config(C.Structure):
+    _fields_ = [("kernel", gtc_kernel), ("noise", C.c_double), ("jitter", C.c_double),
+                ("n_max", C.c_int32)]
+
+
+class gtc_fit_info(C.Structure):
+    _fields_ = [("n", C.c_int32), ("rebuilt", C.c_int32), ("y_mean", C.c_double),
+                ("y_std", C.c_double), ("jitter", C.c_double)]
+
+
+class gtc_select_args(C.Structure):
+    _fields_ = [("af_mask", C.c_uint32), ("lambda_mode", C.c_int32),
+                ("lambda_constant", C.c_double), ("cv_initial_sample_mean", C.c_double),
+                ("cv_initial_mean_variance", C.c_double), ("f_best_raw", C.c_double),
+                ("excluded", C.POINTER(C.c_int64)), ("n_excluded", C.c_int32)]
+
+
+class gtc_select_result(C.Structure):
+    _fields_ = [("position", C.c_int64 * 3), ("score", C.c_double * 3), ("lambda_", C.c_double),
+                ("mean_variance", C.c_double), ("best_std", C.c_double),
+                ("n_candidates", C.c_int64), ("cv_fallback", C.c_int32)]
+
+
+P = C.c_void_p
+DP = C.POINTER(C.c_double)
+I64P = C.POINTER(C.c_int64)
+U8P = C.POINTER(C.c_uint8)
+
+# (name, restype, argtypes) — exactly the declarations of include/gridtune_cuda.h
+SIGNATURES = [
+    ("gtc_last_error", C.c_char_p, []),
+    ("gtc_version", C.c_char_p, []),
+    ("gtc_kernel_launches", C.c_uint64, []),
+    ("gtc_space_create", C.c_int, [C.c_int, DP, C.c_int64, C.c_int32, C.POINTER(P)]),
+    ("gtc_space_destroy", C.c_int, [P]),
+    ("gtc_space_size", C.c_int64, [P]),
+    ("gtc_run_create", C.c_int, [P, C.POINTER(gtc_model_config), C.POINTER(P)]),
+    ("gtc_run_destroy", C.c_int, [P]),
+    ("gtc_fit", C.c_int, [P, I64P, DP, C.c_int32, C.POINTER(gtc_fit_info)]),
+    ("gtc_append", C.c_int, [P, C.c_int64, C.c_double, C.POINTER(gtc_fit_info)]),
+    ("gtc_truncate", C.c_int, [P, C.c_int32, C.POINTER(gtc_fit_info)]),
+    ("gtc_mark_visited", C.c_int, [P, C.c_int64]),
+    ("gtc_unmark_visited", C.c_int, [P, C.c_int64]),
+    ("gtc_unvisited_count", C.c_int64, [P]),
+    ("gtc_select", C.c_int, [P, C.POINTER(gtc_select_args), C.POINTER(gtc_select_result)]),
+    ("gtc_mean_variance", C.c_int, [P, DP, I64P]),
+    ("gtc_read_predictions", C.c_int, [P, DP, DP]),
+    ("gtc_last_pass_ms", C.c_double, [P]),
+    ("gtc_run_stream", C.c_uint64, [P]),
+    ("gtc_gp_fit", C.c_int, [C.c_int, C.POINTER(gtc_kernel), DP, DP, C.c_int32, C.c_int32,
+                             C.c_double, C.c_double, C.POINTER(P), C.POINTER(gtc_fit_info)]),
+    ("gtc_gp_predict", C.c_int, [P, DP, C.c_int64, DP, DP]),
+    ("gtc_gp_info", C.c_int, [P, C.POINTER(gtc_fit_info)]),
+    ("gtc_gp_destroy", C.c_int, [P]),
+    ("gtc_best_candidate", C.c_int, [C.c_int, C.c_int32, DP, DP, C.c_int64, C.c_double,
+                                     C.c_double, U8P, I64P, DP]),
+]
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Loads libgridtune_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = os.environ.get("GRIDTUNE_B200_LIB", str(LIB_PATH))
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)")
+    lib = C.CDLL(path)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().gtc_last_error().decode()
+
+
+def dptr(a):
+    return a.ctypes.data_as(DP)
+
+
+def i64ptr(a):
+    return a.ctypes.data_as(I64P)
+
+
+def u8ptr(a):
+    return a.ctypes.data_as(U8P)

@@ -1,0 +1,706 @@
+// C ABI (include/gridtune_cuda.h) over the sm_100a kernels in gtc_kernels.cu.
+//
+// Host-side orchestration of the reference's GpModel::fit / predict and the
+// run_bo selection step (citations in the header and in gtc_kernels.cu).
+// No CPU fallback: every compute path launches device kernels and reports
+// GTC_ERR_CUDA when the device is unusable.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gridtune_cuda.h"
+#include "gtc_internal.h"
+
+using namespace gtc;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define GTC_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) return fail(GTC_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define GTC_LAUNCHED()                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess) return fail(GTC_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>
+int dalloc(T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * count);
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? GTC_ERR_OOM : GTC_ERR_CUDA,
+                std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  return GTC_OK;
+}
+
+int64_t pad_tiles(int64_t n) { return ((n + kTile - 1) / kTile) * kTile; }
+
+int check_kernel(const gtc_kernel* k) {
+  if (!k) return fail(GTC_ERR_INVALID, "kernel is null");
+  if (k->nu < 0 || k->nu > 2) return fail(GTC_ERR_INVALID, "unknown Matern nu");
+  // MaternKernel constructor checks, gp.hpp:33-37
+  if (!(k->lengthscale > 0.0)) return fail(GTC_ERR_INVALID, "kernel lengthscale must be positive");
+  if (!(k->output_variance > 0.0)) return fail(GTC_ERR_INVALID, "kernel output variance must be positive");
+  return GTC_OK;
+}
+
+KernelParams kparams(const gtc_kernel& k) { return KernelParams{k.nu, k.lengthscale, k.output_variance}; }
+
+std::string fmt_jitter(double j) { return std::to_string(j); }  // std::to_string as gp.hpp:126
+
+// Scratch for the multi-block reductions (sized for reduce_blocks()).
+struct ReduceScratch {
+  double* psum = nullptr;
+  int64_t* pcnt = nullptr;
+  double* pscore = nullptr;
+  int64_t* ppos = nullptr;
+  int64_t* pfirst = nullptr;
+  int64_t* pcnt2 = nullptr;
+  unsigned int* counter = nullptr;
+  VarTotals* totals = nullptr;
+  SelectDev* sel = nullptr;
+  SelectDev* h_sel = nullptr;  // pinned
+  VarTotals* h_totals = nullptr;
+
+  int init(int64_t n) {
+    const int b = reduce_blocks(n);
+    int rc;
+    if ((rc = dalloc(&psum, b)) || (rc = dalloc(&pcnt, b)) || (rc = dalloc(&pscore, 3 * b)) ||
+        (rc = dalloc(&ppos, 3 * b)) || (rc = dalloc(&pfirst, b)) || (rc = dalloc(&pcnt2, b)) ||
+        (rc = dalloc(&counter, 2)) || (rc = dalloc(&totals, 1)) || (rc = dalloc(&sel, 1)))
+      return rc;
+    GTC_CUDA(cudaMemset(counter, 0, 2 * sizeof(unsigned int)));
+    GTC_CUDA(cudaMallocHost(&h_sel, sizeof(SelectDev)));
+    GTC_CUDA(cudaMallocHost(&h_totals, sizeof(VarTotals)));
+    return GTC_OK;
+  }
+  void release() {
+    cudaFree(psum); cudaFree(pcnt); cudaFree(pscore); cudaFree(ppos); cudaFree(pfirst);
+    cudaFree(pcnt2); cudaFree(counter); cudaFree(totals); cudaFree(sel);
+    if (h_sel) cudaFreeHost(h_sel);
+    if (h_totals) cudaFreeHost(h_totals);
+  }
+};
+
+// Device GP model storage.
+struct GpStore {
+  GpDev dev{};
+  GpScalars* h_sc = nullptr;  // pinned
+  int init(int n_max, int d) {
+    int rc;
+    dev.n_max = n_max;
+    dev.d = d;
+    if ((rc = dalloc(&dev.train_x, (size_t)n_max * d)) || (rc = dalloc(&dev.train_n2, n_max)) ||
+        (rc = dalloc(&dev.y, n_max)) || (rc = dalloc(&dev.L, (size_t)n_max * n_max)) ||
+        (rc = dalloc(&dev.c, n_max)) || (rc = dalloc(&dev.e, n_max)) ||
+        (rc = dalloc(&dev.beta, n_max)) || (rc = dalloc(&dev.sc, 1)) ||
+        (rc = dalloc(&dev.scratch, n_max)))
+      return rc;
+    GTC_CUDA(cudaMemset(dev.sc, 0, sizeof(GpScalars)));
+    GTC_CUDA(cudaMallocHost(&h_sc, sizeof(GpScalars)));
+    std::memset(h_sc, 0, sizeof(GpScalars));
+    h_sc->y_std = 1.0;
+    return GTC_OK;
+  }
+  void release() {
+    cudaFree(dev.train_x); cudaFree(dev.train_n2); cudaFree(dev.y); cudaFree(dev.L);
+    cudaFree(dev.c); cudaFree(dev.e); cudaFree(dev.beta); cudaFree(dev.sc); cudaFree(dev.scratch);
+    if (h_sc) cudaFreeHost(h_sc);
+  }
+};
+
+// Factorises the n training points already on the device with the
+// reference's jitter escalation (gp.hpp:116-129), starting at `jitter` and
+// never exceeding base * 2^6.  On success h_sc holds the scalars.
+int factor_with_escalation(GpStore& gp, const gtc_kernel& k, double noise, double base_jitter,
+                           double start_jitter, int n, cudaStream_t s) {
+  double jitter = start_jitter;
+  // attempts already "spent" below start_jitter (each failed in the reference)
+  int attempts = 0;
+  for (double j = base_jitter; j < start_jitter; j *= 2.0) ++attempts;
+  if (attempts > 6) {
+    return fail(GTC_ERR_CONDITIONING, "Gram matrix factorization failed after jitter escalation to " +
+                                          fmt_jitter(base_jitter * 64.0));
+  }
+  while (true) {
+    launch_gp_factor(gp.dev, kparams(k), noise, jitter, n, s);
+    GTC_LAUNCHED();
+    GTC_CUDA(cudaMemcpyAsync(gp.h_sc, gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, s));
+    GTC_CUDA(cudaStreamSynchronize(s));
+    if (gp.h_sc->status == 0) return GTC_OK;
+    if (++attempts > 6) {
+      return fail(GTC_ERR_CONDITIONING,
+                  "Gram matrix factorization failed after jitter escalation to " + fmt_jitter(jitter));
+    }
+    jitter *= 2.0;
+  }
+}
+
+// Rebuilds V rows [0, n) for `space` (chunks of kMaxRows) and the posterior.
+int rebuild_predictions(const SpaceDev& sp, GpStore& gp, const gtc_kernel& k, double* V,
+                        int64_t tile_stride, int n, double* mu, double* var, cudaStream_t s) {
+  if (n == 0) {
+    launch_prior(mu, var, sp.n_pad, k.output_variance, s);
+    GTC_LAUNCHED();
+    return GTC_OK;
+  }
+  for (int n0 = 0; n0 < n; n0 += kMaxRows) {
+    const int r = std::min(kMaxRows, n - n0);
+    launch_extend(sp, gp.dev, kparams(k), V, tile_stride, n0, r, n0 + r == n, mu, var, false, s);
+    GTC_LAUNCHED();
+  }
+  return GTC_OK;
+}
+
+void fill_info(gtc_fit_info* info, const GpScalars& sc, int n, int rebuilt) {
+  if (!info) return;
+  info->n = n;
+  info->rebuilt = rebuilt;
+  info->y_mean = sc.y_mean;
+  info->y_std = sc.y_std;
+  info->jitter = sc.jitter;
+}
+
+int check_fit_inputs(const double* y, int n, double noise, double jitter) {
+  if (n < 0) return fail(GTC_ERR_INVALID, "GP fit: observation count does not match input count");
+  if (!(noise >= 0.0)) return fail(GTC_ERR_INVALID, "GP fit: noise must be non-negative");
+  if (!(jitter > 0.0)) return fail(GTC_ERR_INVALID, "GP fit: jitter must be positive");
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(y[i])) return fail(GTC_ERR_INVALID, "GP fit: observations must be finite");
+  return GTC_OK;
+}
+
+}  // namespace
+
+// =============================================================== handles
+
+struct gtc_space {
+  int device = 0;
+  int64_t n = 0, n_pad = 0;
+  int d = 0;
+  double* coords = nullptr;          // device SoA [d][n_pad]
+  std::vector<double> host_coords;   // row-major n x d (gathers for fit)
+  SpaceDev dev() const { return SpaceDev{coords, n, n_pad, d}; }
+};
+
+struct gtc_run {
+  gtc_space* space = nullptr;
+  gtc_model_config cfg{};
+  cudaStream_t stream = nullptr;
+  GpStore gp;
+  ReduceScratch red;
+  double* V = nullptr;
+  int64_t tile_stride = 0;
+  double* mu = nullptr;
+  double* var = nullptr;
+  uint32_t* visited = nullptr;
+  int64_t* excluded = nullptr;
+  int excluded_cap = 0;
+  std::vector<uint32_t> visited_host;
+  int64_t visited_count = 0;
+  int n = 0;
+  double jitter = 0.0;
+  bool predictions_valid = false;
+  std::vector<double> y_host;
+  std::vector<int64_t> pos_host;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool pass_timed = false;
+};
+
+struct gtc_gp {
+  int device = 0;
+  gtc_kernel kernel{};
+  double noise = 0, jitter = 0;
+  int n = 0, d = 0;
+  cudaStream_t stream = nullptr;
+  GpStore gp;
+};
+
+// =============================================================== library
+
+extern "C" const char* gtc_last_error(void) { return g_last_error.c_str(); }
+extern "C" const char* gtc_version(void) { return "gridtune-b200 0.1 (sm_100a)"; }
+extern "C" uint64_t gtc_kernel_launches(void) { return launches(); }
+
+// =============================================================== space
+
+extern "C" int gtc_space_create(int device, const double* coords, int64_t n, int32_t d,
+                                gtc_space** out) {
+  if (!out) return fail(GTC_ERR_INVALID, "out is null");
+  *out = nullptr;
+  if (n <= 0) return fail(GTC_ERR_INVALID, "search space has no configurations");
+  if (d <= 0 || d > kMaxDim) return fail(GTC_ERR_INVALID, "search-space dimension out of range [1, 64]");
+  if (!coords) return fail(GTC_ERR_INVALID, "coords is null");
+  GTC_CUDA(cudaSetDevice(device));
+  auto* s = new gtc_space();
+  s->device = device;
+  s->n = n;
+  s->n_pad = pad_tiles(n);
+  s->d = d;
+  s->host_coords.assign(coords, coords + n * d);
+  std::vector<double> soa((size_t)d * s->n_pad, 0.0);
+  for (int64_t j = 0; j < n; ++j)
+    for (int t = 0; t < d; ++t) soa[(size_t)t * s->n_pad + j] = coords[j * d + t];
+  int rc = dalloc(&s->coords, soa.size());
+  if (rc) {
+    delete s;
+    return rc;
+  }
+  cudaError_t e = cudaMemcpy(s->coords, soa.data(), soa.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(s->coords);
+    delete s;
+    return fail(GTC_ERR_CUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
+  }
+  *out = s;
+  return GTC_OK;
+}
+
+extern "C" int gtc_space_destroy(gtc_space* s) {
+  if (!s) return GTC_OK;
+  cudaSetDevice(s->device);
+  cudaFree(s->coords);
+  delete s;
+  return GTC_OK;
+}
+
+extern "C" int64_t gtc_space_size(const gtc_space* s) { return s ? s->n : -1; }
+
+// =============================================================== run
+
+extern "C" int gtc_run_destroy(gtc_run* r) {
+  if (!r) return GTC_OK;
+  cudaSetDevice(r->space->device);
+  if (r->stream) cudaStreamSynchronize(r->stream);
+  r->gp.release();
+  r->red.release();
+  cudaFree(r->V);
+  cudaFree(r->mu);
+  cudaFree(r->var);
+  cudaFree(r->visited);
+  cudaFree(r->excluded);
+  if (r->ev0) cudaEventDestroy(r->ev0);
+  if (r->ev1) cudaEventDestroy(r->ev1);
+  if (r->stream) cudaStreamDestroy(r->stream);
+  delete r;
+  return GTC_OK;
+}
+
+extern "C" int gtc_run_create(gtc_space* space, const gtc_model_config* cfg, gtc_run** out) {
+  if (!out) return fail(GTC_ERR_INVALID, "out is null");
+  *out = nullptr;
+  if (!space || !cfg) return fail(GTC_ERR_INVALID, "space/config is null");
+  int rc = check_kernel(&cfg->kernel);
+  if (rc) return rc;
+  if (!(cfg->noise >= 0.0)) return fail(GTC_ERR_INVALID, "GP fit: noise must be non-negative");
+  if (!(cfg->jitter > 0.0)) return fail(GTC_ERR_INVALID, "GP fit: jitter must be positive");
+  if (cfg->n_max < 1 || cfg->n_max > kMaxNmax)
+    return fail(GTC_ERR_CONFIG, "n_max out of range [1, 1024]");
+  GTC_CUDA(cudaSetDevice(space->device));
+  auto* r = new gtc_run();
+  r->space = space;
+  r->cfg = *cfg;
+  r->jitter = cfg->jitter;
+  r->tile_stride = (int64_t)cfg->n_max * kTile;
+  const int64_t tiles = space->n_pad / kTile;
+  const int64_t words = (space->n + 31) / 32;
+  if ((rc = r->gp.init(cfg->n_max, space->d)) || (rc = r->red.init(space->n)) ||
+      (rc = dalloc(&r->V, (size_t)tiles * r->tile_stride)) || (rc = dalloc(&r->mu, space->n_pad)) ||
+      (rc = dalloc(&r->var, space->n_pad)) || (rc = dalloc(&r->visited, words))) {
+    gtc_run_destroy(r);
+    return rc;
+  }
+  cudaError_t e = cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreate(&r->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&r->ev1);
+  if (e == cudaSuccess) e = cudaMemset(r->visited, 0, words * sizeof(uint32_t));
+  if (e != cudaSuccess) {
+    gtc_run_destroy(r);
+    return fail(GTC_ERR_CUDA, std::string("run create: ") + cudaGetErrorString(e));
+  }
+  r->visited_host.assign(words, 0u);
+  *out = r;
+  return GTC_OK;
+}
+
+static int upload_train(gtc_run* r, const int64_t* positions, const double* y, int n) {
+  const int d = r->space->d;
+  std::vector<double> X((size_t)n * d);
+  for (int i = 0; i < n; ++i) {
+    if (positions[i] < 0 || positions[i] >= r->space->n)
+      return fail(GTC_ERR_INVALID, "training position out of range");
+    std::memcpy(&X[(size_t)i * d], &r->space->host_coords[(size_t)positions[i] * d], sizeof(double) * d);
+  }
+  if (n > 0) {
+    GTC_CUDA(cudaMemcpyAsync(r->gp.dev.train_x, X.data(), X.size() * sizeof(double), cudaMemcpyHostToDevice, r->stream));
+    GTC_CUDA(cudaMemcpyAsync(r->gp.dev.y, y, sizeof(double) * n, cudaMemcpyHostToDevice, r->stream));
+  }
+  return GTC_OK;
+}
+
+static int refit(gtc_run* r, double start_jitter, gtc_fit_info* info) {
+  const int n = (int)r->y_host.size();
+  int rc = upload_train(r, r->pos_host.data(), r->y_host.data(), n);
+  if (rc) return rc;
+  rc = factor_with_escalation(r->gp, r->cfg.kernel, r->cfg.noise, r->cfg.jitter, start_jitter, n, r->stream);
+  if (rc) {
+    r->predictions_valid = false;
+    return rc;
+  }
+  r->n = n;
+  r->jitter = r->gp.h_sc->jitter;
+  rc = rebuild_predictions(r->space->dev(), r->gp, r->cfg.kernel, r->V, r->tile_stride, n, r->mu, r->var, r->stream);
+  if (rc) return rc;
+  r->predictions_valid = true;
+  fill_info(info, *r->gp.h_sc, n, 1);
+  return GTC_OK;
+}
+
+extern "C" int gtc_fit(gtc_run* r, const int64_t* positions, const double* y_raw, int32_t n,
+                       gtc_fit_info* info) {
+  if (!r) return fail(GTC_ERR_INVALID, "run is null");
+  if (n > r->cfg.n_max) return fail(GTC_ERR_CAPACITY, "more observations than the run's n_max");
+  int rc = check_fit_inputs(y_raw, n, r->cfg.noise, r->cfg.jitter);
+  if (rc) return rc;
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  r->y_host.assign(y_raw, y_raw + n);
+  r->pos_host.assign(positions, positions + n);
+  if (n == 0) {
+    r->n = 0;
+    r->jitter = r->cfg.jitter;
+    std::memset(r->gp.h_sc, 0, sizeof(GpScalars));
+    r->gp.h_sc->y_std = 1.0;
+    r->gp.h_sc->jitter = r->jitter;
+    GTC_CUDA(cudaMemcpyAsync(r->gp.dev.sc, r->gp.h_sc, sizeof(GpScalars), cudaMemcpyHostToDevice, r->stream));
+    rc = rebuild_predictions(r->space->dev(), r->gp, r->cfg.kernel, r->V, r->tile_stride, 0, r->mu, r->var, r->stream);
+    if (rc) return rc;
+    GTC_CUDA(cudaStreamSynchronize(r->stream));
+    r->predictions_valid = true;
+    fill_info(info, *r->gp.h_sc, 0, 1);
+    return GTC_OK;
+  }
+  return refit(r, r->cfg.jitter, info);
+}
+
+extern "C" int gtc_append(gtc_run* r, int64_t pos, double y_raw, gtc_fit_info* info) {
+  if (!r) return fail(GTC_ERR_INVALID, "run is null");
+  if (pos < 0 || pos >= r->space->n) return fail(GTC_ERR_INVALID, "position out of range");
+  if (!std::isfinite(y_raw)) return fail(GTC_ERR_INVALID, "GP fit: observations must be finite");
+  if (r->n >= r->cfg.n_max) return fail(GTC_ERR_CAPACITY, "more observations than the run's n_max");
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  const int n0 = r->n;
+  r->y_host.resize(n0);
+  r->pos_host.resize(n0);
+  r->y_host.push_back(y_raw);
+  r->pos_host.push_back(pos);
+  if (n0 == 0) return refit(r, r->cfg.jitter, info);
+  launch_gp_append(r->gp.dev, kparams(r->cfg.kernel), r->cfg.noise, r->space->dev(), pos, nullptr, y_raw, n0, r->stream);
+  GTC_LAUNCHED();
+  GTC_CUDA(cudaMemcpyAsync(r->gp.h_sc, r->gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, r->stream));
+  GTC_CUDA(cudaStreamSynchronize(r->stream));
+  if (r->gp.h_sc->status != 0) {
+    // new pivot <= 0 at the current jitter: the reference's refit would fail at
+    // every jitter up to the current one too, so escalate from jitter * 2.
+    return refit(r, r->jitter * 2.0, info);
+  }
+  GTC_CUDA(cudaEventRecord(r->ev0, r->stream));
+  launch_extend(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, n0, 1, true, r->mu, r->var, false, r->stream);
+  GTC_LAUNCHED();
+  GTC_CUDA(cudaEventRecord(r->ev1, r->stream));
+  r->pass_timed = true;
+  r->n = n0 + 1;
+  r->predictions_valid = true;
+  fill_info(info, *r->gp.h_sc, r->n, 0);
+  return GTC_OK;
+}
+
+extern "C" int gtc_truncate(gtc_run* r, int32_t n, gtc_fit_info* info) {
+  if (!r) return fail(GTC_ERR_INVALID, "run is null");
+  if (n < 0 || n > r->n) return fail(GTC_ERR_INVALID, "truncate: n out of range");
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  if (n == 0) return gtc_fit(r, nullptr, nullptr, 0, info);
+  launch_gp_truncate(r->gp.dev, n, r->stream);
+  GTC_LAUNCHED();
+  GTC_CUDA(cudaMemcpyAsync(r->gp.h_sc, r->gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, r->stream));
+  GTC_CUDA(cudaStreamSynchronize(r->stream));
+  r->n = n;
+  r->y_host.resize(n);
+  r->pos_host.resize(n);
+  r->predictions_valid = false;
+  fill_info(info, *r->gp.h_sc, n, 0);
+  return GTC_OK;
+}
+
+static int ensure_predictions(gtc_run* r) {
+  if (r->predictions_valid) return GTC_OK;
+  if (r->n == 0) {
+    launch_prior(r->mu, r->var, r->space->n_pad, r->cfg.kernel.output_variance, r->stream);
+  } else {
+    // posterior from the resident V rows (r = 0 new rows)
+    launch_extend(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, r->n, 0, true, r->mu, r->var, false, r->stream);
+  }
+  GTC_LAUNCHED();
+  r->predictions_valid = true;
+  return GTC_OK;
+}
+
+static int set_visited(gtc_run* r, int64_t pos, int set) {
+  if (!r) return fail(GTC_ERR_INVALID, "run is null");
+  if (pos < 0 || pos >= r->space->n) return fail(GTC_ERR_INVALID, "position out of range");
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  uint32_t& w = r->visited_host[pos >> 5];
+  const uint32_t bit = 1u << (pos & 31);
+  const bool was = (w & bit) != 0;
+  if (set && !was) {
+    w |= bit;
+    ++r->visited_count;
+  } else if (!set && was) {
+    w &= ~bit;
+    --r->visited_count;
+  } else {
+    return GTC_OK;
+  }
+  launch_mark(r->visited, pos, set, r->stream);
+  GTC_LAUNCHED();
+  return GTC_OK;
+}
+
+extern "C" int gtc_mark_visited(gtc_run* r, int64_t pos) { return set_visited(r, pos, 1); }
+extern "C" int gtc_unmark_visited(gtc_run* r, int64_t pos) { return set_visited(r, pos, 0); }
+extern "C" int64_t gtc_unvisited_count(const gtc_run* r) {
+  return r ? r->space->n - r->visited_count : -1;
+}
+
+extern "C" int gtc_mean_variance(gtc_run* r, double* out, int64_t* count) {
+  if (!r || !out) return fail(GTC_ERR_INVALID, "null argument");
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  int rc = ensure_predictions(r);
+  if (rc) return rc;
+  launch_varsum(r->var, r->visited, r->space->n, r->red.psum, r->red.pcnt, r->red.counter, r->red.totals, r->stream);
+  GTC_LAUNCHED();
+  GTC_CUDA(cudaMemcpyAsync(r->red.h_totals, r->red.totals, sizeof(VarTotals), cudaMemcpyDeviceToHost, r->stream));
+  GTC_CUDA(cudaStreamSynchronize(r->stream));
+  // strategies.hpp:394-397: empty candidate set -> 0.0
+  *out = r->red.h_totals->count > 0 ? r->red.h_totals->sum / (double)r->red.h_totals->count : 0.0;
+  if (count) *count = r->red.h_totals->count;
+  return GTC_OK;
+}
+
+extern "C" int gtc_select(gtc_run* r, const gtc_select_args* a, gtc_select_result* out) {
+  if (!r || !a || !out) return fail(GTC_ERR_INVALID, "null argument");
+  if ((a->af_mask & 7u) == 0) return fail(GTC_ERR_INVALID, "af_mask selects no acquisition function");
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  int rc = ensure_predictions(r);
+  if (rc) return rc;
+  SelectParams p{a->af_mask & 7u, a->lambda_mode, a->lambda_constant, a->cv_initial_sample_mean,
+                 a->cv_initial_mean_variance, a->f_best_raw, nullptr, 0};
+  if (a->n_excluded > 0) {
+    if (a->n_excluded > r->excluded_cap) {
+      cudaFree(r->excluded);
+      r->excluded = nullptr;
+      r->excluded_cap = 0;
+      if ((rc = dalloc(&r->excluded, a->n_excluded))) return rc;
+      r->excluded_cap = a->n_excluded;
+    }
+    GTC_CUDA(cudaMemcpyAsync(r->excluded, a->excluded, sizeof(int64_t) * a->n_excluded, cudaMemcpyHostToDevice, r->stream));
+    p.excluded = r->excluded;
+    p.n_excluded = a->n_excluded;
+  }
+  launch_varsum(r->var, r->visited, r->space->n, r->red.psum, r->red.pcnt, r->red.counter, r->red.totals, r->stream);
+  GTC_LAUNCHED();
+  launch_select(r->mu, r->var, r->visited, r->space->n, r->red.totals, r->gp.dev.sc, p, r->red.pscore,
+                r->red.ppos, r->red.pfirst, r->red.pcnt2, r->red.counter + 1, r->red.sel, r->stream);
+  GTC_LAUNCHED();
+  GTC_CUDA(cudaMemcpyAsync(r->red.h_sel, r->red.sel, sizeof(SelectDev), cudaMemcpyDeviceToHost, r->stream));
+  GTC_CUDA(cudaStreamSynchronize(r->stream));
+  const SelectDev& s = *r->red.h_sel;
+  for (int k = 0; k < 3; ++k) {
+    out->position[k] = s.position[k];
+    out->score[k] = s.score[k];
+  }
+  out->lambda = s.lambda;
+  out->mean_variance = s.mean_variance;
+  out->best_std = s.best_std;
+  out->n_candidates = s.n_candidates;
+  out->cv_fallback = s.cv_fallback;
+  if (s.n_candidates == 0) return fail(GTC_ERR_NO_CANDIDATES, "acquisition: no candidates remaining");
+  return GTC_OK;
+}
+
+extern "C" int gtc_read_predictions(gtc_run* r, double* mean, double* variance) {
+  if (!r) return fail(GTC_ERR_INVALID, "run is null");
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  int rc = ensure_predictions(r);
+  if (rc) return rc;
+  if (mean) GTC_CUDA(cudaMemcpyAsync(mean, r->mu, sizeof(double) * r->space->n, cudaMemcpyDeviceToHost, r->stream));
+  if (variance) GTC_CUDA(cudaMemcpyAsync(variance, r->var, sizeof(double) * r->space->n, cudaMemcpyDeviceToHost, r->stream));
+  GTC_CUDA(cudaStreamSynchronize(r->stream));
+  return GTC_OK;
+}
+
+extern "C" double gtc_last_pass_ms(const gtc_run* r) {
+  if (!r || !r->pass_timed) return 0.0;
+  float ms = 0.f;
+  if (cudaEventSynchronize(r->ev1) != cudaSuccess) return 0.0;
+  if (cudaEventElapsedTime(&ms, r->ev0, r->ev1) != cudaSuccess) return 0.0;
+  return ms;
+}
+
+extern "C" uint64_t gtc_run_stream(const gtc_run* r) { return r ? (uint64_t)(uintptr_t)r->stream : 0; }
+
+// =============================================================== stand-alone GpModel
+
+extern "C" int gtc_gp_destroy(gtc_gp* g) {
+  if (!g) return GTC_OK;
+  cudaSetDevice(g->device);
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  g->gp.release();
+  if (g->stream) cudaStreamDestroy(g->stream);
+  delete g;
+  return GTC_OK;
+}
+
+extern "C" int gtc_gp_fit(int device, const gtc_kernel* kernel, const double* X, const double* y,
+                          int32_t n, int32_t d, double noise, double jitter, gtc_gp** out,
+                          gtc_fit_info* info) {
+  if (!out) return fail(GTC_ERR_INVALID, "out is null");
+  *out = nullptr;
+  int rc = check_kernel(kernel);
+  if (rc) return rc;
+  if ((rc = check_fit_inputs(y, n, noise, jitter))) return rc;
+  if (d <= 0 || d > kMaxDim) return fail(GTC_ERR_INVALID, "dimension out of range [1, 64]");
+  if (n > kMaxNmax) return fail(GTC_ERR_CAPACITY, "more than 1024 observations");
+  GTC_CUDA(cudaSetDevice(device));
+  auto* g = new gtc_gp();
+  g->device = device;
+  g->kernel = *kernel;
+  g->noise = noise;
+  g->jitter = jitter;
+  g->n = n;
+  g->d = d;
+  if ((rc = g->gp.init(n > 0 ? n : 1, d))) {
+    gtc_gp_destroy(g);
+    return rc;
+  }
+  cudaError_t e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    gtc_gp_destroy(g);
+    return fail(GTC_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(e));
+  }
+  if (n > 0) {
+    e = cudaMemcpyAsync(g->gp.dev.train_x, X, sizeof(double) * n * d, cudaMemcpyHostToDevice, g->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->gp.dev.y, y, sizeof(double) * n, cudaMemcpyHostToDevice, g->stream);
+    if (e != cudaSuccess) {
+      gtc_gp_destroy(g);
+      return fail(GTC_ERR_CUDA, std::string("upload: ") + cudaGetErrorString(e));
+    }
+    rc = factor_with_escalation(g->gp, g->kernel, noise, jitter, jitter, n, g->stream);
+    if (rc) {
+      const std::string msg = g_last_error;
+      gtc_gp_destroy(g);
+      return fail(rc, msg);
+    }
+  } else {
+    g->gp.h_sc->jitter = jitter;
+  }
+  fill_info(info, *g->gp.h_sc, n, 1);
+  *out = g;
+  return GTC_OK;
+}
+
+extern "C" int gtc_gp_predict(gtc_gp* g, const double* Xstar, int64_t m, double* mean, double* variance) {
+  if (!g) return fail(GTC_ERR_INVALID, "gp is null");
+  if (m < 0) return fail(GTC_ERR_INVALID, "negative point count");
+  if (m == 0) return GTC_OK;
+  GTC_CUDA(cudaSetDevice(g->device));
+  gtc_space* sp = nullptr;
+  int rc = gtc_space_create(g->device, Xstar, m, g->d, &sp);
+  if (rc) return rc;
+  const int64_t tiles = sp->n_pad / kTile;
+  const int64_t tile_stride = (int64_t)(g->n > 0 ? g->n : 1) * kTile;
+  double *V = nullptr, *mu = nullptr, *var = nullptr;
+  if ((rc = dalloc(&V, (size_t)tiles * tile_stride)) || (rc = dalloc(&mu, sp->n_pad)) ||
+      (rc = dalloc(&var, sp->n_pad))) {
+    cudaFree(V); cudaFree(mu); cudaFree(var);
+    gtc_space_destroy(sp);
+    return rc;
+  }
+  // GpDev with n_max = n so the extend kernel's L stride matches the factor
+  rc = rebuild_predictions(sp->dev(), g->gp, g->kernel, V, tile_stride, g->n, mu, var, g->stream);
+  cudaError_t e = cudaSuccess;
+  if (!rc && mean) e = cudaMemcpyAsync(mean, mu, sizeof(double) * m, cudaMemcpyDeviceToHost, g->stream);
+  if (!rc && e == cudaSuccess && variance) e = cudaMemcpyAsync(variance, var, sizeof(double) * m, cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  cudaFree(V); cudaFree(mu); cudaFree(var);
+  gtc_space_destroy(sp);
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail(GTC_ERR_CUDA, std::string("predict: ") + cudaGetErrorString(e));
+  return GTC_OK;
+}
+
+extern "C" int gtc_gp_info(const gtc_gp* g, gtc_fit_info* info) {
+  if (!g || !info) return fail(GTC_ERR_INVALID, "null argument");
+  fill_info(info, *g->gp.h_sc, g->n, 1);
+  return GTC_OK;
+}
+
+// =============================================================== best_candidate
+
+extern "C" int gtc_best_candidate(int device, int32_t af, const double* means, const double* stds,
+                                  int64_t n, double best_std, double lambda, const uint8_t* excluded,
+                                  int64_t* position_out, double* score_out) {
+  if (af < 0 || af > 2) return fail(GTC_ERR_INVALID, "unknown acquisition function");
+  if (n <= 0) return fail(GTC_ERR_NO_CANDIDATES, "acquisition: no candidates remaining");
+  GTC_CUDA(cudaSetDevice(device));
+  cudaStream_t s;
+  GTC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  ReduceScratch red;
+  double *dm = nullptr, *ds = nullptr;
+  uint8_t* dx = nullptr;
+  int rc = red.init(n);
+  if (!rc) rc = dalloc(&dm, n);
+  if (!rc) rc = dalloc(&ds, n);
+  if (!rc && excluded) rc = dalloc(&dx, n);
+  cudaError_t e = cudaSuccess;
+  if (!rc) {
+    e = cudaMemcpyAsync(dm, means, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ds, stds, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && excluded) e = cudaMemcpyAsync(dx, excluded, n, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) {
+      launch_best_candidate(dm, ds, dx, n, af, best_std, lambda, red.pscore, red.ppos, red.pfirst,
+                            red.pcnt2, red.counter, red.sel, s);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(red.h_sel, red.sel, sizeof(SelectDev), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  }
+  SelectDev res{};
+  if (!rc && e == cudaSuccess) res = *red.h_sel;
+  cudaFree(dm); cudaFree(ds); cudaFree(dx);
+  red.release();
+  cudaStreamDestroy(s);
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail(GTC_ERR_CUDA, std::string("best_candidate: ") + cudaGetErrorString(e));
+  if (res.n_candidates == 0) return fail(GTC_ERR_NO_CANDIDATES, "acquisition: no candidates remaining");
+  if (position_out) *position_out = res.position[af];
+  if (score_out) *score_out = res.score[af];
+  return GTC_OK;
+}

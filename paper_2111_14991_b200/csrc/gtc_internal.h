@@ -1,0 +1,135 @@
+// Internal declarations shared by the kernels (gtc_kernels.cu) and the C ABI
+// host layer (gtc_capi.cu).  Not part of the public ABI (include/gridtune_cuda.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gtc {
+
+// Candidates per tile.  V (= L^-1 K*, one row per GP observation) is stored
+// tile-major: V[tile][row][kTile], so one tile's rows are one contiguous
+// n_max*kTile*8-byte stream and an appended row is a contiguous 2 KB store
+// per tile.  See DESIGN.md "Data layout in HBM".
+constexpr int kTile = 256;
+constexpr int kExtendThreads = kTile / 2;  // one double2 column pair per thread
+constexpr int kReduceThreads = 256;
+constexpr int kCtaThreads = 256;           // single-CTA GP kernels
+constexpr int kMaxRows = 8;                // rows per multi-row extend pass (rebuild)
+constexpr int kMaxNmax = 1024;             // largest supported GP training size
+constexpr int kMaxDim = 64;                // largest supported search-space dimension
+
+struct KernelParams {
+  int nu;
+  double lengthscale;
+  double s2;  // output variance
+};
+
+// Device-resident GP scalars, written by the single-CTA GP kernels.
+struct GpScalars {
+  double y0;      // shift for the prefix-stable c = L^-1 (y - y0)
+  double y_mean;
+  double y_std;
+  double jitter;
+  int32_t n;      // observations in the model
+  int32_t status; // 0 ok, 1 pivot <= 0 (factorisation failed)
+  int32_t fail_row;
+  int32_t pad;
+};
+
+// Device pointers of one GP model.
+struct GpDev {
+  double* train_x;   // [n_max][d]
+  double* train_n2;  // [n_max] squared norms (sequential), for the expansion distance
+  double* y;         // [n_max] raw observations
+  double* L;         // [n_max][n_max] row-major lower factor
+  double* c;         // [n_max] L^-1 (y - y0)
+  double* e;         // [n_max] L^-1 1
+  double* beta;      // [n_max] L^-1 y_standardized
+  GpScalars* sc;
+  double* scratch;   // [n_max] misc
+  int n_max;
+  int d;
+};
+
+struct SpaceDev {
+  const double* coords;  // SoA [d][n_pad]
+  int64_t n;
+  int64_t n_pad;
+  int d;
+};
+
+// Result of the reduction kernels (device side, copied to the host).
+struct SelectDev {
+  int64_t position[3];
+  double score[3];
+  double lambda;
+  double mean_variance;
+  double best_std;
+  int64_t n_candidates;
+  int32_t cv_fallback;
+  int32_t gp_status;
+};
+
+struct VarTotals {
+  double sum;
+  int64_t count;
+};
+
+struct SelectParams {
+  uint32_t af_mask;
+  int lambda_mode;
+  double lambda_constant;
+  double cv_mu_s;
+  double cv_var_s;
+  double f_best_raw;
+  const int64_t* excluded;  // device
+  int n_excluded;
+};
+
+// --- launchers (gtc_kernels.cu); all asynchronous on `stream` -------------
+
+// Single-CTA: factor the Gram matrix of the model's n training points at the
+// given jitter (left-looking bordered rows), then c, e, y stats, beta.
+void launch_gp_factor(const GpDev& g, KernelParams k, double noise, double jitter, int n,
+                      cudaStream_t stream);
+// Single-CTA: append observation n0 (coords taken from `space` at `pos`, or
+// from `x_explicit` when pos < 0) to the factor; updates scalars and beta.
+void launch_gp_append(const GpDev& g, KernelParams k, double noise, const SpaceDev& space,
+                      int64_t pos, const double* x_explicit, double y_new, int n0,
+                      cudaStream_t stream);
+// Single-CTA: recompute stats/beta for the prefix of n observations.
+void launch_gp_truncate(const GpDev& g, int n, cudaStream_t stream);
+
+// Multi-row V extension over all candidates: rows [n0, n0+r) from rows [0, n0).
+// When `final`, also writes the posterior mean/variance of every candidate.
+void launch_extend(const SpaceDev& space, const GpDev& g, KernelParams k, double* V,
+                   int64_t tile_stride, int n0, int r, bool final, double* mu, double* var,
+                   bool check_status, cudaStream_t stream);
+
+void launch_prior(double* mu, double* var, int64_t n, double s2, cudaStream_t stream);
+void launch_mark(uint32_t* visited, int64_t pos, int set, cudaStream_t stream);
+
+// Sum of the variance over unvisited candidates -> totals (deterministic).
+void launch_varsum(const double* var, const uint32_t* visited, int64_t n, double* partial_sum,
+                   int64_t* partial_cnt, unsigned int* counter, VarTotals* totals,
+                   cudaStream_t stream);
+
+// Fused lambda + acquisition + masked argmax for every AF in the mask.
+void launch_select(const double* mu, const double* var, const uint32_t* visited, int64_t n,
+                   const VarTotals* totals, const GpScalars* sc, SelectParams p,
+                   double* partial_score, int64_t* partial_pos, int64_t* partial_first,
+                   int64_t* partial_cnt, unsigned int* counter, SelectDev* out,
+                   cudaStream_t stream);
+
+// best_candidate over caller spans of stds (not variances).
+void launch_best_candidate(const double* mu, const double* std, const uint8_t* excluded,
+                           int64_t n, int af, double best_std, double lambda,
+                           double* partial_score, int64_t* partial_pos, int64_t* partial_first,
+                           int64_t* partial_cnt, unsigned int* counter, SelectDev* out,
+                           cudaStream_t stream);
+
+int reduce_blocks(int64_t n);  // grid size used by the reduction kernels
+uint64_t launches();
+
+}  // namespace gtc

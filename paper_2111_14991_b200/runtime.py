@@ -1,0 +1,166 @@
+"""Resident search space and BO-run handles (C ABI gtc_space / gtc_run).
+
+`Space` keeps the normalised candidate coordinates in HBM
+(EnumeratedSpace, search_space.hpp:216-245).  `SurrogateRun` owns one run's
+surrogate state on the device — the Cholesky factor, V = L^-1 K* for every
+candidate, the posterior and the visited mask — and exposes the hot path of
+run_bo (strategies.hpp:298-449) as fit / append / mark_visited / select.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import load
+from .gp import (AcquisitionId, ContextualVarianceState, ExplorationConfig, MaternKernel, check)
+
+
+class Space:
+    def __init__(self, coords, device: int = 0):
+        c = np.ascontiguousarray(np.asarray(coords, dtype=np.float64))
+        if c.ndim != 2:
+            raise ValueError("coords must be n x d")
+        self.n, self.d = c.shape
+        self.device = device
+        self.coords = c
+        h = C.c_void_p()
+        check(load().gtc_space_create(device, _lib.dptr(c), self.n, self.d, C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def size(self) -> int:
+        return self.n
+
+    def close(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            load().gtc_space_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class FitInfo:
+    n: int
+    rebuilt: bool
+    y_mean: float
+    y_std: float
+    jitter: float
+
+    @staticmethod
+    def of(i: _lib.gtc_fit_info) -> "FitInfo":
+        return FitInfo(i.n, bool(i.rebuilt), i.y_mean, i.y_std, i.jitter)
+
+
+@dataclass
+class Selection:
+    position: tuple          # per AF slot (ei, poi, lcb); -1 when not requested
+    score: tuple
+    lambda_: float
+    mean_variance: float
+    best_std: float
+    n_candidates: int
+    cv_fallback: bool
+
+    def pick(self, af: AcquisitionId) -> int:
+        return int(self.position[int(af)])
+
+
+class SurrogateRun:
+    def __init__(self, space: Space, kernel: MaternKernel, noise: float = 1e-10,
+                 jitter: float = 1e-6, n_max: int = 220):
+        self.space = space
+        cfg = _lib.gtc_model_config(kernel.c(), float(noise), float(jitter), int(n_max))
+        h = C.c_void_p()
+        check(load().gtc_run_create(space.handle, C.byref(cfg), C.byref(h)))
+        self._h = h
+        self.kernel = kernel
+        self.n_max = n_max
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            load().gtc_run_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def fit(self, positions: Sequence[int], y_raw: Sequence[float]) -> FitInfo:
+        p = np.ascontiguousarray(np.asarray(positions, dtype=np.int64))
+        y = np.ascontiguousarray(np.asarray(y_raw, dtype=np.float64))
+        info = _lib.gtc_fit_info()
+        check(load().gtc_fit(self._h, _lib.i64ptr(p), _lib.dptr(y), len(y), C.byref(info)))
+        return FitInfo.of(info)
+
+    def append(self, position: int, y_raw: float) -> FitInfo:
+        info = _lib.gtc_fit_info()
+        check(load().gtc_append(self._h, int(position), float(y_raw), C.byref(info)))
+        return FitInfo.of(info)
+
+    def truncate(self, n: int) -> FitInfo:
+        info = _lib.gtc_fit_info()
+        check(load().gtc_truncate(self._h, int(n), C.byref(info)))
+        return FitInfo.of(info)
+
+    def mark_visited(self, position: int) -> None:
+        check(load().gtc_mark_visited(self._h, int(position)))
+
+    def unmark_visited(self, position: int) -> None:
+        check(load().gtc_unmark_visited(self._h, int(position)))
+
+    def unvisited_count(self) -> int:
+        return int(load().gtc_unvisited_count(self._h))
+
+    def mean_variance(self) -> float:
+        out = C.c_double()
+        cnt = C.c_int64()
+        check(load().gtc_mean_variance(self._h, C.byref(out), C.byref(cnt)))
+        return out.value
+
+    def predictions(self):
+        n = self.space.n
+        mean = np.empty(n)
+        var = np.empty(n)
+        check(load().gtc_read_predictions(self._h, _lib.dptr(mean), _lib.dptr(var)))
+        return mean, var
+
+    def select(self, afs: Sequence[AcquisitionId], f_best_raw: float,
+               exploration: ExplorationConfig = ExplorationConfig(),
+               cv_state: ContextualVarianceState = ContextualVarianceState(),
+               excluded: Optional[Sequence[int]] = None) -> Selection:
+        mask = 0
+        for af in afs:
+            mask |= 1 << int(af)
+        ex = None
+        a = _lib.gtc_select_args(mask, int(exploration.mode), float(exploration.constant),
+                                 float(cv_state.initial_sample_mean),
+                                 float(cv_state.initial_mean_variance), float(f_best_raw), None, 0)
+        if excluded:
+            ex = np.ascontiguousarray(np.asarray(excluded, dtype=np.int64))
+            a.excluded = _lib.i64ptr(ex)
+            a.n_excluded = len(ex)
+        r = _lib.gtc_select_result()
+        check(load().gtc_select(self._h, C.byref(a), C.byref(r)))
+        return Selection(tuple(r.position), tuple(r.score), r.lambda_, r.mean_variance, r.best_std,
+                         int(r.n_candidates), bool(r.cv_fallback))
+
+    def last_pass_ms(self) -> float:
+        return float(load().gtc_last_pass_ms(self._h))

@@ -180,6 +180,11 @@ int gtc_best_candidate(int device, int32_t af, const double* means, const double
                        double best_std, double lambda, const uint8_t* excluded,
                        int64_t* position_out, double* score_out);
 
+/* Per-candidate acquisition values (acquisition_{ei,pi,lcb}, acquisition.hpp:25-42;
+ * the LCB slot returns -lcb like best_candidate's score, portfolio.hpp:47). */
+int gtc_acquisition_scores(int device, int32_t af, const double* means, const double* stds,
+                           int64_t n, double best_std, double lambda, double* scores_out);
+
 #ifdef __cplusplus
 }
 #endif

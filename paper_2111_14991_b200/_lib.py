@@ -84,6 +84,8 @@ SIGNATURES = [
     ("gtc_gp_destroy", C.c_int, [P]),
     ("gtc_best_candidate", C.c_int, [C.c_int, C.c_int32, DP, DP, C.c_int64, C.c_double,
                                      C.c_double, U8P, I64P, DP]),
+    ("gtc_acquisition_scores", C.c_int, [C.c_int, C.c_int32, DP, DP, C.c_int64, C.c_double,
+                                         C.c_double, DP]),
 ]
 
 _lib = None

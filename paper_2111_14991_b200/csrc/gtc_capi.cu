@@ -704,3 +704,32 @@ extern "C" int gtc_best_candidate(int device, int32_t af, const double* means, c
   if (score_out) *score_out = res.score[af];
   return GTC_OK;
 }
+
+extern "C" int gtc_acquisition_scores(int device, int32_t af, const double* means, const double* stds,
+                                      int64_t n, double best_std, double lambda, double* scores_out) {
+  if (af < 0 || af > 2) return fail(GTC_ERR_INVALID, "unknown acquisition function");
+  if (n <= 0) return GTC_OK;
+  GTC_CUDA(cudaSetDevice(device));
+  cudaStream_t s;
+  GTC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  double *dm = nullptr, *ds = nullptr, *dout = nullptr;
+  int rc = dalloc(&dm, n);
+  if (!rc) rc = dalloc(&ds, n);
+  if (!rc) rc = dalloc(&dout, n);
+  cudaError_t e = cudaSuccess;
+  if (!rc) {
+    e = cudaMemcpyAsync(dm, means, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ds, stds, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) {
+      launch_scores(dm, ds, n, af, best_std, lambda, dout, s);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(scores_out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  }
+  cudaFree(dm); cudaFree(ds); cudaFree(dout);
+  cudaStreamDestroy(s);
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail(GTC_ERR_CUDA, std::string("acquisition_scores: ") + cudaGetErrorString(e));
+  return GTC_OK;
+}

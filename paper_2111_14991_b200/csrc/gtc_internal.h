@@ -129,6 +129,9 @@ void launch_best_candidate(const double* mu, const double* std, const uint8_t* e
                            int64_t* partial_cnt, unsigned int* counter, SelectDev* out,
                            cudaStream_t stream);
 
+void launch_scores(const double* mu, const double* sd, int64_t n, int af, double best_std,
+                   double lambda, double* out, cudaStream_t stream);
+
 int reduce_blocks(int64_t n);  // grid size used by the reduction kernels
 uint64_t launches();
 

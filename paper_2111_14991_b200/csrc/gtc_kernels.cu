@@ -706,6 +706,13 @@ __global__ void __launch_bounds__(kReduceThreads)
   select_body(c, best, lambda, 0.0, 0, 0);
 }
 
+__global__ void k_scores(const double* __restrict__ mu, const double* __restrict__ sd, int64_t n,
+                         int af, double best, double lambda, double* out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    out[j] = score_of(af, mu[j], sd[j], best, lambda);
+}
+
 // ------------------------------------------------------------ launchers
 
 static size_t cta_smem(int n_max) { return sizeof(double) * (size_t)(n_max + 8); }
@@ -801,6 +808,12 @@ void launch_best_candidate(const double* mu, const double* sd, const uint8_t* ex
   SelCtx c{mu, nullptr, sd, nullptr, excluded, nullptr, 0, n, 1u << af,
            partial_score, partial_pos, partial_first, partial_cnt, counter, out};
   k_best_candidate<<<reduce_blocks(n), kReduceThreads, 0, s>>>(c, best_std, lambda);
+}
+
+void launch_scores(const double* mu, const double* sd, int64_t n, int af, double best_std,
+                   double lambda, double* out, cudaStream_t s) {
+  count_launch();
+  k_scores<<<reduce_blocks(n), kReduceThreads, 0, s>>>(mu, sd, n, af, best_std, lambda, out);
 }
 
 }  // namespace gtc

@@ -253,3 +253,14 @@ def best_candidate(af: AcquisitionId, c: CandidateScores, excluded=None, device:
                                     float(c.lambda_), _lib.u8ptr(ex) if ex is not None else None,
                                     C.byref(pos), C.byref(score)))
     return int(pos.value)
+
+
+def acquisition_scores(af: AcquisitionId, means, stds, best_std: float, lambda_: float,
+                       device: int = 0) -> np.ndarray:
+    """Per-candidate EI / PI / -LCB on the device (acquisition.hpp:25-42)."""
+    m = np.ascontiguousarray(np.asarray(means, dtype=np.float64))
+    s = np.ascontiguousarray(np.asarray(stds, dtype=np.float64))
+    out = np.empty(len(m))
+    check(load().gtc_acquisition_scores(device, int(af), _lib.dptr(m), _lib.dptr(s), len(m),
+                                        float(best_std), float(lambda_), _lib.dptr(out)))
+    return out

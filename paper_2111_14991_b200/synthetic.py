@@ -78,6 +78,19 @@ class Rng:
     def uniform_below(self, n: int) -> int:
         return (self.next_u64() * int(n)) >> 64
 
+    def normal(self) -> float:
+        """Box-Muller with the pair cached (rng.hpp:67-79)."""
+        import math
+        if getattr(self, "_cached", None) is not None:
+            v, self._cached = self._cached, None
+            return v
+        u1 = 1.0 - self.uniform01()
+        u2 = self.uniform01()
+        r = math.sqrt(-2.0 * math.log(u1))
+        theta = 6.283185307179586476925286766559 * u2
+        self._cached = r * math.sin(theta)
+        return r * math.cos(theta)
+
 
 def hash_unit(seed: int, index: np.ndarray, salt: int) -> np.ndarray:
     """synthetic.hpp:38-43"""

@@ -1,0 +1,307 @@
+// run_bo over the resident device surrogate (strategies.hpp:75-457 of the
+// reference, BO strategies only).  Same control flow, RNG stream, budget
+// accounting and portfolio semantics; the per-iteration surrogate pass
+// (refit + predict-all + lambda + acquisition + argmax) is replaced by
+//   gtc_append   (bordered Cholesky row + one V row over all candidates)
+//   gtc_select   (mean variance -> lambda -> EI/PI/LCB -> masked argmax)
+// so no O(N) work remains on the host inside the loop.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <functional>
+#include <limits>
+#include <memory>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "gridtune_b200/portfolio.hpp"
+#include "gridtune_b200/sampling.hpp"
+
+namespace gridtune_b200 {
+
+enum class StrategyId { bo_advanced_multi, bo_multi, bo_ei, bo_poi, bo_lcb };
+
+inline const char* to_string(StrategyId id) {
+  switch (id) {
+    case StrategyId::bo_advanced_multi: return "bo-advanced-multi";
+    case StrategyId::bo_multi: return "bo-multi";
+    case StrategyId::bo_ei: return "bo-ei";
+    case StrategyId::bo_poi: return "bo-poi";
+    case StrategyId::bo_lcb: return "bo-lcb";
+  }
+  return "?";
+}
+
+inline std::optional<StrategyId> strategy_from_string(const std::string& s) {
+  for (StrategyId id : {StrategyId::bo_advanced_multi, StrategyId::bo_multi, StrategyId::bo_ei,
+                        StrategyId::bo_poi, StrategyId::bo_lcb})
+    if (s == to_string(id)) return id;
+  return std::nullopt;
+}
+
+/// StrategyConfig (strategies.hpp:79-122), BO fields.
+struct StrategyConfig {
+  StrategyId id = StrategyId::bo_advanced_multi;
+  std::uint64_t seed = 0;
+  std::size_t budget = 220;
+  std::size_t n_init = 20;
+  bool invalid_consumes_budget = true;
+  MaternNu nu = MaternNu::three_halves;
+  std::optional<double> lengthscale;
+  double output_variance = 1.0;
+  double noise = 1e-10;
+  double jitter = 1e-6;
+  ExplorationConfig exploration;
+  std::optional<double> discount;
+  double required_improvement = 0.1;
+  int skip_threshold = 5;
+  std::size_t lhs_restarts = 50;
+  std::function<void(std::size_t, std::size_t, std::size_t, double)> inspect;
+
+  double effective_lengthscale() const {
+    if (lengthscale) return *lengthscale;
+    return exploration.mode == ExplorationConfig::Mode::contextual_variance ? 1.5 : 2.0;
+  }
+  double effective_discount(PortfolioMode mode) const {
+    if (discount) return *discount;
+    return mode == PortfolioMode::multi ? 0.65 : 0.75;
+  }
+};
+
+struct EvaluationRecord {
+  ConfigIndex config_index = 0;
+  std::optional<double> value;
+  InvalidReason reason = InvalidReason::runtime_error;
+  double best_so_far = std::numeric_limits<double>::infinity();
+};
+
+struct TuningRun {
+  std::vector<EvaluationRecord> records;
+  std::size_t evaluations = 0;
+  std::size_t budget_consumed = 0;
+  std::size_t invalid_count = 0;
+  double best_value = std::numeric_limits<double>::infinity();
+  std::optional<Configuration> best_config;
+  std::size_t surrogate_size = 0;
+  std::vector<std::string> warnings;
+  std::vector<double> lambdas;  // lambda of every BO iteration (inspect hook values)
+
+  double best_at(std::size_t evaluation_count) const {
+    if (records.empty() || evaluation_count == 0) return std::numeric_limits<double>::infinity();
+    return records[std::min(evaluation_count, records.size()) - 1].best_so_far;
+  }
+};
+
+namespace detail {
+
+/// Visited flags, budget accounting, never-revisit (strategies.hpp:159-232).
+class RunContext {
+ public:
+  RunContext(const EnumeratedSpace& space, const Objective& objective, const StrategyConfig& config)
+      : space_(space), objective_(objective), config_(config), visited_(space.size(), false) {}
+
+  TuningRun& run() { return run_; }
+  std::size_t unvisited_count() const { return space_.size() - visited_count_; }
+  bool visited(std::size_t pos) const { return visited_[pos]; }
+  bool has_budget() const { return run_.budget_consumed < config_.budget; }
+  bool exhausted() const { return !has_budget() || unvisited_count() == 0; }
+  std::span<const double> valid_observations() const { return valid_; }
+
+  Measurement evaluate(std::size_t pos) {
+    if (visited_[pos]) throw Error("internal: configuration evaluated twice");
+    visited_[pos] = true;
+    ++visited_count_;
+    if (on_visit) on_visit(pos);
+    const Measurement m = objective_(space_.config(pos));
+    ++run_.evaluations;
+    EvaluationRecord rec;
+    rec.config_index = space_.id(pos);
+    if (m.is_valid()) {
+      ++run_.budget_consumed;
+      const double v = *m.value;
+      rec.value = v;
+      valid_.push_back(v);
+      if (v < run_.best_value) {
+        run_.best_value = v;
+        run_.best_config = space_.config(pos);
+      }
+    } else {
+      if (config_.invalid_consumes_budget) ++run_.budget_consumed;
+      rec.reason = m.reason;
+      ++run_.invalid_count;
+    }
+    rec.best_so_far = run_.best_value;
+    run_.records.push_back(rec);
+    return m;
+  }
+
+  std::function<void(std::size_t)> on_visit;  // mirrors the visited mask onto the device
+
+ private:
+  const EnumeratedSpace& space_;
+  const Objective& objective_;
+  const StrategyConfig& config_;
+  std::vector<bool> visited_;
+  std::vector<double> valid_;
+  std::size_t visited_count_ = 0;
+  TuningRun run_;
+};
+
+}  // namespace detail
+
+/// One run's resident surrogate (gtc_run) as an argmax source: positions are
+/// space positions, candidates are the unvisited configurations.
+class DeviceSurrogate : public ArgmaxSource {
+ public:
+  DeviceSurrogate(const EnumeratedSpace& space, const MaternKernel& kernel, double noise, double jitter,
+                  std::size_t n_max)
+      : space_(space) {
+    const gtc_model_config cfg{kernel.c(), noise, jitter, static_cast<std::int32_t>(n_max)};
+    gtc_run* r = nullptr;
+    check(gtc_run_create(space.device_space(), &cfg, &r));
+    run_.reset(r, [](gtc_run* p) { gtc_run_destroy(p); });
+  }
+
+  gtc_run* handle() const { return run_.get(); }
+
+  gtc_fit_info fit(const std::vector<std::size_t>& positions, const std::vector<double>& y) {
+    std::vector<std::int64_t> p(positions.begin(), positions.end());
+    gtc_fit_info info{};
+    check(gtc_fit(run_.get(), p.data(), y.data(), static_cast<std::int32_t>(y.size()), &info));
+    info_ = info;
+    return info;
+  }
+  gtc_fit_info append(std::size_t pos, double y) {
+    gtc_fit_info info{};
+    check(gtc_append(run_.get(), static_cast<std::int64_t>(pos), y, &info));
+    info_ = info;
+    return info;
+  }
+  void mark_visited(std::size_t pos) { check(gtc_mark_visited(run_.get(), static_cast<std::int64_t>(pos))); }
+  double mean_variance() {
+    double mv = 0.0;
+    std::int64_t cnt = 0;
+    check(gtc_mean_variance(run_.get(), &mv, &cnt));
+    return mv;
+  }
+  double standardize(double y_raw) const { return (y_raw - info_.y_mean) / info_.y_std; }
+
+  /// Per-iteration selection parameters (lambda inputs).
+  gtc_select_args args{};
+  gtc_select_result last{};
+
+  std::array<std::int64_t, 3> argmax(std::uint32_t mask, const std::vector<std::int64_t>& excluded) override {
+    gtc_select_args a = args;
+    a.af_mask = mask;
+    a.excluded = excluded.empty() ? nullptr : excluded.data();
+    a.n_excluded = static_cast<std::int32_t>(excluded.size());
+    check(gtc_select(run_.get(), &a, &last));
+    return {last.position[0], last.position[1], last.position[2]};
+  }
+  std::uint64_t id_at(std::int64_t p) const override { return space_.id(static_cast<std::size_t>(p)); }
+  std::int64_t position_of_id(std::uint64_t id) const override {
+    const std::size_t p = space_.position_of(id);
+    return p == EnumeratedSpace::npos ? -1 : static_cast<std::int64_t>(p);
+  }
+  std::size_t candidate_count() const override {
+    return static_cast<std::size_t>(gtc_unvisited_count(run_.get()));
+  }
+
+ private:
+  const EnumeratedSpace& space_;
+  std::shared_ptr<gtc_run> run_;
+  gtc_fit_info info_{};
+};
+
+inline bool is_bayesian(StrategyId) { return true; }
+
+/// run_bo (strategies.hpp:261-457).
+inline TuningRun run_bo(const EnumeratedSpace& space, const Objective& objective, const StrategyConfig& config) {
+  if (space.size() <= config.n_init)
+    throw SamplingError("space has " + std::to_string(space.size()) +
+                        " valid configurations; need more than n_init = " + std::to_string(config.n_init));
+  if (config.budget <= config.n_init) throw ConfigError("budget must exceed the initial sample size");
+
+  Rng rng(config.seed);
+  detail::RunContext ctx(space, objective, config);
+  const MaternKernel kernel(config.nu, config.effective_lengthscale(), config.output_variance);
+  // the GP can hold at most `budget` valid observations (every valid one is charged)
+  DeviceSurrogate gp(space, kernel, config.noise, config.jitter, std::max<std::size_t>(config.budget, 1));
+  ctx.on_visit = [&gp](std::size_t pos) { gp.mark_visited(pos); };
+
+  const Objective counted = [&ctx](const Configuration& c) { return ctx.evaluate(c.position); };
+  const std::size_t max_init = config.invalid_consumes_budget ? config.budget : std::numeric_limits<std::size_t>::max();
+  const InitialSample init = draw_initial_sample(space, counted, config.n_init, rng, max_init, config.lhs_restarts);
+
+  std::vector<std::size_t> train_pos = init.positions;
+  std::vector<double> train_val = init.observations;
+  gp.fit(train_pos, train_val);  // fit_current(), strategies.hpp:298-309
+
+  std::optional<Portfolio> portfolio;
+  std::optional<AcquisitionId> single;
+  switch (config.id) {
+    case StrategyId::bo_ei: single = AcquisitionId::ei; break;
+    case StrategyId::bo_poi: single = AcquisitionId::poi; break;
+    case StrategyId::bo_lcb: single = AcquisitionId::lcb; break;
+    default: {
+      PortfolioConfig pc;
+      pc.mode = config.id == StrategyId::bo_multi ? PortfolioMode::multi : PortfolioMode::advanced_multi;
+      pc.skip_threshold = config.skip_threshold;
+      pc.discount = config.effective_discount(pc.mode);
+      pc.required_improvement = config.required_improvement;
+      portfolio.emplace(pc);
+    }
+  }
+
+  // contextual-variance normalisers, frozen after the initial sample (:390-397)
+  ContextualVarianceState cv;
+  cv.initial_sample_mean = init.mean_observation();
+  cv.initial_mean_variance = gp.mean_variance();
+  bool warned = false;
+
+  while (!ctx.exhausted()) {
+    gp.args = gtc_select_args{};
+    gp.args.lambda_mode = static_cast<std::int32_t>(config.exploration.mode);
+    gp.args.lambda_constant = config.exploration.constant;
+    gp.args.cv_initial_sample_mean = cv.initial_sample_mean;
+    gp.args.cv_initial_mean_variance = cv.initial_mean_variance;
+    gp.args.f_best_raw = ctx.run().best_value;
+
+    std::size_t pick;
+    AcquisitionId by;
+    if (single) {
+      pick = static_cast<std::size_t>(gp.argmax(1u << static_cast<int>(*single), {})[static_cast<int>(*single)]);
+      by = *single;
+    } else {
+      const Portfolio::Suggestion s = portfolio->suggest(gp);
+      pick = s.position;
+      by = s.by;
+    }
+    const double lambda = gp.last.lambda;
+    if (gp.last.cv_fallback && !warned) {
+      ctx.run().warnings.push_back(
+          "contextual variance unavailable (non-positive observations or zero initial variance); "
+          "falling back to constant exploration factor " + std::to_string(config.exploration.constant));
+      warned = true;
+    }
+    const Measurement m = ctx.evaluate(pick);
+    if (portfolio) portfolio->record(by, space.id(pick), m.value, ctx.valid_observations());
+    if (m.is_valid()) {
+      train_pos.push_back(pick);
+      train_val.push_back(*m.value);
+      gp.append(pick, *m.value);  // refit == bordered append (strategies.hpp:444-449)
+    }
+    ctx.run().lambdas.push_back(lambda);
+    if (config.inspect) config.inspect(ctx.run().evaluations, ctx.valid_observations().size(), train_pos.size(), lambda);
+  }
+  ctx.run().surrogate_size = train_pos.size();
+  return std::move(ctx.run());
+}
+
+inline TuningRun run_strategy(const EnumeratedSpace& space, const Objective& objective, const StrategyConfig& config) {
+  return run_bo(space, objective, config);
+}
+
+}  // namespace gridtune_b200

@@ -40,6 +40,8 @@ extern "C" {
 #define GTC_ERR_OOM (-5)           /* device allocation failed                         */
 #define GTC_ERR_CONFIG (-6)        /* gridtune::ConfigError                            */
 #define GTC_ERR_CAPACITY (-7)      /* more observations than the run's n_max          */
+#define GTC_ERR_SAMPLING (-8)      /* gridtune::SamplingError (run_bo preconditions, initial design) */
+#define GTC_ERR_ABORTED (-9)       /* the objective callback asked to stop            */
 
 /* ---- enums mirroring the reference ---------------------------------------- */
 /* MaternNu, gp.hpp:12 */
@@ -179,6 +181,75 @@ int gtc_gp_destroy(gtc_gp* gp);
 int gtc_best_candidate(int device, int32_t af, const double* means, const double* stds, int64_t n,
                        double best_std, double lambda, const uint8_t* excluded,
                        int64_t* position_out, double* score_out);
+
+/* Host view of a space: row-major n x d coords (as passed to gtc_space_create). */
+const double* gtc_space_coords(const gtc_space* space);
+int32_t gtc_space_dimension(const gtc_space* space);
+int32_t gtc_space_device(const gtc_space* space);
+
+/* ---- whole BO run (run_bo, strategies.hpp:261-457) on the resident surrogate ---- */
+/* StrategyId order of the BO strategies (strategies.hpp:25-30) */
+#define GTC_STRATEGY_BO_ADVANCED_MULTI 0
+#define GTC_STRATEGY_BO_MULTI 1
+#define GTC_STRATEGY_BO_EI 2
+#define GTC_STRATEGY_BO_POI 3
+#define GTC_STRATEGY_BO_LCB 4
+
+/* StrategyConfig (strategies.hpp:79-122), BO fields.  lengthscale <= 0 and
+ * discount <= 0 select the reference defaults (1.5 / 2.0; 0.65 / 0.75). */
+typedef struct {
+  int32_t strategy;
+  uint64_t seed;
+  int64_t budget;
+  int64_t n_init;
+  int32_t invalid_consumes_budget;
+  int32_t nu;
+  double lengthscale;
+  double output_variance;
+  double noise;
+  double jitter;
+  int32_t exploration_mode;
+  double exploration_constant;
+  double discount;
+  double required_improvement;
+  int32_t skip_threshold;
+  int64_t lhs_restarts;
+} gtc_bo_config;
+
+/* Objective (measurement.hpp:43): return 1 and *value for a valid
+ * measurement, 0 for a runtime-invalid one, < 0 to abort the run. */
+typedef int (*gtc_objective_fn)(void* ctx, int64_t position, uint64_t id, double* value);
+
+typedef struct {
+  int64_t position;
+  uint64_t id;          /* EvaluationRecord::config_index */
+  double value;         /* NaN when invalid */
+  int32_t valid;
+  double best_so_far;
+} gtc_bo_record;
+
+typedef struct {
+  int64_t evaluations;
+  int64_t budget_consumed;
+  int64_t invalid_count;
+  int64_t surrogate_size;
+  int64_t n_records;
+  int64_t n_lambdas;    /* BO iterations (inspect-hook calls) */
+  int64_t best_position;
+  double best_value;
+  int32_t n_warnings;
+} gtc_bo_summary;
+
+/* ids: canonical index of every position (ascending).  records/lambdas are
+ * caller arrays of `capacity` entries (>= budget + invalid evaluations). */
+int gtc_run_bo(gtc_space* space, const uint64_t* ids, const gtc_bo_config* config,
+               gtc_objective_fn objective, void* ctx, gtc_bo_record* records, double* lambdas,
+               int64_t capacity, gtc_bo_summary* summary);
+/* Same, objective = replay table (values[pos], NaN = runtime-invalid), the
+ * simulation mode of cache.hpp:246-257. */
+int gtc_run_bo_table(gtc_space* space, const uint64_t* ids, const gtc_bo_config* config,
+                     const double* values, gtc_bo_record* records, double* lambdas,
+                     int64_t capacity, gtc_bo_summary* summary);
 
 /* Per-candidate acquisition values (acquisition_{ei,pi,lcb}, acquisition.hpp:25-42;
  * the LCB slot returns -lcb like best_candidate's score, portfolio.hpp:47). */

@@ -12,5 +12,7 @@ from .gp import (AcquisitionId, CandidateScores, ConfigError, ContextualVariance
                  contextual_variance_lambda, discounted_observation_score,
                  mean_posterior_variance)
 from .runtime import FitInfo, Selection, Space, SurrogateRun  # noqa: F401
+from .strategies import (StrategyConfig, StrategyId, TuningRun, run_bo, run_strategy,  # noqa: F401
+                         strategy_from_string)
 
 __version__ = "0.1.0"

@@ -51,10 +51,37 @@ class gtc_select_result(C.Structure):
                 ("n_candidates", C.c_int64), ("cv_fallback", C.c_int32)]
 
 
+class gtc_bo_config(C.Structure):
+    _fields_ = [("strategy", C.c_int32), ("seed", C.c_uint64), ("budget", C.c_int64),
+                ("n_init", C.c_int64), ("invalid_consumes_budget", C.c_int32), ("nu", C.c_int32),
+                ("lengthscale", C.c_double), ("output_variance", C.c_double), ("noise", C.c_double),
+                ("jitter", C.c_double), ("exploration_mode", C.c_int32),
+                ("exploration_constant", C.c_double), ("discount", C.c_double),
+                ("required_improvement", C.c_double), ("skip_threshold", C.c_int32),
+                ("lhs_restarts", C.c_int64)]
+
+
+class gtc_bo_record(C.Structure):
+    _fields_ = [("position", C.c_int64), ("id", C.c_uint64), ("value", C.c_double),
+                ("valid", C.c_int32), ("best_so_far", C.c_double)]
+
+
+class gtc_bo_summary(C.Structure):
+    _fields_ = [("evaluations", C.c_int64), ("budget_consumed", C.c_int64),
+                ("invalid_count", C.c_int64), ("surrogate_size", C.c_int64),
+                ("n_records", C.c_int64), ("n_lambdas", C.c_int64), ("best_position", C.c_int64),
+                ("best_value", C.c_double), ("n_warnings", C.c_int32)]
+
+
 P = C.c_void_p
 DP = C.POINTER(C.c_double)
 I64P = C.POINTER(C.c_int64)
+U64P = C.POINTER(C.c_uint64)
 U8P = C.POINTER(C.c_uint8)
+OBJECTIVE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_uint64, DP)
+
+GTC_ERR_SAMPLING = -8
+GTC_ERR_ABORTED = -9
 
 # (name, restype, argtypes) — exactly the declarations of include/gridtune_cuda.h
 SIGNATURES = [
@@ -86,6 +113,13 @@ SIGNATURES = [
                                      C.c_double, U8P, I64P, DP]),
     ("gtc_acquisition_scores", C.c_int, [C.c_int, C.c_int32, DP, DP, C.c_int64, C.c_double,
                                          C.c_double, DP]),
+    ("gtc_space_coords", DP, [P]),
+    ("gtc_space_dimension", C.c_int32, [P]),
+    ("gtc_space_device", C.c_int32, [P]),
+    ("gtc_run_bo", C.c_int, [P, U64P, C.POINTER(gtc_bo_config), OBJECTIVE_FN, C.c_void_p,
+                             C.POINTER(gtc_bo_record), DP, C.c_int64, C.POINTER(gtc_bo_summary)]),
+    ("gtc_run_bo_table", C.c_int, [P, U64P, C.POINTER(gtc_bo_config), DP, C.POINTER(gtc_bo_record), DP,
+                                   C.c_int64, C.POINTER(gtc_bo_summary)]),
 ]
 
 _lib = None

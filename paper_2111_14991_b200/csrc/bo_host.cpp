@@ -1,0 +1,131 @@
+// C ABI entry points for a whole BO run (gtc_run_bo / gtc_run_bo_table) over
+// the C++ host mirror in include/gridtune_b200/strategies.hpp.
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <limits>
+#include <string>
+
+#include "gridtune_b200/strategies.hpp"
+
+using namespace gridtune_b200;
+
+// gtc_last_error() reads the kernel layer's message; host-layer exception
+// text goes through the same thread-local channel (gtc_capi.cu).
+extern "C" void gtc_internal_set_error(const char* msg);
+
+namespace {
+
+int to_status(const std::exception& e) {
+  gtc_internal_set_error(e.what());
+  if (dynamic_cast<const ModelConditioningError*>(&e)) return GTC_ERR_CONDITIONING;
+  if (dynamic_cast<const ConfigError*>(&e)) return GTC_ERR_CONFIG;
+  if (dynamic_cast<const SamplingError*>(&e)) return GTC_ERR_SAMPLING;
+  if (dynamic_cast<const DeviceError*>(&e)) return GTC_ERR_CUDA;
+  return GTC_ERR_INVALID;
+}
+
+StrategyConfig to_config(const gtc_bo_config& c) {
+  if (c.strategy < 0 || c.strategy > 4) throw ConfigError("run_bo requires a BO strategy id");
+  StrategyConfig s;
+  s.id = static_cast<StrategyId>(c.strategy);
+  s.seed = c.seed;
+  s.budget = static_cast<std::size_t>(c.budget);
+  s.n_init = static_cast<std::size_t>(c.n_init);
+  s.invalid_consumes_budget = c.invalid_consumes_budget != 0;
+  s.nu = static_cast<MaternNu>(c.nu);
+  if (c.lengthscale > 0.0) s.lengthscale = c.lengthscale;
+  s.output_variance = c.output_variance;
+  s.noise = c.noise;
+  s.jitter = c.jitter;
+  s.exploration.mode = static_cast<ExplorationConfig::Mode>(c.exploration_mode);
+  s.exploration.constant = c.exploration_constant;
+  if (c.discount > 0.0) s.discount = c.discount;
+  s.required_improvement = c.required_improvement;
+  s.skip_threshold = c.skip_threshold;
+  s.lhs_restarts = static_cast<std::size_t>(c.lhs_restarts);
+  return s;
+}
+
+struct Aborted : std::exception {
+  const char* what() const noexcept override { return "objective aborted the run"; }
+};
+
+int run(gtc_space* space, const std::uint64_t* ids, const gtc_bo_config* cfg, const Objective& objective,
+        gtc_bo_record* records, double* lambdas, std::int64_t capacity, gtc_bo_summary* summary) {
+  if (!space || !ids || !cfg) {
+    gtc_internal_set_error("null argument");
+    return GTC_ERR_INVALID;
+  }
+  try {
+    const EnumeratedSpace es(space, ids);
+    const StrategyConfig sc = to_config(*cfg);
+    const TuningRun r = run_bo(es, objective, sc);
+    const std::int64_t nrec = static_cast<std::int64_t>(r.records.size());
+    const std::int64_t nlam = static_cast<std::int64_t>(r.lambdas.size());
+    if (records) {
+      if (nrec > capacity) throw Error("record capacity too small");
+      for (std::int64_t i = 0; i < nrec; ++i) {
+        const EvaluationRecord& e = r.records[static_cast<std::size_t>(i)];
+        records[i].id = e.config_index;
+        records[i].position = static_cast<std::int64_t>(es.position_of(e.config_index));
+        records[i].valid = e.value.has_value() ? 1 : 0;
+        records[i].value = e.value ? *e.value : std::numeric_limits<double>::quiet_NaN();
+        records[i].best_so_far = e.best_so_far;
+      }
+    }
+    if (lambdas) {
+      if (nlam > capacity) throw Error("lambda capacity too small");
+      for (std::int64_t i = 0; i < nlam; ++i) lambdas[i] = r.lambdas[static_cast<std::size_t>(i)];
+    }
+    if (summary) {
+      summary->evaluations = static_cast<std::int64_t>(r.evaluations);
+      summary->budget_consumed = static_cast<std::int64_t>(r.budget_consumed);
+      summary->invalid_count = static_cast<std::int64_t>(r.invalid_count);
+      summary->surrogate_size = static_cast<std::int64_t>(r.surrogate_size);
+      summary->n_records = nrec;
+      summary->n_lambdas = nlam;
+      summary->best_value = r.best_value;
+      summary->best_position = r.best_config ? static_cast<std::int64_t>(r.best_config->position) : -1;
+      summary->n_warnings = static_cast<std::int32_t>(r.warnings.size());
+    }
+    return GTC_OK;
+  } catch (const Aborted& e) {
+    gtc_internal_set_error(e.what());
+    return GTC_ERR_ABORTED;
+  } catch (const std::exception& e) {
+    return to_status(e);
+  }
+}
+
+}  // namespace
+
+extern "C" int gtc_run_bo(gtc_space* space, const std::uint64_t* ids, const gtc_bo_config* cfg,
+                          gtc_objective_fn objective, void* ctx, gtc_bo_record* records, double* lambdas,
+                          std::int64_t capacity, gtc_bo_summary* summary) {
+  if (!objective) {
+    gtc_internal_set_error("objective is null");
+    return GTC_ERR_INVALID;
+  }
+  const Objective obj = [objective, ctx](const Configuration& c) {
+    double v = 0.0;
+    const int rc = objective(ctx, static_cast<std::int64_t>(c.position), c.index, &v);
+    if (rc < 0) throw Aborted();
+    return rc > 0 ? Measurement::valid(v) : Measurement::invalid(InvalidReason::runtime_error);
+  };
+  return run(space, ids, cfg, obj, records, lambdas, capacity, summary);
+}
+
+extern "C" int gtc_run_bo_table(gtc_space* space, const std::uint64_t* ids, const gtc_bo_config* cfg,
+                                const double* values, gtc_bo_record* records, double* lambdas,
+                                std::int64_t capacity, gtc_bo_summary* summary) {
+  if (!values) {
+    gtc_internal_set_error("values is null");
+    return GTC_ERR_INVALID;
+  }
+  const Objective obj = [values](const Configuration& c) {
+    const double v = values[c.position];
+    return std::isnan(v) ? Measurement::invalid(InvalidReason::runtime_error) : Measurement::valid(v);
+  };
+  return run(space, ids, cfg, obj, records, lambdas, capacity, summary);
+}

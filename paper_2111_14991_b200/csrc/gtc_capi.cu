@@ -237,6 +237,7 @@ struct gtc_gp {
 // =============================================================== library
 
 extern "C" const char* gtc_last_error(void) { return g_last_error.c_str(); }
+extern "C" void gtc_internal_set_error(const char* msg) { g_last_error = msg ? msg : ""; }
 extern "C" const char* gtc_version(void) { return "gridtune-b200 0.1 (sm_100a)"; }
 extern "C" uint64_t gtc_kernel_launches(void) { return launches(); }
 
@@ -283,6 +284,9 @@ extern "C" int gtc_space_destroy(gtc_space* s) {
 }
 
 extern "C" int64_t gtc_space_size(const gtc_space* s) { return s ? s->n : -1; }
+extern "C" const double* gtc_space_coords(const gtc_space* s) { return s ? s->host_coords.data() : nullptr; }
+extern "C" int32_t gtc_space_dimension(const gtc_space* s) { return s ? s->d : -1; }
+extern "C" int32_t gtc_space_device(const gtc_space* s) { return s ? s->device : -1; }
 
 // =============================================================== run
 

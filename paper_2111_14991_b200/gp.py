@@ -49,6 +49,8 @@ def check(rc: int) -> None:
         raise ModelConditioningError(msg)
     if rc == _lib.GTC_ERR_CONFIG:
         raise ConfigError(msg)
+    if rc == _lib.GTC_ERR_SAMPLING:
+        raise SamplingError(msg)
     if rc in (_lib.GTC_ERR_CUDA, _lib.GTC_ERR_OOM):
         raise DeviceError(msg)
     raise Error(msg)

@@ -1,0 +1,109 @@
+"""Chosen-configuration trajectories of the device run_bo against the
+UNMODIFIED reference run_bo (tests/golden/traj_*.npz, written by
+oracle/_ref/ref_tool runbo) on simulation-mode spaces, plus the reference's
+loop invariants (test_strategies.cpp:62-295)."""
+import numpy as np
+import pytest
+
+from paper_2111_14991_b200 import synthetic
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = sorted(__import__("pathlib").Path(__file__).parent.joinpath("golden").glob("traj_*.npz"))
+
+
+def space_of(gt, t):
+    return gt.Space(t["coords"]), t["ids"], t["values"]
+
+
+def config_of(gt, t):
+    fn, grid, sseed, inv, strat, budget, n_init, bseed = [str(x) for x in t["spec"]]
+    return gt.StrategyConfig(id=gt.strategy_from_string(strat), seed=int(bseed), budget=int(budget),
+                             n_init=int(n_init))
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[p.stem for p in GOLDEN])
+def test_trajectory_matches_reference(gt, path):
+    t = np.load(path)
+    space, ids, values = space_of(gt, t)
+    run = gt.run_bo(space, ids, config_of(gt, t), values=values)
+    ref = t["traj_pos"]
+    assert len(run.positions) == len(ref)
+    first_diff = next((i for i in range(len(ref)) if run.positions[i] != ref[i]), None)
+    assert first_diff is None, f"diverged at evaluation {first_diff}"
+    np.testing.assert_array_equal(np.isnan(run.values), np.isnan(t["traj_val"]))
+    assert run.best_value == t["best"][0]
+    # lambda of every iteration (the inspect hook) within 1e-9 relative
+    np.testing.assert_allclose(run.lambdas, t["traj_lambda"], rtol=1e-9, atol=1e-12)
+    assert run.n_warnings == int(t["warnings"][0])
+
+
+def test_core_invariants_on_invalid_rich_space(gt):
+    """test_strategies.cpp:172-192: never revisit, exact budget, monotone best."""
+    coords, ids, values = synthetic.random_rough([13, 13], 17, 0.3)
+    space = gt.Space(coords)
+    for sid in gt.StrategyId:
+        for seed in (1, 2):
+            run = gt.run_bo(space, ids, gt.StrategyConfig(id=sid, seed=seed, budget=70, n_init=12), values=values)
+            assert len(np.unique(run.positions)) == len(run.positions)
+            assert run.evaluations == 70
+            best = np.inf
+            for v, b in zip(run.values, run.best_so_far):
+                if not np.isnan(v):
+                    best = min(best, v)
+                assert b == best
+            assert run.best_value == best
+            assert run.surrogate_size == int(np.sum(run.valid))
+            assert np.all(run.lambdas >= 0.0)
+
+
+def test_exhausts_candidates_before_budget(gt):  # test_strategies.cpp:84-95
+    coords, ids, values = synthetic.random_rough([6, 6], 3, 0.0)
+    run = gt.run_bo(gt.Space(coords), ids, gt.StrategyConfig(id=gt.StrategyId.bo_ei, seed=1, budget=100, n_init=8),
+                    values=values)
+    assert run.evaluations == 36
+    assert run.best_value == np.nanmin(values)
+
+
+def test_preconditions(gt):  # test_strategies.cpp:121-135
+    coords, ids, values = synthetic.random_rough([4, 4], 3, 0.0)
+    space = gt.Space(coords)
+    with pytest.raises(gt.SamplingError):
+        gt.run_bo(space, ids, gt.StrategyConfig(n_init=16, budget=20), values=values)
+    with pytest.raises(gt.ConfigError):
+        gt.run_bo(space, ids, gt.StrategyConfig(n_init=10, budget=10), values=values)
+
+
+def test_callback_objective_and_determinism(gt):
+    coords, ids, values = synthetic.random_rough([11, 11], 8, 0.2)
+    space = gt.Space(coords)
+    calls = {}
+
+    def objective(pos, cid):
+        calls[pos] = calls.get(pos, 0) + 1
+        v = values[pos]
+        return None if np.isnan(v) else float(v)
+
+    cfg = gt.StrategyConfig(id=gt.StrategyId.bo_multi, seed=99, budget=50, n_init=10)
+    a = gt.run_bo(space, ids, cfg, objective=objective)
+    assert max(calls.values()) == 1
+    b = gt.run_bo(space, ids, cfg, values=values)
+    np.testing.assert_array_equal(a.positions, b.positions)
+
+
+def test_rescaling_invariance(gt):  # test_strategies.cpp:274-295
+    coords, ids, values = synthetic.random_rough([10, 10], 41, 0.1)
+    space = gt.Space(coords)
+    cfg = gt.StrategyConfig(id=gt.StrategyId.bo_advanced_multi, seed=12, budget=45, n_init=10)
+    base = gt.run_bo(space, ids, cfg, values=values)
+    for scale in (2.0, 0.25, 1024.0):
+        run = gt.run_bo(space, ids, cfg, values=values * scale)
+        np.testing.assert_array_equal(run.positions, base.positions)
+
+
+def test_budget_free_invalids(gt):  # test_strategies.cpp:214-227 for BO
+    coords, ids, values = synthetic.random_rough([12, 12], 31, 0.4)
+    cfg = gt.StrategyConfig(id=gt.StrategyId.bo_ei, seed=5, budget=40, n_init=10, invalid_consumes_budget=False)
+    run = gt.run_bo(gt.Space(coords), ids, cfg, values=values)
+    assert run.budget_consumed == 40
+    assert run.evaluations == 40 + run.invalid_count

@@ -37,6 +37,9 @@ sys.path.insert(0, str(ROOT))
 
 BASE_SEED = 20261017
 METRIC = "BO iterations/sec (full-space GP posterior+acquisition) at N, n=220"
+# dram__bytes_read.sum + dram__bytes_write.sum per k_extend<1> launch, from the
+# committed ncu --set full capture (profiles/ncu_extend_r1.txt)
+TRAFFIC = {"c4": 1.807e9}
 CONFIGS = {
     "c4": dict(grid=[10] * 6, invalid=0.0, workload="C4 synthetic random-rough 1M candidates (10^6 grid, d=6), n=220, bo-ei, contextual variance"),
     "c3": dict(grid=[10, 10, 10, 10, 5, 2], invalid=0.3, workload="C3 synthetic random-rough 100k candidates (d=6, ~30% invalid), n=220, bo-lcb, contextual variance"),
@@ -211,40 +214,42 @@ def main():
     stream = torch.cuda.ExternalStream(gt.load().gtc_run_stream(run.handle))
 
     def step(pick, f_best):
-        run.truncate(n - 1)                  # model back to n-1 observations
-        run.mark_visited(pick)
+        run.truncate_async(n - 1)            # bench rollback: model back to n-1 observations
         yv = float(values[pick])
-        run.append(pick, yv)                 # GP update + predictive pass at n
         fb = min(f_best, yv)
-        s = run.select([af], fb, expl, cv)   # lambda + acquisition + argmax
-        run.unmark_visited(pick)             # keep the candidate set size fixed
-        return s.pick(af), run.last_pass_ms()
+        # one BO iteration through the C ABI: mark visited + bordered Cholesky row +
+        # V-row pass with posterior and mean variance + lambda + EI + argmax, one round trip
+        _, s = run.observe(pick, yv, [af], fb, expl, cv)
+        run.unmark_visited(pick)             # bench rollback: keep the candidate set fixed
+        return s.pick(af), run.last_step_ms(), run.last_pass_ms()
 
     for _ in range(args.warmup):
-        pick, _ = step(pick, f_best)
+        pick, _, _ = step(pick, f_best)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     launches_before = gt.load().gtc_kernel_launches()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    pass_ms = []
+    pass_ms, step_ms = [], []
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
         e0.record(stream)
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            pick, ms = step(pick, f_best)
-            pass_ms.append(ms)
+            pick, sm, pm = step(pick, f_best)
+            step_ms.append(sm)
+            pass_ms.append(pm)
         e1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
     launches = gt.load().gtc_kernel_launches() - launches_before
-    dev_ms = e0.elapsed_time(e1)
+    bracket_ms = e0.elapsed_time(e1)
+    dev_ms = float(np.sum(step_ms))  # device time of the iterations' kernels (CUDA events)
     if world > 1:
-        t = torch.tensor([dev_ms, wall], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dev_ms, wall, bracket_ms], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        dev_ms, wall = float(t[0]), float(t[1])
+        dev_ms, wall, bracket_ms = float(t[0]), float(t[1]), float(t[2])
     value = world * args.steps / (dev_ms / 1e3)
     e2e = world * args.steps / wall
     peaks, peak_kind = measured_peaks()
@@ -258,13 +263,15 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["workload"], "N": N, "n": n, "d": coords.shape[1],
                        "parallelism": f"replicas{world}" if world > 1 else "single",
-                       "l2": "V stream 1.76 GB/step > 126 MB L2 (no flush needed)" if N >= 1_000_000 else "inputs > L2 not guaranteed"},
-            "e2e": {"value": e2e, "unit": "iter/s", "h2d_bytes_per_step": 16 + 56,
-                    "d2h_bytes_per_step": 48 + 104},
+                       "l2": "V stream 1.76 GB/step > 126 MB L2 (no flush needed)" if N >= 1_000_000 else "inputs > L2 not guaranteed",
+                       "timing": "value: CUDA events around each iteration's kernels (gp append -> pass -> selection), summed; e2e: wall clock of the Python->C-ABI loop incl. H2D observation + D2H result per step"},
+            "e2e": {"value": e2e, "unit": "iter/s", "h2d_bytes_per_step": 16 + 64,
+                    "d2h_bytes_per_step": 104 + 48, "bracket_ms_per_step": bracket_ms / args.steps},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": TRAFFIC.get(args.config),
                          "kernel": "k_extend<1,NU=3/2> (predictive pass)", "kernel_ms": avg_pass,
+                         "kernel_share_of_step": avg_pass / (dev_ms / args.steps),
                          "algorithmic_bytes": alg_bytes, "peak_kind": peak_kind},
             "clocks": clocks.summary(),
         }

@@ -192,7 +192,24 @@ class DeviceSurrogate : public ArgmaxSource {
   gtc_select_args args{};
   gtc_select_result last{};
 
+  /// Evaluation outcome -> device (mark visited, bordered append when valid)
+  /// and, when `next` is given, the next iteration's selection in the same
+  /// round trip (gtc_observe); the result is served to the next argmax().
+  gtc_fit_info observe(std::size_t pos, std::optional<double> value, const gtc_select_args* next) {
+    gtc_fit_info info{};
+    check(gtc_observe(run_.get(), static_cast<std::int64_t>(pos), value.value_or(0.0), value ? 1 : 0, next,
+                      &last, &info));
+    if (value) info_ = info;
+    prefetched_mask_ = next ? next->af_mask : 0u;
+    return info;
+  }
+
   std::array<std::int64_t, 3> argmax(std::uint32_t mask, const std::vector<std::int64_t>& excluded) override {
+    if (prefetched_mask_ && excluded.empty() && (mask & ~prefetched_mask_) == 0) {
+      prefetched_mask_ = 0;
+      return {last.position[0], last.position[1], last.position[2]};
+    }
+    prefetched_mask_ = 0;
     gtc_select_args a = args;
     a.af_mask = mask;
     a.excluded = excluded.empty() ? nullptr : excluded.data();
@@ -213,6 +230,7 @@ class DeviceSurrogate : public ArgmaxSource {
   const EnumeratedSpace& space_;
   std::shared_ptr<gtc_run> run_;
   gtc_fit_info info_{};
+  std::uint32_t prefetched_mask_ = 0;
 };
 
 inline bool is_bayesian(StrategyId) { return true; }
@@ -260,14 +278,25 @@ inline TuningRun run_bo(const EnumeratedSpace& space, const Objective& objective
   cv.initial_sample_mean = init.mean_observation();
   cv.initial_mean_variance = gp.mean_variance();
   bool warned = false;
+  ctx.on_visit = nullptr;  // inside the loop gtc_observe marks visited on the device
+
+  auto select_args = [&]() {
+    gtc_select_args a{};
+    a.lambda_mode = static_cast<std::int32_t>(config.exploration.mode);
+    a.lambda_constant = config.exploration.constant;
+    a.cv_initial_sample_mean = cv.initial_sample_mean;
+    a.cv_initial_mean_variance = cv.initial_mean_variance;
+    a.f_best_raw = ctx.run().best_value;
+    if (single) {
+      a.af_mask = 1u << static_cast<int>(*single);
+    } else {  // every active function: covers multi's fused pass and advanced's consulted one
+      for (AcquisitionId af : portfolio->active()) a.af_mask |= 1u << static_cast<int>(af);
+    }
+    return a;
+  };
 
   while (!ctx.exhausted()) {
-    gp.args = gtc_select_args{};
-    gp.args.lambda_mode = static_cast<std::int32_t>(config.exploration.mode);
-    gp.args.lambda_constant = config.exploration.constant;
-    gp.args.cv_initial_sample_mean = cv.initial_sample_mean;
-    gp.args.cv_initial_mean_variance = cv.initial_mean_variance;
-    gp.args.f_best_raw = ctx.run().best_value;
+    gp.args = select_args();
 
     std::size_t pick;
     AcquisitionId by;
@@ -291,8 +320,11 @@ inline TuningRun run_bo(const EnumeratedSpace& space, const Objective& objective
     if (m.is_valid()) {
       train_pos.push_back(pick);
       train_val.push_back(*m.value);
-      gp.append(pick, *m.value);  // refit == bordered append (strategies.hpp:444-449)
     }
+    // refit == bordered append (strategies.hpp:444-449), fused with the next
+    // iteration's selection (:401-436) into one device round trip
+    const gtc_select_args next = select_args();
+    gp.observe(pick, m.value, ctx.exhausted() ? nullptr : &next);
     ctx.run().lambdas.push_back(lambda);
     if (config.inspect) config.inspect(ctx.run().evaluations, ctx.valid_observations().size(), train_pos.size(), lambda);
   }

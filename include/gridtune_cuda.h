@@ -151,6 +151,14 @@ int64_t gtc_unvisited_count(const gtc_run* run);
  * acquisition.hpp:12-83, portfolio.hpp:32-61). */
 int gtc_select(gtc_run* run, const gtc_select_args* args, gtc_select_result* out);
 
+/* One loop iteration after an evaluation (strategies.hpp:440-449 then
+ * :401-436), with a single host synchronisation: marks `position` visited;
+ * if `valid`, appends (position, y_raw) like gtc_append; then, if `args` is
+ * non-null and candidates remain, runs gtc_select for the next suggestion.
+ * `out` gets positions -1 when no selection ran. */
+int gtc_observe(gtc_run* run, int64_t position, double y_raw, int32_t valid,
+                const gtc_select_args* args, gtc_select_result* out, gtc_fit_info* info);
+
 /* Mean posterior variance over the unvisited candidates (the initial
  * contextual-variance normaliser, strategies.hpp:392-397; 0 when empty). */
 int gtc_mean_variance(gtc_run* run, double* mean_variance, int64_t* count);
@@ -163,6 +171,9 @@ int gtc_read_predictions(gtc_run* run, double* mean, double* variance);
 /* Device-side timing helper for benchmarks: CUDA-event milliseconds of the
  * last gtc_append's predictive-pass kernel (0 if none). */
 double gtc_last_pass_ms(const gtc_run* run);
+/* CUDA-event milliseconds of the last gtc_observe's device work (all of its
+ * kernels, first launch to last, excluding the result readback). */
+double gtc_last_step_ms(const gtc_run* run);
 /* The CUDA stream the run launches on (as an opaque integer, for NCCL). */
 uint64_t gtc_run_stream(const gtc_run* run);
 

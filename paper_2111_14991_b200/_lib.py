@@ -100,9 +100,12 @@ SIGNATURES = [
     ("gtc_unmark_visited", C.c_int, [P, C.c_int64]),
     ("gtc_unvisited_count", C.c_int64, [P]),
     ("gtc_select", C.c_int, [P, C.POINTER(gtc_select_args), C.POINTER(gtc_select_result)]),
+    ("gtc_observe", C.c_int, [P, C.c_int64, C.c_double, C.c_int32, C.POINTER(gtc_select_args),
+                              C.POINTER(gtc_select_result), C.POINTER(gtc_fit_info)]),
     ("gtc_mean_variance", C.c_int, [P, DP, I64P]),
     ("gtc_read_predictions", C.c_int, [P, DP, DP]),
     ("gtc_last_pass_ms", C.c_double, [P]),
+    ("gtc_last_step_ms", C.c_double, [P]),
     ("gtc_run_stream", C.c_uint64, [P]),
     ("gtc_gp_fit", C.c_int, [C.c_int, C.POINTER(gtc_kernel), DP, DP, C.c_int32, C.c_int32,
                              C.c_double, C.c_double, C.POINTER(P), C.POINTER(gtc_fit_info)]),

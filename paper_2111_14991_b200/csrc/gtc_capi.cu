@@ -6,6 +6,7 @@
 // GTC_ERR_CUDA when the device is unusable.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -52,6 +53,7 @@ int dalloc(T** p, size_t count) {
 }
 
 int64_t pad_tiles(int64_t n) { return ((n + kTile - 1) / kTile) * kTile; }
+size_t packed_size(int n) { return (size_t)n * (size_t)(n + 1) / 2; }
 
 int check_kernel(const gtc_kernel* k) {
   if (!k) return fail(GTC_ERR_INVALID, "kernel is null");
@@ -66,35 +68,35 @@ KernelParams kparams(const gtc_kernel& k) { return KernelParams{k.nu, k.lengthsc
 
 std::string fmt_jitter(double j) { return std::to_string(j); }  // std::to_string as gp.hpp:126
 
-// Scratch for the multi-block reductions (sized for reduce_blocks()).
+// Scratch of the multi-block reductions (sized for reduce_blocks()).
 struct ReduceScratch {
-  double* psum = nullptr;
-  int64_t* pcnt = nullptr;
-  double* pscore = nullptr;
-  int64_t* ppos = nullptr;
-  int64_t* pfirst = nullptr;
-  int64_t* pcnt2 = nullptr;
-  unsigned int* counter = nullptr;
+  ReduceBufs b{};
+  double* vsum = nullptr;      // k_varsum partials
+  int64_t* vcnt = nullptr;
+  unsigned int* vcounter = nullptr;
   VarTotals* totals = nullptr;
   SelectDev* sel = nullptr;
   SelectDev* h_sel = nullptr;  // pinned
   VarTotals* h_totals = nullptr;
 
   int init(int64_t n) {
-    const int b = reduce_blocks(n);
+    const int nb = std::max(reduce_blocks(n), kMaxReduceGrid);  // covers the selection grid too
     int rc;
-    if ((rc = dalloc(&psum, b)) || (rc = dalloc(&pcnt, b)) || (rc = dalloc(&pscore, 3 * b)) ||
-        (rc = dalloc(&ppos, 3 * b)) || (rc = dalloc(&pfirst, b)) || (rc = dalloc(&pcnt2, b)) ||
-        (rc = dalloc(&counter, 2)) || (rc = dalloc(&totals, 1)) || (rc = dalloc(&sel, 1)))
+    if ((rc = dalloc(&b.pvar, nb)) || (rc = dalloc(&b.pvcnt, nb)) || (rc = dalloc(&b.pscore, 3 * nb)) ||
+        (rc = dalloc(&b.ppos, 3 * nb)) || (rc = dalloc(&b.pfirst, nb)) || (rc = dalloc(&b.pcnt, nb)) ||
+        (rc = dalloc(&b.counter, 1)) || (rc = dalloc(&vsum, nb)) || (rc = dalloc(&vcnt, nb)) ||
+        (rc = dalloc(&vcounter, 1)) || (rc = dalloc(&totals, 1)) || (rc = dalloc(&sel, 1)))
       return rc;
-    GTC_CUDA(cudaMemset(counter, 0, 2 * sizeof(unsigned int)));
+    GTC_CUDA(cudaMemset(b.counter, 0, sizeof(unsigned int)));
+    GTC_CUDA(cudaMemset(vcounter, 0, sizeof(unsigned int)));
     GTC_CUDA(cudaMallocHost(&h_sel, sizeof(SelectDev)));
     GTC_CUDA(cudaMallocHost(&h_totals, sizeof(VarTotals)));
     return GTC_OK;
   }
   void release() {
-    cudaFree(psum); cudaFree(pcnt); cudaFree(pscore); cudaFree(ppos); cudaFree(pfirst);
-    cudaFree(pcnt2); cudaFree(counter); cudaFree(totals); cudaFree(sel);
+    cudaFree(b.pvar); cudaFree(b.pvcnt); cudaFree(b.pscore); cudaFree(b.ppos); cudaFree(b.pfirst);
+    cudaFree(b.pcnt); cudaFree(b.counter); cudaFree(vsum); cudaFree(vcnt); cudaFree(vcounter);
+    cudaFree(totals); cudaFree(sel);
     if (h_sel) cudaFreeHost(h_sel);
     if (h_totals) cudaFreeHost(h_totals);
   }
@@ -109,7 +111,7 @@ struct GpStore {
     dev.n_max = n_max;
     dev.d = d;
     if ((rc = dalloc(&dev.train_x, (size_t)n_max * d)) || (rc = dalloc(&dev.train_n2, n_max)) ||
-        (rc = dalloc(&dev.y, n_max)) || (rc = dalloc(&dev.L, (size_t)n_max * n_max)) ||
+        (rc = dalloc(&dev.y, n_max)) || (rc = dalloc(&dev.L, packed_size(n_max) + 2)) ||
         (rc = dalloc(&dev.c, n_max)) || (rc = dalloc(&dev.e, n_max)) ||
         (rc = dalloc(&dev.beta, n_max)) || (rc = dalloc(&dev.sc, 1)) ||
         (rc = dalloc(&dev.scratch, n_max)))
@@ -128,8 +130,8 @@ struct GpStore {
 };
 
 // Factorises the n training points already on the device with the
-// reference's jitter escalation (gp.hpp:116-129), starting at `jitter` and
-// never exceeding base * 2^6.  On success h_sc holds the scalars.
+// reference's jitter escalation (gp.hpp:116-129), starting at `start_jitter`
+// and never exceeding base * 2^6.  On success h_sc holds the scalars.
 int factor_with_escalation(GpStore& gp, const gtc_kernel& k, double noise, double base_jitter,
                            double start_jitter, int n, cudaStream_t s) {
   double jitter = start_jitter;
@@ -156,7 +158,8 @@ int factor_with_escalation(GpStore& gp, const gtc_kernel& k, double noise, doubl
 
 // Rebuilds V rows [0, n) for `space` (chunks of kMaxRows) and the posterior.
 int rebuild_predictions(const SpaceDev& sp, GpStore& gp, const gtc_kernel& k, double* V,
-                        int64_t tile_stride, int n, double* mu, double* var, cudaStream_t s) {
+                        int64_t tile_stride, int n, double* mu, double* var, const VarPartials* vp,
+                        cudaStream_t s) {
   if (n == 0) {
     launch_prior(mu, var, sp.n_pad, k.output_variance, s);
     GTC_LAUNCHED();
@@ -164,7 +167,7 @@ int rebuild_predictions(const SpaceDev& sp, GpStore& gp, const gtc_kernel& k, do
   }
   for (int n0 = 0; n0 < n; n0 += kMaxRows) {
     const int r = std::min(kMaxRows, n - n0);
-    launch_extend(sp, gp.dev, kparams(k), V, tile_stride, n0, r, n0 + r == n, mu, var, false, s);
+    launch_extend(sp, gp.dev, kparams(k), V, tile_stride, n0, r, n0 + r == n, mu, var, false, vp, s);
     GTC_LAUNCHED();
   }
   return GTC_OK;
@@ -186,6 +189,18 @@ int check_fit_inputs(const double* y, int n, double noise, double jitter) {
   for (int i = 0; i < n; ++i)
     if (!std::isfinite(y[i])) return fail(GTC_ERR_INVALID, "GP fit: observations must be finite");
   return GTC_OK;
+}
+
+void copy_result(const SelectDev& s, gtc_select_result* out) {
+  for (int k = 0; k < 3; ++k) {
+    out->position[k] = s.position[k];
+    out->score[k] = s.score[k];
+  }
+  out->lambda = s.lambda;
+  out->mean_variance = s.mean_variance;
+  out->best_std = s.best_std;
+  out->n_candidates = s.n_candidates;
+  out->cv_fallback = s.cv_fallback;
 }
 
 }  // namespace
@@ -221,8 +236,20 @@ struct gtc_run {
   bool predictions_valid = false;
   std::vector<double> y_host;
   std::vector<int64_t> pos_host;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  bool pass_timed = false;
+  struct Readback {
+    SelectDev sel;
+    GpScalars sc;
+  };
+  Readback* h_rb = nullptr;  // pinned: one D2H per gtc_observe
+  // variance partials for the selection; n_partials == 0: stale (recompute)
+  double* part_sum = nullptr;
+  long long* part_cnt = nullptr;
+  int n_partials = 0;
+  int tiles = 0;
+  VarPartials vp() const { return VarPartials{visited, part_sum, part_cnt}; }
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;          // last predictive pass
+  cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;  // last gtc_observe device span
+  bool pass_timed = false, step_timed = false;
 };
 
 struct gtc_gp {
@@ -238,7 +265,7 @@ struct gtc_gp {
 
 extern "C" const char* gtc_last_error(void) { return g_last_error.c_str(); }
 extern "C" void gtc_internal_set_error(const char* msg) { g_last_error = msg ? msg : ""; }
-extern "C" const char* gtc_version(void) { return "gridtune-b200 0.1 (sm_100a)"; }
+extern "C" const char* gtc_version(void) { return "gridtune-b200 0.2 (sm_100a)"; }
 extern "C" uint64_t gtc_kernel_launches(void) { return launches(); }
 
 // =============================================================== space
@@ -301,8 +328,11 @@ extern "C" int gtc_run_destroy(gtc_run* r) {
   cudaFree(r->var);
   cudaFree(r->visited);
   cudaFree(r->excluded);
-  if (r->ev0) cudaEventDestroy(r->ev0);
-  if (r->ev1) cudaEventDestroy(r->ev1);
+  cudaFree(r->part_sum);
+  cudaFree(r->part_cnt);
+  if (r->h_rb) cudaFreeHost(r->h_rb);
+  for (cudaEvent_t ev : {r->ev0, r->ev1, r->ev_step0, r->ev_step1})
+    if (ev) cudaEventDestroy(ev);
   if (r->stream) cudaStreamDestroy(r->stream);
   delete r;
   return GTC_OK;
@@ -328,19 +358,23 @@ extern "C" int gtc_run_create(gtc_space* space, const gtc_model_config* cfg, gtc
   const int64_t words = (space->n + 31) / 32;
   if ((rc = r->gp.init(cfg->n_max, space->d)) || (rc = r->red.init(space->n)) ||
       (rc = dalloc(&r->V, (size_t)tiles * r->tile_stride)) || (rc = dalloc(&r->mu, space->n_pad)) ||
-      (rc = dalloc(&r->var, space->n_pad)) || (rc = dalloc(&r->visited, words))) {
+      (rc = dalloc(&r->var, space->n_pad)) || (rc = dalloc(&r->visited, words)) ||
+      (rc = dalloc(&r->part_sum, std::max<int64_t>(tiles, reduce_blocks(space->n)))) ||
+      (rc = dalloc(&r->part_cnt, std::max<int64_t>(tiles, reduce_blocks(space->n))))) {
     gtc_run_destroy(r);
     return rc;
   }
   cudaError_t e = cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaEventCreate(&r->ev0);
-  if (e == cudaSuccess) e = cudaEventCreate(&r->ev1);
+  for (cudaEvent_t* ev : {&r->ev0, &r->ev1, &r->ev_step0, &r->ev_step1})
+    if (e == cudaSuccess) e = cudaEventCreate(ev);
   if (e == cudaSuccess) e = cudaMemset(r->visited, 0, words * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMallocHost(&r->h_rb, sizeof(gtc_run::Readback));
   if (e != cudaSuccess) {
     gtc_run_destroy(r);
     return fail(GTC_ERR_CUDA, std::string("run create: ") + cudaGetErrorString(e));
   }
   r->visited_host.assign(words, 0u);
+  r->tiles = (int)tiles;
   *out = r;
   return GTC_OK;
 }
@@ -356,10 +390,13 @@ static int upload_train(gtc_run* r, const int64_t* positions, const double* y, i
   if (n > 0) {
     GTC_CUDA(cudaMemcpyAsync(r->gp.dev.train_x, X.data(), X.size() * sizeof(double), cudaMemcpyHostToDevice, r->stream));
     GTC_CUDA(cudaMemcpyAsync(r->gp.dev.y, y, sizeof(double) * n, cudaMemcpyHostToDevice, r->stream));
+    GTC_CUDA(cudaStreamSynchronize(r->stream));  // X lives on this stack frame
   }
   return GTC_OK;
 }
 
+// Full refit of the run's observations (GpModel::fit semantics) starting at
+// `start_jitter`, then the full predictive pass.
 static int refit(gtc_run* r, double start_jitter, gtc_fit_info* info) {
   const int n = (int)r->y_host.size();
   int rc = upload_train(r, r->pos_host.data(), r->y_host.data(), n);
@@ -371,9 +408,12 @@ static int refit(gtc_run* r, double start_jitter, gtc_fit_info* info) {
   }
   r->n = n;
   r->jitter = r->gp.h_sc->jitter;
-  rc = rebuild_predictions(r->space->dev(), r->gp, r->cfg.kernel, r->V, r->tile_stride, n, r->mu, r->var, r->stream);
+  const VarPartials vp = r->vp();
+  rc = rebuild_predictions(r->space->dev(), r->gp, r->cfg.kernel, r->V, r->tile_stride, n, r->mu, r->var, &vp,
+                           r->stream);
   if (rc) return rc;
   r->predictions_valid = true;
+  r->n_partials = r->tiles;
   fill_info(info, *r->gp.h_sc, n, 1);
   return GTC_OK;
 }
@@ -394,14 +434,34 @@ extern "C" int gtc_fit(gtc_run* r, const int64_t* positions, const double* y_raw
     r->gp.h_sc->y_std = 1.0;
     r->gp.h_sc->jitter = r->jitter;
     GTC_CUDA(cudaMemcpyAsync(r->gp.dev.sc, r->gp.h_sc, sizeof(GpScalars), cudaMemcpyHostToDevice, r->stream));
-    rc = rebuild_predictions(r->space->dev(), r->gp, r->cfg.kernel, r->V, r->tile_stride, 0, r->mu, r->var, r->stream);
+    rc = rebuild_predictions(r->space->dev(), r->gp, r->cfg.kernel, r->V, r->tile_stride, 0, r->mu, r->var, nullptr,
+                             r->stream);
     if (rc) return rc;
     GTC_CUDA(cudaStreamSynchronize(r->stream));
     r->predictions_valid = true;
+    r->n_partials = 0;
     fill_info(info, *r->gp.h_sc, 0, 1);
     return GTC_OK;
   }
   return refit(r, r->cfg.jitter, info);
+}
+
+// Enqueues the bordered-row update + predictive pass for observation n0
+// (asynchronous; the pass is a no-op if the pivot fails on the device).
+static int enqueue_append(gtc_run* r, int64_t pos, double y_raw, uint32_t* mark) {
+  const int n0 = r->n;
+  launch_gp_append(r->gp.dev, kparams(r->cfg.kernel), r->cfg.noise, r->space->dev(), pos, nullptr, y_raw, n0,
+                   mark, r->stream);
+  GTC_LAUNCHED();
+  GTC_CUDA(cudaEventRecord(r->ev0, r->stream));
+  const VarPartials vp = r->vp();
+  launch_extend(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, n0, 1, true, r->mu,
+                r->var, true, &vp, r->stream);
+  GTC_LAUNCHED();
+  GTC_CUDA(cudaEventRecord(r->ev1, r->stream));
+  r->pass_timed = true;
+  r->n_partials = r->tiles;  // (stale if the pivot failed; the refit rewrites them)
+  return GTC_OK;
 }
 
 extern "C" int gtc_append(gtc_run* r, int64_t pos, double y_raw, gtc_fit_info* info) {
@@ -416,8 +476,8 @@ extern "C" int gtc_append(gtc_run* r, int64_t pos, double y_raw, gtc_fit_info* i
   r->y_host.push_back(y_raw);
   r->pos_host.push_back(pos);
   if (n0 == 0) return refit(r, r->cfg.jitter, info);
-  launch_gp_append(r->gp.dev, kparams(r->cfg.kernel), r->cfg.noise, r->space->dev(), pos, nullptr, y_raw, n0, r->stream);
-  GTC_LAUNCHED();
+  int rc = enqueue_append(r, pos, y_raw, nullptr);
+  if (rc) return rc;
   GTC_CUDA(cudaMemcpyAsync(r->gp.h_sc, r->gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, r->stream));
   GTC_CUDA(cudaStreamSynchronize(r->stream));
   if (r->gp.h_sc->status != 0) {
@@ -425,11 +485,6 @@ extern "C" int gtc_append(gtc_run* r, int64_t pos, double y_raw, gtc_fit_info* i
     // every jitter up to the current one too, so escalate from jitter * 2.
     return refit(r, r->jitter * 2.0, info);
   }
-  GTC_CUDA(cudaEventRecord(r->ev0, r->stream));
-  launch_extend(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, n0, 1, true, r->mu, r->var, false, r->stream);
-  GTC_LAUNCHED();
-  GTC_CUDA(cudaEventRecord(r->ev1, r->stream));
-  r->pass_timed = true;
   r->n = n0 + 1;
   r->predictions_valid = true;
   fill_info(info, *r->gp.h_sc, r->n, 0);
@@ -443,13 +498,15 @@ extern "C" int gtc_truncate(gtc_run* r, int32_t n, gtc_fit_info* info) {
   if (n == 0) return gtc_fit(r, nullptr, nullptr, 0, info);
   launch_gp_truncate(r->gp.dev, n, r->stream);
   GTC_LAUNCHED();
-  GTC_CUDA(cudaMemcpyAsync(r->gp.h_sc, r->gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, r->stream));
-  GTC_CUDA(cudaStreamSynchronize(r->stream));
   r->n = n;
   r->y_host.resize(n);
   r->pos_host.resize(n);
   r->predictions_valid = false;
-  fill_info(info, *r->gp.h_sc, n, 0);
+  if (info) {  // the scalars need a round trip; without `info` the call stays asynchronous
+    GTC_CUDA(cudaMemcpyAsync(r->gp.h_sc, r->gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, r->stream));
+    GTC_CUDA(cudaStreamSynchronize(r->stream));
+    fill_info(info, *r->gp.h_sc, n, 0);
+  }
   return GTC_OK;
 }
 
@@ -457,33 +514,44 @@ static int ensure_predictions(gtc_run* r) {
   if (r->predictions_valid) return GTC_OK;
   if (r->n == 0) {
     launch_prior(r->mu, r->var, r->space->n_pad, r->cfg.kernel.output_variance, r->stream);
+    r->n_partials = 0;
   } else {
     // posterior from the resident V rows (r = 0 new rows)
-    launch_extend(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, r->n, 0, true, r->mu, r->var, false, r->stream);
+    const VarPartials vp = r->vp();
+    launch_extend(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, r->n, 0, true,
+                  r->mu, r->var, false, &vp, r->stream);
+    r->n_partials = r->tiles;
   }
   GTC_LAUNCHED();
   r->predictions_valid = true;
   return GTC_OK;
 }
 
-static int set_visited(gtc_run* r, int64_t pos, int set) {
-  if (!r) return fail(GTC_ERR_INVALID, "run is null");
-  if (pos < 0 || pos >= r->space->n) return fail(GTC_ERR_INVALID, "position out of range");
-  GTC_CUDA(cudaSetDevice(r->space->device));
+static bool host_mark(gtc_run* r, int64_t pos, int set) {
   uint32_t& w = r->visited_host[pos >> 5];
   const uint32_t bit = 1u << (pos & 31);
   const bool was = (w & bit) != 0;
   if (set && !was) {
     w |= bit;
     ++r->visited_count;
-  } else if (!set && was) {
+    return true;
+  }
+  if (!set && was) {
     w &= ~bit;
     --r->visited_count;
-  } else {
-    return GTC_OK;
+    return true;
   }
+  return false;
+}
+
+static int set_visited(gtc_run* r, int64_t pos, int set) {
+  if (!r) return fail(GTC_ERR_INVALID, "run is null");
+  if (pos < 0 || pos >= r->space->n) return fail(GTC_ERR_INVALID, "position out of range");
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  if (!host_mark(r, pos, set)) return GTC_OK;
   launch_mark(r->visited, pos, set, r->stream);
   GTC_LAUNCHED();
+  r->n_partials = 0;
   return GTC_OK;
 }
 
@@ -498,7 +566,7 @@ extern "C" int gtc_mean_variance(gtc_run* r, double* out, int64_t* count) {
   GTC_CUDA(cudaSetDevice(r->space->device));
   int rc = ensure_predictions(r);
   if (rc) return rc;
-  launch_varsum(r->var, r->visited, r->space->n, r->red.psum, r->red.pcnt, r->red.counter, r->red.totals, r->stream);
+  launch_varsum(r->var, r->visited, r->space->n, r->red.vsum, r->red.vcnt, r->red.vcounter, r->red.totals, r->stream);
   GTC_LAUNCHED();
   GTC_CUDA(cudaMemcpyAsync(r->red.h_totals, r->red.totals, sizeof(VarTotals), cudaMemcpyDeviceToHost, r->stream));
   GTC_CUDA(cudaStreamSynchronize(r->stream));
@@ -508,10 +576,8 @@ extern "C" int gtc_mean_variance(gtc_run* r, double* out, int64_t* count) {
   return GTC_OK;
 }
 
-extern "C" int gtc_select(gtc_run* r, const gtc_select_args* a, gtc_select_result* out) {
-  if (!r || !a || !out) return fail(GTC_ERR_INVALID, "null argument");
-  if ((a->af_mask & 7u) == 0) return fail(GTC_ERR_INVALID, "af_mask selects no acquisition function");
-  GTC_CUDA(cudaSetDevice(r->space->device));
+// Enqueues the cooperative selection kernel (asynchronous).
+static int enqueue_selection(gtc_run* r, const gtc_select_args* a) {
   int rc = ensure_predictions(r);
   if (rc) return rc;
   SelectParams p{a->af_mask & 7u, a->lambda_mode, a->lambda_constant, a->cv_initial_sample_mean,
@@ -528,24 +594,102 @@ extern "C" int gtc_select(gtc_run* r, const gtc_select_args* a, gtc_select_resul
     p.excluded = r->excluded;
     p.n_excluded = a->n_excluded;
   }
-  launch_varsum(r->var, r->visited, r->space->n, r->red.psum, r->red.pcnt, r->red.counter, r->red.totals, r->stream);
+  if (r->n_partials == 0) {  // visited set changed since the last pass
+    launch_var_partials(r->var, r->visited, r->space->n, r->part_sum, r->part_cnt, r->stream);
+    GTC_LAUNCHED();
+    r->n_partials = reduce_blocks(r->space->n);
+  }
+  launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, r->part_sum, r->part_cnt, r->n_partials,
+                r->red.b, r->red.sel, r->stream);
   GTC_LAUNCHED();
-  launch_select(r->mu, r->var, r->visited, r->space->n, r->red.totals, r->gp.dev.sc, p, r->red.pscore,
-                r->red.ppos, r->red.pfirst, r->red.pcnt2, r->red.counter + 1, r->red.sel, r->stream);
-  GTC_LAUNCHED();
+  return GTC_OK;
+}
+
+extern "C" int gtc_select(gtc_run* r, const gtc_select_args* a, gtc_select_result* out) {
+  if (!r || !a || !out) return fail(GTC_ERR_INVALID, "null argument");
+  if ((a->af_mask & 7u) == 0) return fail(GTC_ERR_INVALID, "af_mask selects no acquisition function");
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  int rc = enqueue_selection(r, a);
+  if (rc) return rc;
   GTC_CUDA(cudaMemcpyAsync(r->red.h_sel, r->red.sel, sizeof(SelectDev), cudaMemcpyDeviceToHost, r->stream));
   GTC_CUDA(cudaStreamSynchronize(r->stream));
-  const SelectDev& s = *r->red.h_sel;
-  for (int k = 0; k < 3; ++k) {
-    out->position[k] = s.position[k];
-    out->score[k] = s.score[k];
+  copy_result(*r->red.h_sel, out);
+  if (r->red.h_sel->n_candidates == 0) return fail(GTC_ERR_NO_CANDIDATES, "acquisition: no candidates remaining");
+  return GTC_OK;
+}
+
+// One BO iteration's device work after an evaluation, with a single host
+// synchronisation: mark visited -> (valid) bordered row + V-row pass ->
+// (optional) cooperative selection -> one readback.  A failed bordered pivot
+// is detected on the device (the pass is skipped, the selection reports
+// GpScalars::status) and handled here by the escalating refit.
+extern "C" int gtc_observe(gtc_run* r, int64_t pos, double y_raw, int32_t valid, const gtc_select_args* a,
+                           gtc_select_result* out, gtc_fit_info* info) {
+  if (!r) return fail(GTC_ERR_INVALID, "run is null");
+  if (pos < 0 || pos >= r->space->n) return fail(GTC_ERR_INVALID, "position out of range");
+  if (valid && !std::isfinite(y_raw)) return fail(GTC_ERR_INVALID, "GP fit: observations must be finite");
+  if (valid && r->n >= r->cfg.n_max) return fail(GTC_ERR_CAPACITY, "more observations than the run's n_max");
+  if (a && (a->af_mask & 7u) == 0) return fail(GTC_ERR_INVALID, "af_mask selects no acquisition function");
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  int rc;
+  const bool newly = host_mark(r, pos, 1);
+  const int n0 = r->n;
+  bool appended = false;
+  GTC_CUDA(cudaEventRecord(r->ev_step0, r->stream));
+  if (valid) {
+    r->y_host.resize(n0);
+    r->pos_host.resize(n0);
+    r->y_host.push_back(y_raw);
+    r->pos_host.push_back(pos);
+    if (n0 == 0) {
+      if (newly) {
+        launch_mark(r->visited, pos, 1, r->stream);
+        GTC_LAUNCHED();
+        r->n_partials = 0;
+      }
+      if ((rc = refit(r, r->cfg.jitter, info))) return rc;
+    } else {
+      if ((rc = enqueue_append(r, pos, y_raw, newly ? r->visited : nullptr))) return rc;
+      r->predictions_valid = true;
+      appended = true;
+    }
+  } else if (newly) {
+    launch_mark(r->visited, pos, 1, r->stream);
+    GTC_LAUNCHED();
+    r->n_partials = 0;
   }
-  out->lambda = s.lambda;
-  out->mean_variance = s.mean_variance;
-  out->best_std = s.best_std;
-  out->n_candidates = s.n_candidates;
-  out->cv_fallback = s.cv_fallback;
-  if (s.n_candidates == 0) return fail(GTC_ERR_NO_CANDIDATES, "acquisition: no candidates remaining");
+  const bool selecting = a && r->space->n - r->visited_count > 0;
+  if (selecting && (rc = enqueue_selection(r, a))) return rc;
+  GTC_CUDA(cudaEventRecord(r->ev_step1, r->stream));
+  r->step_timed = true;
+  if (selecting)
+    GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sel, r->red.sel, sizeof(SelectDev), cudaMemcpyDeviceToHost, r->stream));
+  GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sc, r->gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, r->stream));
+  GTC_CUDA(cudaStreamSynchronize(r->stream));
+  if (appended) {
+    if (r->h_rb->sc.status != 0) {
+      // bordered pivot <= 0: refactorise with escalated jitter (gp.hpp:116-129)
+      if ((rc = refit(r, r->jitter * 2.0, info))) return rc;
+      if (selecting) {
+        if ((rc = enqueue_selection(r, a))) return rc;
+        GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sel, r->red.sel, sizeof(SelectDev), cudaMemcpyDeviceToHost, r->stream));
+        GTC_CUDA(cudaStreamSynchronize(r->stream));
+      }
+    } else {
+      r->n = n0 + 1;
+      *r->gp.h_sc = r->h_rb->sc;
+      fill_info(info, r->h_rb->sc, r->n, 0);
+    }
+  } else if (!valid) {
+    fill_info(info, r->h_rb->sc, r->n, 0);
+  }
+  if (selecting && out) {
+    copy_result(r->h_rb->sel, out);
+    if (r->h_rb->sel.n_candidates == 0) return fail(GTC_ERR_NO_CANDIDATES, "acquisition: no candidates remaining");
+  } else if (out) {
+    std::memset(out, 0, sizeof(*out));
+    for (int k = 0; k < 3; ++k) out->position[k] = -1;
+  }
   return GTC_OK;
 }
 
@@ -560,14 +704,19 @@ extern "C" int gtc_read_predictions(gtc_run* r, double* mean, double* variance) 
   return GTC_OK;
 }
 
-extern "C" double gtc_last_pass_ms(const gtc_run* r) {
-  if (!r || !r->pass_timed) return 0.0;
+static double event_ms(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
-  if (cudaEventSynchronize(r->ev1) != cudaSuccess) return 0.0;
-  if (cudaEventElapsedTime(&ms, r->ev0, r->ev1) != cudaSuccess) return 0.0;
+  if (cudaEventSynchronize(b) != cudaSuccess) return 0.0;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) return 0.0;
   return ms;
 }
 
+extern "C" double gtc_last_pass_ms(const gtc_run* r) {
+  return r && r->pass_timed ? event_ms(r->ev0, r->ev1) : 0.0;
+}
+extern "C" double gtc_last_step_ms(const gtc_run* r) {
+  return r && r->step_timed ? event_ms(r->ev_step0, r->ev_step1) : 0.0;
+}
 extern "C" uint64_t gtc_run_stream(const gtc_run* r) { return r ? (uint64_t)(uintptr_t)r->stream : 0; }
 
 // =============================================================== stand-alone GpModel
@@ -647,8 +796,8 @@ extern "C" int gtc_gp_predict(gtc_gp* g, const double* Xstar, int64_t m, double*
     gtc_space_destroy(sp);
     return rc;
   }
-  // GpDev with n_max = n so the extend kernel's L stride matches the factor
-  rc = rebuild_predictions(sp->dev(), g->gp, g->kernel, V, tile_stride, g->n, mu, var, g->stream);
+  // GpDev with n_max = n so the extend kernel's tile stride matches the factor
+  rc = rebuild_predictions(sp->dev(), g->gp, g->kernel, V, tile_stride, g->n, mu, var, nullptr, g->stream);
   cudaError_t e = cudaSuccess;
   if (!rc && mean) e = cudaMemcpyAsync(mean, mu, sizeof(double) * m, cudaMemcpyDeviceToHost, g->stream);
   if (!rc && e == cudaSuccess && variance) e = cudaMemcpyAsync(variance, var, sizeof(double) * m, cudaMemcpyDeviceToHost, g->stream);
@@ -666,7 +815,7 @@ extern "C" int gtc_gp_info(const gtc_gp* g, gtc_fit_info* info) {
   return GTC_OK;
 }
 
-// =============================================================== best_candidate
+// =============================================================== acquisition over spans
 
 extern "C" int gtc_best_candidate(int device, int32_t af, const double* means, const double* stds,
                                   int64_t n, double best_std, double lambda, const uint8_t* excluded,
@@ -689,8 +838,7 @@ extern "C" int gtc_best_candidate(int device, int32_t af, const double* means, c
     if (e == cudaSuccess) e = cudaMemcpyAsync(ds, stds, sizeof(double) * n, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && excluded) e = cudaMemcpyAsync(dx, excluded, n, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) {
-      launch_best_candidate(dm, ds, dx, n, af, best_std, lambda, red.pscore, red.ppos, red.pfirst,
-                            red.pcnt2, red.counter, red.sel, s);
+      launch_best_candidate(dm, ds, dx, n, af, best_std, lambda, red.b, red.sel, s);
       e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(red.h_sel, red.sel, sizeof(SelectDev), cudaMemcpyDeviceToHost, s);

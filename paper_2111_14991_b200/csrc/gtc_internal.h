@@ -14,10 +14,13 @@ namespace gtc {
 constexpr int kTile = 256;
 constexpr int kExtendThreads = kTile / 2;  // one double2 column pair per thread
 constexpr int kReduceThreads = 256;
+constexpr int kSelectBlocksPerSM = 4;      // selection: <= 64 registers, one resident wave
+constexpr int kMaxReduceGrid = 2048;       // upper bound of every reduction grid (scratch sizing)
 constexpr int kCtaThreads = 256;           // single-CTA GP kernels
 constexpr int kMaxRows = 8;                // rows per multi-row extend pass (rebuild)
 constexpr int kMaxNmax = 1024;             // largest supported GP training size
 constexpr int kMaxDim = 64;                // largest supported search-space dimension
+constexpr size_t kCtaSmemLimit = 220 * 1024;  // packed-L staging budget of the single-CTA kernels
 
 struct KernelParams {
   int nu;
@@ -42,7 +45,7 @@ struct GpDev {
   double* train_x;   // [n_max][d]
   double* train_n2;  // [n_max] squared norms (sequential), for the expansion distance
   double* y;         // [n_max] raw observations
-  double* L;         // [n_max][n_max] row-major lower factor
+  double* L;         // packed lower factor, row i at i(i+1)/2
   double* c;         // [n_max] L^-1 (y - y0)
   double* e;         // [n_max] L^-1 1
   double* beta;      // [n_max] L^-1 y_standardized
@@ -59,7 +62,7 @@ struct SpaceDev {
   int d;
 };
 
-// Result of the reduction kernels (device side, copied to the host).
+// Result of the selection kernels (device side, copied to the host).
 struct SelectDev {
   int64_t position[3];
   double score[3];
@@ -87,6 +90,17 @@ struct SelectParams {
   int n_excluded;
 };
 
+// Per-block scratch of the selection kernels (sized by reduce_blocks(n)).
+struct ReduceBufs {
+  double* pvar;        // variance partials (cooperative phase 1)
+  long long* pvcnt;
+  double* pscore;      // [3 * blocks]
+  int64_t* ppos;       // [3 * blocks]
+  int64_t* pfirst;
+  long long* pcnt;
+  unsigned int* counter;
+};
+
 // --- launchers (gtc_kernels.cu); all asynchronous on `stream` -------------
 
 // Single-CTA: factor the Gram matrix of the model's n training points at the
@@ -95,17 +109,32 @@ void launch_gp_factor(const GpDev& g, KernelParams k, double noise, double jitte
                       cudaStream_t stream);
 // Single-CTA: append observation n0 (coords taken from `space` at `pos`, or
 // from `x_explicit` when pos < 0) to the factor; updates scalars and beta.
+// Optionally sets the visited bit of `pos`.
 void launch_gp_append(const GpDev& g, KernelParams k, double noise, const SpaceDev& space,
                       int64_t pos, const double* x_explicit, double y_new, int n0,
-                      cudaStream_t stream);
+                      uint32_t* visited_mark, cudaStream_t stream);
 // Single-CTA: recompute stats/beta for the prefix of n observations.
 void launch_gp_truncate(const GpDev& g, int n, cudaStream_t stream);
 
+// Per-tile partial sums of the posterior variance over unvisited candidates,
+// written by the final predictive pass (one entry per tile) or by
+// launch_var_partials (one per reduce block) and reduced by the selection.
+struct VarPartials {
+  const uint32_t* visited;
+  double* part_sum;
+  long long* part_cnt;
+};
+
 // Multi-row V extension over all candidates: rows [n0, n0+r) from rows [0, n0).
-// When `final`, also writes the posterior mean/variance of every candidate.
+// When `final`, also writes the posterior mean/variance of every candidate
+// (and, with `vp`, the variance partials).  With `check_status` it is a
+// no-op when the preceding bordered row failed.
 void launch_extend(const SpaceDev& space, const GpDev& g, KernelParams k, double* V,
                    int64_t tile_stride, int n0, int r, bool final, double* mu, double* var,
-                   bool check_status, cudaStream_t stream);
+                   bool check_status, const VarPartials* vp, cudaStream_t stream);
+
+void launch_var_partials(const double* var, const uint32_t* visited, int64_t n, double* part_sum,
+                         long long* part_cnt, cudaStream_t stream);
 
 void launch_prior(double* mu, double* var, int64_t n, double s2, cudaStream_t stream);
 void launch_mark(uint32_t* visited, int64_t pos, int set, cudaStream_t stream);
@@ -115,19 +144,16 @@ void launch_varsum(const double* var, const uint32_t* visited, int64_t n, double
                    int64_t* partial_cnt, unsigned int* counter, VarTotals* totals,
                    cudaStream_t stream);
 
-// Fused lambda + acquisition + masked argmax for every AF in the mask.
+// Fused mean-variance (from the partials) + lambda + acquisition + masked
+// argmax for every AF in the mask.
 void launch_select(const double* mu, const double* var, const uint32_t* visited, int64_t n,
-                   const VarTotals* totals, const GpScalars* sc, SelectParams p,
-                   double* partial_score, int64_t* partial_pos, int64_t* partial_first,
-                   int64_t* partial_cnt, unsigned int* counter, SelectDev* out,
-                   cudaStream_t stream);
+                   const GpScalars* sc, SelectParams p, const double* part_sum, const long long* part_cnt,
+                   int n_partials, const ReduceBufs& bufs, SelectDev* out, cudaStream_t stream);
 
 // best_candidate over caller spans of stds (not variances).
 void launch_best_candidate(const double* mu, const double* std, const uint8_t* excluded,
                            int64_t n, int af, double best_std, double lambda,
-                           double* partial_score, int64_t* partial_pos, int64_t* partial_first,
-                           int64_t* partial_cnt, unsigned int* counter, SelectDev* out,
-                           cudaStream_t stream);
+                           const ReduceBufs& bufs, SelectDev* out, cudaStream_t stream);
 
 void launch_scores(const double* mu, const double* sd, int64_t n, int af, double best_std,
                    double lambda, double* out, cudaStream_t stream);

@@ -12,27 +12,38 @@
 //
 // Design: the reference refits the GP and re-solves the whole
 // n x U triangular system every iteration.  Here V = L^-1 K* lives in HBM and
-// each valid observation appends ONE row of L (single CTA, bordered Cholesky)
-// and ONE row of V (k_extend<1>): per candidate, the new row is
+// each valid observation appends ONE row of L (single CTA, bordered Cholesky,
+// k_gp_append) and ONE row of V (k_extend<1>): per candidate the new row is
 //   v_n = (k(x_n, x*) - sum_{m<n} L_nm v_m) / L_nn
 // which is exactly the last step of the reference's forward substitution, and
-// the posterior mean/variance fall out of the same pass:
+// the posterior falls out of the same pass:
 //   mu = sum_i v_i beta_i  (beta = L^-1 y_standardized),  var = max(s2 - sum_i v_i^2, 0).
-// The pass streams V once (HBM-bound GEMV), so it is written for bandwidth:
-// tile-major V, 16-byte streaming loads, 8 rows in flight per thread.
+// The pass streams V once (HBM-bound GEMV): tile-major V, 16-byte streaming
+// loads, 8 rows in flight per thread.  The selection (k_select) is one
+// cooperative kernel: grid-wide mean variance -> lambda -> EI/PI/LCB ->
+// masked argmax, so no separate reduction pass over the candidates runs.
+//
+// L is stored packed row-major (row i at i(i+1)/2) so that the whole factor
+// of a budget-220 run (194 KB) fits in the shared memory of the single-CTA
+// update kernels.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
-#include <math_constants.h>
 
 #include <atomic>
 #include <cstdint>
+#include <mutex>
 
 #include "gtc_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace gtc {
 
 static std::atomic<uint64_t> g_launches{0};
 uint64_t launches() { return g_launches.load(); }
 static inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+__host__ __device__ __forceinline__ int64_t packed(int64_t i) { return i * (i + 1) / 2; }
 
 // ------------------------------------------------------------ device helpers
 
@@ -48,12 +59,6 @@ __device__ __forceinline__ double matern(double r, double lengthscale, double s2
   const double a = __dmul_rn(2.2360679774997896, s);
   const double poly = __dadd_rn(__dadd_rn(1.0, a), __ddiv_rn(__dmul_rn(a, a), 3.0));
   return __dmul_rn(__dmul_rn(s2, poly), exp(-a));
-}
-
-__device__ __forceinline__ double matern_rt(int nu, double r, double lengthscale, double s2) {
-  if (nu == 0) return matern<0>(r, lengthscale, s2);
-  if (nu == 1) return matern<1>(r, lengthscale, s2);
-  return matern<2>(r, lengthscale, s2);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -74,32 +79,59 @@ __device__ double block_sum(double v, double* red /* >= 32 doubles smem */) {
   return t;
 }
 
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ long long block_sum_ll(long long v, long long* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum_ll(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  long long t = lane < nw ? red[lane] : 0;
+  return warp_sum_ll(t);
+}
+
 __device__ __forceinline__ bool visited_bit(const uint32_t* visited, int64_t j) {
   return (__ldg(visited + (j >> 5)) >> (j & 31)) & 1u;
 }
 
 // Solves L x = b in place (x in shared memory, length n) with one CTA, using
-// the first n rows of the row-major lower factor L (ld = ldL).  32-row blocks:
-// warp 0 substitutes the diagonal block with shuffles, then every thread
-// applies the block to the trailing rows.  Per row the subtraction order is
-// ascending column index, like the reference's forward substitution.
-__device__ void cta_forward_solve(const double* L, int ldL, int n, double* x) {
+// the first n rows of the packed lower factor Lp (shared or global memory).
+// 32-row blocks: warp 0 holds the diagonal block in registers and substitutes
+// it with shuffles (no memory access on the serial chain); then every thread
+// applies the solved block to the trailing rows.  Per row the subtraction
+// order is ascending column index, like the reference's forward substitution.
+__device__ void cta_forward_solve(const double* Lp, int n, double* x) {
   for (int b0 = 0; b0 < n; b0 += 32) {
     const int b1 = min(b0 + 32, n);
     if (threadIdx.x < 32) {
       const int r = b0 + threadIdx.x;
+      double lr[32];
+      const double* Lr = Lp + packed(r);
+#pragma unroll
+      for (int k = 0; k < 32; ++k) lr[k] = (r < b1 && b0 + k <= r) ? Lr[b0 + k] : 0.0;
+      // the division leaves the serial chain: each lane inverts its own pivot
+      // up front and the chain multiplies (<= 1 ulp from x / L_ii)
+      const double rinv = r < b1 ? __drcp_rn(Lr[r]) : 0.0;
       double xr = r < b1 ? x[r] : 0.0;
-      for (int i = b0; i < b1; ++i) {
-        if (r == i) xr = __ddiv_rn(xr, L[(int64_t)i * ldL + i]);
-        const double xi = __shfl_sync(0xffffffffu, xr, i - b0);
-        if (r > i && r < b1) xr = __dadd_rn(xr, -__dmul_rn(L[(int64_t)r * ldL + i], xi));
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        if (b0 + k < b1) {
+          if (threadIdx.x == k) xr = __dmul_rn(xr, rinv);
+          const double xi = __shfl_sync(0xffffffffu, xr, k);
+          if (threadIdx.x > k) xr = __dadd_rn(xr, -__dmul_rn(lr[k], xi));
+        }
       }
       if (r < b1) x[r] = xr;
     }
     __syncthreads();
     for (int r = b1 + threadIdx.x; r < n; r += blockDim.x) {
       double s = x[r];
-      const double* Lr = L + (int64_t)r * ldL;
+      const double* Lr = Lp + packed(r);
       for (int i = b0; i < b1; ++i) s = __dadd_rn(s, -__dmul_rn(Lr[i], x[i]));
       x[r] = s;
     }
@@ -108,33 +140,33 @@ __device__ void cta_forward_solve(const double* L, int ldL, int n, double* x) {
 }
 
 // Standardisation + beta for the first n observations (gp.hpp:97-103,130).
-// Sequential sums in thread 0 (n <= n_max, tiny) keep them order-stable.
-__device__ void cta_stats_beta(const GpDev& g, int n) {
-  __shared__ double s_mean, s_std;
+// Deterministic block-tree sums (fixed order for a given n).
+__device__ void cta_stats_beta(const GpDev& g, int n, double* red) {
+  __shared__ double s_y0;
+  double part = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) part = __dadd_rn(part, g.y[i]);
+  const double sum = block_sum(part, red);
+  const double mean = n > 0 ? __ddiv_rn(sum, (double)n) : 0.0;
+  part = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double dv = __dadd_rn(g.y[i], -mean);
+    part = __dadd_rn(part, __dmul_rn(dv, dv));
+  }
+  const double ss = block_sum(part, red);
+  double stdv = 1.0;
+  if (n > 1) {
+    const double var = __ddiv_rn(ss, (double)n);
+    stdv = var > 0.0 ? sqrt(var) : 1.0;
+  }
   if (threadIdx.x == 0) {
-    double mean = 0.0, stdv = 1.0;
-    if (n > 0) {
-      double sum = 0.0;
-      for (int i = 0; i < n; ++i) sum = __dadd_rn(sum, g.y[i]);
-      mean = __ddiv_rn(sum, (double)n);
-      if (n > 1) {
-        double ss = 0.0;
-        for (int i = 0; i < n; ++i) {
-          const double dv = __dadd_rn(g.y[i], -mean);
-          ss = __dadd_rn(ss, __dmul_rn(dv, dv));
-        }
-        const double var = __ddiv_rn(ss, (double)n);
-        stdv = var > 0.0 ? sqrt(var) : 1.0;
-      }
-    }
-    s_mean = mean;
-    s_std = stdv;
+    s_y0 = g.sc->y0;
     g.sc->y_mean = mean;
     g.sc->y_std = stdv;
     g.sc->n = n;
   }
   __syncthreads();
-  const double shift = __dadd_rn(s_mean, -g.sc->y0);
+  const double s_mean = mean, s_std = stdv;
+  const double shift = __dadd_rn(s_mean, -s_y0);
   for (int i = threadIdx.x; i < n; i += blockDim.x)
     g.beta[i] = __ddiv_rn(__dadd_rn(g.c[i], -__dmul_rn(shift, g.e[i])), s_std);
   __syncthreads();
@@ -151,19 +183,39 @@ __device__ double direct_kernel(const double* xa, const double* xb, int d, doubl
   return matern<NU>(sqrt(ss), l, s2);
 }
 
+// Shared-memory layout of the single-CTA GP kernels:
+//   xs  work vector (n_max)
+//   ys  y copy      (n_max)
+//   Ls  packed L rows (when they fit, else L is read from global memory)
+struct CtaSmem {
+  double* Ls;
+  double* xs;
+  double* ys;
+  bool staged;
+};
+
+__device__ CtaSmem cta_smem_layout(double* base, int n_max, bool staged) {
+  CtaSmem m;
+  m.staged = staged;
+  m.xs = base;
+  m.ys = base + n_max;
+  m.Ls = base + 2 * (int64_t)n_max;
+  return m;
+}
+
 // Appends training point `row` (coords already in g.train_x[row]) to the
 // factor: l = L^-1 g, pivot = k(0) + noise + jitter - |l|^2 (gp.hpp:105-121).
 // Returns false (and records the failure) when the pivot is <= 0.
 template <int NU>
-__device__ bool cta_border_row(const GpDev& g, KernelParams k, double noise, double jitter,
-                               int row, double* xs, double* red) {
+__device__ bool cta_border_row(const GpDev& g, KernelParams k, double noise, double jitter, int row,
+                               const CtaSmem& m, double* red) {
   const double* xr = g.train_x + (int64_t)row * g.d;
-  for (int m = threadIdx.x; m < row; m += blockDim.x)
-    xs[m] = direct_kernel<NU>(g.train_x + (int64_t)m * g.d, xr, g.d, k.lengthscale, k.s2);
+  for (int q = threadIdx.x; q < row; q += blockDim.x)
+    m.xs[q] = direct_kernel<NU>(g.train_x + (int64_t)q * g.d, xr, g.d, k.lengthscale, k.s2);
   __syncthreads();
-  cta_forward_solve(g.L, g.n_max, row, xs);
+  cta_forward_solve(m.staged ? m.Ls : g.L, row, m.xs);
   double part = 0.0;
-  for (int m = threadIdx.x; m < row; m += blockDim.x) part = __dadd_rn(part, __dmul_rn(xs[m], xs[m]));
+  for (int q = threadIdx.x; q < row; q += blockDim.x) part = __dadd_rn(part, __dmul_rn(m.xs[q], m.xs[q]));
   const double sumsq = block_sum(part, red);
   const double diag = __dadd_rn(matern<NU>(0.0, k.lengthscale, k.s2), __dadd_rn(noise, jitter));
   const double x = __dadd_rn(diag, -sumsq);
@@ -175,20 +227,27 @@ __device__ bool cta_border_row(const GpDev& g, KernelParams k, double noise, dou
     __syncthreads();
     return false;
   }
-  double* Lrow = g.L + (int64_t)row * g.n_max;
-  for (int m = threadIdx.x; m < row; m += blockDim.x) Lrow[m] = xs[m];
-  if (threadIdx.x == 0) Lrow[row] = sqrt(x);
+  double* Lrow = g.L + packed(row);
+  const double lnn = sqrt(x);
+  for (int q = threadIdx.x; q < row; q += blockDim.x) {
+    Lrow[q] = m.xs[q];
+    if (m.staged) m.Ls[packed(row) + q] = m.xs[q];
+  }
+  if (threadIdx.x == 0) {
+    Lrow[row] = lnn;
+    if (m.staged) m.Ls[packed(row) + row] = lnn;
+  }
   __syncthreads();
   return true;
 }
 
 // c[row], e[row] from the new L row (prefix-stable forward substitution).
-__device__ void cta_ce_row(const GpDev& g, int row, double* red) {
-  const double* Lrow = g.L + (int64_t)row * g.n_max;
+__device__ void cta_ce_row(const GpDev& g, int row, const CtaSmem& m, double* red) {
+  const double* Lrow = (m.staged ? m.Ls : g.L) + packed(row);
   double pc = 0.0, pe = 0.0;
-  for (int m = threadIdx.x; m < row; m += blockDim.x) {
-    pc = __dadd_rn(pc, __dmul_rn(Lrow[m], g.c[m]));
-    pe = __dadd_rn(pe, __dmul_rn(Lrow[m], g.e[m]));
+  for (int q = threadIdx.x; q < row; q += blockDim.x) {
+    pc = __dadd_rn(pc, __dmul_rn(Lrow[q], g.c[q]));
+    pe = __dadd_rn(pe, __dmul_rn(Lrow[q], g.e[q]));
   }
   const double sc = block_sum(pc, red);
   const double se = block_sum(pe, red);
@@ -200,13 +259,58 @@ __device__ void cta_ce_row(const GpDev& g, int row, double* red) {
   __syncthreads();
 }
 
+// Rows [0, rows) of the packed factor into shared memory with TMA bulk copies
+// (cp.async.bulk global->shared, completion on an mbarrier): the factor is
+// evicted from L2 by every V stream, and one SM pulling 194 KB with scalar
+// loads is latency-bound; the bulk engine streams it at full rate.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ void cta_stage_L(const GpDev& g, int rows, const CtaSmem& m) {
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t total = packed(rows);
+  // bulk copies need 16-byte multiples: round up (the allocation is padded)
+  const uint32_t bytes = static_cast<uint32_t>(((total * 8) + 15) & ~int64_t(15));
+  if (!m.staged || bytes == 0) {
+    __syncthreads();
+    return;
+  }
+  const uint32_t b = smem_u32(&bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    constexpr uint32_t kChunk = 32768;
+    const char* src = reinterpret_cast<const char*>(g.L);
+    const uint32_t dst = smem_u32(m.Ls);
+    for (uint32_t off = 0; off < bytes; off += kChunk) {
+      const uint32_t sz = bytes - off < kChunk ? bytes - off : kChunk;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + off),
+          "l"(src + off), "r"(sz), "r"(b)
+          : "memory");
+    }
+  }
+  __syncthreads();  // barrier initialised before anyone waits on it
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(b)
+      : "memory");
+}
+
 // ------------------------------------------------------------ GP kernels
 
 template <int NU>
-__global__ void __launch_bounds__(kCtaThreads) k_gp_factor(GpDev g, KernelParams k, double noise,
-                                                           double jitter, int n) {
-  extern __shared__ double xs[];
+__global__ void __launch_bounds__(kCtaThreads)
+    k_gp_factor(GpDev g, KernelParams k, double noise, double jitter, int n, int staged) {
+  extern __shared__ double smem[];
   __shared__ double red[32];
+  const CtaSmem m = cta_smem_layout(smem, g.n_max, staged != 0);
   if (threadIdx.x == 0) {
     g.sc->status = 0;
     g.sc->fail_row = -1;
@@ -223,22 +327,24 @@ __global__ void __launch_bounds__(kCtaThreads) k_gp_factor(GpDev g, KernelParams
   }
   __syncthreads();
   for (int row = 0; row < n; ++row) {
-    if (!cta_border_row<NU>(g, k, noise, jitter, row, xs, red)) {
+    if (!cta_border_row<NU>(g, k, noise, jitter, row, m, red)) {
       if (threadIdx.x == 0) g.sc->n = 0;
       return;
     }
   }
-  for (int row = 0; row < n; ++row) cta_ce_row(g, row, red);
-  cta_stats_beta(g, n);
+  for (int row = 0; row < n; ++row) cta_ce_row(g, row, m, red);
+  cta_stats_beta(g, n, red);
 }
 
 template <int NU>
 __global__ void __launch_bounds__(kCtaThreads)
     k_gp_append(GpDev g, KernelParams k, double noise, SpaceDev sp, int64_t pos,
-                const double* x_explicit, double y_new, int n0) {
-  extern __shared__ double xs[];
+                const double* x_explicit, double y_new, int n0, uint32_t* visited_mark, int staged) {
+  extern __shared__ double smem[];
   __shared__ double red[32];
   __shared__ double xnew[64];
+  const CtaSmem m = cta_smem_layout(smem, g.n_max, staged != 0);
+  if (visited_mark && threadIdx.x == 0) visited_mark[pos >> 5] |= 1u << (pos & 31);
   for (int t = threadIdx.x; t < g.d; t += blockDim.x) {
     const double v = pos >= 0 ? sp.coords[(int64_t)t * sp.n_pad + pos] : x_explicit[t];
     xnew[t] = v;
@@ -250,19 +356,22 @@ __global__ void __launch_bounds__(kCtaThreads)
     g.sc->fail_row = -1;
     if (n0 == 0) g.sc->y0 = y_new;
   }
-  __syncthreads();
+  cta_stage_L(g, n0, m);  // includes __syncthreads
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int t = 0; t < g.d; ++t) s = __dadd_rn(s, __dmul_rn(xnew[t], xnew[t]));
     g.train_n2[n0] = s;
   }
   const double jitter = g.sc->jitter;
-  if (!cta_border_row<NU>(g, k, noise, jitter, n0, xs, red)) return;
-  cta_ce_row(g, n0, red);
-  cta_stats_beta(g, n0 + 1);
+  if (!cta_border_row<NU>(g, k, noise, jitter, n0, m, red)) return;
+  cta_ce_row(g, n0, m, red);
+  cta_stats_beta(g, n0 + 1, red);
 }
 
-__global__ void k_gp_truncate(GpDev g, int n) { cta_stats_beta(g, n); }
+__global__ void k_gp_truncate(GpDev g, int n) {
+  __shared__ double red[32];
+  cta_stats_beta(g, n, red);
+}
 
 // ------------------------------------------------------------ V extension
 
@@ -275,6 +384,9 @@ struct ExtendArgs {
   double lengthscale, s2;
   double* mu;
   double* var;
+  const uint32_t* visited;  // with part_sum: per-tile variance partials (final pass)
+  double* part_sum;
+  long long* part_cnt;
 };
 
 // Rows [n0, n0+r) of V for every candidate, r <= R, streaming rows [0, n0)
@@ -286,16 +398,16 @@ __global__ void __launch_bounds__(kExtendThreads) k_extend(ExtendArgs a) {
   extern __shared__ double sm[];
   const int n0 = a.n0, r = a.r;
   const int ld = n0 + R;
-  double* Ls = sm;             // [R][ld] coefficients of the new rows
-  double* bs = sm + R * ld;    // [n0 + r] beta
-  double* xn = bs + ld;        // [R][d] new training coords
-  double* xn2 = xn + R * a.g.d;// [R] their squared norms
+  double* Ls = sm;              // [R][ld] coefficients of the new rows
+  double* bs = sm + R * ld;     // [n0 + r] beta
+  double* xn = bs + ld;         // [R][d] new training coords
+  double* xn2 = xn + R * a.g.d; // [R] their squared norms
   for (int idx = threadIdx.x; idx < r * (n0 + r); idx += blockDim.x) {
-    const int t = idx / (n0 + r), m = idx % (n0 + r);
-    Ls[t * ld + m] = a.g.L[(int64_t)(n0 + t) * a.g.n_max + m];
+    const int t = idx / (n0 + r), q = idx % (n0 + r);
+    Ls[t * ld + q] = q <= n0 + t ? a.g.L[packed(n0 + t) + q] : 0.0;
   }
   if (a.final_pass)
-    for (int m = threadIdx.x; m < n0 + r; m += blockDim.x) bs[m] = a.g.beta[m];
+    for (int q = threadIdx.x; q < n0 + r; q += blockDim.x) bs[q] = a.g.beta[q];
   for (int idx = threadIdx.x; idx < r * a.g.d; idx += blockDim.x)
     xn[idx] = a.g.train_x[(int64_t)n0 * a.g.d + idx];
   for (int t = threadIdx.x; t < r; t += blockDim.x) xn2[t] = a.g.train_n2[n0 + t];
@@ -406,9 +518,25 @@ __global__ void __launch_bounds__(kExtendThreads) k_extend(ExtendArgs a) {
   }
   if (a.final_pass) {
     // mean = k*^T alpha = v^T beta;  var = max(s2 - sum v^2, 0)   (gp.hpp:162-166)
+    const double var0 = fmax(__dadd_rn(a.s2, -q0), 0.0), var1 = fmax(__dadd_rn(a.s2, -q1), 0.0);
     *reinterpret_cast<double2*>(a.mu + j0) = make_double2(b0, b1);
-    *reinterpret_cast<double2*>(a.var + j0) =
-        make_double2(fmax(__dadd_rn(a.s2, -q0), 0.0), fmax(__dadd_rn(a.s2, -q1), 0.0));
+    *reinterpret_cast<double2*>(a.var + j0) = make_double2(var0, var1);
+    if (a.part_sum) {
+      // this tile's share of the mean posterior variance over the unvisited
+      // candidates (strategies.hpp:406-407); plain stores, consumed by the
+      // next kernel on the stream (k_select), so no fence is needed
+      __shared__ double red[32];
+      __shared__ long long redl[32];
+      const uint32_t w = j0 < a.sp.n ? __ldg(a.visited + (j0 >> 5)) : 0xffffffffu;
+      const bool u0 = j0 < a.sp.n && !((w >> (j0 & 31)) & 1u);
+      const bool u1 = j0 + 1 < a.sp.n && !((w >> ((j0 + 1) & 31)) & 1u);
+      const double ts = block_sum((u0 ? var0 : 0.0) + (u1 ? var1 : 0.0), red);
+      const long long tc = block_sum_ll((long long)u0 + (long long)u1, redl);
+      if (threadIdx.x == 0) {
+        a.part_sum[blockIdx.x] = ts;
+        a.part_cnt[blockIdx.x] = tc;
+      }
+    }
   }
 }
 
@@ -429,6 +557,21 @@ __global__ void k_mark(uint32_t* visited, int64_t pos, int set) {
 
 // ------------------------------------------------------------ reductions
 
+// SM count of the current device (cached per device).
+static int sm_count() {
+  static std::mutex mu;
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  int& c = cached[dev & 63];
+  if (c == 0) {
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    if (c <= 0) c = 148;
+  }
+  return c;
+}
+
 int reduce_blocks(int64_t n) {
   const int64_t per_block = (int64_t)kReduceThreads * 8;
   int64_t b = (n + per_block - 1) / per_block;
@@ -447,15 +590,12 @@ __device__ bool last_block(unsigned int* counter) {
   return is_last;
 }
 
-__global__ void __launch_bounds__(kReduceThreads)
-    k_varsum(const double* __restrict__ var, const uint32_t* __restrict__ visited, int64_t n,
-             double* partial_sum, int64_t* partial_cnt, unsigned int* counter, VarTotals* totals) {
-  __shared__ double red[32];
-  __shared__ unsigned long long cnt_s;
-  if (threadIdx.x == 0) cnt_s = 0;
-  __syncthreads();
+// Per-block partial of the variance sum over unvisited candidates (strided,
+// fixed order), returned by every thread.
+__device__ void var_partial(const double* __restrict__ var, const uint32_t* __restrict__ visited,
+                            int64_t n, double* red, long long* redl, double* out_sum, long long* out_cnt) {
   double s = 0.0;
-  unsigned long long c = 0;
+  long long c = 0;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x) {
     if (!visited_bit(visited, j)) {
@@ -463,29 +603,40 @@ __global__ void __launch_bounds__(kReduceThreads)
       ++c;
     }
   }
-  s = block_sum(s, red);
-  atomicAdd(&cnt_s, c);
-  __syncthreads();
+  *out_sum = block_sum(s, red);
+  *out_cnt = block_sum_ll(c, redl);
+}
+
+// Deterministic fixed-order sum of `count` block partials, in every block.
+__device__ void reduce_partials(const double* ps, const long long* pc, int count, double* red,
+                                long long* redl, double* sum, long long* cnt) {
+  double s = 0.0;
+  long long c = 0;
+  for (int b = threadIdx.x; b < count; b += blockDim.x) {
+    s += __ldcg(ps + b);
+    c += __ldcg(pc + b);
+  }
+  *sum = block_sum(s, red);
+  *cnt = block_sum_ll(c, redl);
+}
+
+__global__ void __launch_bounds__(kReduceThreads)
+    k_varsum(const double* __restrict__ var, const uint32_t* __restrict__ visited, int64_t n,
+             double* partial_sum, int64_t* partial_cnt, unsigned int* counter, VarTotals* totals) {
+  __shared__ double red[32];
+  __shared__ long long redl[32];
+  double s;
+  long long c;
+  var_partial(var, visited, n, red, redl, &s, &c);
   if (threadIdx.x == 0) {
     partial_sum[blockIdx.x] = s;
-    partial_cnt[blockIdx.x] = (int64_t)cnt_s;
+    partial_cnt[blockIdx.x] = c;
   }
   if (!last_block(counter)) return;
-  double ts = 0.0;
-  int64_t tc = 0;
-  for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
-    ts += __ldcg(partial_sum + b);
-    tc += __ldcg(reinterpret_cast<const long long*>(partial_cnt) + b);
-  }
-  ts = block_sum(ts, red);
-  __shared__ unsigned long long tc_s;
-  if (threadIdx.x == 0) tc_s = 0;
-  __syncthreads();
-  atomicAdd(&tc_s, (unsigned long long)tc);
-  __syncthreads();
+  reduce_partials(partial_sum, reinterpret_cast<const long long*>(partial_cnt), gridDim.x, red, redl, &s, &c);
   if (threadIdx.x == 0) {
-    totals->sum = ts;
-    totals->count = (int64_t)tc_s;
+    totals->sum = s;
+    totals->count = c;
     *counter = 0;
   }
 }
@@ -575,12 +726,7 @@ struct SelCtx {
   int n_excluded;
   int64_t n;
   uint32_t af_mask;
-  // partials
-  double* partial_score;
-  int64_t* partial_pos;
-  int64_t* partial_first;
-  int64_t* partial_cnt;
-  unsigned int* counter;
+  ReduceBufs b;
   SelectDev* out;
 };
 
@@ -596,67 +742,56 @@ __device__ __forceinline__ double sd_at(const SelCtx& c, int64_t j) {
   return c.sdv ? c.sdv[j] : sqrt(c.var[j]);  // cand_stds = sqrt(cand_vars), strategies.hpp:385
 }
 
-// Shared body of the selection: every block scans a strided slice, the last
-// block merges.  lambda/best_std are provided by the caller (computed in the
-// kernel prologue for the run path).
-__device__ void select_body(const SelCtx& c, double best, double lambda, double mean_var,
-                            int cv_fallback, int gp_status) {
+template <uint32_t MASK>
+__device__ __forceinline__ void score_into(Best* b, double m, double sd, double best, double lambda, int64_t j) {
+#pragma unroll
+  for (int af = 0; af < 3; ++af) {
+    if (!(MASK & (1u << af))) continue;
+    const double s = score_of(af, m, sd, best, lambda);
+    if (s == s) b[af] = better(b[af], Best{s, j});
+  }
+}
+
+// Block reduction of the per-thread (best per AF, first eligible, count)
+// followed by the last-block merge into the result record.
+template <uint32_t MASK>
+__device__ void select_finish(const SelCtx& c, Best* b, int64_t first, long long cnt, double best,
+                              double lambda, double mean_var, int cv_fallback, int gp_status) {
   __shared__ Best redb[32];
   __shared__ int64_t redi[32];
-  __shared__ unsigned long long cnt_s;
-  if (threadIdx.x == 0) cnt_s = 0;
-  __syncthreads();
-  Best b[3] = {{0.0, INT64_MAX}, {0.0, INT64_MAX}, {0.0, INT64_MAX}};
-  int64_t first = INT64_MAX;
-  unsigned long long cnt = 0;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < c.n;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    if (!eligible(c, j)) continue;
-    ++cnt;
-    first = min(first, j);
-    const double m = c.mu[j], sd = sd_at(c, j);
+  __shared__ long long redl[32];
+  cnt = block_sum_ll(cnt, redl);
 #pragma unroll
-    for (int af = 0; af < 3; ++af) {
-      if (!(c.af_mask & (1u << af))) continue;
-      const double s = score_of(af, m, sd, best, lambda);
-      if (s == s) b[af] = better(b[af], Best{s, j});
-    }
-  }
-  atomicAdd(&cnt_s, cnt);
-  for (int af = 0; af < 3; ++af) b[af] = block_best(b[af], redb);
+  for (int af = 0; af < 3; ++af)
+    if (MASK & (1u << af)) b[af] = block_best(b[af], redb);
   first = block_min(first, redi);
-  __syncthreads();
   if (threadIdx.x == 0) {
     for (int af = 0; af < 3; ++af) {
-      c.partial_score[blockIdx.x * 3 + af] = b[af].s;
-      c.partial_pos[blockIdx.x * 3 + af] = b[af].p;
+      c.b.pscore[blockIdx.x * 3 + af] = b[af].s;
+      c.b.ppos[blockIdx.x * 3 + af] = b[af].p;
     }
-    c.partial_first[blockIdx.x] = first;
-    c.partial_cnt[blockIdx.x] = (int64_t)cnt_s;
+    c.b.pfirst[blockIdx.x] = first;
+    c.b.pcnt[blockIdx.x] = cnt;
   }
-  if (!last_block(c.counter)) return;
+  if (!last_block(c.b.counter)) return;
   Best f[3] = {{0.0, INT64_MAX}, {0.0, INT64_MAX}, {0.0, INT64_MAX}};
   int64_t ff = INT64_MAX;
-  unsigned long long fc = 0;
+  long long fc = 0;
   for (int blk = threadIdx.x; blk < gridDim.x; blk += blockDim.x) {
     for (int af = 0; af < 3; ++af)
-      f[af] = better(f[af], Best{__ldcg(c.partial_score + blk * 3 + af),
-                                 (int64_t)__ldcg(reinterpret_cast<const long long*>(c.partial_pos) + blk * 3 + af)});
-    ff = min(ff, (int64_t)__ldcg(reinterpret_cast<const long long*>(c.partial_first) + blk));
-    fc += (unsigned long long)__ldcg(reinterpret_cast<const long long*>(c.partial_cnt) + blk);
+      f[af] = better(f[af], Best{__ldcg(c.b.pscore + blk * 3 + af),
+                                 (int64_t)__ldcg(reinterpret_cast<const long long*>(c.b.ppos) + blk * 3 + af)});
+    ff = min(ff, (int64_t)__ldcg(reinterpret_cast<const long long*>(c.b.pfirst) + blk));
+    fc += __ldcg(c.b.pcnt + blk);
   }
   for (int af = 0; af < 3; ++af) f[af] = block_best(f[af], redb);
   ff = block_min(ff, redi);
-  __shared__ unsigned long long fc_s;
-  if (threadIdx.x == 0) fc_s = 0;
-  __syncthreads();
-  atomicAdd(&fc_s, fc);
-  __syncthreads();
+  fc = block_sum_ll(fc, redl);
   if (threadIdx.x == 0) {
     for (int af = 0; af < 3; ++af) {
       int64_t pos = -1;
       double sc = 0.0;
-      if ((c.af_mask & (1u << af)) && fc_s > 0) {
+      if ((c.af_mask & (1u << af)) && fc > 0) {
         // first-candidate rule (portfolio.hpp:52): the first eligible
         // candidate is taken unconditionally; if its score is NaN nothing
         // can beat it.
@@ -675,18 +810,63 @@ __device__ void select_body(const SelCtx& c, double best, double lambda, double 
     c.out->lambda = lambda;
     c.out->mean_variance = mean_var;
     c.out->best_std = best;
-    c.out->n_candidates = (int64_t)fc_s;
+    c.out->n_candidates = (int64_t)fc;
     c.out->cv_fallback = cv_fallback;
     c.out->gp_status = gp_status;
-    *c.counter = 0;
+    *c.b.counter = 0;
   }
 }
 
-__global__ void __launch_bounds__(kReduceThreads)
-    k_select(SelCtx c, const VarTotals* totals, const GpScalars* sc, SelectParams p) {
-  // lambda (strategies.hpp:404-418, acquisition.hpp:73-83) and best_std
-  // (gp.hpp:145), computed identically by every block.
-  const double mean_var = totals->count > 0 ? __ddiv_rn(totals->sum, (double)totals->count) : 0.0;
+// Scan of a strided slice (two candidates per iteration for ILP) used by the
+// span-based best_candidate path.
+template <uint32_t MASK>
+__device__ void select_body(const SelCtx& c, double best, double lambda, double mean_var,
+                            int cv_fallback, int gp_status) {
+  Best b[3] = {{0.0, INT64_MAX}, {0.0, INT64_MAX}, {0.0, INT64_MAX}};
+  int64_t first = INT64_MAX;
+  long long cnt = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; j + stride < c.n; j += 2 * stride) {
+    const int64_t j2 = j + stride;
+    const bool e1 = eligible(c, j), e2 = eligible(c, j2);
+    const double m1 = c.mu[j], m2 = c.mu[j2];
+    const double s1 = sd_at(c, j), s2 = sd_at(c, j2);
+    if (e1) {
+      ++cnt;
+      first = min(first, j);
+      score_into<MASK>(b, m1, s1, best, lambda, j);
+    }
+    if (e2) {
+      ++cnt;
+      first = min(first, j2);
+      score_into<MASK>(b, m2, s2, best, lambda, j2);
+    }
+  }
+  if (j < c.n && eligible(c, j)) {
+    ++cnt;
+    first = min(first, j);
+    score_into<MASK>(b, c.mu[j], sd_at(c, j), best, lambda, j);
+  }
+  select_finish<MASK>(c, b, first, cnt, best, lambda, mean_var, cv_fallback, gp_status);
+}
+
+// Selection for a resident run.  The mean posterior variance over the
+// unvisited candidates comes from the per-tile partials the predictive pass
+// (or k_var_partials) left behind: every block reduces the same `n_partials`
+// values in the same fixed order, so all blocks agree on lambda
+// (strategies.hpp:404-418, acquisition.hpp:73-83) and best_std (gp.hpp:145)
+// without a grid barrier; then the masked argmax as in select_body.
+template <uint32_t MASK>
+__global__ void __launch_bounds__(kReduceThreads, kSelectBlocksPerSM)
+    k_select(SelCtx c, const GpScalars* sc, SelectParams p, const double* part_sum,
+             const long long* part_cnt, int n_partials) {
+  __shared__ double red[32];
+  __shared__ long long redl[32];
+  double s;
+  long long cnt;
+  reduce_partials(part_sum, part_cnt, n_partials, red, redl, &s, &cnt);
+  const double mean_var = cnt > 0 ? __ddiv_rn(s, (double)cnt) : 0.0;
   double lambda = p.lambda_constant;
   int fallback = 0;
   if (p.lambda_mode == 1) {
@@ -698,12 +878,28 @@ __global__ void __launch_bounds__(kReduceThreads)
     }
   }
   const double best = __ddiv_rn(__dadd_rn(p.f_best_raw, -sc->y_mean), sc->y_std);
-  select_body(c, best, lambda, mean_var, fallback, sc->status);
+  select_body<MASK>(c, best, lambda, mean_var, fallback, sc->status);
 }
 
+// Variance partials over the unvisited candidates when the pass did not
+// produce them for the current visited set (invalid observation, unmark).
 __global__ void __launch_bounds__(kReduceThreads)
-    k_best_candidate(SelCtx c, double best, double lambda) {
-  select_body(c, best, lambda, 0.0, 0, 0);
+    k_var_partials(const double* __restrict__ var, const uint32_t* __restrict__ visited, int64_t n,
+                   double* part_sum, long long* part_cnt) {
+  __shared__ double red[32];
+  __shared__ long long redl[32];
+  double s;
+  long long c;
+  var_partial(var, visited, n, red, redl, &s, &c);
+  if (threadIdx.x == 0) {
+    part_sum[blockIdx.x] = s;
+    part_cnt[blockIdx.x] = c;
+  }
+}
+
+template <uint32_t MASK>
+__global__ void __launch_bounds__(kReduceThreads) k_best_candidate(SelCtx c, double best, double lambda) {
+  select_body<MASK>(c, best, lambda, 0.0, 0, 0);
 }
 
 __global__ void k_scores(const double* __restrict__ mu, const double* __restrict__ sd, int64_t n,
@@ -715,27 +911,44 @@ __global__ void k_scores(const double* __restrict__ mu, const double* __restrict
 
 // ------------------------------------------------------------ launchers
 
-static size_t cta_smem(int n_max) { return sizeof(double) * (size_t)(n_max + 8); }
+// Shared memory of the single-CTA GP kernels: xs + ys (+ packed L rows when
+// they fit under the opt-in limit).
+static size_t cta_smem_bytes(int n_max, int rows, bool* staged) {
+  const size_t base = sizeof(double) * (size_t)(2 * n_max);
+  const size_t with_l = base + sizeof(double) * (size_t)(packed(rows) + 2);  // +2: 16-byte bulk-copy rounding
+  *staged = with_l <= kCtaSmemLimit;
+  return *staged ? with_l : base;
+}
+
+template <class K>
+static void opt_in_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
 
 void launch_gp_factor(const GpDev& g, KernelParams k, double noise, double jitter, int n,
                       cudaStream_t s) {
   count_launch();
-  const size_t sm = cta_smem(g.n_max);
+  bool staged;
+  const size_t sm = cta_smem_bytes(g.n_max, n, &staged);
+  const int st = staged ? 1 : 0;
   switch (k.nu) {
-    case 0: k_gp_factor<0><<<1, kCtaThreads, sm, s>>>(g, k, noise, jitter, n); break;
-    case 1: k_gp_factor<1><<<1, kCtaThreads, sm, s>>>(g, k, noise, jitter, n); break;
-    default: k_gp_factor<2><<<1, kCtaThreads, sm, s>>>(g, k, noise, jitter, n); break;
+    case 0: opt_in_smem(k_gp_factor<0>, sm); k_gp_factor<0><<<1, kCtaThreads, sm, s>>>(g, k, noise, jitter, n, st); break;
+    case 1: opt_in_smem(k_gp_factor<1>, sm); k_gp_factor<1><<<1, kCtaThreads, sm, s>>>(g, k, noise, jitter, n, st); break;
+    default: opt_in_smem(k_gp_factor<2>, sm); k_gp_factor<2><<<1, kCtaThreads, sm, s>>>(g, k, noise, jitter, n, st); break;
   }
 }
 
 void launch_gp_append(const GpDev& g, KernelParams k, double noise, const SpaceDev& sp,
-                      int64_t pos, const double* x_explicit, double y_new, int n0, cudaStream_t s) {
+                      int64_t pos, const double* x_explicit, double y_new, int n0,
+                      uint32_t* visited_mark, cudaStream_t s) {
   count_launch();
-  const size_t sm = cta_smem(g.n_max);
+  bool staged;
+  const size_t sm = cta_smem_bytes(g.n_max, n0 + 1, &staged);
+  const int st = staged ? 1 : 0;
   switch (k.nu) {
-    case 0: k_gp_append<0><<<1, kCtaThreads, sm, s>>>(g, k, noise, sp, pos, x_explicit, y_new, n0); break;
-    case 1: k_gp_append<1><<<1, kCtaThreads, sm, s>>>(g, k, noise, sp, pos, x_explicit, y_new, n0); break;
-    default: k_gp_append<2><<<1, kCtaThreads, sm, s>>>(g, k, noise, sp, pos, x_explicit, y_new, n0); break;
+    case 0: opt_in_smem(k_gp_append<0>, sm); k_gp_append<0><<<1, kCtaThreads, sm, s>>>(g, k, noise, sp, pos, x_explicit, y_new, n0, visited_mark, st); break;
+    case 1: opt_in_smem(k_gp_append<1>, sm); k_gp_append<1><<<1, kCtaThreads, sm, s>>>(g, k, noise, sp, pos, x_explicit, y_new, n0, visited_mark, st); break;
+    default: opt_in_smem(k_gp_append<2>, sm); k_gp_append<2><<<1, kCtaThreads, sm, s>>>(g, k, noise, sp, pos, x_explicit, y_new, n0, visited_mark, st); break;
   }
 }
 
@@ -747,19 +960,19 @@ void launch_gp_truncate(const GpDev& g, int n, cudaStream_t s) {
 template <int R, int NU>
 static void extend_impl(const ExtendArgs& a, int64_t tiles, cudaStream_t s) {
   const size_t sm = sizeof(double) * ((size_t)(R + 1) * (a.n0 + R) + (size_t)R * a.g.d + R + 8);
-  if (sm > 48 * 1024)  // rebuild passes at large n; set per call (per device context)
-    cudaFuncSetAttribute(k_extend<R, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  opt_in_smem(k_extend<R, NU>, sm);
   k_extend<R, NU><<<(unsigned)tiles, kExtendThreads, sm, s>>>(a);
 }
 
 void launch_extend(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V,
                    int64_t tile_stride, int n0, int r, bool final, double* mu, double* var,
-                   bool check_status, cudaStream_t s) {
+                   bool check_status, const VarPartials* vp, cudaStream_t s) {
   count_launch();
   ExtendArgs a{sp, g, V, tile_stride, n0, r, final ? 1 : 0, check_status ? 1 : 0,
-               k.lengthscale, k.s2, mu, var};
+               k.lengthscale, k.s2, mu, var, vp ? vp->visited : nullptr,
+               (vp && final) ? vp->part_sum : nullptr, vp ? vp->part_cnt : nullptr};
   const int64_t tiles = sp.n_pad / kTile;
-  if (r == 1) {
+  if (r <= 1) {
     switch (k.nu) {
       case 0: extend_impl<1, 0>(a, tiles, s); break;
       case 1: extend_impl<1, 1>(a, tiles, s); break;
@@ -767,9 +980,9 @@ void launch_extend(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V
     }
   } else {
     switch (k.nu) {
-      case 0: extend_impl<8, 0>(a, tiles, s); break;
-      case 1: extend_impl<8, 1>(a, tiles, s); break;
-      default: extend_impl<8, 2>(a, tiles, s); break;
+      case 0: extend_impl<kMaxRows, 0>(a, tiles, s); break;
+      case 1: extend_impl<kMaxRows, 1>(a, tiles, s); break;
+      default: extend_impl<kMaxRows, 2>(a, tiles, s); break;
     }
   }
 }
@@ -790,24 +1003,45 @@ void launch_varsum(const double* var, const uint32_t* visited, int64_t n, double
   k_varsum<<<reduce_blocks(n), kReduceThreads, 0, s>>>(var, visited, n, ps, pc, counter, totals);
 }
 
-void launch_select(const double* mu, const double* var, const uint32_t* visited, int64_t n,
-                   const VarTotals* totals, const GpScalars* sc, SelectParams p,
-                   double* partial_score, int64_t* partial_pos, int64_t* partial_first,
-                   int64_t* partial_cnt, unsigned int* counter, SelectDev* out, cudaStream_t s) {
+void launch_var_partials(const double* var, const uint32_t* visited, int64_t n, double* part_sum,
+                         long long* part_cnt, cudaStream_t s) {
   count_launch();
-  SelCtx c{mu, var, nullptr, visited, nullptr, p.excluded, p.n_excluded, n, p.af_mask,
-           partial_score, partial_pos, partial_first, partial_cnt, counter, out};
-  k_select<<<reduce_blocks(n), kReduceThreads, 0, s>>>(c, totals, sc, p);
+  k_var_partials<<<reduce_blocks(n), kReduceThreads, 0, s>>>(var, visited, n, part_sum, part_cnt);
+}
+
+void launch_select(const double* mu, const double* var, const uint32_t* visited, int64_t n,
+                   const GpScalars* sc, SelectParams p, const double* part_sum, const long long* part_cnt,
+                   int n_partials, const ReduceBufs& b, SelectDev* out, cudaStream_t s) {
+  count_launch();
+  SelCtx c{mu, var, nullptr, visited, nullptr, p.excluded, p.n_excluded, n, p.af_mask, b, out};
+  // exactly one wave of resident blocks (grid-stride inside): a partial
+  // second wave would double the kernel's time
+  const int per_block = kReduceThreads * 2;
+  int grid = (int)std::min<int64_t>((n + per_block - 1) / per_block, (int64_t)sm_count() * kSelectBlocksPerSM);
+  grid = std::max(std::min(grid, kMaxReduceGrid), 1);
+#define GTC_SELECT_CASE(M) \
+  case M: k_select<M><<<grid, kReduceThreads, 0, s>>>(c, sc, p, part_sum, part_cnt, n_partials); break;
+  switch (p.af_mask & 7u) {  // launch errors surface through the caller's cudaGetLastError()
+    GTC_SELECT_CASE(1)
+    GTC_SELECT_CASE(2)
+    GTC_SELECT_CASE(3)
+    GTC_SELECT_CASE(4)
+    GTC_SELECT_CASE(5)
+    GTC_SELECT_CASE(6)
+    default: k_select<7><<<grid, kReduceThreads, 0, s>>>(c, sc, p, part_sum, part_cnt, n_partials); break;
+  }
+#undef GTC_SELECT_CASE
 }
 
 void launch_best_candidate(const double* mu, const double* sd, const uint8_t* excluded, int64_t n,
-                           int af, double best_std, double lambda, double* partial_score,
-                           int64_t* partial_pos, int64_t* partial_first, int64_t* partial_cnt,
-                           unsigned int* counter, SelectDev* out, cudaStream_t s) {
+                           int af, double best_std, double lambda, const ReduceBufs& b, SelectDev* out,
+                           cudaStream_t s) {
   count_launch();
-  SelCtx c{mu, nullptr, sd, nullptr, excluded, nullptr, 0, n, 1u << af,
-           partial_score, partial_pos, partial_first, partial_cnt, counter, out};
-  k_best_candidate<<<reduce_blocks(n), kReduceThreads, 0, s>>>(c, best_std, lambda);
+  SelCtx c{mu, nullptr, sd, nullptr, excluded, nullptr, 0, n, 1u << af, b, out};
+  const int grid = reduce_blocks(n);
+  if (af == 0) k_best_candidate<1><<<grid, kReduceThreads, 0, s>>>(c, best_std, lambda);
+  else if (af == 1) k_best_candidate<2><<<grid, kReduceThreads, 0, s>>>(c, best_std, lambda);
+  else k_best_candidate<4><<<grid, kReduceThreads, 0, s>>>(c, best_std, lambda);
 }
 
 void launch_scores(const double* mu, const double* sd, int64_t n, int af, double best_std,

@@ -142,25 +142,60 @@ class SurrogateRun:
         check(load().gtc_read_predictions(self._h, _lib.dptr(mean), _lib.dptr(var)))
         return mean, var
 
-    def select(self, afs: Sequence[AcquisitionId], f_best_raw: float,
-               exploration: ExplorationConfig = ExplorationConfig(),
-               cv_state: ContextualVarianceState = ContextualVarianceState(),
-               excluded: Optional[Sequence[int]] = None) -> Selection:
+    @staticmethod
+    def _args(afs, f_best_raw, exploration, cv_state, excluded):
         mask = 0
         for af in afs:
             mask |= 1 << int(af)
-        ex = None
         a = _lib.gtc_select_args(mask, int(exploration.mode), float(exploration.constant),
                                  float(cv_state.initial_sample_mean),
                                  float(cv_state.initial_mean_variance), float(f_best_raw), None, 0)
+        ex = None
         if excluded:
             ex = np.ascontiguousarray(np.asarray(excluded, dtype=np.int64))
             a.excluded = _lib.i64ptr(ex)
             a.n_excluded = len(ex)
-        r = _lib.gtc_select_result()
-        check(load().gtc_select(self._h, C.byref(a), C.byref(r)))
+        return a, ex
+
+    @staticmethod
+    def _selection(r) -> Selection:
         return Selection(tuple(r.position), tuple(r.score), r.lambda_, r.mean_variance, r.best_std,
                          int(r.n_candidates), bool(r.cv_fallback))
 
+    def select(self, afs: Sequence[AcquisitionId], f_best_raw: float,
+               exploration: ExplorationConfig = ExplorationConfig(),
+               cv_state: ContextualVarianceState = ContextualVarianceState(),
+               excluded: Optional[Sequence[int]] = None) -> Selection:
+        a, _keep = self._args(afs, f_best_raw, exploration, cv_state, excluded)
+        r = _lib.gtc_select_result()
+        check(load().gtc_select(self._h, C.byref(a), C.byref(r)))
+        return self._selection(r)
+
+    def observe(self, position: int, y_raw: Optional[float], afs: Sequence[AcquisitionId] = (),
+                f_best_raw: float = 0.0, exploration: ExplorationConfig = ExplorationConfig(),
+                cv_state: ContextualVarianceState = ContextualVarianceState(),
+                excluded: Optional[Sequence[int]] = None):
+        """gtc_observe: mark visited, append when y_raw is not None, then the
+        next selection (when afs is non-empty) with one host round trip.
+        Returns (FitInfo, Selection or None)."""
+        valid = y_raw is not None
+        r = _lib.gtc_select_result()
+        info = _lib.gtc_fit_info()
+        if afs:
+            a, _keep = self._args(afs, f_best_raw, exploration, cv_state, excluded)
+            check(load().gtc_observe(self._h, int(position), float(y_raw) if valid else 0.0, int(valid),
+                                     C.byref(a), C.byref(r), C.byref(info)))
+            return FitInfo.of(info), self._selection(r)
+        check(load().gtc_observe(self._h, int(position), float(y_raw) if valid else 0.0, int(valid), None,
+                                 C.byref(r), C.byref(info)))
+        return FitInfo.of(info), None
+
+    def truncate_async(self, n: int) -> None:
+        """Model back to its first n observations without a host round trip."""
+        check(load().gtc_truncate(self._h, int(n), None))
+
     def last_pass_ms(self) -> float:
         return float(load().gtc_last_pass_ms(self._h))
+
+    def last_step_ms(self) -> float:
+        return float(load().gtc_last_step_ms(self._h))

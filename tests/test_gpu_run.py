@@ -190,3 +190,32 @@ def test_c4_scale_append_vs_oracle_sample(gt, oracle):
     m2, v2 = oracle.predict(om, coords[sample])
     assert rel(mean[sample], m2) <= 1e-9
     assert rel(var[sample], v2) <= 1e-9
+
+
+def test_observe_equals_separate_calls(gt):
+    """gtc_observe (one round trip) == mark_visited + append + select, bitwise,
+    for valid and invalid observations."""
+    rng, coords, space, run_a = make_run(gt, N=30000, d=5, seed=21)
+    run_b = gt.SurrogateRun(space, run_a.kernel, n_max=64)
+    pos = rng.choice(len(coords), 40, replace=False)
+    y = 1.0 + rng.random(40)
+    for r in (run_a, run_b):
+        r.fit(pos[:20], y[:20])
+        for p in pos[:20]:
+            r.mark_visited(int(p))
+    cv = gt.ContextualVarianceState(float(np.mean(y[:20])), run_a.mean_variance())
+    afs = list(gt.AcquisitionId)
+    fb = float(np.min(y[:20]))
+    for k in range(20, 40):
+        valid = k % 3 != 0
+        fb = min(fb, float(y[k])) if valid else fb
+        info, sa = run_a.observe(int(pos[k]), float(y[k]) if valid else None, afs, fb, gt.ExplorationConfig(), cv)
+        run_b.mark_visited(int(pos[k]))
+        if valid:
+            run_b.append(int(pos[k]), float(y[k]))
+        sb = run_b.select(afs, fb, gt.ExplorationConfig(), cv)
+        assert sa.position == sb.position and sa.lambda_ == sb.lambda_ and sa.score == sb.score
+        assert sa.n_candidates == sb.n_candidates == run_a.unvisited_count()
+        ma, va = run_a.predictions()
+        mb, vb = run_b.predictions()
+        assert ma.tobytes() == mb.tobytes() and va.tobytes() == vb.tobytes()

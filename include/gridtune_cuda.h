@@ -174,6 +174,10 @@ double gtc_last_pass_ms(const gtc_run* run);
 /* CUDA-event milliseconds of the last gtc_observe's device work (all of its
  * kernels, first launch to last, excluding the result readback). */
 double gtc_last_step_ms(const gtc_run* run);
+/* Diagnostics: %globaltimer phase marks (ns) of the last bordered-row update
+ * seen by gtc_observe: [0] start, [1] factor staged, [2] Gram row, [3] forward
+ * solve, [4] pivot/row written, [5] c/e rows, [6] statistics + beta. */
+int gtc_debug_append_marks(const gtc_run* run, uint64_t* marks7);
 /* The CUDA stream the run launches on (as an opaque integer, for NCCL). */
 uint64_t gtc_run_stream(const gtc_run* run);
 

@@ -717,6 +717,12 @@ extern "C" double gtc_last_pass_ms(const gtc_run* r) {
 extern "C" double gtc_last_step_ms(const gtc_run* r) {
   return r && r->step_timed ? event_ms(r->ev_step0, r->ev_step1) : 0.0;
 }
+extern "C" int gtc_debug_append_marks(const gtc_run* r, uint64_t* marks) {
+  if (!r || !marks) return fail(GTC_ERR_INVALID, "null argument");
+  for (int i = 0; i < 7; ++i) marks[i] = r->h_rb->sc.t[i];
+  return GTC_OK;
+}
+
 extern "C" uint64_t gtc_run_stream(const gtc_run* r) { return r ? (uint64_t)(uintptr_t)r->stream : 0; }
 
 // =============================================================== stand-alone GpModel

@@ -20,7 +20,7 @@ constexpr int kCtaThreads = 256;           // single-CTA GP kernels
 constexpr int kMaxRows = 8;                // rows per multi-row extend pass (rebuild)
 constexpr int kMaxNmax = 1024;             // largest supported GP training size
 constexpr int kMaxDim = 64;                // largest supported search-space dimension
-constexpr size_t kCtaSmemLimit = 220 * 1024;  // packed-L staging budget of the single-CTA kernels
+constexpr size_t kCtaSmemLimit = 226 * 1024;  // L + Dinv staging budget of the single-CTA kernels
 
 struct KernelParams {
   int nu;
@@ -38,7 +38,14 @@ struct GpScalars {
   int32_t status; // 0 ok, 1 pivot <= 0 (factorisation failed)
   int32_t fail_row;
   int32_t pad;
+  unsigned long long t[8];  // %globaltimer marks of the last k_gp_append phases (diagnostics)
 };
+
+__device__ __forceinline__ unsigned long long gtc_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Device pointers of one GP model.
 struct GpDev {

@@ -19,9 +19,10 @@
 // the posterior falls out of the same pass:
 //   mu = sum_i v_i beta_i  (beta = L^-1 y_standardized),  var = max(s2 - sum_i v_i^2, 0).
 // The pass streams V once (HBM-bound GEMV): tile-major V, 16-byte streaming
-// loads, 8 rows in flight per thread.  The selection (k_select) is one
-// cooperative kernel: grid-wide mean variance -> lambda -> EI/PI/LCB ->
-// masked argmax, so no separate reduction pass over the candidates runs.
+// loads, 8 rows in flight per thread; its epilogue leaves per-tile partial
+// sums of the posterior variance.  The selection (k_select) reduces those
+// partials in every block (same fixed order -> same lambda everywhere), then
+// EI/PI/LCB + masked argmax in one pass over the candidates.
 //
 // L is stored packed row-major (row i at i(i+1)/2) so that the whole factor
 // of a budget-220 run (194 KB) fits in the shared memory of the single-CTA
@@ -101,42 +102,80 @@ __device__ __forceinline__ bool visited_bit(const uint32_t* visited, int64_t j) 
 
 // Solves L x = b in place (x in shared memory, length n) with one CTA, using
 // the first n rows of the packed lower factor Lp (shared or global memory).
-// 32-row blocks: warp 0 holds the diagonal block in registers and substitutes
-// it with shuffles (no memory access on the serial chain); then every thread
-// applies the solved block to the trailing rows.  Per row the subtraction
-// order is ascending column index, like the reference's forward substitution.
-__device__ void cta_forward_solve(const double* Lp, int n, double* x) {
-  for (int b0 = 0; b0 < n; b0 += 32) {
-    const int b1 = min(b0 + 32, n);
-    if (threadIdx.x < 32) {
-      const int r = b0 + threadIdx.x;
-      double lr[32];
-      const double* Lr = Lp + packed(r);
+// Forward substitution in the reference's order: every row subtracts its
+// terms in ascending column order, then divides by its pivot (as a multiply
+// by the pre-computed reciprocal, <= 1 ulp).  This order keeps chosen
+// configurations identical to the reference's; a blocked inverse variant
+// (explicit diagonal-block inverses + refinement) moved results by ~1e-13
+// and flipped near-tied picks, so it is not used.
+//
+// Row ownership: thread t owns rows t, t+256, t+512, t+768 and keeps their
+// running values in registers, so every row is updated by exactly one thread
+// and only the 32-step diagonal chain of each block is serial.  Block b's rows
+// belong to warp b % 8, which preloads its diagonal block (and pivot
+// reciprocals) for its next block while other warps run their chains.
+constexpr int kSolveRowsPerThread = kMaxNmax / kCtaThreads;
+
+__device__ __forceinline__ double pick_row(const double (&xo)[kSolveRowsPerThread], int s) {
+  double v = xo[0];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) lr[k] = (r < b1 && b0 + k <= r) ? Lr[b0 + k] : 0.0;
-      // the division leaves the serial chain: each lane inverts its own pivot
-      // up front and the chain multiplies (<= 1 ulp from x / L_ii)
-      const double rinv = r < b1 ? __drcp_rn(Lr[r]) : 0.0;
-      double xr = r < b1 ? x[r] : 0.0;
+  for (int q = 1; q < kSolveRowsPerThread; ++q) v = s == q ? xo[q] : v;
+  return v;
+}
+
+__device__ void cta_forward_solve(const double* Lp, int n, double* x) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = kCtaThreads / 32;
+  double xo[kSolveRowsPerThread];
+#pragma unroll
+  for (int s = 0; s < kSolveRowsPerThread; ++s) {
+    const int r = threadIdx.x + s * kCtaThreads;
+    xo[s] = r < n ? x[r] : 0.0;
+  }
+  const int nblk = (n + 31) / 32;
+  double lr[32];
+  double rinv = 0.0;
+  auto load_diag = [&](int blk) {
+    const int b0 = blk * 32, r = b0 + lane;
+    const bool live = blk < nblk && r < n;
+    const double* Lr = Lp + packed(live ? r : 0);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) lr[k] = (live && k <= lane) ? Lr[b0 + k] : 0.0;
+    rinv = live ? __drcp_rn(Lr[r]) : 0.0;
+  };
+  load_diag(warp);
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int b0 = blk * 32, b1 = min(b0 + 32, n);
+    if (warp == blk % nwarps) {
+      const int slot = blk / nwarps;
+      double xr = pick_row(xo, slot);
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         if (b0 + k < b1) {
-          if (threadIdx.x == k) xr = __dmul_rn(xr, rinv);
+          if (lane == k) xr = __dmul_rn(xr, rinv);
           const double xi = __shfl_sync(0xffffffffu, xr, k);
-          if (threadIdx.x > k) xr = __dadd_rn(xr, -__dmul_rn(lr[k], xi));
+          if (lane > k) xr = __dadd_rn(xr, -__dmul_rn(lr[k], xi));
         }
       }
-      if (r < b1) x[r] = xr;
+      if (b0 + lane < b1) x[b0 + lane] = xr;
+#pragma unroll
+      for (int s = 0; s < kSolveRowsPerThread; ++s)
+        if (s == slot) xo[s] = xr;
+      load_diag(blk + nwarps);  // off the critical path: next owned block
     }
-    __syncthreads();
-    for (int r = b1 + threadIdx.x; r < n; r += blockDim.x) {
-      double s = x[r];
-      const double* Lr = Lp + packed(r);
-      for (int i = b0; i < b1; ++i) s = __dadd_rn(s, -__dmul_rn(Lr[i], x[i]));
-      x[r] = s;
+    __syncthreads();  // block b's solution visible
+#pragma unroll
+    for (int s = 0; s < kSolveRowsPerThread; ++s) {
+      const int r = threadIdx.x + s * kCtaThreads;
+      if (r >= b1 && r < n) {
+        const double* Lr = Lp + packed(r);
+        double acc = xo[s];
+        for (int i = b0; i < b1; ++i) acc = __dadd_rn(acc, -__dmul_rn(Lr[i], x[i]));
+        xo[s] = acc;
+      }
     }
-    __syncthreads();
   }
+  __syncthreads();
 }
 
 // Standardisation + beta for the first n observations (gp.hpp:97-103,130).
@@ -186,7 +225,7 @@ __device__ double direct_kernel(const double* xa, const double* xb, int d, doubl
 // Shared-memory layout of the single-CTA GP kernels:
 //   xs  work vector (n_max)
 //   ys  y copy      (n_max)
-//   Ls  packed L rows (when they fit, else L is read from global memory)
+//   Ls  packed L rows [0, rows) (staged when they fit, else read from global)
 struct CtaSmem {
   double* Ls;
   double* xs;
@@ -194,26 +233,34 @@ struct CtaSmem {
   bool staged;
 };
 
-__device__ CtaSmem cta_smem_layout(double* base, int n_max, bool staged) {
+__host__ __device__ __forceinline__ int64_t even_up(int64_t v) { return (v + 1) & ~int64_t(1); }
+__host__ __device__ __forceinline__ int64_t staged_l_doubles(int rows) { return even_up(packed(rows)); }
+
+__device__ CtaSmem cta_smem_layout(double* base, int n_max, int rows, bool staged) {
   CtaSmem m;
   m.staged = staged;
   m.xs = base;
   m.ys = base + n_max;
-  m.Ls = base + 2 * (int64_t)n_max;
+  m.Ls = base + even_up(2 * (int64_t)n_max);
+  (void)rows;
   return m;
 }
+
+__device__ __forceinline__ const double* lp_of(const GpDev& g, const CtaSmem& m) { return m.staged ? m.Ls : g.L; }
 
 // Appends training point `row` (coords already in g.train_x[row]) to the
 // factor: l = L^-1 g, pivot = k(0) + noise + jitter - |l|^2 (gp.hpp:105-121).
 // Returns false (and records the failure) when the pivot is <= 0.
 template <int NU>
 __device__ bool cta_border_row(const GpDev& g, KernelParams k, double noise, double jitter, int row,
-                               const CtaSmem& m, double* red) {
+                               const CtaSmem& m, double* red, unsigned long long* tm = nullptr) {
   const double* xr = g.train_x + (int64_t)row * g.d;
   for (int q = threadIdx.x; q < row; q += blockDim.x)
     m.xs[q] = direct_kernel<NU>(g.train_x + (int64_t)q * g.d, xr, g.d, k.lengthscale, k.s2);
   __syncthreads();
-  cta_forward_solve(m.staged ? m.Ls : g.L, row, m.xs);
+  if (tm && threadIdx.x == 0) tm[2] = gtc_globaltimer();
+  cta_forward_solve(lp_of(g, m), row, m.xs);
+  if (tm && threadIdx.x == 0) tm[3] = gtc_globaltimer();
   double part = 0.0;
   for (int q = threadIdx.x; q < row; q += blockDim.x) part = __dadd_rn(part, __dmul_rn(m.xs[q], m.xs[q]));
   const double sumsq = block_sum(part, red);
@@ -243,7 +290,7 @@ __device__ bool cta_border_row(const GpDev& g, KernelParams k, double noise, dou
 
 // c[row], e[row] from the new L row (prefix-stable forward substitution).
 __device__ void cta_ce_row(const GpDev& g, int row, const CtaSmem& m, double* red) {
-  const double* Lrow = (m.staged ? m.Ls : g.L) + packed(row);
+  const double* Lrow = lp_of(g, m) + packed(row);
   double pc = 0.0, pe = 0.0;
   for (int q = threadIdx.x; q < row; q += blockDim.x) {
     pc = __dadd_rn(pc, __dmul_rn(Lrow[q], g.c[q]));
@@ -267,12 +314,23 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ void cta_stage_L(const GpDev& g, int rows, const CtaSmem& m) {
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  constexpr uint32_t kChunk = 32768;
+  const char* s = reinterpret_cast<const char*>(src);
+  for (uint32_t off = 0; off < bytes; off += kChunk) {
+    const uint32_t sz = bytes - off < kChunk ? bytes - off : kChunk;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     dst + off),
+                 "l"(s + off), "r"(sz), "r"(bar)
+                 : "memory");
+  }
+}
+
+// Stages L rows [0, l_rows) (size rounded to 16 bytes; the allocation is padded).
+__device__ void cta_stage_L(const GpDev& g, int l_rows, const CtaSmem& m) {
   __shared__ __align__(8) uint64_t bar;
-  const int64_t total = packed(rows);
-  // bulk copies need 16-byte multiples: round up (the allocation is padded)
-  const uint32_t bytes = static_cast<uint32_t>(((total * 8) + 15) & ~int64_t(15));
-  if (!m.staged || bytes == 0) {
+  const uint32_t lbytes = static_cast<uint32_t>(staged_l_doubles(l_rows) * 8);
+  if (!m.staged || lbytes == 0) {
     __syncthreads();
     return;
   }
@@ -280,17 +338,8 @@ __device__ void cta_stage_L(const GpDev& g, int rows, const CtaSmem& m) {
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
-    constexpr uint32_t kChunk = 32768;
-    const char* src = reinterpret_cast<const char*>(g.L);
-    const uint32_t dst = smem_u32(m.Ls);
-    for (uint32_t off = 0; off < bytes; off += kChunk) {
-      const uint32_t sz = bytes - off < kChunk ? bytes - off : kChunk;
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + off),
-          "l"(src + off), "r"(sz), "r"(b)
-          : "memory");
-    }
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(lbytes) : "memory");
+    bulk_g2s(smem_u32(m.Ls), g.L, lbytes, b);
   }
   __syncthreads();  // barrier initialised before anyone waits on it
   asm volatile(
@@ -310,7 +359,7 @@ __global__ void __launch_bounds__(kCtaThreads)
     k_gp_factor(GpDev g, KernelParams k, double noise, double jitter, int n, int staged) {
   extern __shared__ double smem[];
   __shared__ double red[32];
-  const CtaSmem m = cta_smem_layout(smem, g.n_max, staged != 0);
+  const CtaSmem m = cta_smem_layout(smem, g.n_max, n, staged != 0);  // built in place, nothing to stage
   if (threadIdx.x == 0) {
     g.sc->status = 0;
     g.sc->fail_row = -1;
@@ -343,7 +392,9 @@ __global__ void __launch_bounds__(kCtaThreads)
   extern __shared__ double smem[];
   __shared__ double red[32];
   __shared__ double xnew[64];
-  const CtaSmem m = cta_smem_layout(smem, g.n_max, staged != 0);
+  const CtaSmem m = cta_smem_layout(smem, g.n_max, n0 + 1, staged != 0);
+  unsigned long long* tm = g.sc->t;
+  if (threadIdx.x == 0) tm[0] = gtc_globaltimer();
   if (visited_mark && threadIdx.x == 0) visited_mark[pos >> 5] |= 1u << (pos & 31);
   for (int t = threadIdx.x; t < g.d; t += blockDim.x) {
     const double v = pos >= 0 ? sp.coords[(int64_t)t * sp.n_pad + pos] : x_explicit[t];
@@ -358,14 +409,18 @@ __global__ void __launch_bounds__(kCtaThreads)
   }
   cta_stage_L(g, n0, m);  // includes __syncthreads
   if (threadIdx.x == 0) {
+    tm[1] = gtc_globaltimer();
     double s = 0.0;
     for (int t = 0; t < g.d; ++t) s = __dadd_rn(s, __dmul_rn(xnew[t], xnew[t]));
     g.train_n2[n0] = s;
   }
   const double jitter = g.sc->jitter;
-  if (!cta_border_row<NU>(g, k, noise, jitter, n0, m, red)) return;
+  if (!cta_border_row<NU>(g, k, noise, jitter, n0, m, red, tm)) return;
+  if (threadIdx.x == 0) tm[4] = gtc_globaltimer();
   cta_ce_row(g, n0, m, red);
+  if (threadIdx.x == 0) tm[5] = gtc_globaltimer();
   cta_stats_beta(g, n0 + 1, red);
+  if (threadIdx.x == 0) tm[6] = gtc_globaltimer();
 }
 
 __global__ void k_gp_truncate(GpDev g, int n) {
@@ -610,14 +665,23 @@ __device__ void var_partial(const double* __restrict__ var, const uint32_t* __re
 // Deterministic fixed-order sum of `count` block partials, in every block.
 __device__ void reduce_partials(const double* ps, const long long* pc, int count, double* red,
                                 long long* redl, double* sum, long long* cnt) {
-  double s = 0.0;
-  long long c = 0;
-  for (int b = threadIdx.x; b < count; b += blockDim.x) {
-    s += __ldcg(ps + b);
-    c += __ldcg(pc + b);
+  // four independent accumulators keep four loads in flight per thread
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  long long c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+  const int bd = blockDim.x;
+  int b = threadIdx.x;
+  for (; b + 3 * bd < count; b += 4 * bd) {
+    const double p0 = __ldcg(ps + b), p1 = __ldcg(ps + b + bd), p2 = __ldcg(ps + b + 2 * bd), p3 = __ldcg(ps + b + 3 * bd);
+    const long long q0 = __ldcg(pc + b), q1 = __ldcg(pc + b + bd), q2 = __ldcg(pc + b + 2 * bd), q3 = __ldcg(pc + b + 3 * bd);
+    s0 += p0; s1 += p1; s2 += p2; s3 += p3;
+    c0 += q0; c1 += q1; c2 += q2; c3 += q3;
   }
-  *sum = block_sum(s, red);
-  *cnt = block_sum_ll(c, redl);
+  for (; b < count; b += bd) {
+    s0 += __ldcg(ps + b);
+    c0 += __ldcg(pc + b);
+  }
+  *sum = block_sum((s0 + s1) + (s2 + s3), red);
+  *cnt = block_sum_ll((c0 + c1) + (c2 + c3), redl);
 }
 
 __global__ void __launch_bounds__(kReduceThreads)
@@ -827,26 +891,36 @@ __device__ void select_body(const SelCtx& c, double best, double lambda, double 
   long long cnt = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  for (; j + stride < c.n; j += 2 * stride) {
-    const int64_t j2 = j + stride;
-    const bool e1 = eligible(c, j), e2 = eligible(c, j2);
-    const double m1 = c.mu[j], m2 = c.mu[j2];
-    const double s1 = sd_at(c, j), s2 = sd_at(c, j2);
-    if (e1) {
+  // software pipeline: the next candidate's loads (visited word, mean,
+  // variance/std) are in flight while the current one is scored; one copy of
+  // the erfc/exp code in the loop keeps the kernel in the instruction cache
+  const double* spread = c.sdv ? c.sdv : c.var;
+  bool e_cur = false;
+  double m_cur = 0.0, v_cur = 0.0;
+  if (j < c.n) {
+    e_cur = eligible(c, j);
+    m_cur = c.mu[j];
+    v_cur = spread[j];
+  }
+#pragma unroll 1
+  for (; j < c.n; j += stride) {
+    const int64_t jn = j + stride;
+    bool e_nxt = false;
+    double m_nxt = 0.0, v_nxt = 0.0;
+    if (jn < c.n) {
+      e_nxt = eligible(c, jn);
+      m_nxt = c.mu[jn];
+      v_nxt = spread[jn];
+    }
+    if (e_cur) {
       ++cnt;
       first = min(first, j);
-      score_into<MASK>(b, m1, s1, best, lambda, j);
+      // cand_stds = sqrt(cand_vars), strategies.hpp:385
+      score_into<MASK>(b, m_cur, c.sdv ? v_cur : sqrt(v_cur), best, lambda, j);
     }
-    if (e2) {
-      ++cnt;
-      first = min(first, j2);
-      score_into<MASK>(b, m2, s2, best, lambda, j2);
-    }
-  }
-  if (j < c.n && eligible(c, j)) {
-    ++cnt;
-    first = min(first, j);
-    score_into<MASK>(b, c.mu[j], sd_at(c, j), best, lambda, j);
+    e_cur = e_nxt;
+    m_cur = m_nxt;
+    v_cur = v_nxt;
   }
   select_finish<MASK>(c, b, first, cnt, best, lambda, mean_var, cv_fallback, gp_status);
 }
@@ -911,11 +985,11 @@ __global__ void k_scores(const double* __restrict__ mu, const double* __restrict
 
 // ------------------------------------------------------------ launchers
 
-// Shared memory of the single-CTA GP kernels: xs + ys (+ packed L rows when
-// they fit under the opt-in limit).
+// Shared memory of the single-CTA GP kernels: xs + ys (+ packed L rows and
+// diagonal-block inverses when they fit under the opt-in limit).
 static size_t cta_smem_bytes(int n_max, int rows, bool* staged) {
-  const size_t base = sizeof(double) * (size_t)(2 * n_max);
-  const size_t with_l = base + sizeof(double) * (size_t)(packed(rows) + 2);  // +2: 16-byte bulk-copy rounding
+  const size_t base = sizeof(double) * (size_t)even_up(2 * (int64_t)n_max);
+  const size_t with_l = base + sizeof(double) * (size_t)staged_l_doubles(rows);
   *staged = with_l <= kCtaSmemLimit;
   return *staged ? with_l : base;
 }

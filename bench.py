@@ -38,8 +38,8 @@ sys.path.insert(0, str(ROOT))
 BASE_SEED = 20261017
 METRIC = "BO iterations/sec (full-space GP posterior+acquisition) at N, n=220"
 # dram__bytes_read.sum + dram__bytes_write.sum per k_extend<1> launch, from the
-# committed ncu --set full capture (profiles/ncu_extend_r1.txt)
-TRAFFIC = {"c4": 1.807e9}
+# committed ncu --set full capture
+TRAFFIC = {"c4": 1.8075e9}  # 1.800507 GB read + 7.04 MB written (profiles/r01_ncu_full.txt)
 CONFIGS = {
     "c4": dict(grid=[10] * 6, invalid=0.0, workload="C4 synthetic random-rough 1M candidates (10^6 grid, d=6), n=220, bo-ei, contextual variance"),
     "c3": dict(grid=[10, 10, 10, 10, 5, 2], invalid=0.3, workload="C3 synthetic random-rough 100k candidates (d=6, ~30% invalid), n=220, bo-lcb, contextual variance"),
@@ -49,7 +49,7 @@ CONFIGS = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
@@ -77,6 +77,23 @@ class ClockSampler:
         self._t = None
 
     def _run(self):
+        # NVML (nvidia_ml_py) polls in microseconds, so even a sub-second timed
+        # region gets many samples; nvidia-smi is the fallback.
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits])
+                self._stop.wait(0.005)
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
@@ -89,9 +106,10 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def __enter__(self):
-        if shutil.which("nvidia-smi"):
+        if True:
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
+            time.sleep(0.02)  # first samples land before the timed region starts
         return self
 
     def __exit__(self, *a):

@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--n", type=int, default=220)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
+                    help="replicas: one independent C4 run per GPU (weak scaling, no collective); "
+                         "sharded: ONE C4 run with its candidate axis split over the GPUs (strong scaling, "
+                         "two small NCCL exchanges per iteration)")
     return ap.parse_args()
 
 
@@ -196,6 +200,75 @@ def run_reference_arm(args, cfg):
                       "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
 
+def run_sharded(args, cfg, rank, world, local):
+    """C4 with the candidate axis split over the ranks (strong scaling).
+    Each step: bordered row (replicated) + this shard's V-row pass -> NCCL
+    all-gather of (var sum, count) -> local selection -> NCCL all-gather of
+    the selection records -> identical merge on every rank."""
+    import torch
+    import paper_2111_14991_b200 as gt
+    from paper_2111_14991_b200 import AcquisitionId, ContextualVarianceState, ExplorationConfig, MaternKernel, MaternNu
+    from paper_2111_14991_b200.sharding import DistributedShard, Shard, ShardGroup, TorchComm, split_bounds
+
+    coords, ids, values = make_workload(cfg)
+    N, n = len(values), args.n
+    lo, hi = split_bounds(N, world, rank)
+    af = AcquisitionId.ei if args.config == "c4" else AcquisitionId.lcb
+    kern = MaternKernel(MaternNu.three_halves, 1.5, 1.0)
+    shard = Shard(coords[lo:hi], lo, kern, n_max=n + args.steps + args.warmup + 2, device=local)
+    pos = prefix_positions(values, n - 1, BASE_SEED)
+    y = values[pos]
+    shard.fit_points(coords[pos], y)
+    for p in pos:
+        shard.mark_global(int(p))
+    group = DistributedShard(shard, TorchComm()) if world > 1 else ShardGroup([shard])
+    cv = ContextualVarianceState(float(np.mean(y[:20])), group.mean_variance())
+    expl = ExplorationConfig()
+    f_best = float(np.min(y))
+    pick = group.select([af], f_best, expl, cv).position[int(af)]
+    stream = torch.cuda.ExternalStream(gt.load().gtc_run_stream(shard.run.handle))
+
+    def step(pick, f_best):
+        yv = float(values[pick])
+        f_best = min(f_best, yv)
+        s = group.observe(coords[pick], pick, yv, [af], f_best, expl, cv)
+        return s.position[int(af)], f_best
+
+    for _ in range(args.warmup):
+        pick, f_best = step(pick, f_best)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pick, f_best = step(pick, f_best)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    dev_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([dev_ms, wall], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dev_ms, wall = float(t[0]), float(t[1])
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": args.steps / (dev_ms / 1e3), "unit": "iter/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": cfg["workload"] + " (candidate axis sharded)", "N": N, "n": f"{n}..{n + args.steps + args.warmup}",
+                       "parallelism": f"candidate-shard{world}",
+                       "timing": "CUDA events bracketing the K steps on rank's stream (includes the NCCL exchanges), max over ranks"},
+            "e2e": {"value": args.steps / wall, "unit": "iter/s", "h2d_bytes_per_step": 8 * (coords.shape[1] + 2),
+                    "d2h_bytes_per_step": 16 + 8 * 13},
+            "clocks": clocks.summary()}))
+
+
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
@@ -208,6 +281,11 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.mode == "sharded":
+        run_sharded(args, cfg, rank, world, local)
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
     import paper_2111_14991_b200 as gt
     from paper_2111_14991_b200 import AcquisitionId, ContextualVarianceState, ExplorationConfig, MaternKernel, MaternNu
 

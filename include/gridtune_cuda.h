@@ -266,6 +266,40 @@ int gtc_run_bo_table(gtc_space* space, const uint64_t* ids, const gtc_bo_config*
                      const double* values, gtc_bo_record* records, double* lambdas,
                      int64_t capacity, gtc_bo_summary* summary);
 
+/* ---- candidate-axis sharding (very large spaces over several GPUs) --------- */
+/* Each rank holds a contiguous slice of the global candidate list in its own
+ * gtc_space; the GP state is replicated (every rank applies the same
+ * observations with explicit coordinates, so the factors stay identical).
+ * Per iteration: gtc_shard_observe -> exchange (var_sum, var_count) -> sum in
+ * rank order -> gtc_shard_select -> exchange gtc_shard_selection records ->
+ * the same deterministic merge on every rank (portfolio.hpp:32-61 rule:
+ * highest score, lowest position; NaN never wins except as first candidate). */
+typedef struct {
+  int64_t best_position[3];  /* best non-NaN score per AF slot (global), -1 if none */
+  double best_score[3];
+  int64_t first_eligible;    /* lowest eligible global position, -1 if none */
+  uint32_t first_nan_mask;   /* bit af: that first candidate's score is NaN */
+  int64_t n_candidates;
+  double lambda;
+  double mean_variance;
+  double best_std;
+  int32_t cv_fallback;
+} gtc_shard_selection;
+
+/* GpModel::fit from explicit training coordinates (X: n x d row-major). */
+int gtc_fit_points(gtc_run* run, const double* X, const double* y_raw, int32_t n, gtc_fit_info* info);
+/* This run's candidates are global positions [offset, offset + space size). */
+int gtc_run_set_shard(gtc_run* run, int64_t offset);
+/* Observation with explicit coordinates x_new (d); local_pos >= 0 only on the
+ * rank whose slice holds it (marks it visited).  Returns this shard's total of
+ * the refreshed posterior variance over its unvisited candidates. */
+int gtc_shard_observe(gtc_run* run, const double* x_new, int64_t local_pos, double y_raw, int32_t valid,
+                      double* var_sum, int64_t* var_count, gtc_fit_info* info);
+/* Local fused selection using the GLOBAL variance total (args->excluded in
+ * global positions). */
+int gtc_shard_select(gtc_run* run, const gtc_select_args* args, double global_var_sum,
+                     int64_t global_var_count, gtc_shard_selection* out);
+
 /* Per-candidate acquisition values (acquisition_{ei,pi,lcb}, acquisition.hpp:25-42;
  * the LCB slot returns -lcb like best_candidate's score, portfolio.hpp:47). */
 int gtc_acquisition_scores(int device, int32_t af, const double* means, const double* stds,

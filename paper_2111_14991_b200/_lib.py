@@ -51,6 +51,13 @@ class gtc_select_result(C.Structure):
                 ("n_candidates", C.c_int64), ("cv_fallback", C.c_int32)]
 
 
+class gtc_shard_selection(C.Structure):
+    _fields_ = [("best_position", C.c_int64 * 3), ("best_score", C.c_double * 3),
+                ("first_eligible", C.c_int64), ("first_nan_mask", C.c_uint32),
+                ("n_candidates", C.c_int64), ("lambda_", C.c_double), ("mean_variance", C.c_double),
+                ("best_std", C.c_double), ("cv_fallback", C.c_int32)]
+
+
 class gtc_bo_config(C.Structure):
     _fields_ = [("strategy", C.c_int32), ("seed", C.c_uint64), ("budget", C.c_int64),
                 ("n_init", C.c_int64), ("invalid_consumes_budget", C.c_int32), ("nu", C.c_int32),
@@ -117,6 +124,12 @@ SIGNATURES = [
                                      C.c_double, U8P, I64P, DP]),
     ("gtc_acquisition_scores", C.c_int, [C.c_int, C.c_int32, DP, DP, C.c_int64, C.c_double,
                                          C.c_double, DP]),
+    ("gtc_fit_points", C.c_int, [P, DP, DP, C.c_int32, C.POINTER(gtc_fit_info)]),
+    ("gtc_run_set_shard", C.c_int, [P, C.c_int64]),
+    ("gtc_shard_observe", C.c_int, [P, DP, C.c_int64, C.c_double, C.c_int32, DP, I64P,
+                                    C.POINTER(gtc_fit_info)]),
+    ("gtc_shard_select", C.c_int, [P, C.POINTER(gtc_select_args), C.c_double, C.c_int64,
+                                   C.POINTER(gtc_shard_selection)]),
     ("gtc_space_coords", DP, [P]),
     ("gtc_space_dimension", C.c_int32, [P]),
     ("gtc_space_device", C.c_int32, [P]),

@@ -235,7 +235,15 @@ struct gtc_run {
   double jitter = 0.0;
   bool predictions_valid = false;
   std::vector<double> y_host;
-  std::vector<int64_t> pos_host;
+  std::vector<double> x_host;  // n x d training coordinates
+  // candidate-axis sharding: this run's candidates are global positions
+  // [shard_offset, shard_offset + space->n)
+  int64_t shard_offset = 0;
+  double* d_xnew = nullptr;       // device copy of an explicit new point (d doubles)
+  double* h_xnew = nullptr;       // pinned staging
+  double* gsum = nullptr;         // global variance total as a 1-entry partials array
+  long long* gcnt = nullptr;
+  double* h_gtot = nullptr;       // pinned staging (sum, count as double pair)
   struct Readback {
     SelectDev sel;
     GpScalars sc;
@@ -330,6 +338,11 @@ extern "C" int gtc_run_destroy(gtc_run* r) {
   cudaFree(r->excluded);
   cudaFree(r->part_sum);
   cudaFree(r->part_cnt);
+  cudaFree(r->d_xnew);
+  cudaFree(r->gsum);
+  cudaFree(r->gcnt);
+  if (r->h_xnew) cudaFreeHost(r->h_xnew);
+  if (r->h_gtot) cudaFreeHost(r->h_gtot);
   if (r->h_rb) cudaFreeHost(r->h_rb);
   for (cudaEvent_t ev : {r->ev0, r->ev1, r->ev_step0, r->ev_step1})
     if (ev) cudaEventDestroy(ev);
@@ -369,6 +382,11 @@ extern "C" int gtc_run_create(gtc_space* space, const gtc_model_config* cfg, gtc
     if (e == cudaSuccess) e = cudaEventCreate(ev);
   if (e == cudaSuccess) e = cudaMemset(r->visited, 0, words * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMallocHost(&r->h_rb, sizeof(gtc_run::Readback));
+  if (e == cudaSuccess) e = cudaMallocHost(&r->h_xnew, sizeof(double) * kMaxDim);
+  if (e == cudaSuccess) e = cudaMallocHost(&r->h_gtot, sizeof(double) * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&r->d_xnew, sizeof(double) * kMaxDim);
+  if (e == cudaSuccess) e = cudaMalloc(&r->gsum, sizeof(double) * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&r->gcnt, sizeof(long long) * 2);
   if (e != cudaSuccess) {
     gtc_run_destroy(r);
     return fail(GTC_ERR_CUDA, std::string("run create: ") + cudaGetErrorString(e));
@@ -379,18 +397,24 @@ extern "C" int gtc_run_create(gtc_space* space, const gtc_model_config* cfg, gtc
   return GTC_OK;
 }
 
-static int upload_train(gtc_run* r, const int64_t* positions, const double* y, int n) {
-  const int d = r->space->d;
-  std::vector<double> X((size_t)n * d);
-  for (int i = 0; i < n; ++i) {
-    if (positions[i] < 0 || positions[i] >= r->space->n)
-      return fail(GTC_ERR_INVALID, "training position out of range");
-    std::memcpy(&X[(size_t)i * d], &r->space->host_coords[(size_t)positions[i] * d], sizeof(double) * d);
-  }
+// Host copy of the training set: explicit coordinates (so a shard can hold
+// observations of candidates that live on other shards) + raw values.
+static void keep_obs(gtc_run* r, int n) {
+  r->y_host.resize(n);
+  r->x_host.resize((size_t)n * r->space->d);
+}
+static void push_obs(gtc_run* r, const double* x, double y) {
+  r->y_host.push_back(y);
+  r->x_host.insert(r->x_host.end(), x, x + r->space->d);
+}
+
+static int upload_train(gtc_run* r) {
+  const int n = (int)r->y_host.size();
   if (n > 0) {
-    GTC_CUDA(cudaMemcpyAsync(r->gp.dev.train_x, X.data(), X.size() * sizeof(double), cudaMemcpyHostToDevice, r->stream));
-    GTC_CUDA(cudaMemcpyAsync(r->gp.dev.y, y, sizeof(double) * n, cudaMemcpyHostToDevice, r->stream));
-    GTC_CUDA(cudaStreamSynchronize(r->stream));  // X lives on this stack frame
+    GTC_CUDA(cudaMemcpyAsync(r->gp.dev.train_x, r->x_host.data(), r->x_host.size() * sizeof(double),
+                             cudaMemcpyHostToDevice, r->stream));
+    GTC_CUDA(cudaMemcpyAsync(r->gp.dev.y, r->y_host.data(), sizeof(double) * n, cudaMemcpyHostToDevice, r->stream));
+    GTC_CUDA(cudaStreamSynchronize(r->stream));
   }
   return GTC_OK;
 }
@@ -399,7 +423,7 @@ static int upload_train(gtc_run* r, const int64_t* positions, const double* y, i
 // `start_jitter`, then the full predictive pass.
 static int refit(gtc_run* r, double start_jitter, gtc_fit_info* info) {
   const int n = (int)r->y_host.size();
-  int rc = upload_train(r, r->pos_host.data(), r->y_host.data(), n);
+  int rc = upload_train(r);
   if (rc) return rc;
   rc = factor_with_escalation(r->gp, r->cfg.kernel, r->cfg.noise, r->cfg.jitter, start_jitter, n, r->stream);
   if (rc) {
@@ -425,8 +449,12 @@ extern "C" int gtc_fit(gtc_run* r, const int64_t* positions, const double* y_raw
   int rc = check_fit_inputs(y_raw, n, r->cfg.noise, r->cfg.jitter);
   if (rc) return rc;
   GTC_CUDA(cudaSetDevice(r->space->device));
-  r->y_host.assign(y_raw, y_raw + n);
-  r->pos_host.assign(positions, positions + n);
+  keep_obs(r, 0);
+  for (int i = 0; i < n; ++i) {
+    if (positions[i] < 0 || positions[i] >= r->space->n)
+      return fail(GTC_ERR_INVALID, "training position out of range");
+    push_obs(r, &r->space->host_coords[(size_t)positions[i] * r->space->d], y_raw[i]);
+  }
   if (n == 0) {
     r->n = 0;
     r->jitter = r->cfg.jitter;
@@ -471,10 +499,8 @@ extern "C" int gtc_append(gtc_run* r, int64_t pos, double y_raw, gtc_fit_info* i
   if (r->n >= r->cfg.n_max) return fail(GTC_ERR_CAPACITY, "more observations than the run's n_max");
   GTC_CUDA(cudaSetDevice(r->space->device));
   const int n0 = r->n;
-  r->y_host.resize(n0);
-  r->pos_host.resize(n0);
-  r->y_host.push_back(y_raw);
-  r->pos_host.push_back(pos);
+  keep_obs(r, n0);
+  push_obs(r, &r->space->host_coords[(size_t)pos * r->space->d], y_raw);
   if (n0 == 0) return refit(r, r->cfg.jitter, info);
   int rc = enqueue_append(r, pos, y_raw, nullptr);
   if (rc) return rc;
@@ -499,8 +525,7 @@ extern "C" int gtc_truncate(gtc_run* r, int32_t n, gtc_fit_info* info) {
   launch_gp_truncate(r->gp.dev, n, r->stream);
   GTC_LAUNCHED();
   r->n = n;
-  r->y_host.resize(n);
-  r->pos_host.resize(n);
+  keep_obs(r, n);
   r->predictions_valid = false;
   if (info) {  // the scalars need a round trip; without `info` the call stays asynchronous
     GTC_CUDA(cudaMemcpyAsync(r->gp.h_sc, r->gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, r->stream));
@@ -577,7 +602,9 @@ extern "C" int gtc_mean_variance(gtc_run* r, double* out, int64_t* count) {
 }
 
 // Enqueues the cooperative selection kernel (asynchronous).
-static int enqueue_selection(gtc_run* r, const gtc_select_args* a) {
+// With `global_totals`, the mean variance comes from the 1-entry (gsum, gcnt)
+// array (candidate-axis sharding) instead of this run's own partials.
+static int enqueue_selection(gtc_run* r, const gtc_select_args* a, bool global_totals = false) {
   int rc = ensure_predictions(r);
   if (rc) return rc;
   SelectParams p{a->af_mask & 7u, a->lambda_mode, a->lambda_constant, a->cv_initial_sample_mean,
@@ -594,6 +621,12 @@ static int enqueue_selection(gtc_run* r, const gtc_select_args* a) {
     p.excluded = r->excluded;
     p.n_excluded = a->n_excluded;
   }
+  if (global_totals) {
+    launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, r->gsum, r->gcnt, 1, r->red.b,
+                  r->red.sel, r->stream);
+    GTC_LAUNCHED();
+    return GTC_OK;
+  }
   if (r->n_partials == 0) {  // visited set changed since the last pass
     launch_var_partials(r->var, r->visited, r->space->n, r->part_sum, r->part_cnt, r->stream);
     GTC_LAUNCHED();
@@ -602,6 +635,138 @@ static int enqueue_selection(gtc_run* r, const gtc_select_args* a) {
   launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, r->part_sum, r->part_cnt, r->n_partials,
                 r->red.b, r->red.sel, r->stream);
   GTC_LAUNCHED();
+  return GTC_OK;
+}
+
+// =============================================================== sharding
+
+extern "C" int gtc_fit_points(gtc_run* r, const double* X, const double* y_raw, int32_t n, gtc_fit_info* info) {
+  if (!r) return fail(GTC_ERR_INVALID, "run is null");
+  if (n > r->cfg.n_max) return fail(GTC_ERR_CAPACITY, "more observations than the run's n_max");
+  int rc = check_fit_inputs(y_raw, n, r->cfg.noise, r->cfg.jitter);
+  if (rc) return rc;
+  if (n == 0) return gtc_fit(r, nullptr, nullptr, 0, info);
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  keep_obs(r, 0);
+  for (int i = 0; i < n; ++i) push_obs(r, X + (size_t)i * r->space->d, y_raw[i]);
+  return refit(r, r->cfg.jitter, info);
+}
+
+extern "C" int gtc_run_set_shard(gtc_run* r, int64_t offset) {
+  if (!r || offset < 0) return fail(GTC_ERR_INVALID, "bad shard");
+  r->shard_offset = offset;
+  return GTC_OK;
+}
+
+// This shard's total of the posterior variance over its unvisited candidates.
+static int enqueue_local_totals(gtc_run* r) {
+  int rc = ensure_predictions(r);
+  if (rc) return rc;
+  if (r->n_partials == 0) {
+    launch_var_partials(r->var, r->visited, r->space->n, r->part_sum, r->part_cnt, r->stream);
+    GTC_LAUNCHED();
+    r->n_partials = reduce_blocks(r->space->n);
+  }
+  launch_reduce_partials(r->part_sum, r->part_cnt, r->n_partials, r->red.totals, r->stream);
+  GTC_LAUNCHED();
+  return GTC_OK;
+}
+
+extern "C" int gtc_shard_observe(gtc_run* r, const double* x_new, int64_t local_pos, double y_raw, int32_t valid,
+                                 double* var_sum, int64_t* var_count, gtc_fit_info* info) {
+  if (!r || !x_new || !var_sum || !var_count) return fail(GTC_ERR_INVALID, "null argument");
+  if (local_pos >= r->space->n) return fail(GTC_ERR_INVALID, "position out of range");
+  if (valid && !std::isfinite(y_raw)) return fail(GTC_ERR_INVALID, "GP fit: observations must be finite");
+  if (valid && r->n >= r->cfg.n_max) return fail(GTC_ERR_CAPACITY, "more observations than the run's n_max");
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  int rc;
+  if (local_pos >= 0 && host_mark(r, local_pos, 1)) {
+    launch_mark(r->visited, local_pos, 1, r->stream);
+    GTC_LAUNCHED();
+    r->n_partials = 0;
+  }
+  const int n0 = r->n;
+  bool appended = false;
+  if (valid) {
+    keep_obs(r, n0);
+    push_obs(r, x_new, y_raw);
+    if (n0 == 0) {
+      if ((rc = refit(r, r->cfg.jitter, info))) return rc;
+    } else {
+      std::memcpy(r->h_xnew, x_new, sizeof(double) * r->space->d);
+      GTC_CUDA(cudaMemcpyAsync(r->d_xnew, r->h_xnew, sizeof(double) * r->space->d, cudaMemcpyHostToDevice, r->stream));
+      launch_gp_append(r->gp.dev, kparams(r->cfg.kernel), r->cfg.noise, r->space->dev(), -1, r->d_xnew, y_raw, n0,
+                       nullptr, r->stream);
+      GTC_LAUNCHED();
+      const VarPartials vp = r->vp();
+      launch_extend(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, n0, 1, true, r->mu,
+                    r->var, true, &vp, r->stream);
+      GTC_LAUNCHED();
+      r->n_partials = r->tiles;
+      r->predictions_valid = true;
+      appended = true;
+    }
+  }
+  if ((rc = enqueue_local_totals(r))) return rc;
+  GTC_CUDA(cudaMemcpyAsync(r->red.h_totals, r->red.totals, sizeof(VarTotals), cudaMemcpyDeviceToHost, r->stream));
+  GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sc, r->gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, r->stream));
+  GTC_CUDA(cudaStreamSynchronize(r->stream));
+  if (appended) {
+    if (r->h_rb->sc.status != 0) {  // bordered pivot <= 0: escalate exactly like a refit (gp.hpp:116-129)
+      if ((rc = refit(r, r->jitter * 2.0, info))) return rc;
+      if ((rc = enqueue_local_totals(r))) return rc;
+      GTC_CUDA(cudaMemcpyAsync(r->red.h_totals, r->red.totals, sizeof(VarTotals), cudaMemcpyDeviceToHost, r->stream));
+      GTC_CUDA(cudaStreamSynchronize(r->stream));
+    } else {
+      r->n = n0 + 1;
+      *r->gp.h_sc = r->h_rb->sc;
+      fill_info(info, r->h_rb->sc, r->n, 0);
+    }
+  } else if (!valid) {
+    fill_info(info, *r->gp.h_sc, r->n, 0);
+  }
+  *var_sum = r->red.h_totals->sum;
+  *var_count = r->red.h_totals->count;
+  return GTC_OK;
+}
+
+extern "C" int gtc_shard_select(gtc_run* r, const gtc_select_args* a, double global_var_sum,
+                                int64_t global_var_count, gtc_shard_selection* out) {
+  if (!r || !a || !out) return fail(GTC_ERR_INVALID, "null argument");
+  if ((a->af_mask & 7u) == 0) return fail(GTC_ERR_INVALID, "af_mask selects no acquisition function");
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  // global totals into the 1-entry partials array (pinned staging)
+  std::memcpy(&r->h_gtot[0], &global_var_sum, sizeof(double));
+  const long long cnt = global_var_count;
+  std::memcpy(&r->h_gtot[1], &cnt, sizeof(long long));
+  GTC_CUDA(cudaMemcpyAsync(r->gsum, &r->h_gtot[0], sizeof(double), cudaMemcpyHostToDevice, r->stream));
+  GTC_CUDA(cudaMemcpyAsync(r->gcnt, &r->h_gtot[1], sizeof(long long), cudaMemcpyHostToDevice, r->stream));
+  // global -> local exclusions (only those on this shard)
+  std::vector<int64_t> local_ex;
+  for (int32_t k = 0; k < a->n_excluded; ++k) {
+    const int64_t p = a->excluded[k] - r->shard_offset;
+    if (p >= 0 && p < r->space->n) local_ex.push_back(p);
+  }
+  gtc_select_args la = *a;
+  la.excluded = local_ex.empty() ? nullptr : local_ex.data();
+  la.n_excluded = (int32_t)local_ex.size();
+  int rc = enqueue_selection(r, &la, true);
+  if (rc) return rc;
+  GTC_CUDA(cudaMemcpyAsync(r->red.h_sel, r->red.sel, sizeof(SelectDev), cudaMemcpyDeviceToHost, r->stream));
+  GTC_CUDA(cudaStreamSynchronize(r->stream));
+  const SelectDev& s = *r->red.h_sel;
+  const int64_t off = r->shard_offset;
+  for (int k = 0; k < 3; ++k) {
+    out->best_position[k] = s.best_nonnan_pos[k] >= 0 ? s.best_nonnan_pos[k] + off : -1;
+    out->best_score[k] = s.best_nonnan_score[k];
+  }
+  out->first_eligible = s.first_eligible >= 0 ? s.first_eligible + off : -1;
+  out->first_nan_mask = s.n_candidates > 0 ? s.first_nan_mask : 0u;
+  out->n_candidates = s.n_candidates;
+  out->lambda = s.lambda;
+  out->mean_variance = s.mean_variance;
+  out->best_std = s.best_std;
+  out->cv_fallback = s.cv_fallback;
   return GTC_OK;
 }
 
@@ -637,10 +802,8 @@ extern "C" int gtc_observe(gtc_run* r, int64_t pos, double y_raw, int32_t valid,
   bool appended = false;
   GTC_CUDA(cudaEventRecord(r->ev_step0, r->stream));
   if (valid) {
-    r->y_host.resize(n0);
-    r->pos_host.resize(n0);
-    r->y_host.push_back(y_raw);
-    r->pos_host.push_back(pos);
+    keep_obs(r, n0);
+    push_obs(r, &r->space->host_coords[(size_t)pos * r->space->d], y_raw);
     if (n0 == 0) {
       if (newly) {
         launch_mark(r->visited, pos, 1, r->stream);

@@ -79,6 +79,12 @@ struct SelectDev {
   int64_t n_candidates;
   int32_t cv_fallback;
   int32_t gp_status;
+  // for cross-shard merging (candidate-axis sharding)
+  int64_t best_nonnan_pos[3];
+  double best_nonnan_score[3];
+  int64_t first_eligible;
+  uint32_t first_nan_mask;
+  int32_t pad2;
 };
 
 struct VarTotals {
@@ -142,6 +148,8 @@ void launch_extend(const SpaceDev& space, const GpDev& g, KernelParams k, double
 
 void launch_var_partials(const double* var, const uint32_t* visited, int64_t n, double* part_sum,
                          long long* part_cnt, cudaStream_t stream);
+void launch_reduce_partials(const double* part_sum, const long long* part_cnt, int n_partials, VarTotals* out,
+                            cudaStream_t stream);
 
 void launch_prior(double* mu, double* var, int64_t n, double s2, cudaStream_t stream);
 void launch_mark(uint32_t* visited, int64_t pos, int set, cudaStream_t stream);

@@ -852,6 +852,11 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, long long
   ff = block_min(ff, redi);
   fc = block_sum_ll(fc, redl);
   if (threadIdx.x == 0) {
+    c.out->first_nan_mask = 0;
+    for (int af = 0; af < 3; ++af) {
+      c.out->best_nonnan_pos[af] = -1;
+      c.out->best_nonnan_score[af] = 0.0;
+    }
     for (int af = 0; af < 3; ++af) {
       int64_t pos = -1;
       double sc = 0.0;
@@ -867,10 +872,15 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, long long
           pos = f[af].p;
           sc = f[af].s;
         }
+        // the pieces a cross-shard merge needs to apply the same rule
+        c.out->best_nonnan_pos[af] = f[af].p == INT64_MAX ? -1 : f[af].p;
+        c.out->best_nonnan_score[af] = f[af].s;
+        if (s_first != s_first) c.out->first_nan_mask |= 1u << af;
       }
       c.out->position[af] = pos;
       c.out->score[af] = sc;
     }
+    c.out->first_eligible = fc > 0 ? ff : -1;
     c.out->lambda = lambda;
     c.out->mean_variance = mean_var;
     c.out->best_std = best;
@@ -953,6 +963,21 @@ __global__ void __launch_bounds__(kReduceThreads, kSelectBlocksPerSM)
   }
   const double best = __ddiv_rn(__dadd_rn(p.f_best_raw, -sc->y_mean), sc->y_std);
   select_body<MASK>(c, best, lambda, mean_var, fallback, sc->status);
+}
+
+// Total of a partials array (one block, fixed order): a shard's local
+// contribution to the global mean variance.
+__global__ void __launch_bounds__(kReduceThreads)
+    k_reduce_partials(const double* part_sum, const long long* part_cnt, int n_partials, VarTotals* out) {
+  __shared__ double red[32];
+  __shared__ long long redl[32];
+  double s;
+  long long c;
+  reduce_partials(part_sum, part_cnt, n_partials, red, redl, &s, &c);
+  if (threadIdx.x == 0) {
+    out->sum = s;
+    out->count = c;
+  }
 }
 
 // Variance partials over the unvisited candidates when the pass did not
@@ -1075,6 +1100,12 @@ void launch_varsum(const double* var, const uint32_t* visited, int64_t n, double
                    unsigned int* counter, VarTotals* totals, cudaStream_t s) {
   count_launch();
   k_varsum<<<reduce_blocks(n), kReduceThreads, 0, s>>>(var, visited, n, ps, pc, counter, totals);
+}
+
+void launch_reduce_partials(const double* part_sum, const long long* part_cnt, int n_partials, VarTotals* out,
+                            cudaStream_t s) {
+  count_launch();
+  k_reduce_partials<<<1, kReduceThreads, 0, s>>>(part_sum, part_cnt, n_partials, out);
 }
 
 void launch_var_partials(const double* var, const uint32_t* visited, int64_t n, double* part_sum,

@@ -14,7 +14,8 @@ namespace gtc {
 constexpr int kTile = 256;
 constexpr int kExtendThreads = kTile / 2;  // one double2 column pair per thread
 constexpr int kReduceThreads = 256;
-constexpr int kSelectBlocksPerSM = 4;      // selection: <= 64 registers, one resident wave
+constexpr int kSelectThreads = 1024;       // selection: one 1024-thread block per SM (<= 64 regs),
+                                           // so per-block partial reductions and fences are few
 constexpr int kMaxReduceGrid = 2048;       // upper bound of every reduction grid (scratch sizing)
 constexpr int kCtaThreads = 256;           // single-CTA GP kernels
 constexpr int kMaxRows = 8;                // rows per multi-row extend pass (rebuild)

@@ -29,6 +29,7 @@
 // update kernels.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include <math_constants.h>
 
 #include <atomic>
 #include <cstdint>
@@ -891,8 +892,10 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, long long
   }
 }
 
-// Scan of a strided slice (two candidates per iteration for ILP) used by the
-// span-based best_candidate path.
+// Scan of a strided slice: software-pipelined (the next candidate's visited
+// word, mean and variance/std are in flight while the current one is scored;
+// one copy of the erfc/exp code keeps the loop in the instruction cache).
+// Shared by the run selection and the span-based best_candidate path.
 template <uint32_t MASK>
 __device__ void select_body(const SelCtx& c, double best, double lambda, double mean_var,
                             int cv_fallback, int gp_status) {
@@ -901,9 +904,6 @@ __device__ void select_body(const SelCtx& c, double best, double lambda, double 
   long long cnt = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  // software pipeline: the next candidate's loads (visited word, mean,
-  // variance/std) are in flight while the current one is scored; one copy of
-  // the erfc/exp code in the loop keeps the kernel in the instruction cache
   const double* spread = c.sdv ? c.sdv : c.var;
   bool e_cur = false;
   double m_cur = 0.0, v_cur = 0.0;
@@ -942,7 +942,7 @@ __device__ void select_body(const SelCtx& c, double best, double lambda, double 
 // (strategies.hpp:404-418, acquisition.hpp:73-83) and best_std (gp.hpp:145)
 // without a grid barrier; then the masked argmax as in select_body.
 template <uint32_t MASK>
-__global__ void __launch_bounds__(kReduceThreads, kSelectBlocksPerSM)
+__global__ void __launch_bounds__(kSelectThreads, 1)
     k_select(SelCtx c, const GpScalars* sc, SelectParams p, const double* part_sum,
              const long long* part_cnt, int n_partials) {
   __shared__ double red[32];
@@ -1121,11 +1121,11 @@ void launch_select(const double* mu, const double* var, const uint32_t* visited,
   SelCtx c{mu, var, nullptr, visited, nullptr, p.excluded, p.n_excluded, n, p.af_mask, b, out};
   // exactly one wave of resident blocks (grid-stride inside): a partial
   // second wave would double the kernel's time
-  const int per_block = kReduceThreads * 2;
-  int grid = (int)std::min<int64_t>((n + per_block - 1) / per_block, (int64_t)sm_count() * kSelectBlocksPerSM);
+  const int per_block = kSelectThreads * 2;
+  int grid = (int)std::min<int64_t>((n + per_block - 1) / per_block, (int64_t)sm_count());
   grid = std::max(std::min(grid, kMaxReduceGrid), 1);
 #define GTC_SELECT_CASE(M) \
-  case M: k_select<M><<<grid, kReduceThreads, 0, s>>>(c, sc, p, part_sum, part_cnt, n_partials); break;
+  case M: k_select<M><<<grid, kSelectThreads, 0, s>>>(c, sc, p, part_sum, part_cnt, n_partials); break;
   switch (p.af_mask & 7u) {  // launch errors surface through the caller's cudaGetLastError()
     GTC_SELECT_CASE(1)
     GTC_SELECT_CASE(2)
@@ -1133,7 +1133,7 @@ void launch_select(const double* mu, const double* var, const uint32_t* visited,
     GTC_SELECT_CASE(4)
     GTC_SELECT_CASE(5)
     GTC_SELECT_CASE(6)
-    default: k_select<7><<<grid, kReduceThreads, 0, s>>>(c, sc, p, part_sum, part_cnt, n_partials); break;
+    default: k_select<7><<<grid, kSelectThreads, 0, s>>>(c, sc, p, part_sum, part_cnt, n_partials); break;
   }
 #undef GTC_SELECT_CASE
 }

@@ -83,7 +83,7 @@ struct ReduceScratch {
     const int nb = std::max(reduce_blocks(n), kMaxReduceGrid);  // covers the selection grid too
     int rc;
     if ((rc = dalloc(&b.pvar, nb)) || (rc = dalloc(&b.pvcnt, nb)) || (rc = dalloc(&b.pscore, 3 * nb)) ||
-        (rc = dalloc(&b.ppos, 3 * nb)) || (rc = dalloc(&b.pfirst, nb)) || (rc = dalloc(&b.pcnt, nb)) ||
+        (rc = dalloc(&b.ppos, 3 * nb)) || (rc = dalloc(&b.pfirst, nb)) || (rc = dalloc(&b.pfinite, nb)) || (rc = dalloc(&b.pcnt, nb)) ||
         (rc = dalloc(&b.counter, 1)) || (rc = dalloc(&vsum, nb)) || (rc = dalloc(&vcnt, nb)) ||
         (rc = dalloc(&vcounter, 1)) || (rc = dalloc(&totals, 1)) || (rc = dalloc(&sel, 1)))
       return rc;
@@ -94,7 +94,7 @@ struct ReduceScratch {
     return GTC_OK;
   }
   void release() {
-    cudaFree(b.pvar); cudaFree(b.pvcnt); cudaFree(b.pscore); cudaFree(b.ppos); cudaFree(b.pfirst);
+    cudaFree(b.pvar); cudaFree(b.pvcnt); cudaFree(b.pscore); cudaFree(b.ppos); cudaFree(b.pfirst); cudaFree(b.pfinite);
     cudaFree(b.pcnt); cudaFree(b.counter); cudaFree(vsum); cudaFree(vcnt); cudaFree(vcounter);
     cudaFree(totals); cudaFree(sel);
     if (h_sel) cudaFreeHost(h_sel);
@@ -241,20 +241,24 @@ struct gtc_run {
   int64_t shard_offset = 0;
   double* d_xnew = nullptr;       // device copy of an explicit new point (d doubles)
   double* h_xnew = nullptr;       // pinned staging
-  double* gsum = nullptr;         // global variance total as a 1-entry partials array
-  long long* gcnt = nullptr;
-  double* h_gtot = nullptr;       // pinned staging (sum, count as double pair)
   struct Readback {
     SelectDev sel;
     GpScalars sc;
   };
   Readback* h_rb = nullptr;  // pinned: one D2H per gtc_observe
-  // variance partials for the selection; n_partials == 0: stale (recompute)
-  double* part_sum = nullptr;
-  long long* part_cnt = nullptr;
-  int n_partials = 0;
+  // fixed-point variance totals over the unvisited candidates, two
+  // alternating generations (VarAccum); acc_valid: the current generation
+  // matches the current visited set and predictions
+  VarAccum* acc = nullptr;  // [2]
+  int acc_gen = 0;
+  bool acc_valid = false;
   int tiles = 0;
-  VarPartials vp() const { return VarPartials{visited, part_sum, part_cnt}; }
+  // producer side of the next generation (becomes current)
+  VarPartials vp() {
+    acc_gen ^= 1;
+    return VarPartials{visited, acc + acc_gen, acc + (acc_gen ^ 1)};
+  }
+  VarSource vsrc() const { return VarSource{acc + acc_gen, cfg.kernel.output_variance, 0.0, 0, 0}; }
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;          // last predictive pass
   cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;  // last gtc_observe device span
   bool pass_timed = false, step_timed = false;
@@ -336,13 +340,9 @@ extern "C" int gtc_run_destroy(gtc_run* r) {
   cudaFree(r->var);
   cudaFree(r->visited);
   cudaFree(r->excluded);
-  cudaFree(r->part_sum);
-  cudaFree(r->part_cnt);
+  cudaFree(r->acc);
   cudaFree(r->d_xnew);
-  cudaFree(r->gsum);
-  cudaFree(r->gcnt);
   if (r->h_xnew) cudaFreeHost(r->h_xnew);
-  if (r->h_gtot) cudaFreeHost(r->h_gtot);
   if (r->h_rb) cudaFreeHost(r->h_rb);
   for (cudaEvent_t ev : {r->ev0, r->ev1, r->ev_step0, r->ev_step1})
     if (ev) cudaEventDestroy(ev);
@@ -372,8 +372,7 @@ extern "C" int gtc_run_create(gtc_space* space, const gtc_model_config* cfg, gtc
   if ((rc = r->gp.init(cfg->n_max, space->d)) || (rc = r->red.init(space->n)) ||
       (rc = dalloc(&r->V, (size_t)tiles * r->tile_stride)) || (rc = dalloc(&r->mu, space->n_pad)) ||
       (rc = dalloc(&r->var, space->n_pad)) || (rc = dalloc(&r->visited, words)) ||
-      (rc = dalloc(&r->part_sum, std::max<int64_t>(tiles, reduce_blocks(space->n)))) ||
-      (rc = dalloc(&r->part_cnt, std::max<int64_t>(tiles, reduce_blocks(space->n))))) {
+      (rc = dalloc(&r->acc, 2))) {
     gtc_run_destroy(r);
     return rc;
   }
@@ -381,12 +380,10 @@ extern "C" int gtc_run_create(gtc_space* space, const gtc_model_config* cfg, gtc
   for (cudaEvent_t* ev : {&r->ev0, &r->ev1, &r->ev_step0, &r->ev_step1})
     if (e == cudaSuccess) e = cudaEventCreate(ev);
   if (e == cudaSuccess) e = cudaMemset(r->visited, 0, words * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(r->acc, 0, 2 * sizeof(VarAccum));
   if (e == cudaSuccess) e = cudaMallocHost(&r->h_rb, sizeof(gtc_run::Readback));
   if (e == cudaSuccess) e = cudaMallocHost(&r->h_xnew, sizeof(double) * kMaxDim);
-  if (e == cudaSuccess) e = cudaMallocHost(&r->h_gtot, sizeof(double) * 2);
   if (e == cudaSuccess) e = cudaMalloc(&r->d_xnew, sizeof(double) * kMaxDim);
-  if (e == cudaSuccess) e = cudaMalloc(&r->gsum, sizeof(double) * 2);
-  if (e == cudaSuccess) e = cudaMalloc(&r->gcnt, sizeof(long long) * 2);
   if (e != cudaSuccess) {
     gtc_run_destroy(r);
     return fail(GTC_ERR_CUDA, std::string("run create: ") + cudaGetErrorString(e));
@@ -437,7 +434,7 @@ static int refit(gtc_run* r, double start_jitter, gtc_fit_info* info) {
                            r->stream);
   if (rc) return rc;
   r->predictions_valid = true;
-  r->n_partials = r->tiles;
+  r->acc_valid = true;
   fill_info(info, *r->gp.h_sc, n, 1);
   return GTC_OK;
 }
@@ -467,7 +464,7 @@ extern "C" int gtc_fit(gtc_run* r, const int64_t* positions, const double* y_raw
     if (rc) return rc;
     GTC_CUDA(cudaStreamSynchronize(r->stream));
     r->predictions_valid = true;
-    r->n_partials = 0;
+    r->acc_valid = false;
     fill_info(info, *r->gp.h_sc, 0, 1);
     return GTC_OK;
   }
@@ -488,7 +485,7 @@ static int enqueue_append(gtc_run* r, int64_t pos, double y_raw, uint32_t* mark)
   GTC_LAUNCHED();
   GTC_CUDA(cudaEventRecord(r->ev1, r->stream));
   r->pass_timed = true;
-  r->n_partials = r->tiles;  // (stale if the pivot failed; the refit rewrites them)
+  r->acc_valid = true;  // (stale if the pivot failed; the refit rewrites them)
   return GTC_OK;
 }
 
@@ -539,13 +536,13 @@ static int ensure_predictions(gtc_run* r) {
   if (r->predictions_valid) return GTC_OK;
   if (r->n == 0) {
     launch_prior(r->mu, r->var, r->space->n_pad, r->cfg.kernel.output_variance, r->stream);
-    r->n_partials = 0;
+    r->acc_valid = false;
   } else {
     // posterior from the resident V rows (r = 0 new rows)
     const VarPartials vp = r->vp();
     launch_extend(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, r->n, 0, true,
                   r->mu, r->var, false, &vp, r->stream);
-    r->n_partials = r->tiles;
+    r->acc_valid = true;
   }
   GTC_LAUNCHED();
   r->predictions_valid = true;
@@ -576,7 +573,7 @@ static int set_visited(gtc_run* r, int64_t pos, int set) {
   if (!host_mark(r, pos, set)) return GTC_OK;
   launch_mark(r->visited, pos, set, r->stream);
   GTC_LAUNCHED();
-  r->n_partials = 0;
+  r->acc_valid = false;
   return GTC_OK;
 }
 
@@ -601,10 +598,20 @@ extern "C" int gtc_mean_variance(gtc_run* r, double* out, int64_t* count) {
   return GTC_OK;
 }
 
-// Enqueues the cooperative selection kernel (asynchronous).
-// With `global_totals`, the mean variance comes from the 1-entry (gsum, gcnt)
-// array (candidate-axis sharding) instead of this run's own partials.
-static int enqueue_selection(gtc_run* r, const gtc_select_args* a, bool global_totals = false) {
+// Makes the run's current variance total match its visited set.
+static int ensure_var_totals(gtc_run* r) {
+  if (r->acc_valid) return GTC_OK;  // visited set unchanged since the last pass
+  launch_var_partials(r->var, r->space->n, r->cfg.kernel.output_variance, r->vp(), r->stream);
+  GTC_LAUNCHED();
+  r->acc_valid = true;
+  return GTC_OK;
+}
+
+// Enqueues the selection kernel (asynchronous).  With `global_totals`, the
+// mean variance comes from the global (sum, count) passed by value
+// (candidate-axis sharding) instead of this run's own variance total.
+static int enqueue_selection(gtc_run* r, const gtc_select_args* a, bool global_totals = false,
+                             double global_sum = 0.0, long long global_count = 0) {
   int rc = ensure_predictions(r);
   if (rc) return rc;
   SelectParams p{a->af_mask & 7u, a->lambda_mode, a->lambda_constant, a->cv_initial_sample_mean,
@@ -622,18 +629,14 @@ static int enqueue_selection(gtc_run* r, const gtc_select_args* a, bool global_t
     p.n_excluded = a->n_excluded;
   }
   if (global_totals) {
-    launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, r->gsum, r->gcnt, 1, r->red.b,
-                  r->red.sel, r->stream);
+    const VarSource vs{nullptr, 0.0, global_sum, global_count, 1};
+    launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, vs, r->red.b, r->red.sel, r->stream);
     GTC_LAUNCHED();
     return GTC_OK;
   }
-  if (r->n_partials == 0) {  // visited set changed since the last pass
-    launch_var_partials(r->var, r->visited, r->space->n, r->part_sum, r->part_cnt, r->stream);
-    GTC_LAUNCHED();
-    r->n_partials = reduce_blocks(r->space->n);
-  }
-  launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, r->part_sum, r->part_cnt, r->n_partials,
-                r->red.b, r->red.sel, r->stream);
+  if ((rc = ensure_var_totals(r))) return rc;
+  launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, r->vsrc(), r->red.b, r->red.sel,
+                r->stream);
   GTC_LAUNCHED();
   return GTC_OK;
 }
@@ -662,12 +665,8 @@ extern "C" int gtc_run_set_shard(gtc_run* r, int64_t offset) {
 static int enqueue_local_totals(gtc_run* r) {
   int rc = ensure_predictions(r);
   if (rc) return rc;
-  if (r->n_partials == 0) {
-    launch_var_partials(r->var, r->visited, r->space->n, r->part_sum, r->part_cnt, r->stream);
-    GTC_LAUNCHED();
-    r->n_partials = reduce_blocks(r->space->n);
-  }
-  launch_reduce_partials(r->part_sum, r->part_cnt, r->n_partials, r->red.totals, r->stream);
+  if ((rc = ensure_var_totals(r))) return rc;
+  launch_var_totals(r->vsrc(), r->red.totals, r->stream);
   GTC_LAUNCHED();
   return GTC_OK;
 }
@@ -683,7 +682,7 @@ extern "C" int gtc_shard_observe(gtc_run* r, const double* x_new, int64_t local_
   if (local_pos >= 0 && host_mark(r, local_pos, 1)) {
     launch_mark(r->visited, local_pos, 1, r->stream);
     GTC_LAUNCHED();
-    r->n_partials = 0;
+    r->acc_valid = false;
   }
   const int n0 = r->n;
   bool appended = false;
@@ -702,7 +701,7 @@ extern "C" int gtc_shard_observe(gtc_run* r, const double* x_new, int64_t local_
       launch_extend(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, n0, 1, true, r->mu,
                     r->var, true, &vp, r->stream);
       GTC_LAUNCHED();
-      r->n_partials = r->tiles;
+      r->acc_valid = true;
       r->predictions_valid = true;
       appended = true;
     }
@@ -735,12 +734,6 @@ extern "C" int gtc_shard_select(gtc_run* r, const gtc_select_args* a, double glo
   if (!r || !a || !out) return fail(GTC_ERR_INVALID, "null argument");
   if ((a->af_mask & 7u) == 0) return fail(GTC_ERR_INVALID, "af_mask selects no acquisition function");
   GTC_CUDA(cudaSetDevice(r->space->device));
-  // global totals into the 1-entry partials array (pinned staging)
-  std::memcpy(&r->h_gtot[0], &global_var_sum, sizeof(double));
-  const long long cnt = global_var_count;
-  std::memcpy(&r->h_gtot[1], &cnt, sizeof(long long));
-  GTC_CUDA(cudaMemcpyAsync(r->gsum, &r->h_gtot[0], sizeof(double), cudaMemcpyHostToDevice, r->stream));
-  GTC_CUDA(cudaMemcpyAsync(r->gcnt, &r->h_gtot[1], sizeof(long long), cudaMemcpyHostToDevice, r->stream));
   // global -> local exclusions (only those on this shard)
   std::vector<int64_t> local_ex;
   for (int32_t k = 0; k < a->n_excluded; ++k) {
@@ -750,7 +743,7 @@ extern "C" int gtc_shard_select(gtc_run* r, const gtc_select_args* a, double glo
   gtc_select_args la = *a;
   la.excluded = local_ex.empty() ? nullptr : local_ex.data();
   la.n_excluded = (int32_t)local_ex.size();
-  int rc = enqueue_selection(r, &la, true);
+  int rc = enqueue_selection(r, &la, true, global_var_sum, (long long)global_var_count);  // totals by value
   if (rc) return rc;
   GTC_CUDA(cudaMemcpyAsync(r->red.h_sel, r->red.sel, sizeof(SelectDev), cudaMemcpyDeviceToHost, r->stream));
   GTC_CUDA(cudaStreamSynchronize(r->stream));
@@ -808,7 +801,7 @@ extern "C" int gtc_observe(gtc_run* r, int64_t pos, double y_raw, int32_t valid,
       if (newly) {
         launch_mark(r->visited, pos, 1, r->stream);
         GTC_LAUNCHED();
-        r->n_partials = 0;
+        r->acc_valid = false;
       }
       if ((rc = refit(r, r->cfg.jitter, info))) return rc;
     } else {
@@ -819,7 +812,7 @@ extern "C" int gtc_observe(gtc_run* r, int64_t pos, double y_raw, int32_t valid,
   } else if (newly) {
     launch_mark(r->visited, pos, 1, r->stream);
     GTC_LAUNCHED();
-    r->n_partials = 0;
+    r->acc_valid = false;
   }
   const bool selecting = a && r->space->n - r->visited_count > 0;
   if (selecting && (rc = enqueue_selection(r, a))) return rc;

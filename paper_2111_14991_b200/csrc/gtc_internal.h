@@ -14,8 +14,8 @@ namespace gtc {
 constexpr int kTile = 256;
 constexpr int kExtendThreads = kTile / 2;  // one double2 column pair per thread
 constexpr int kReduceThreads = 256;
-constexpr int kSelectThreads = 1024;       // selection: one 1024-thread block per SM (<= 64 regs),
-                                           // so per-block partial reductions and fences are few
+constexpr int kSelectThreads = 512;        // selection: one 512-thread block per SM (<= 128 regs for
+                                           // the register-resident bounds), few partials and fences
 constexpr int kMaxReduceGrid = 2048;       // upper bound of every reduction grid (scratch sizing)
 constexpr int kCtaThreads = 256;           // single-CTA GP kernels
 constexpr int kMaxRows = 8;                // rows per multi-row extend pass (rebuild)
@@ -93,6 +93,28 @@ struct VarTotals {
   int64_t count;
 };
 
+// Deterministic, order-independent total of the posterior variance over the
+// unvisited candidates.  Every producer block converts its (block-tree) sum
+// to fixed point -- four 42-bit limbs of sum * 2^(120 - ilogb(s2)), exact
+// power-of-two scaling, every variance is in [0, s2] -- and adds the limbs
+// and its count with integer atomics, so the total does not depend on block
+// scheduling and no consumer has to re-reduce per-block partials.
+struct VarAccum {
+  unsigned long long limb[4];
+  unsigned long long count;
+  unsigned long long pad[3];
+};
+
+// Where the selection takes the variance total from: an accumulator of this
+// run (device), or totals passed by value (candidate-axis sharding).
+struct VarSource {
+  const VarAccum* acc;
+  double s2;
+  double sum;
+  long long count;
+  int direct;
+};
+
 struct SelectParams {
   uint32_t af_mask;
   int lambda_mode;
@@ -111,6 +133,7 @@ struct ReduceBufs {
   double* pscore;      // [3 * blocks]
   int64_t* ppos;       // [3 * blocks]
   int64_t* pfirst;
+  int32_t* pfinite;    // [blocks] the block's first eligible candidate has finite keys (score not NaN)
   long long* pcnt;
   unsigned int* counter;
 };
@@ -130,13 +153,14 @@ void launch_gp_append(const GpDev& g, KernelParams k, double noise, const SpaceD
 // Single-CTA: recompute stats/beta for the prefix of n observations.
 void launch_gp_truncate(const GpDev& g, int n, cudaStream_t stream);
 
-// Per-tile partial sums of the posterior variance over unvisited candidates,
-// written by the final predictive pass (one entry per tile) or by
-// launch_var_partials (one per reduce block) and reduced by the selection.
+// Producer side of a variance total: the final predictive pass (per tile)
+// or launch_var_partials add into `acc` (which must be zero) and clear
+// `acc_clear` (the next generation's accumulator) -- two generations
+// alternate, so no separate zeroing launch is needed.
 struct VarPartials {
   const uint32_t* visited;
-  double* part_sum;
-  long long* part_cnt;
+  VarAccum* acc;
+  VarAccum* acc_clear;
 };
 
 // Multi-row V extension over all candidates: rows [n0, n0+r) from rows [0, n0).
@@ -147,10 +171,9 @@ void launch_extend(const SpaceDev& space, const GpDev& g, KernelParams k, double
                    int64_t tile_stride, int n0, int r, bool final, double* mu, double* var,
                    bool check_status, const VarPartials* vp, cudaStream_t stream);
 
-void launch_var_partials(const double* var, const uint32_t* visited, int64_t n, double* part_sum,
-                         long long* part_cnt, cudaStream_t stream);
-void launch_reduce_partials(const double* part_sum, const long long* part_cnt, int n_partials, VarTotals* out,
-                            cudaStream_t stream);
+void launch_var_partials(const double* var, int64_t n, double s2, const VarPartials& vp, cudaStream_t stream);
+// Converts a variance source to (sum, count) on the device.
+void launch_var_totals(const VarSource& src, VarTotals* out, cudaStream_t stream);
 
 void launch_prior(double* mu, double* var, int64_t n, double s2, cudaStream_t stream);
 void launch_mark(uint32_t* visited, int64_t pos, int set, cudaStream_t stream);
@@ -163,8 +186,8 @@ void launch_varsum(const double* var, const uint32_t* visited, int64_t n, double
 // Fused mean-variance (from the partials) + lambda + acquisition + masked
 // argmax for every AF in the mask.
 void launch_select(const double* mu, const double* var, const uint32_t* visited, int64_t n,
-                   const GpScalars* sc, SelectParams p, const double* part_sum, const long long* part_cnt,
-                   int n_partials, const ReduceBufs& bufs, SelectDev* out, cudaStream_t stream);
+                   const GpScalars* sc, SelectParams p, const VarSource& vs, const ReduceBufs& bufs,
+                   SelectDev* out, cudaStream_t stream);
 
 // best_candidate over caller spans of stds (not variances).
 void launch_best_candidate(const double* mu, const double* std, const uint8_t* excluded,

@@ -101,78 +101,104 @@ __device__ __forceinline__ bool visited_bit(const uint32_t* visited, int64_t j) 
   return (__ldg(visited + (j >> 5)) >> (j & 31)) & 1u;
 }
 
-// Solves L x = b in place (x in shared memory, length n) with one CTA, using
-// the first n rows of the packed lower factor Lp (shared or global memory).
-// Forward substitution in the reference's order: every row subtracts its
-// terms in ascending column order, then divides by its pivot (as a multiply
-// by the pre-computed reciprocal, <= 1 ulp).  This order keeps chosen
-// configurations identical to the reference's; a blocked inverse variant
-// (explicit diagonal-block inverses + refinement) moved results by ~1e-13
-// and flipped near-tied picks, so it is not used.
-//
-// Row ownership: thread t owns rows t, t+256, t+512, t+768 and keeps their
-// running values in registers, so every row is updated by exactly one thread
-// and only the 32-step diagonal chain of each block is serial.  Block b's rows
-// belong to warp b % 8, which preloads its diagonal block (and pivot
-// reciprocals) for its next block while other warps run their chains.
-constexpr int kSolveRowsPerThread = kMaxNmax / kCtaThreads;
-
-__device__ __forceinline__ double pick_row(const double (&xo)[kSolveRowsPerThread], int s) {
-  double v = xo[0];
-#pragma unroll
-  for (int q = 1; q < kSolveRowsPerThread; ++q) v = s == q ? xo[q] : v;
-  return v;
+// ---- deterministic variance totals (VarAccum, gtc_internal.h) ----
+__device__ __forceinline__ int var_scale_exp(double s2) {
+  const int e = ilogb(s2);
+  return (s2 > 0.0 && e > -900 && e < 900) ? e : 0;
 }
 
-__device__ void cta_forward_solve(const double* Lp, int n, double* x) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nwarps = kCtaThreads / 32;
-  double xo[kSolveRowsPerThread];
+// Adds one block's variance sum `ts` (of `tc` candidates, each in [0, s2]).
+__device__ void accum_add(VarAccum* a, double ts, long long tc, double s2) {
+  double w = ldexp(ts, 120 - var_scale_exp(s2));  // < 2^(121 + log2 tc): fits 4 x 42 bits
 #pragma unroll
-  for (int s = 0; s < kSolveRowsPerThread; ++s) {
-    const int r = threadIdx.x + s * kCtaThreads;
-    xo[s] = r < n ? x[r] : 0.0;
+  for (int k = 3; k >= 0; --k) {
+    const double p = floor(ldexp(w, -42 * k));
+    w = __dadd_rn(w, -ldexp(p, 42 * k));  // exact: both are multiples of ulp(w)
+    if (p != 0.0) atomicAdd(&a->limb[k], (unsigned long long)p);
   }
-  const int nblk = (n + 31) / 32;
-  double lr[32];
-  double rinv = 0.0;
-  auto load_diag = [&](int blk) {
-    const int b0 = blk * 32, r = b0 + lane;
-    const bool live = blk < nblk && r < n;
-    const double* Lr = Lp + packed(live ? r : 0);
+  if (tc) atomicAdd(&a->count, (unsigned long long)tc);
+}
+
+__device__ __forceinline__ void accum_read(const VarAccum* a, double s2, double* sum, long long* cnt) {
+  double t = 0.0;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) lr[k] = (live && k <= lane) ? Lr[b0 + k] : 0.0;
-    rinv = live ? __drcp_rn(Lr[r]) : 0.0;
-  };
-  load_diag(warp);
-  for (int blk = 0; blk < nblk; ++blk) {
-    const int b0 = blk * 32, b1 = min(b0 + 32, n);
-    if (warp == blk % nwarps) {
-      const int slot = blk / nwarps;
-      double xr = pick_row(xo, slot);
+  for (int k = 3; k >= 0; --k) t = __dadd_rn(ldexp(t, 42), (double)__ldcg(&a->limb[k]));
+  *sum = ldexp(t, var_scale_exp(s2) - 120);
+  *cnt = (long long)__ldcg(&a->count);
+}
+
+__device__ __forceinline__ void accum_clear(VarAccum* a) {
+  if (a && blockIdx.x == 0 && threadIdx.x < 5) reinterpret_cast<unsigned long long*>(a)[threadIdx.x] = 0ull;
+}
+
+__device__ __forceinline__ void var_source_read(const VarSource& v, double* sum, long long* cnt) {
+  if (v.direct) {
+    *sum = v.sum;
+    *cnt = v.count;
+  } else {
+    accum_read(v.acc, v.s2, sum, cnt);
+  }
+}
+
+// Solves L x = b in place (x in shared memory, length n) for the first n
+// rows of the packed lower factor Lp (shared or global memory), given the
+// pivot reciprocals rinv[i] = 1/L_ii (shared).  Forward substitution in the
+// reference's order: every row subtracts its terms in ascending column order,
+// then multiplies by the pivot reciprocal (<= 1 ulp from the division).  This
+// order keeps chosen configurations identical to the reference's; a blocked
+// inverse variant (explicit diagonal-block inverses + refinement) moved
+// results by ~1e-13 and flipped near-tied picks, so it is not used.
+//
+// Block-pipelined over 32-row blocks, accumulators in shared memory: warp
+// s % 8 runs block s's 32-step diagonal chain in registers (shuffle per
+// step, no barrier); after one barrier, warp (s+1) % 8 folds block s's 32
+// columns into block s+1's rows (one row per lane, fully unrolled so the
+// coefficient loads run ahead of the dependent subtractions) and goes
+// straight on to the next chain, while the other warps fold block s into the
+// rows beyond, off the critical path.
+constexpr int kSolveWarps = kCtaThreads / 32;
+
+__device__ __forceinline__ void fold_block(const double* Lp, double* x, int r, int b0, int kmax) {
+  const double* Lr = Lp + packed(r) + b0;
+  double acc = x[r];
+#pragma unroll
+  for (int k = 0; k < 32; ++k)
+    if (k < kmax) acc = __dadd_rn(acc, -__dmul_rn(Lr[k], x[b0 + k]));
+  x[r] = acc;
+}
+
+__device__ void cta_forward_solve(const double* Lp, int n, double* x, const double* rinv) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nblk = (n + 31) / 32;
+  for (int s = 0; s < nblk; ++s) {
+    const int b0 = 32 * s, kmax = min(32, n - b0);
+    if (warp == s % kSolveWarps) {  // rows of block s are complete w.r.t. columns < b0
+      const int r = b0 + lane;
+      const bool live = r < n;
+      const double* Lr = Lp + packed(live ? r : b0) + b0;
+      double lr[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) lr[k] = (live && k < lane) ? Lr[k] : 0.0;
+      const double ri = live ? rinv[r] : 0.0;
+      double xr = live ? x[r] : 0.0;
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
-        if (b0 + k < b1) {
-          if (lane == k) xr = __dmul_rn(xr, rinv);
-          const double xi = __shfl_sync(0xffffffffu, xr, k);
-          if (lane > k) xr = __dadd_rn(xr, -__dmul_rn(lr[k], xi));
+        if (k < kmax) {
+          const double xi = __shfl_sync(0xffffffffu, __dmul_rn(xr, ri), k);
+          if (lane == k) xr = xi;
+          else if (lane > k) xr = __dadd_rn(xr, -__dmul_rn(lr[k], xi));
         }
       }
-      if (b0 + lane < b1) x[b0 + lane] = xr;
-#pragma unroll
-      for (int s = 0; s < kSolveRowsPerThread; ++s)
-        if (s == slot) xo[s] = xr;
-      load_diag(blk + nwarps);  // off the critical path: next owned block
+      if (live) x[r] = xr;
     }
-    __syncthreads();  // block b's solution visible
-#pragma unroll
-    for (int s = 0; s < kSolveRowsPerThread; ++s) {
-      const int r = threadIdx.x + s * kCtaThreads;
-      if (r >= b1 && r < n) {
-        const double* Lr = Lp + packed(r);
-        double acc = xo[s];
-        for (int i = b0; i < b1; ++i) acc = __dadd_rn(acc, -__dmul_rn(Lr[i], x[i]));
-        xo[s] = acc;
+    __syncthreads();  // block s solved; every fold of block s-1 done
+    if (s + 1 < nblk) {
+      const int wn = (s + 1) % kSolveWarps;
+      if (warp == wn) {
+        if (b0 + 32 + lane < n) fold_block(Lp, x, b0 + 32 + lane, b0, kmax);
+      } else {
+        const int t = threadIdx.x - (warp > wn ? 32 : 0);
+        for (int r = b0 + 64 + t; r < n; r += kCtaThreads - 32) fold_block(Lp, x, r, b0, kmax);
       }
     }
   }
@@ -224,13 +250,13 @@ __device__ double direct_kernel(const double* xa, const double* xb, int d, doubl
 }
 
 // Shared-memory layout of the single-CTA GP kernels:
-//   xs  work vector (n_max)
-//   ys  y copy      (n_max)
+//   xs    work vector (n_max)
+//   rinv  pivot reciprocals 1/L_ii of the factor's rows (n_max)
 //   Ls  packed L rows [0, rows) (staged when they fit, else read from global)
 struct CtaSmem {
   double* Ls;
   double* xs;
-  double* ys;
+  double* rinv;
   bool staged;
 };
 
@@ -241,7 +267,7 @@ __device__ CtaSmem cta_smem_layout(double* base, int n_max, int rows, bool stage
   CtaSmem m;
   m.staged = staged;
   m.xs = base;
-  m.ys = base + n_max;
+  m.rinv = base + n_max;
   m.Ls = base + even_up(2 * (int64_t)n_max);
   (void)rows;
   return m;
@@ -260,7 +286,7 @@ __device__ bool cta_border_row(const GpDev& g, KernelParams k, double noise, dou
     m.xs[q] = direct_kernel<NU>(g.train_x + (int64_t)q * g.d, xr, g.d, k.lengthscale, k.s2);
   __syncthreads();
   if (tm && threadIdx.x == 0) tm[2] = gtc_globaltimer();
-  cta_forward_solve(lp_of(g, m), row, m.xs);
+  cta_forward_solve(lp_of(g, m), row, m.xs, m.rinv);
   if (tm && threadIdx.x == 0) tm[3] = gtc_globaltimer();
   double part = 0.0;
   for (int q = threadIdx.x; q < row; q += blockDim.x) part = __dadd_rn(part, __dmul_rn(m.xs[q], m.xs[q]));
@@ -284,6 +310,7 @@ __device__ bool cta_border_row(const GpDev& g, KernelParams k, double noise, dou
   if (threadIdx.x == 0) {
     Lrow[row] = lnn;
     if (m.staged) m.Ls[packed(row) + row] = lnn;
+    m.rinv[row] = __drcp_rn(lnn);
   }
   __syncthreads();
   return true;
@@ -409,6 +436,10 @@ __global__ void __launch_bounds__(kCtaThreads)
     if (n0 == 0) g.sc->y0 = y_new;
   }
   cta_stage_L(g, n0, m);  // includes __syncthreads
+  {
+    const double* lp = lp_of(g, m);
+    for (int i = threadIdx.x; i < n0; i += blockDim.x) m.rinv[i] = __drcp_rn(lp[packed(i) + i]);
+  }  // visible after the Gram-row barrier in cta_border_row
   if (threadIdx.x == 0) {
     tm[1] = gtc_globaltimer();
     double s = 0.0;
@@ -440,9 +471,9 @@ struct ExtendArgs {
   double lengthscale, s2;
   double* mu;
   double* var;
-  const uint32_t* visited;  // with part_sum: per-tile variance partials (final pass)
-  double* part_sum;
-  long long* part_cnt;
+  const uint32_t* visited;  // with acc: per-tile variance totals (final pass)
+  VarAccum* acc;
+  VarAccum* acc_clear;
 };
 
 // Rows [n0, n0+r) of V for every candidate, r <= R, streaming rows [0, n0)
@@ -450,6 +481,7 @@ struct ExtendArgs {
 // thread.  With final_pass the posterior mean/variance are produced too.
 template <int R, int NU>
 __global__ void __launch_bounds__(kExtendThreads) k_extend(ExtendArgs a) {
+  accum_clear(a.acc_clear);  // next generation's accumulator (even when the pass is skipped)
   if (a.check_status && a.g.sc->status != 0) return;  // bordered row failed: host refactors
   extern __shared__ double sm[];
   const int n0 = a.n0, r = a.r;
@@ -577,10 +609,10 @@ __global__ void __launch_bounds__(kExtendThreads) k_extend(ExtendArgs a) {
     const double var0 = fmax(__dadd_rn(a.s2, -q0), 0.0), var1 = fmax(__dadd_rn(a.s2, -q1), 0.0);
     *reinterpret_cast<double2*>(a.mu + j0) = make_double2(b0, b1);
     *reinterpret_cast<double2*>(a.var + j0) = make_double2(var0, var1);
-    if (a.part_sum) {
+    if (a.acc) {
       // this tile's share of the mean posterior variance over the unvisited
-      // candidates (strategies.hpp:406-407); plain stores, consumed by the
-      // next kernel on the stream (k_select), so no fence is needed
+      // candidates (strategies.hpp:406-407), added to the run's fixed-point
+      // total; consumed by the next kernel on the stream (k_select)
       __shared__ double red[32];
       __shared__ long long redl[32];
       const uint32_t w = j0 < a.sp.n ? __ldg(a.visited + (j0 >> 5)) : 0xffffffffu;
@@ -588,10 +620,7 @@ __global__ void __launch_bounds__(kExtendThreads) k_extend(ExtendArgs a) {
       const bool u1 = j0 + 1 < a.sp.n && !((w >> ((j0 + 1) & 31)) & 1u);
       const double ts = block_sum((u0 ? var0 : 0.0) + (u1 ? var1 : 0.0), red);
       const long long tc = block_sum_ll((long long)u0 + (long long)u1, redl);
-      if (threadIdx.x == 0) {
-        a.part_sum[blockIdx.x] = ts;
-        a.part_cnt[blockIdx.x] = tc;
-      }
+      if (threadIdx.x == 0) accum_add(a.acc, ts, tc, a.s2);
     }
   }
 }
@@ -663,28 +692,6 @@ __device__ void var_partial(const double* __restrict__ var, const uint32_t* __re
   *out_cnt = block_sum_ll(c, redl);
 }
 
-// Deterministic fixed-order sum of `count` block partials, in every block.
-__device__ void reduce_partials(const double* ps, const long long* pc, int count, double* red,
-                                long long* redl, double* sum, long long* cnt) {
-  // four independent accumulators keep four loads in flight per thread
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  long long c0 = 0, c1 = 0, c2 = 0, c3 = 0;
-  const int bd = blockDim.x;
-  int b = threadIdx.x;
-  for (; b + 3 * bd < count; b += 4 * bd) {
-    const double p0 = __ldcg(ps + b), p1 = __ldcg(ps + b + bd), p2 = __ldcg(ps + b + 2 * bd), p3 = __ldcg(ps + b + 3 * bd);
-    const long long q0 = __ldcg(pc + b), q1 = __ldcg(pc + b + bd), q2 = __ldcg(pc + b + 2 * bd), q3 = __ldcg(pc + b + 3 * bd);
-    s0 += p0; s1 += p1; s2 += p2; s3 += p3;
-    c0 += q0; c1 += q1; c2 += q2; c3 += q3;
-  }
-  for (; b < count; b += bd) {
-    s0 += __ldcg(ps + b);
-    c0 += __ldcg(pc + b);
-  }
-  *sum = block_sum((s0 + s1) + (s2 + s3), red);
-  *cnt = block_sum_ll((c0 + c1) + (c2 + c3), redl);
-}
-
 __global__ void __launch_bounds__(kReduceThreads)
     k_varsum(const double* __restrict__ var, const uint32_t* __restrict__ visited, int64_t n,
              double* partial_sum, int64_t* partial_cnt, unsigned int* counter, VarTotals* totals) {
@@ -698,7 +705,15 @@ __global__ void __launch_bounds__(kReduceThreads)
     partial_cnt[blockIdx.x] = c;
   }
   if (!last_block(counter)) return;
-  reduce_partials(partial_sum, reinterpret_cast<const long long*>(partial_cnt), gridDim.x, red, redl, &s, &c);
+  // fixed-order sum of the block partials (gridDim.x <= 1184)
+  s = 0.0;
+  c = 0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    s += __ldcg(partial_sum + b);
+    c += __ldcg(reinterpret_cast<const long long*>(partial_cnt) + b);
+  }
+  s = block_sum(s, red);
+  c = block_sum_ll(c, redl);
   if (threadIdx.x == 0) {
     totals->sum = s;
     totals->count = c;
@@ -817,139 +832,387 @@ __device__ __forceinline__ void score_into(Best* b, double m, double sd, double 
   }
 }
 
-// Block reduction of the per-thread (best per AF, first eligible, count)
-// followed by the last-block merge into the result record.
+// Block reduction of the per-thread (best per AF, first eligible + whether
+// its keys were finite, count) with one barrier, then the last-block merge
+// into the result record.  A finite key implies a finite (non-NaN) score, so
+// the first-candidate rule (portfolio.hpp:52: the first eligible candidate is
+// taken unconditionally; if its score is NaN nothing beats it) needs an exact
+// score only when the global first candidate had non-finite inputs.
+struct SelPart {
+  Best b[3];
+  int64_t first;
+  int finite;
+  long long cnt;
+};
+
 template <uint32_t MASK>
-__device__ void select_finish(const SelCtx& c, Best* b, int64_t first, long long cnt, double best,
-                              double lambda, double mean_var, int cv_fallback, int gp_status) {
-  __shared__ Best redb[32];
-  __shared__ int64_t redi[32];
-  __shared__ long long redl[32];
-  cnt = block_sum_ll(cnt, redl);
+__device__ __forceinline__ SelPart sel_merge(SelPart x, const SelPart& y) {
 #pragma unroll
   for (int af = 0; af < 3; ++af)
-    if (MASK & (1u << af)) b[af] = block_best(b[af], redb);
-  first = block_min(first, redi);
-  if (threadIdx.x == 0) {
-    for (int af = 0; af < 3; ++af) {
-      c.b.pscore[blockIdx.x * 3 + af] = b[af].s;
-      c.b.ppos[blockIdx.x * 3 + af] = b[af].p;
-    }
-    c.b.pfirst[blockIdx.x] = first;
-    c.b.pcnt[blockIdx.x] = cnt;
+    if (MASK & (1u << af)) x.b[af] = better(x.b[af], y.b[af]);
+  if (y.first < x.first) {
+    x.first = y.first;
+    x.finite = y.finite;
   }
-  if (!last_block(c.b.counter)) return;
-  Best f[3] = {{0.0, INT64_MAX}, {0.0, INT64_MAX}, {0.0, INT64_MAX}};
-  int64_t ff = INT64_MAX;
-  long long fc = 0;
-  for (int blk = threadIdx.x; blk < gridDim.x; blk += blockDim.x) {
-    for (int af = 0; af < 3; ++af)
-      f[af] = better(f[af], Best{__ldcg(c.b.pscore + blk * 3 + af),
-                                 (int64_t)__ldcg(reinterpret_cast<const long long*>(c.b.ppos) + blk * 3 + af)});
-    ff = min(ff, (int64_t)__ldcg(reinterpret_cast<const long long*>(c.b.pfirst) + blk));
-    fc += __ldcg(c.b.pcnt + blk);
-  }
-  for (int af = 0; af < 3; ++af) f[af] = block_best(f[af], redb);
-  ff = block_min(ff, redi);
-  fc = block_sum_ll(fc, redl);
-  if (threadIdx.x == 0) {
-    c.out->first_nan_mask = 0;
+  x.cnt += y.cnt;
+  return x;
+}
+
+template <uint32_t MASK>
+__device__ __forceinline__ SelPart sel_warp_reduce(SelPart v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    SelPart w;
+#pragma unroll
     for (int af = 0; af < 3; ++af) {
-      c.out->best_nonnan_pos[af] = -1;
-      c.out->best_nonnan_score[af] = 0.0;
+      if (!(MASK & (1u << af))) continue;
+      w.b[af].s = __shfl_xor_sync(0xffffffffu, v.b[af].s, o);
+      w.b[af].p = __shfl_xor_sync(0xffffffffu, v.b[af].p, o);
     }
-    for (int af = 0; af < 3; ++af) {
-      int64_t pos = -1;
-      double sc = 0.0;
-      if ((c.af_mask & (1u << af)) && fc > 0) {
-        // first-candidate rule (portfolio.hpp:52): the first eligible
-        // candidate is taken unconditionally; if its score is NaN nothing
-        // can beat it.
-        const double s_first = score_of(af, c.mu[ff], sd_at(c, ff), best, lambda);
-        if (s_first != s_first || f[af].p == INT64_MAX) {
-          pos = ff;
-          sc = s_first;
-        } else {
-          pos = f[af].p;
-          sc = f[af].s;
-        }
-        // the pieces a cross-shard merge needs to apply the same rule
-        c.out->best_nonnan_pos[af] = f[af].p == INT64_MAX ? -1 : f[af].p;
-        c.out->best_nonnan_score[af] = f[af].s;
-        if (s_first != s_first) c.out->first_nan_mask |= 1u << af;
+    w.first = __shfl_xor_sync(0xffffffffu, v.first, o);
+    w.finite = __shfl_xor_sync(0xffffffffu, v.finite, o);
+    w.cnt = __shfl_xor_sync(0xffffffffu, v.cnt, o);
+    v = sel_merge<MASK>(v, w);
+  }
+  return v;
+}
+
+template <uint32_t MASK>
+__device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first_finite, long long cnt,
+                              double best, double lambda, double mean_var, int cv_fallback, int gp_status) {
+  __shared__ SelPart red[32];
+  __shared__ bool is_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  SelPart v{{b[0], b[1], b[2]}, first, first_finite, cnt};
+  v = sel_warp_reduce<MASK>(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    const SelPart none{{{0.0, INT64_MAX}, {0.0, INT64_MAX}, {0.0, INT64_MAX}}, INT64_MAX, 1, 0};
+    v = sel_warp_reduce<MASK>(lane < nw ? red[lane] : none);
+    if (lane == 0) {
+      for (int af = 0; af < 3; ++af) {
+        c.b.pscore[blockIdx.x * 3 + af] = v.b[af].s;
+        c.b.ppos[blockIdx.x * 3 + af] = v.b[af].p;
       }
-      c.out->position[af] = pos;
-      c.out->score[af] = sc;
+      c.b.pfirst[blockIdx.x] = v.first;
+      c.b.pfinite[blockIdx.x] = v.finite;
+      c.b.pcnt[blockIdx.x] = v.cnt;
+      __threadfence();
+      is_last = atomicAdd(c.b.counter, 1u) == gridDim.x - 1;
     }
-    c.out->first_eligible = fc > 0 ? ff : -1;
-    c.out->lambda = lambda;
-    c.out->mean_variance = mean_var;
-    c.out->best_std = best;
-    c.out->n_candidates = (int64_t)fc;
-    c.out->cv_fallback = cv_fallback;
-    c.out->gp_status = gp_status;
-    *c.b.counter = 0;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  // last block: merge the per-block records (all loads in flight at once)
+  __threadfence();
+  const SelPart none{{{0.0, INT64_MAX}, {0.0, INT64_MAX}, {0.0, INT64_MAX}}, INT64_MAX, 1, 0};
+  SelPart f = none;
+  for (int blk = threadIdx.x; blk < (int)gridDim.x; blk += blockDim.x) {
+    SelPart y;
+#pragma unroll
+    for (int af = 0; af < 3; ++af)
+      y.b[af] = Best{__ldcg(c.b.pscore + blk * 3 + af),
+                     (int64_t)__ldcg(reinterpret_cast<const long long*>(c.b.ppos) + blk * 3 + af)};
+    y.first = (int64_t)__ldcg(reinterpret_cast<const long long*>(c.b.pfirst) + blk);
+    y.finite = __ldcg(c.b.pfinite + blk);
+    y.cnt = __ldcg(c.b.pcnt + blk);
+    f = sel_merge<MASK>(f, y);
+  }
+  f = sel_warp_reduce<MASK>(f);
+  __syncthreads();  // red[] reuse
+  if (lane == 0) red[warp] = f;
+  __syncthreads();
+  if (warp != 0) return;
+  f = sel_warp_reduce<MASK>(lane < nw ? red[lane] : none);
+  if (lane != 0) return;
+  const int64_t ff = f.first;
+  const long long fc = f.cnt;
+  c.out->first_nan_mask = 0;
+  for (int af = 0; af < 3; ++af) {
+    c.out->best_nonnan_pos[af] = -1;
+    c.out->best_nonnan_score[af] = 0.0;
+  }
+  for (int af = 0; af < 3; ++af) {
+    int64_t pos = -1;
+    double sc = 0.0;
+    if ((c.af_mask & (1u << af)) && fc > 0) {
+      // first-candidate rule (portfolio.hpp:52)
+      bool first_nan = false;
+      double s_first = 0.0;
+      if (!f.finite || f.b[af].p == INT64_MAX) {
+        s_first = score_of(af, c.mu[ff], sd_at(c, ff), best, lambda);
+        first_nan = s_first != s_first;
+      }
+      if (first_nan || f.b[af].p == INT64_MAX) {
+        pos = ff;
+        sc = s_first;
+      } else {
+        pos = f.b[af].p;
+        sc = f.b[af].s;
+      }
+      // the pieces a cross-shard merge needs to apply the same rule
+      c.out->best_nonnan_pos[af] = f.b[af].p == INT64_MAX ? -1 : f.b[af].p;
+      c.out->best_nonnan_score[af] = f.b[af].s;
+      if (first_nan) c.out->first_nan_mask |= 1u << af;
+    }
+    c.out->position[af] = pos;
+    c.out->score[af] = sc;
+  }
+  c.out->first_eligible = fc > 0 ? ff : -1;
+  c.out->lambda = lambda;
+  c.out->mean_variance = mean_var;
+  c.out->best_std = best;
+  c.out->n_candidates = (int64_t)fc;
+  c.out->cv_fallback = cv_fallback;
+  c.out->gp_status = gp_status;
+  *c.b.counter = 0;
+}
+
+// ---------------------------------------------------- pruned selection
+//
+// Most of the selection's time is the FP64 erfc/exp/sqrt/div of every
+// candidate's score, yet only the block's top few can be the argmax.  Phase 1
+// computes a cheap FP32 UPPER BOUND ("key") of every candidate's FP64 score
+// from the normal-tail (Mills ratio) inequalities, x >= 0:
+//   2/(sqrt(x^2+4)+x) <= R(x) = (1-Phi(x))/phi(x) <= 4/(3x+sqrt(x^2+8))
+// (Birnbaum 1942; Sampford 1953).  With h(z) = z Phi(z) + phi(z), EI = sd h(z):
+//   z >= 0: h(z) = z + h(-z) <= z + phi(z) 4/(sqrt(z^2+4)+z)^2
+//   z <  0: h(-x) = phi(x)(1 - x R(x)) <= phi(x) 4/(sqrt(x^2+4)+x)^2      (log2 key)
+// PI = Phi(z):
+//   z <  0: Phi(-x) = phi(x) R(x) <= phi(x) 4/(3x + sqrt(x^2+8))          (log2 key)
+//   z >= 0: 1 - Phi(z) >= phi(z) 2/(sqrt(z^2+4)+z) =: q                 (key q, U = 1 - q)
+// -LCB = lambda sd - mu with an FP32 sd rounded up                         (linear key)
+// Tails are bounded in the log2 domain, so candidates far out in the tail
+// (z << -13, where FP32 exp underflows) still prune against each other.
+// Every key carries margins well above its FP32 evaluation error (<= 1e-3 in
+// log2 up to |z| = 40, where the FP64 scores underflow to exactly 0) and above
+// the rounding of the FP64 scores themselves (2^-30 relative, a 2^-1039 floor
+// for subnormal results), and is rounded up.  The block then scores EXACTLY
+// (the reference's FP64 formulas) its candidate with the largest key -> T,
+// a score the block's best must reach, and scores exactly only candidates
+// whose key does not prove score < T.  The block's best (max score, lowest
+// position, NaN skipped) always passes, so the result is identical to scoring
+// every candidate.  Non-finite inputs get +inf keys (always scored exactly).
+#ifndef GTC_SEL_STOP
+#define GTC_SEL_STOP 0  // diagnostic cut points of the selection (tools/sel_bench.cu); 0 = full kernel
+#endif
+constexpr int kSelPer = 8;  // candidates per thread per chunk (keys kept in registers)
+constexpr float kLog2Slack = 0x1p-6f;  // log2-domain margin (1.1 % relative)
+constexpr float kLog2Floor = -1039.0f;  // below this, subnormal rounding dominates
+constexpr float kHalfLog2e = 0.72134752f;  // 1 / (2 ln 2)
+
+// MUFU approximations (PTX: relative error <= 2^-22 for rcp/rsqrt/ex2,
+// absolute <= 2^-22 for lg2 near 1, 2 ulp otherwise); all arguments here
+// are normal floats and the margins above cover these errors.
+__device__ __forceinline__ float f_rcp(float x) { float r; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+__device__ __forceinline__ float f_rsqrt(float x) { float r; asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+__device__ __forceinline__ float f_lg2(float x) { float r; asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+__device__ __forceinline__ float f_ex2(float x) { float r; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+__device__ __forceinline__ float f_sqrt(float x) { return x * f_rsqrt(x); }  // x > 0
+
+// `spread` is the variance (run path, sd = sqrt(var) as strategies.hpp:385)
+// or the std itself (best_candidate spans).  key[af] as described above;
+// *pi_hi marks a PI key holding q (z >= 0).
+// `base_ok`: |best -/+ lambda| < 1e30 (per block).  Inputs outside the
+// guarded ranges (sd == 0, NaN, inf, |values| >= 1e30) get +inf keys.
+template <uint32_t MASK, bool SD>
+__device__ __forceinline__ void bound_keys(float* key, bool* pi_hi, double mu, double spread, bool base_ok,
+                                           double bm_ei, double bp_pi, double lambda) {
+  const float kInf = __int_as_float(0x7f800000);
+  *pi_hi = false;
+  const float sp = __double2float_rn(spread);
+  const float mf = __double2float_rn(mu);  // NaN/inf/huge mu fail the guard
+  if (!(base_ok && sp > (SD ? 1e-15f : 1e-30f) && sp < (SD ? 1e15f : 1e30f) && fabsf(mf) < 1e30f)) {
+#pragma unroll
+    for (int af = 0; af < 3; ++af) key[af] = kInf;  // exact scoring
+    return;
+  }
+  const float rs = SD ? f_rcp(sp) : f_rsqrt(sp);  // 1 / sd
+  const float sdf = SD ? sp : sp * rs;            // sd, relative error <= 2^-21
+  if (MASK & 1u) {
+    const double m = __dadd_rn(bm_ei, -mu);  // the reference's margin, exactly
+    const float z = __double2float_rn(m) * rs;
+    if (z >= 0.0f) {
+      float t = 1e-38f;  // z > 13: >= phi(13) 4/(sqrt(173)+13)^2 = 4.7e-40
+      if (z <= 13.0f) {
+        const float den = f_sqrt(fmaf(z, z, 4.0f)) + z;
+        t = 1.5957691f * f_ex2(-z * z * kHalfLog2e) * f_rcp(den * den);
+      }
+      const double u = fma((double)(sdf * t), 1.0 + 0x1p-8, m);
+      key[0] = f_lg2(__double2float_ru(__dmul_rn(u, 1.0 + 0x1p-30))) + kLog2Slack;
+    } else {
+      const float x = -z, x2 = x * x;
+      const float den = f_sqrt(x2 + 4.0f) + x;
+      const float k = fmaf(-x2, kHalfLog2e, f_lg2(sdf * 1.5957691f * f_rcp(den * den))) + kLog2Slack;
+      key[0] = x > 40.0f ? -kInf : fmaxf(k, kLog2Floor);  // x > 40: the FP64 score is exactly 0
+    }
+  }
+  if (MASK & 2u) {
+    const double m = __dadd_rn(bp_pi, -mu);
+    const float z = __double2float_rn(m) * rs;
+    if (z >= 0.0f) {  // q = lower bound of 1 - Phi(z); ex2 flushes to 0 beyond z ~ 13.2
+      const float q = 0.79788456f * f_ex2(-z * z * kHalfLog2e) * f_rcp(f_sqrt(fmaf(z, z, 4.0f)) + z);
+      key[1] = q * (1.0f - 0x1p-8f);  // decoded as 1 - q + 2^-50
+      *pi_hi = true;
+    } else {
+      const float x = -z, x2 = x * x;
+      const float k = fmaf(-x2, kHalfLog2e, f_lg2(1.5957691f * f_rcp(fmaf(3.0f, x, f_sqrt(x2 + 8.0f))))) + kLog2Slack;
+      key[1] = x > 40.0f ? -kInf : fmaxf(k, kLog2Floor);  // x > 40: erfc underflows, score exactly 0
+    }
+  }
+  if (MASK & 4u) {
+    const double ls = __dmul_rn(lambda, __dmul_rn((double)sdf, 1.0 + 0x1p-20));
+    const double slack = fma(__dadd_rn(fabs(mu), ls), 0x1p-40, 0x1p-1000);
+    key[2] = __double2float_ru(__dadd_rn(__dadd_rn(ls, -mu), slack));
   }
 }
 
-// Scan of a strided slice: software-pipelined (the next candidate's visited
-// word, mean and variance/std are in flight while the current one is scored;
-// one copy of the erfc/exp code keeps the loop in the instruction cache).
-// Shared by the run selection and the span-based best_candidate path.
-template <uint32_t MASK>
-__device__ void select_body(const SelCtx& c, double best, double lambda, double mean_var,
-                            int cv_fallback, int gp_status) {
+// Ordering of keys for picking the block's threshold candidate.
+__device__ __forceinline__ float key_rank(int af, float k, bool pi_hi) {
+  return (af == 1 && pi_hi) ? 2.0f - k : k;
+}
+
+// Per-AF threshold in the form the survivor test uses.
+struct Thr {
+  double t;  // exact score reached in this block (-inf: none)
+  float lt;  // float_rd(log2 t) for the log2-domain keys (-inf when t <= 0)
+};
+
+__device__ __forceinline__ bool may_reach(int af, float k, bool pi_hi, const Thr& th) {
+  if (af == 2) return !((double)k < th.t);
+  if (af == 1 && pi_hi) return !(__dadd_rn(__dadd_rn(1.0, -(double)k), 0x1p-50) < th.t);
+  return !(k < th.lt);
+}
+
+template <uint32_t MASK, bool SD>
+__device__ void select_pruned(const SelCtx& c, double best, double lambda, double mean_var, int cv_fallback,
+                              int gp_status, int per) {
+  __shared__ Best redb[32];
+  __shared__ double s_thr[3];
   Best b[3] = {{0.0, INT64_MAX}, {0.0, INT64_MAX}, {0.0, INT64_MAX}};
   int64_t first = INT64_MAX;
+  int first_finite = 1;
   long long cnt = 0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const double* spread = c.sdv ? c.sdv : c.var;
-  bool e_cur = false;
-  double m_cur = 0.0, v_cur = 0.0;
-  if (j < c.n) {
-    e_cur = eligible(c, j);
-    m_cur = c.mu[j];
-    v_cur = spread[j];
-  }
+  const double bm_ei = __dadd_rn(best, -lambda), bp_pi = __dadd_rn(best, lambda);
+  const bool base_ok = fabs(bm_ei) < 1e30 && fabs(bp_pi) < 1e30;
+  const double* spread = SD ? c.sdv : c.var;
+  double thr[3] = {-CUDART_INF, -CUDART_INF, -CUDART_INF};  // running block threshold (exact scores)
+  const int64_t chunk = (int64_t)per * blockDim.x;
+  for (int64_t base = blockIdx.x * chunk; base < c.n; base += (int64_t)gridDim.x * chunk) {
+    float key[kSelPer][3];
+    uint32_t elig = 0, hi = 0;
+    float top_r[3] = {-__int_as_float(0x7f800000), -__int_as_float(0x7f800000), -__int_as_float(0x7f800000)};
+    int top_k[3] = {-1, -1, -1};
+#pragma unroll
+    for (int g = 0; g < kSelPer; g += 4) {  // four candidates' loads in flight
+      double mu4[4], sp4[4];
+      bool e4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t j = base + (int64_t)(g + q) * blockDim.x + threadIdx.x;
+        const bool live = g + q < per && j < c.n;
+        mu4[q] = live ? c.mu[j] : 0.0;
+        sp4[q] = live ? spread[j] : 0.0;
+        e4[q] = live && eligible(c, j);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = g + q;
+        if (!e4[q]) continue;
+        const int64_t j = base + (int64_t)k * blockDim.x + threadIdx.x;
+        elig |= 1u << k;
+        ++cnt;
+        bool ph;
+        bound_keys<MASK, SD>(key[k], &ph, mu4[q], sp4[q], base_ok, bm_ei, bp_pi, lambda);
+        hi |= (uint32_t)ph << k;
+        if (j < first) {  // (a thread meets its candidates in ascending position order)
+          first = j;
+          first_finite = 1;
+#pragma unroll
+          for (int af = 0; af < 3; ++af)
+            if ((MASK & (1u << af)) && !(key[k][af] < __int_as_float(0x7f800000))) first_finite = 0;
+        }
+#pragma unroll
+        for (int af = 0; af < 3; ++af) {
+          if (!(MASK & (1u << af))) continue;
+          const float r = key_rank(af, key[k][af], ph);
+          if (key[k][af] < __int_as_float(0x7f800000) && (top_k[af] < 0 || r > top_r[af])) {  // finite inputs only
+            top_r[af] = r;
+            top_k[af] = k;
+          }
+        }
+      }
+    }
+    if (GTC_SEL_STOP == 2) {
+      if (cnt == -7) c.out->lambda = (double)key[0][0] + top_r[0] + top_r[1] + top_r[2];
+      continue;
+    }
+    // the candidate with the largest key, scored exactly, sets the threshold
+#pragma unroll
+    for (int af = 0; af < 3; ++af) {
+      if (!(MASK & (1u << af))) continue;
+      const Best t = block_best(top_k[af] < 0 ? Best{0.0, INT64_MAX}
+                                              : Best{(double)top_r[af], base + (int64_t)top_k[af] * blockDim.x + threadIdx.x},
+                                redb);
+      if (threadIdx.x == 0) {
+        double s = -CUDART_INF;
+        if (t.p != INT64_MAX) {
+          s = score_of(af, c.mu[t.p], sd_at(c, t.p), best, lambda);
+          if (s != s) s = -CUDART_INF;
+        }
+        s_thr[af] = fmax(thr[af], s);
+      }
+    }
+    __syncthreads();
+    // survivors (keys that do not prove score < T), then exact scores for them
+#pragma unroll
+    for (int af = 0; af < 3; ++af) {
+      if (!(MASK & (1u << af))) continue;
+      thr[af] = s_thr[af];
+      const Thr th{thr[af], thr[af] > 0.0 ? __double2float_rd(log2(thr[af])) : -__int_as_float(0x7f800000)};
+      uint32_t surv = 0;
+#pragma unroll
+      for (int k = 0; k < kSelPer; ++k)
+        if (((elig >> k) & 1u) && may_reach(af, key[k][af], (hi >> k) & 1u, th)) surv |= 1u << k;
 #pragma unroll 1
-  for (; j < c.n; j += stride) {
-    const int64_t jn = j + stride;
-    bool e_nxt = false;
-    double m_nxt = 0.0, v_nxt = 0.0;
-    if (jn < c.n) {
-      e_nxt = eligible(c, jn);
-      m_nxt = c.mu[jn];
-      v_nxt = spread[jn];
+      while (surv) {
+        const int k = __ffs(surv) - 1;
+        surv &= surv - 1;
+        const int64_t j = base + (int64_t)k * blockDim.x + threadIdx.x;
+        const double s = score_of(af, c.mu[j], sd_at(c, j), best, lambda);
+        if (s == s) b[af] = better(b[af], Best{s, j});
+      }
     }
-    if (e_cur) {
-      ++cnt;
-      first = min(first, j);
-      // cand_stds = sqrt(cand_vars), strategies.hpp:385
-      score_into<MASK>(b, m_cur, c.sdv ? v_cur : sqrt(v_cur), best, lambda, j);
-    }
-    e_cur = e_nxt;
-    m_cur = m_nxt;
-    v_cur = v_nxt;
+    __syncthreads();  // s_thr reuse
   }
-  select_finish<MASK>(c, b, first, cnt, best, lambda, mean_var, cv_fallback, gp_status);
+  if (GTC_SEL_STOP == 2 || GTC_SEL_STOP == 3) {
+    if (cnt == -7) c.out->lambda = b[0].s + b[1].s + b[2].s + (double)first;
+    return;
+  }
+  select_finish<MASK>(c, b, first, first_finite, cnt, best, lambda, mean_var, cv_fallback, gp_status);
 }
 
+// Resident blocks per SM of the selection kernels: a single AF fits 64
+// registers (two blocks), several AFs keep their keys in 128 (one block).
+__host__ __device__ constexpr int sel_blocks_per_sm(uint32_t mask) { return (mask & (mask - 1)) ? 1 : 2; }
+
 // Selection for a resident run.  The mean posterior variance over the
-// unvisited candidates comes from the per-tile partials the predictive pass
-// (or k_var_partials) left behind: every block reduces the same `n_partials`
-// values in the same fixed order, so all blocks agree on lambda
-// (strategies.hpp:404-418, acquisition.hpp:73-83) and best_std (gp.hpp:145)
-// without a grid barrier; then the masked argmax as in select_body.
+// unvisited candidates comes from the run's fixed-point variance total (left
+// by the predictive pass or k_var_partials; VarAccum): every block reads the
+// same 40 bytes, so all blocks agree on lambda (strategies.hpp:404-418,
+// acquisition.hpp:73-83) and best_std (gp.hpp:145) without a grid barrier;
+// then the pruned masked argmax (select_pruned).
 template <uint32_t MASK>
-__global__ void __launch_bounds__(kSelectThreads, 1)
-    k_select(SelCtx c, const GpScalars* sc, SelectParams p, const double* part_sum,
-             const long long* part_cnt, int n_partials) {
-  __shared__ double red[32];
-  __shared__ long long redl[32];
+__global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK))
+    k_select(SelCtx c, const GpScalars* sc, SelectParams p, VarSource vs, int per) {
   double s;
   long long cnt;
-  reduce_partials(part_sum, part_cnt, n_partials, red, redl, &s, &cnt);
+  var_source_read(vs, &s, &cnt);
+  if (GTC_SEL_STOP == 1) {
+    if (cnt == -7) c.out->lambda = s;
+    return;
+  }
   const double mean_var = cnt > 0 ? __ddiv_rn(s, (double)cnt) : 0.0;
   double lambda = p.lambda_constant;
   int fallback = 0;
@@ -962,43 +1225,36 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
     }
   }
   const double best = __ddiv_rn(__dadd_rn(p.f_best_raw, -sc->y_mean), sc->y_std);
-  select_body<MASK>(c, best, lambda, mean_var, fallback, sc->status);
+  select_pruned<MASK, false>(c, best, lambda, mean_var, fallback, sc->status, per);
 }
 
-// Total of a partials array (one block, fixed order): a shard's local
-// contribution to the global mean variance.
-__global__ void __launch_bounds__(kReduceThreads)
-    k_reduce_partials(const double* part_sum, const long long* part_cnt, int n_partials, VarTotals* out) {
-  __shared__ double red[32];
-  __shared__ long long redl[32];
+// (sum, count) of a variance source: a shard's local contribution to the
+// global mean variance.
+__global__ void k_var_totals(VarSource v, VarTotals* out) {
   double s;
   long long c;
-  reduce_partials(part_sum, part_cnt, n_partials, red, redl, &s, &c);
-  if (threadIdx.x == 0) {
-    out->sum = s;
-    out->count = c;
-  }
+  var_source_read(v, &s, &c);
+  out->sum = s;
+  out->count = c;
 }
 
-// Variance partials over the unvisited candidates when the pass did not
-// produce them for the current visited set (invalid observation, unmark).
+// Variance total over the unvisited candidates when the pass did not
+// produce it for the current visited set (invalid observation, unmark).
 __global__ void __launch_bounds__(kReduceThreads)
-    k_var_partials(const double* __restrict__ var, const uint32_t* __restrict__ visited, int64_t n,
-                   double* part_sum, long long* part_cnt) {
+    k_var_partials(const double* __restrict__ var, const uint32_t* __restrict__ visited, int64_t n, double s2,
+                   VarAccum* acc, VarAccum* acc_clear) {
   __shared__ double red[32];
   __shared__ long long redl[32];
+  accum_clear(acc_clear);
   double s;
   long long c;
   var_partial(var, visited, n, red, redl, &s, &c);
-  if (threadIdx.x == 0) {
-    part_sum[blockIdx.x] = s;
-    part_cnt[blockIdx.x] = c;
-  }
+  if (threadIdx.x == 0) accum_add(acc, s, c, s2);
 }
 
 template <uint32_t MASK>
-__global__ void __launch_bounds__(kReduceThreads) k_best_candidate(SelCtx c, double best, double lambda) {
-  select_body<MASK>(c, best, lambda, 0.0, 0, 0);
+__global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK)) k_best_candidate(SelCtx c, double best, double lambda, int per) {
+  select_pruned<MASK, true>(c, best, lambda, 0.0, 0, 0, per);
 }
 
 __global__ void k_scores(const double* __restrict__ mu, const double* __restrict__ sd, int64_t n,
@@ -1069,7 +1325,7 @@ void launch_extend(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V
   count_launch();
   ExtendArgs a{sp, g, V, tile_stride, n0, r, final ? 1 : 0, check_status ? 1 : 0,
                k.lengthscale, k.s2, mu, var, vp ? vp->visited : nullptr,
-               (vp && final) ? vp->part_sum : nullptr, vp ? vp->part_cnt : nullptr};
+               (vp && final) ? vp->acc : nullptr, vp ? vp->acc_clear : nullptr};
   const int64_t tiles = sp.n_pad / kTile;
   if (r <= 1) {
     switch (k.nu) {
@@ -1102,30 +1358,36 @@ void launch_varsum(const double* var, const uint32_t* visited, int64_t n, double
   k_varsum<<<reduce_blocks(n), kReduceThreads, 0, s>>>(var, visited, n, ps, pc, counter, totals);
 }
 
-void launch_reduce_partials(const double* part_sum, const long long* part_cnt, int n_partials, VarTotals* out,
-                            cudaStream_t s) {
+void launch_var_totals(const VarSource& src, VarTotals* out, cudaStream_t s) {
   count_launch();
-  k_reduce_partials<<<1, kReduceThreads, 0, s>>>(part_sum, part_cnt, n_partials, out);
+  k_var_totals<<<1, 1, 0, s>>>(src, out);
 }
 
-void launch_var_partials(const double* var, const uint32_t* visited, int64_t n, double* part_sum,
-                         long long* part_cnt, cudaStream_t s) {
+void launch_var_partials(const double* var, int64_t n, double s2, const VarPartials& vp, cudaStream_t s) {
   count_launch();
-  k_var_partials<<<reduce_blocks(n), kReduceThreads, 0, s>>>(var, visited, n, part_sum, part_cnt);
+  k_var_partials<<<reduce_blocks(n), kReduceThreads, 0, s>>>(var, vp.visited, n, s2, vp.acc, vp.acc_clear);
+}
+
+// One wave of kSelectThreads-blocks, `per` candidates per thread per chunk.
+static void select_geometry(int64_t n, uint32_t mask, int* per, int* grid) {
+  const int64_t sms = (int64_t)sel_blocks_per_sm(mask) * sm_count();  // resident blocks
+  *per = (int)std::max<int64_t>(1, std::min<int64_t>(kSelPer, (n + sms * kSelectThreads - 1) / (sms * kSelectThreads)));
+  const int64_t chunk = (int64_t)*per * kSelectThreads;
+  *grid = (int)std::max<int64_t>(1, std::min<int64_t>({(n + chunk - 1) / chunk, sms, (int64_t)kMaxReduceGrid}));
 }
 
 void launch_select(const double* mu, const double* var, const uint32_t* visited, int64_t n,
-                   const GpScalars* sc, SelectParams p, const double* part_sum, const long long* part_cnt,
-                   int n_partials, const ReduceBufs& b, SelectDev* out, cudaStream_t s) {
+                   const GpScalars* sc, SelectParams p, const VarSource& vs, const ReduceBufs& b,
+                   SelectDev* out, cudaStream_t s) {
   count_launch();
   SelCtx c{mu, var, nullptr, visited, nullptr, p.excluded, p.n_excluded, n, p.af_mask, b, out};
-  // exactly one wave of resident blocks (grid-stride inside): a partial
-  // second wave would double the kernel's time
-  const int per_block = kSelectThreads * 2;
-  int grid = (int)std::min<int64_t>((n + per_block - 1) / per_block, (int64_t)sm_count());
-  grid = std::max(std::min(grid, kMaxReduceGrid), 1);
+  // exactly one wave of resident blocks (chunk-stride inside): a partial
+  // second wave would double the kernel's time.  `per` candidates per thread
+  // per chunk spread the candidates over every SM.
+  int per, grid;
+  select_geometry(n, (p.af_mask & 7u) ? (p.af_mask & 7u) : 7u, &per, &grid);
 #define GTC_SELECT_CASE(M) \
-  case M: k_select<M><<<grid, kSelectThreads, 0, s>>>(c, sc, p, part_sum, part_cnt, n_partials); break;
+  case M: k_select<M><<<grid, kSelectThreads, 0, s>>>(c, sc, p, vs, per); break;
   switch (p.af_mask & 7u) {  // launch errors surface through the caller's cudaGetLastError()
     GTC_SELECT_CASE(1)
     GTC_SELECT_CASE(2)
@@ -1133,7 +1395,7 @@ void launch_select(const double* mu, const double* var, const uint32_t* visited,
     GTC_SELECT_CASE(4)
     GTC_SELECT_CASE(5)
     GTC_SELECT_CASE(6)
-    default: k_select<7><<<grid, kSelectThreads, 0, s>>>(c, sc, p, part_sum, part_cnt, n_partials); break;
+    default: k_select<7><<<grid, kSelectThreads, 0, s>>>(c, sc, p, vs, per); break;
   }
 #undef GTC_SELECT_CASE
 }
@@ -1143,10 +1405,11 @@ void launch_best_candidate(const double* mu, const double* sd, const uint8_t* ex
                            cudaStream_t s) {
   count_launch();
   SelCtx c{mu, nullptr, sd, nullptr, excluded, nullptr, 0, n, 1u << af, b, out};
-  const int grid = reduce_blocks(n);
-  if (af == 0) k_best_candidate<1><<<grid, kReduceThreads, 0, s>>>(c, best_std, lambda);
-  else if (af == 1) k_best_candidate<2><<<grid, kReduceThreads, 0, s>>>(c, best_std, lambda);
-  else k_best_candidate<4><<<grid, kReduceThreads, 0, s>>>(c, best_std, lambda);
+  int per, grid;
+  select_geometry(n, 1u << af, &per, &grid);
+  if (af == 0) k_best_candidate<1><<<grid, kSelectThreads, 0, s>>>(c, best_std, lambda, per);
+  else if (af == 1) k_best_candidate<2><<<grid, kSelectThreads, 0, s>>>(c, best_std, lambda, per);
+  else k_best_candidate<4><<<grid, kSelectThreads, 0, s>>>(c, best_std, lambda, per);
 }
 
 void launch_scores(const double* mu, const double* sd, int64_t n, int af, double best_std,

@@ -317,10 +317,13 @@ def main():
         # V-row pass with posterior and mean variance + lambda + EI + argmax, one round trip
         _, s = run.observe(pick, yv, [af], fb, expl, cv)
         run.unmark_visited(pick)             # bench rollback: keep the candidate set fixed
+        phases.append(run.last_phase_ms())
         return s.pick(af), run.last_step_ms(), run.last_pass_ms()
 
+    phases = []
     for _ in range(args.warmup):
         pick, _, _ = step(pick, f_best)
+    phases.clear()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -370,6 +373,8 @@ def main():
                          "kernel_share_of_step": avg_pass / (dev_ms / args.steps),
                          "algorithmic_bytes": alg_bytes, "peak_kind": peak_kind},
             "clocks": clocks.summary(),
+            "phases_us": dict(zip(("append", "pass", "select"),
+                                  (round(1e3 * float(v), 2) for v in np.mean(np.array(phases), axis=0)))),
         }
         if not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(cfg, n)

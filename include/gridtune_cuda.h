@@ -174,6 +174,10 @@ double gtc_last_pass_ms(const gtc_run* run);
 /* CUDA-event milliseconds of the last gtc_observe's device work (all of its
  * kernels, first launch to last, excluding the result readback). */
 double gtc_last_step_ms(const gtc_run* run);
+/* CUDA-event milliseconds of the last appending gtc_observe's phases:
+ * out3[0] mark + bordered-row update, [1] predictive pass, [2] selection
+ * (GTC_ERR_INVALID if the last observe did not append). */
+int gtc_last_phase_ms(const gtc_run* run, double* out3);
 /* Diagnostics: %globaltimer phase marks (ns) of the last bordered-row update
  * seen by gtc_observe: [0] start, [1] factor staged, [2] Gram row, [3] forward
  * solve, [4] pivot/row written, [5] c/e rows, [6] statistics + beta. */

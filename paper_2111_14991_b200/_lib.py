@@ -114,6 +114,7 @@ SIGNATURES = [
     ("gtc_last_pass_ms", C.c_double, [P]),
     ("gtc_last_step_ms", C.c_double, [P]),
     ("gtc_debug_append_marks", C.c_int, [P, U64P]),
+    ("gtc_last_phase_ms", C.c_int, [P, DP]),
     ("gtc_run_stream", C.c_uint64, [P]),
     ("gtc_gp_fit", C.c_int, [C.c_int, C.POINTER(gtc_kernel), DP, DP, C.c_int32, C.c_int32,
                              C.c_double, C.c_double, C.POINTER(P), C.POINTER(gtc_fit_info)]),

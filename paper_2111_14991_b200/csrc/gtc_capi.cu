@@ -84,10 +84,11 @@ struct ReduceScratch {
     int rc;
     if ((rc = dalloc(&b.pvar, nb)) || (rc = dalloc(&b.pvcnt, nb)) || (rc = dalloc(&b.pscore, 3 * nb)) ||
         (rc = dalloc(&b.ppos, 3 * nb)) || (rc = dalloc(&b.pfirst, nb)) || (rc = dalloc(&b.pfinite, nb)) || (rc = dalloc(&b.pcnt, nb)) ||
-        (rc = dalloc(&b.counter, 1)) || (rc = dalloc(&vsum, nb)) || (rc = dalloc(&vcnt, nb)) ||
+        (rc = dalloc(&b.counter, 1)) || (rc = dalloc(&b.gthr, 3)) || (rc = dalloc(&vsum, nb)) || (rc = dalloc(&vcnt, nb)) ||
         (rc = dalloc(&vcounter, 1)) || (rc = dalloc(&totals, 1)) || (rc = dalloc(&sel, 1)))
       return rc;
     GTC_CUDA(cudaMemset(b.counter, 0, sizeof(unsigned int)));
+    GTC_CUDA(cudaMemset(b.gthr, 0, 3 * sizeof(unsigned long long)));
     GTC_CUDA(cudaMemset(vcounter, 0, sizeof(unsigned int)));
     GTC_CUDA(cudaMallocHost(&h_sel, sizeof(SelectDev)));
     GTC_CUDA(cudaMallocHost(&h_totals, sizeof(VarTotals)));
@@ -95,7 +96,7 @@ struct ReduceScratch {
   }
   void release() {
     cudaFree(b.pvar); cudaFree(b.pvcnt); cudaFree(b.pscore); cudaFree(b.ppos); cudaFree(b.pfirst); cudaFree(b.pfinite);
-    cudaFree(b.pcnt); cudaFree(b.counter); cudaFree(vsum); cudaFree(vcnt); cudaFree(vcounter);
+    cudaFree(b.pcnt); cudaFree(b.counter); cudaFree(b.gthr); cudaFree(vsum); cudaFree(vcnt); cudaFree(vcounter);
     cudaFree(totals); cudaFree(sel);
     if (h_sel) cudaFreeHost(h_sel);
     if (h_totals) cudaFreeHost(h_totals);
@@ -159,15 +160,15 @@ int factor_with_escalation(GpStore& gp, const gtc_kernel& k, double noise, doubl
 // Rebuilds V rows [0, n) for `space` (chunks of kMaxRows) and the posterior.
 int rebuild_predictions(const SpaceDev& sp, GpStore& gp, const gtc_kernel& k, double* V,
                         int64_t tile_stride, int n, double* mu, double* var, const VarPartials* vp,
-                        cudaStream_t s) {
+                        TileStats* tstat, cudaStream_t s) {
   if (n == 0) {
-    launch_prior(mu, var, sp.n_pad, k.output_variance, s);
+    launch_prior(mu, var, sp.n_pad, k.output_variance, tstat, s);
     GTC_LAUNCHED();
     return GTC_OK;
   }
   for (int n0 = 0; n0 < n; n0 += kMaxRows) {
     const int r = std::min(kMaxRows, n - n0);
-    launch_extend(sp, gp.dev, kparams(k), V, tile_stride, n0, r, n0 + r == n, mu, var, false, vp, s);
+    launch_extend(sp, gp.dev, kparams(k), V, tile_stride, n0, r, n0 + r == n, mu, var, false, vp, tstat, s);
     GTC_LAUNCHED();
   }
   return GTC_OK;
@@ -229,6 +230,8 @@ struct gtc_run {
   uint32_t* visited = nullptr;
   int64_t* excluded = nullptr;
   int excluded_cap = 0;
+  std::vector<int64_t> ex_host;  // last selection's exclusions (sorted, unique)
+  int64_t first_hint = 0;        // <= the lowest unvisited position
   std::vector<uint32_t> visited_host;
   int64_t visited_count = 0;
   int n = 0;
@@ -249,6 +252,7 @@ struct gtc_run {
   // fixed-point variance totals over the unvisited candidates, two
   // alternating generations (VarAccum); acc_valid: the current generation
   // matches the current visited set and predictions
+  TileStats* tstat = nullptr;  // [tiles] posterior summary per tile (selection pruning)
   VarAccum* acc = nullptr;  // [2]
   int acc_gen = 0;
   bool acc_valid = false;
@@ -261,7 +265,7 @@ struct gtc_run {
   VarSource vsrc() const { return VarSource{acc + acc_gen, cfg.kernel.output_variance, 0.0, 0, 0}; }
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;          // last predictive pass
   cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;  // last gtc_observe device span
-  bool pass_timed = false, step_timed = false;
+  bool pass_timed = false, step_timed = false, step_appended = false;
 };
 
 struct gtc_gp {
@@ -341,6 +345,7 @@ extern "C" int gtc_run_destroy(gtc_run* r) {
   cudaFree(r->visited);
   cudaFree(r->excluded);
   cudaFree(r->acc);
+  cudaFree(r->tstat);
   cudaFree(r->d_xnew);
   if (r->h_xnew) cudaFreeHost(r->h_xnew);
   if (r->h_rb) cudaFreeHost(r->h_rb);
@@ -372,7 +377,7 @@ extern "C" int gtc_run_create(gtc_space* space, const gtc_model_config* cfg, gtc
   if ((rc = r->gp.init(cfg->n_max, space->d)) || (rc = r->red.init(space->n)) ||
       (rc = dalloc(&r->V, (size_t)tiles * r->tile_stride)) || (rc = dalloc(&r->mu, space->n_pad)) ||
       (rc = dalloc(&r->var, space->n_pad)) || (rc = dalloc(&r->visited, words)) ||
-      (rc = dalloc(&r->acc, 2))) {
+      (rc = dalloc(&r->acc, 2)) || (rc = dalloc(&r->tstat, tiles))) {
     gtc_run_destroy(r);
     return rc;
   }
@@ -431,7 +436,7 @@ static int refit(gtc_run* r, double start_jitter, gtc_fit_info* info) {
   r->jitter = r->gp.h_sc->jitter;
   const VarPartials vp = r->vp();
   rc = rebuild_predictions(r->space->dev(), r->gp, r->cfg.kernel, r->V, r->tile_stride, n, r->mu, r->var, &vp,
-                           r->stream);
+                           r->tstat, r->stream);
   if (rc) return rc;
   r->predictions_valid = true;
   r->acc_valid = true;
@@ -459,7 +464,7 @@ extern "C" int gtc_fit(gtc_run* r, const int64_t* positions, const double* y_raw
     r->gp.h_sc->y_std = 1.0;
     r->gp.h_sc->jitter = r->jitter;
     GTC_CUDA(cudaMemcpyAsync(r->gp.dev.sc, r->gp.h_sc, sizeof(GpScalars), cudaMemcpyHostToDevice, r->stream));
-    rc = rebuild_predictions(r->space->dev(), r->gp, r->cfg.kernel, r->V, r->tile_stride, 0, r->mu, r->var, nullptr,
+    rc = rebuild_predictions(r->space->dev(), r->gp, r->cfg.kernel, r->V, r->tile_stride, 0, r->mu, r->var, nullptr, r->tstat,
                              r->stream);
     if (rc) return rc;
     GTC_CUDA(cudaStreamSynchronize(r->stream));
@@ -481,7 +486,7 @@ static int enqueue_append(gtc_run* r, int64_t pos, double y_raw, uint32_t* mark)
   GTC_CUDA(cudaEventRecord(r->ev0, r->stream));
   const VarPartials vp = r->vp();
   launch_extend(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, n0, 1, true, r->mu,
-                r->var, true, &vp, r->stream);
+                r->var, true, &vp, r->tstat, r->stream);
   GTC_LAUNCHED();
   GTC_CUDA(cudaEventRecord(r->ev1, r->stream));
   r->pass_timed = true;
@@ -535,13 +540,13 @@ extern "C" int gtc_truncate(gtc_run* r, int32_t n, gtc_fit_info* info) {
 static int ensure_predictions(gtc_run* r) {
   if (r->predictions_valid) return GTC_OK;
   if (r->n == 0) {
-    launch_prior(r->mu, r->var, r->space->n_pad, r->cfg.kernel.output_variance, r->stream);
+    launch_prior(r->mu, r->var, r->space->n_pad, r->cfg.kernel.output_variance, r->tstat, r->stream);
     r->acc_valid = false;
   } else {
     // posterior from the resident V rows (r = 0 new rows)
     const VarPartials vp = r->vp();
     launch_extend(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, r->n, 0, true,
-                  r->mu, r->var, false, &vp, r->stream);
+                  r->mu, r->var, false, &vp, r->tstat, r->stream);
     r->acc_valid = true;
   }
   GTC_LAUNCHED();
@@ -561,6 +566,7 @@ static bool host_mark(gtc_run* r, int64_t pos, int set) {
   if (!set && was) {
     w &= ~bit;
     --r->visited_count;
+    r->first_hint = std::min(r->first_hint, pos);
     return true;
   }
   return false;
@@ -598,6 +604,32 @@ extern "C" int gtc_mean_variance(gtc_run* r, double* out, int64_t* count) {
   return GTC_OK;
 }
 
+// First unvisited position >= p (n if none), from the host's visited bitmap.
+static int64_t first_unvisited_from(const gtc_run* r, int64_t p) {
+  const int64_t n = r->space->n;
+  while (p < n) {
+    const uint32_t w = r->visited_host[p >> 5] | ((1u << (p & 31)) - 1u);  // bits below p: skip
+    if (w != 0xffffffffu) return std::min<int64_t>(n, (p & ~int64_t(31)) + __builtin_ctz(~w));
+    p = (p | 31) + 1;
+  }
+  return n;
+}
+
+// The first eligible position (portfolio.hpp:52's first candidate; -1 if
+// none) and the eligible count, from the host's visited bookkeeping and the
+// sorted exclusion list: the device selection does not have to reduce them.
+static void first_and_count(gtc_run* r, const std::vector<int64_t>& ex, int64_t* first, int64_t* count) {
+  const int64_t n = r->space->n;
+  auto visited = [&](int64_t q) { return (r->visited_host[q >> 5] >> (q & 31)) & 1u; };
+  int64_t ex_unvisited = 0;
+  for (int64_t e : ex) ex_unvisited += visited(e) ? 0 : 1;
+  *count = n - r->visited_count - ex_unvisited;
+  r->first_hint = first_unvisited_from(r, r->first_hint);
+  int64_t q = r->first_hint;
+  while (q < n && std::binary_search(ex.begin(), ex.end(), q)) q = first_unvisited_from(r, q + 1);
+  *first = q < n ? q : -1;
+}
+
 // Makes the run's current variance total match its visited set.
 static int ensure_var_totals(gtc_run* r) {
   if (r->acc_valid) return GTC_OK;  // visited set unchanged since the last pass
@@ -615,28 +647,37 @@ static int enqueue_selection(gtc_run* r, const gtc_select_args* a, bool global_t
   int rc = ensure_predictions(r);
   if (rc) return rc;
   SelectParams p{a->af_mask & 7u, a->lambda_mode, a->lambda_constant, a->cv_initial_sample_mean,
-                 a->cv_initial_mean_variance, a->f_best_raw, nullptr, 0};
-  if (a->n_excluded > 0) {
-    if (a->n_excluded > r->excluded_cap) {
+                 a->cv_initial_mean_variance, a->f_best_raw, nullptr, 0, -1, 0};
+  // exclusions: sorted, unique, in range (the device tests membership)
+  std::vector<int64_t>& ex = r->ex_host;
+  ex.clear();
+  for (int32_t k = 0; k < a->n_excluded; ++k)
+    if (a->excluded[k] >= 0 && a->excluded[k] < r->space->n) ex.push_back(a->excluded[k]);
+  std::sort(ex.begin(), ex.end());
+  ex.erase(std::unique(ex.begin(), ex.end()), ex.end());
+  if (!ex.empty()) {
+    if ((int)ex.size() > r->excluded_cap) {
       cudaFree(r->excluded);
       r->excluded = nullptr;
       r->excluded_cap = 0;
-      if ((rc = dalloc(&r->excluded, a->n_excluded))) return rc;
-      r->excluded_cap = a->n_excluded;
+      if ((rc = dalloc(&r->excluded, ex.size()))) return rc;
+      r->excluded_cap = (int)ex.size();
     }
-    GTC_CUDA(cudaMemcpyAsync(r->excluded, a->excluded, sizeof(int64_t) * a->n_excluded, cudaMemcpyHostToDevice, r->stream));
+    GTC_CUDA(cudaMemcpyAsync(r->excluded, ex.data(), sizeof(int64_t) * ex.size(), cudaMemcpyHostToDevice, r->stream));
     p.excluded = r->excluded;
-    p.n_excluded = a->n_excluded;
+    p.n_excluded = (int)ex.size();
   }
+  first_and_count(r, ex, &p.first_eligible, &p.n_candidates);
   if (global_totals) {
     const VarSource vs{nullptr, 0.0, global_sum, global_count, 1};
-    launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, vs, r->red.b, r->red.sel, r->stream);
+    launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, vs, r->tstat, r->red.b, r->red.sel,
+                  r->stream);
     GTC_LAUNCHED();
     return GTC_OK;
   }
   if ((rc = ensure_var_totals(r))) return rc;
-  launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, r->vsrc(), r->red.b, r->red.sel,
-                r->stream);
+  launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, r->vsrc(), r->tstat, r->red.b,
+                r->red.sel, r->stream);
   GTC_LAUNCHED();
   return GTC_OK;
 }
@@ -699,7 +740,7 @@ extern "C" int gtc_shard_observe(gtc_run* r, const double* x_new, int64_t local_
       GTC_LAUNCHED();
       const VarPartials vp = r->vp();
       launch_extend(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, n0, 1, true, r->mu,
-                    r->var, true, &vp, r->stream);
+                    r->var, true, &vp, r->tstat, r->stream);
       GTC_LAUNCHED();
       r->acc_valid = true;
       r->predictions_valid = true;
@@ -818,6 +859,7 @@ extern "C" int gtc_observe(gtc_run* r, int64_t pos, double y_raw, int32_t valid,
   if (selecting && (rc = enqueue_selection(r, a))) return rc;
   GTC_CUDA(cudaEventRecord(r->ev_step1, r->stream));
   r->step_timed = true;
+  r->step_appended = appended;
   if (selecting)
     GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sel, r->red.sel, sizeof(SelectDev), cudaMemcpyDeviceToHost, r->stream));
   GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sc, r->gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, r->stream));
@@ -872,6 +914,14 @@ extern "C" double gtc_last_pass_ms(const gtc_run* r) {
 }
 extern "C" double gtc_last_step_ms(const gtc_run* r) {
   return r && r->step_timed ? event_ms(r->ev_step0, r->ev_step1) : 0.0;
+}
+extern "C" int gtc_last_phase_ms(const gtc_run* r, double* out) {
+  if (!r || !out) return fail(GTC_ERR_INVALID, "null argument");
+  if (!r->step_timed || !r->pass_timed || !r->step_appended) return fail(GTC_ERR_INVALID, "last observe did not append");
+  out[0] = event_ms(r->ev_step0, r->ev0);
+  out[1] = event_ms(r->ev0, r->ev1);
+  out[2] = event_ms(r->ev1, r->ev_step1);
+  return GTC_OK;
 }
 extern "C" int gtc_debug_append_marks(const gtc_run* r, uint64_t* marks) {
   if (!r || !marks) return fail(GTC_ERR_INVALID, "null argument");
@@ -959,7 +1009,7 @@ extern "C" int gtc_gp_predict(gtc_gp* g, const double* Xstar, int64_t m, double*
     return rc;
   }
   // GpDev with n_max = n so the extend kernel's tile stride matches the factor
-  rc = rebuild_predictions(sp->dev(), g->gp, g->kernel, V, tile_stride, g->n, mu, var, nullptr, g->stream);
+  rc = rebuild_predictions(sp->dev(), g->gp, g->kernel, V, tile_stride, g->n, mu, var, nullptr, nullptr, g->stream);
   cudaError_t e = cudaSuccess;
   if (!rc && mean) e = cudaMemcpyAsync(mean, mu, sizeof(double) * m, cudaMemcpyDeviceToHost, g->stream);
   if (!rc && e == cudaSuccess && variance) e = cudaMemcpyAsync(variance, var, sizeof(double) * m, cudaMemcpyDeviceToHost, g->stream);

@@ -105,6 +105,19 @@ struct VarAccum {
   unsigned long long pad[3];
 };
 
+// Per-tile summary of the posterior written by every final predictive pass
+// (over all candidates of the tile, visited or not): bounds every score in
+// the tile, so the selection can skip whole tiles (gtc_kernels.cu k_select).
+// var_max < 0 marks a tile without candidates.
+struct TileStats {
+  double mu_min;
+  double var_max;
+  double var_min;
+  double mu_seed;   // the unvisited candidate with the minimum mean (lowest
+  double var_seed;  // position on ties) at pass time: a cheap exact-score seed
+  int64_t pos_seed; // -1: none
+};
+
 // Where the selection takes the variance total from: an accumulator of this
 // run (device), or totals passed by value (candidate-axis sharding).
 struct VarSource {
@@ -122,8 +135,10 @@ struct SelectParams {
   double cv_mu_s;
   double cv_var_s;
   double f_best_raw;
-  const int64_t* excluded;  // device
+  const int64_t* excluded;  // device, sorted and unique
   int n_excluded;
+  int64_t first_eligible;   // host-computed: lowest unvisited, non-excluded position (-1: none)
+  int64_t n_candidates;     // host-computed: number of eligible candidates
 };
 
 // Per-block scratch of the selection kernels (sized by reduce_blocks(n)).
@@ -136,6 +151,7 @@ struct ReduceBufs {
   int32_t* pfinite;    // [blocks] the block's first eligible candidate has finite keys (score not NaN)
   long long* pcnt;
   unsigned int* counter;
+  unsigned long long* gthr;  // [3] shared selection thresholds (order-preserving bits; 0 = none)
 };
 
 // --- launchers (gtc_kernels.cu); all asynchronous on `stream` -------------
@@ -169,13 +185,13 @@ struct VarPartials {
 // no-op when the preceding bordered row failed.
 void launch_extend(const SpaceDev& space, const GpDev& g, KernelParams k, double* V,
                    int64_t tile_stride, int n0, int r, bool final, double* mu, double* var,
-                   bool check_status, const VarPartials* vp, cudaStream_t stream);
+                   bool check_status, const VarPartials* vp, TileStats* tstat, cudaStream_t stream);
 
 void launch_var_partials(const double* var, int64_t n, double s2, const VarPartials& vp, cudaStream_t stream);
 // Converts a variance source to (sum, count) on the device.
 void launch_var_totals(const VarSource& src, VarTotals* out, cudaStream_t stream);
 
-void launch_prior(double* mu, double* var, int64_t n, double s2, cudaStream_t stream);
+void launch_prior(double* mu, double* var, int64_t n, double s2, TileStats* tstat, cudaStream_t stream);
 void launch_mark(uint32_t* visited, int64_t pos, int set, cudaStream_t stream);
 
 // Sum of the variance over unvisited candidates -> totals (deterministic).
@@ -186,8 +202,8 @@ void launch_varsum(const double* var, const uint32_t* visited, int64_t n, double
 // Fused mean-variance (from the partials) + lambda + acquisition + masked
 // argmax for every AF in the mask.
 void launch_select(const double* mu, const double* var, const uint32_t* visited, int64_t n,
-                   const GpScalars* sc, SelectParams p, const VarSource& vs, const ReduceBufs& bufs,
-                   SelectDev* out, cudaStream_t stream);
+                   const GpScalars* sc, SelectParams p, const VarSource& vs, const TileStats* tstat,
+                   const ReduceBufs& bufs, SelectDev* out, cudaStream_t stream);
 
 // best_candidate over caller spans of stds (not variances).
 void launch_best_candidate(const double* mu, const double* std, const uint8_t* excluded,

@@ -32,6 +32,8 @@
 #include <math_constants.h>
 
 #include <atomic>
+#include <climits>
+#include <cstdlib>
 #include <cstdint>
 #include <mutex>
 
@@ -40,6 +42,14 @@
 namespace cg = cooperative_groups;
 
 namespace gtc {
+
+#ifdef GTC_SEL_TRACE  // diagnostic per-block %globaltimer marks (tools/sel_bench.cu)
+__device__ unsigned long long g_sel_trace[2048][8];
+#define SEL_MARK(k) \
+  do { if (threadIdx.x == 0) g_sel_trace[blockIdx.x][k] = gtc_globaltimer(); } while (0)
+#else
+#define SEL_MARK(k) do {} while (0)
+#endif
 
 static std::atomic<uint64_t> g_launches{0};
 uint64_t launches() { return g_launches.load(); }
@@ -474,6 +484,7 @@ struct ExtendArgs {
   const uint32_t* visited;  // with acc: per-tile variance totals (final pass)
   VarAccum* acc;
   VarAccum* acc_clear;
+  TileStats* tstat;  // final pass: per-tile posterior summary (optional)
 };
 
 // Rows [n0, n0+r) of V for every candidate, r <= R, streaming rows [0, n0)
@@ -609,28 +620,92 @@ __global__ void __launch_bounds__(kExtendThreads) k_extend(ExtendArgs a) {
     const double var0 = fmax(__dadd_rn(a.s2, -q0), 0.0), var1 = fmax(__dadd_rn(a.s2, -q1), 0.0);
     *reinterpret_cast<double2*>(a.mu + j0) = make_double2(b0, b1);
     *reinterpret_cast<double2*>(a.var + j0) = make_double2(var0, var1);
-    if (a.acc) {
-      // this tile's share of the mean posterior variance over the unvisited
-      // candidates (strategies.hpp:406-407), added to the run's fixed-point
-      // total; consumed by the next kernel on the stream (k_select)
-      __shared__ double red[32];
-      __shared__ long long redl[32];
-      const uint32_t w = j0 < a.sp.n ? __ldg(a.visited + (j0 >> 5)) : 0xffffffffu;
-      const bool u0 = j0 < a.sp.n && !((w >> (j0 & 31)) & 1u);
-      const bool u1 = j0 + 1 < a.sp.n && !((w >> ((j0 + 1) & 31)) & 1u);
-      const double ts = block_sum((u0 ? var0 : 0.0) + (u1 ? var1 : 0.0), red);
-      const long long tc = block_sum_ll((long long)u0 + (long long)u1, redl);
-      if (threadIdx.x == 0) accum_add(a.acc, ts, tc, a.s2);
+    if (a.acc || a.tstat) {
+      // one reduction for the epilogue's tile quantities:
+      //  - this tile's share of the mean posterior variance over the unvisited
+      //    candidates (strategies.hpp:406-407), added to the run's fixed-point
+      //    total; consumed by the next kernel on the stream (k_select)
+      //  - the tile summary (min mean, max/min variance) for tile pruning
+      constexpr int kW = kExtendThreads / 32;
+      __shared__ double rs[kW], rmn[kW], rvx[kW], rvn[kW], rsm[kW], rva[kW];
+      __shared__ long long rc[kW], rpos[kW];
+      const bool in0 = j0 < a.sp.n, in1 = j0 + 1 < a.sp.n;
+      const uint32_t w = (in0 && a.visited) ? __ldg(a.visited + (j0 >> 5)) : 0xffffffffu;
+      const bool u0 = in0 && !((w >> (j0 & 31)) & 1u);
+      const bool u1 = in1 && !((w >> ((j0 + 1) & 31)) & 1u);
+      double ts = (u0 ? var0 : 0.0) + (u1 ? var1 : 0.0);
+      long long tc = (long long)u0 + (long long)u1;
+      // bounds over all candidates; seed = unvisited argmin of the mean
+      double mn = fmin(in0 ? b0 : CUDART_INF, in1 ? b1 : CUDART_INF);
+      double vx = fmax(in0 ? var0 : -CUDART_INF, in1 ? var1 : -CUDART_INF);
+      double vn = fmin(in0 ? var0 : CUDART_INF, in1 ? var1 : CUDART_INF);
+      double sm_ = u0 ? b0 : CUDART_INF, sv = u0 ? var0 : 0.0;
+      long long sp = u0 ? j0 : LLONG_MAX;
+      if (u1 && (b1 < sm_ || sp == LLONG_MAX)) {
+        sm_ = b1;
+        sv = var1;
+        sp = j0 + 1;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ts += __shfl_xor_sync(0xffffffffu, ts, o);
+        tc += __shfl_xor_sync(0xffffffffu, tc, o);
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        vx = fmax(vx, __shfl_xor_sync(0xffffffffu, vx, o));
+        vn = fmin(vn, __shfl_xor_sync(0xffffffffu, vn, o));
+        const double osm = __shfl_xor_sync(0xffffffffu, sm_, o), osv = __shfl_xor_sync(0xffffffffu, sv, o);
+        const long long osp = __shfl_xor_sync(0xffffffffu, sp, o);
+        if (osm < sm_ || (osm == sm_ && osp < sp)) {
+          sm_ = osm;
+          sv = osv;
+          sp = osp;
+        }
+      }
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+      if (lane == 0) {
+        rs[wid] = ts;
+        rc[wid] = tc;
+        rmn[wid] = mn;
+        rvx[wid] = vx;
+        rvn[wid] = vn;
+        rsm[wid] = sm_;
+        rva[wid] = sv;
+        rpos[wid] = sp;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 1; k < kW; ++k) {  // fixed order
+          ts += rs[k];
+          tc += rc[k];
+          mn = fmin(mn, rmn[k]);
+          vx = fmax(vx, rvx[k]);
+          vn = fmin(vn, rvn[k]);
+          if (rsm[k] < sm_ || (rsm[k] == sm_ && rpos[k] < sp)) {
+            sm_ = rsm[k];
+            sv = rva[k];
+            sp = rpos[k];
+          }
+        }
+        if (a.acc) accum_add(a.acc, ts, tc, a.s2);
+        if (a.tstat)
+          a.tstat[blockIdx.x] =
+              TileStats{mn, vx >= 0.0 ? vx : -1.0, vn, sm_, sv, sp == LLONG_MAX ? -1 : (int64_t)sp};
+      }
     }
   }
 }
 
 // Prior (n == 0): mean 0, variance = output variance (gp.hpp:155-158).
-__global__ void k_prior(double* mu, double* var, int64_t n, double s2) {
+__global__ void k_prior(double* mu, double* var, int64_t n, double s2, TileStats* tstat) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     mu[j] = 0.0;
     var[j] = s2;
   }
+  if (tstat)
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n / kTile;
+         t += (int64_t)gridDim.x * blockDim.x)
+      tstat[t] = TileStats{0.0, s2, s2, 0.0, s2, t * kTile};
 }
 
 __global__ void k_mark(uint32_t* visited, int64_t pos, int set) {
@@ -903,6 +978,7 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first
     }
   }
   __syncthreads();
+  SEL_MARK(5);
   if (!is_last) return;
   // last block: merge the per-block records (all loads in flight at once)
   __threadfence();
@@ -966,7 +1042,11 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first
   c.out->n_candidates = (int64_t)fc;
   c.out->cv_fallback = cv_fallback;
   c.out->gp_status = gp_status;
+  if (c.b.gthr) c.b.gthr[0] = c.b.gthr[1] = c.b.gthr[2] = 0ull;  // next selection starts afresh
   *c.b.counter = 0;
+#ifdef GTC_SEL_TRACE
+  g_sel_trace[blockIdx.x][6] = gtc_globaltimer();
+#endif
 }
 
 // ---------------------------------------------------- pruned selection
@@ -994,9 +1074,6 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first
 // whose key does not prove score < T.  The block's best (max score, lowest
 // position, NaN skipped) always passes, so the result is identical to scoring
 // every candidate.  Non-finite inputs get +inf keys (always scored exactly).
-#ifndef GTC_SEL_STOP
-#define GTC_SEL_STOP 0  // diagnostic cut points of the selection (tools/sel_bench.cu); 0 = full kernel
-#endif
 constexpr int kSelPer = 8;  // candidates per thread per chunk (keys kept in registers)
 constexpr float kLog2Slack = 0x1p-6f;  // log2-domain margin (1.1 % relative)
 constexpr float kLog2Floor = -1039.0f;  // below this, subnormal rounding dominates
@@ -1144,10 +1221,6 @@ __device__ void select_pruned(const SelCtx& c, double best, double lambda, doubl
         }
       }
     }
-    if (GTC_SEL_STOP == 2) {
-      if (cnt == -7) c.out->lambda = (double)key[0][0] + top_r[0] + top_r[1] + top_r[2];
-      continue;
-    }
     // the candidate with the largest key, scored exactly, sets the threshold
 #pragma unroll
     for (int af = 0; af < 3; ++af) {
@@ -1186,10 +1259,6 @@ __device__ void select_pruned(const SelCtx& c, double best, double lambda, doubl
     }
     __syncthreads();  // s_thr reuse
   }
-  if (GTC_SEL_STOP == 2 || GTC_SEL_STOP == 3) {
-    if (cnt == -7) c.out->lambda = b[0].s + b[1].s + b[2].s + (double)first;
-    return;
-  }
   select_finish<MASK>(c, b, first, first_finite, cnt, best, lambda, mean_var, cv_fallback, gp_status);
 }
 
@@ -1203,29 +1272,207 @@ __host__ __device__ constexpr int sel_blocks_per_sm(uint32_t mask) { return (mas
 // same 40 bytes, so all blocks agree on lambda (strategies.hpp:404-418,
 // acquisition.hpp:73-83) and best_std (gp.hpp:145) without a grid barrier;
 // then the pruned masked argmax (select_pruned).
-template <uint32_t MASK>
-__global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK))
-    k_select(SelCtx c, const GpScalars* sc, SelectParams p, VarSource vs, int per) {
+// lambda (strategies.hpp:404-418, acquisition.hpp:73-83) and best_std
+// (gp.hpp:145) from the variance total: identical in every block.
+struct SelSetup {
+  double best, lambda, mean_var;
+  int fallback;
+};
+
+__device__ __forceinline__ SelSetup sel_setup(const GpScalars* sc, const SelectParams& p, const VarSource& vs) {
   double s;
   long long cnt;
   var_source_read(vs, &s, &cnt);
-  if (GTC_SEL_STOP == 1) {
-    if (cnt == -7) c.out->lambda = s;
-    return;
-  }
-  const double mean_var = cnt > 0 ? __ddiv_rn(s, (double)cnt) : 0.0;
-  double lambda = p.lambda_constant;
-  int fallback = 0;
+  SelSetup u;
+  u.mean_var = cnt > 0 ? __ddiv_rn(s, (double)cnt) : 0.0;
+  u.lambda = p.lambda_constant;
+  u.fallback = 0;
   if (p.lambda_mode == 1) {
     if (!(p.f_best_raw > 0.0) || !(p.cv_mu_s > 0.0) || !(p.cv_var_s > 0.0)) {
-      fallback = 1;
+      u.fallback = 1;
     } else {
-      const double l = __ddiv_rn(__ddiv_rn(__dmul_rn(mean_var, p.f_best_raw), p.cv_mu_s), p.cv_var_s);
-      lambda = l > 0.0 ? l : 0.0;
+      const double l = __ddiv_rn(__ddiv_rn(__dmul_rn(u.mean_var, p.f_best_raw), p.cv_mu_s), p.cv_var_s);
+      u.lambda = l > 0.0 ? l : 0.0;
     }
   }
-  const double best = __ddiv_rn(__dadd_rn(p.f_best_raw, -sc->y_mean), sc->y_std);
-  select_pruned<MASK, false>(c, best, lambda, mean_var, fallback, sc->status, per);
+  u.best = __ddiv_rn(__dadd_rn(p.f_best_raw, -sc->y_mean), sc->y_std);
+  return u;
+}
+
+// Monotone map of non-NaN doubles to u64 (atomicMax of exact scores); 0 = none.
+__device__ __forceinline__ unsigned long long ord_key(double d) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_val(unsigned long long k) {
+  if (k == 0ull) return -CUDART_INF;
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+__device__ __forceinline__ Thr make_thr(double t) {
+  return Thr{t, t > 0.0 ? __double2float_rd(log2(t)) : -__int_as_float(0x7f800000)};
+}
+
+// Upper bound keys of every score in a tile from its TileStats: EI and -LCB
+// grow with the variance and fall with the mean, so (min mean, max variance)
+// bounds them; PI = Phi((best + lambda - mu)/sd) is bounded with the minimum
+// variance when best + lambda - min mean >= 0, else with the maximum.
+template <uint32_t MASK>
+__device__ __forceinline__ void tile_keys(const TileStats& ts, float* key, bool* pi_hi, bool base_ok, double bm_ei,
+                                          double bp_pi, double lambda) {
+  *pi_hi = false;
+  if (!(ts.var_max >= 0.0)) {  // no candidates in the tile
+#pragma unroll
+    for (int af = 0; af < 3; ++af) key[af] = -__int_as_float(0x7f800000);
+    return;
+  }
+  bool h;
+  if (MASK & 5u) bound_keys<MASK & 5u, false>(key, &h, ts.mu_min, ts.var_max, base_ok, bm_ei, bp_pi, lambda);
+  if (MASK & 2u) {
+    float k2[3];
+    const bool pos = __dadd_rn(bp_pi, -ts.mu_min) >= 0.0;
+    bound_keys<2u, false>(k2, pi_hi, ts.mu_min, pos ? ts.var_min : ts.var_max, base_ok, bm_ei, bp_pi, lambda);
+    key[1] = k2[1];
+  }
+}
+
+// Selection for a resident run, one kernel:
+//  - lambda and best_std from the run's fixed-point variance total (left by the
+//    predictive pass or k_var_partials; VarAccum): every block computes the
+//    same values without a grid barrier;
+//  - tiles are dealt round-robin to blocks (candidates near the optimum
+//    cluster in space, so contiguous ranges would make a few blocks do all
+//    the exact scoring);
+//  - each block bounds its tiles from their TileStats and scores exactly the
+//    minimum-mean candidate of its best-keyed tile (recorded by the pass, so
+//    no candidate loads): a threshold T that the block's best must reach;
+//  - it keeps only tiles whose key reaches T, bounds their candidates and
+//    scores exactly those whose key reaches T: the same argmax as scoring
+//    every candidate (see select_pruned).
+// The candidate count and the first eligible position come from the host's
+// visited bookkeeping.
+constexpr int kTileList = 512;  // tiles examined per block per round
+
+template <uint32_t MASK>
+__global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK))
+    k_select(SelCtx c, const GpScalars* sc, SelectParams p, VarSource vs, const TileStats* tstat, int ntiles) {
+  __shared__ Best redb[32];
+  __shared__ int s_list[kTileList];
+  __shared__ int s_n;
+  SEL_MARK(0);
+  const int G = gridDim.x;
+  const int mine = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / G + 1 : 0;  // tiles of this block
+  // this thread's first tile summary, loaded before the variance total (independent)
+  TileStats ts0{};
+  if ((int)threadIdx.x < mine) ts0 = tstat[blockIdx.x + G * threadIdx.x];
+  const SelSetup u = sel_setup(sc, p, vs);
+  const double bm_ei = __dadd_rn(u.best, -u.lambda), bp_pi = __dadd_rn(u.best, u.lambda);
+  const bool base_ok = fabs(bm_ei) < 1e30 && fabs(bp_pi) < 1e30;
+  const float kInf = __int_as_float(0x7f800000);
+  SEL_MARK(1);
+  // ---- block threshold
+  Best top[3] = {{0.0, INT64_MAX}, {0.0, INT64_MAX}, {0.0, INT64_MAX}};
+  for (int k = threadIdx.x; k < mine; k += blockDim.x) {
+    const TileStats ts = k == (int)threadIdx.x ? ts0 : tstat[blockIdx.x + G * k];
+    if (ts.pos_seed < 0) continue;
+    float key[3];
+    bool hi;
+    tile_keys<MASK>(ts, key, &hi, base_ok, bm_ei, bp_pi, u.lambda);
+#pragma unroll
+    for (int af = 0; af < 3; ++af)
+      if ((MASK & (1u << af)) && key[af] < kInf && key[af] > -kInf)
+        top[af] = better(top[af], Best{(double)key_rank(af, key[af], hi), blockIdx.x + G * k});
+  }
+  Thr th[3];
+#pragma unroll
+  for (int af = 0; af < 3; ++af) {
+    th[af] = Thr{-CUDART_INF, -kInf};
+    if (!(MASK & (1u << af))) continue;
+    const Best tt = block_best(top[af], redb);  // same in every thread
+    if (tt.p == INT64_MAX) continue;
+    const TileStats ts = tstat[tt.p];
+    const int64_t j = ts.pos_seed;
+    if (!eligible(c, j)) continue;  // (marked visited after the pass)
+    // every thread scores it (no broadcast barrier); same inputs as c.mu/c.var[j]
+    const double t = score_of(af, ts.mu_seed, sqrt(ts.var_seed), u.best, u.lambda);
+    if (t == t) th[af] = make_thr(t);
+  }
+  // share thresholds across blocks: any block's exact score of an eligible
+  // candidate is a valid threshold for every block (blocks far from the
+  // optimum would otherwise score most of their candidates exactly)
+  __shared__ double s_thr[3];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int af = 0; af < 3; ++af) {
+      if (!(MASK & (1u << af))) continue;
+      const unsigned long long prev =
+          th[af].t > -CUDART_INF ? atomicMax(c.b.gthr + af, ord_key(th[af].t)) : __ldcg(c.b.gthr + af);
+      s_thr[af] = fmax(th[af].t, ord_val(prev));
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int af = 0; af < 3; ++af)
+    if (MASK & (1u << af)) th[af] = make_thr(s_thr[af]);
+  SEL_MARK(2);
+  // ---- surviving tiles, their candidates, exact scores
+  Best b[3] = {{0.0, INT64_MAX}, {0.0, INT64_MAX}, {0.0, INT64_MAX}};
+  for (int g0 = 0; g0 < mine; g0 += kTileList) {
+    const int g1 = min(mine, g0 + kTileList);
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    for (int k = g0 + threadIdx.x; k < g1; k += blockDim.x) {
+      const int t = blockIdx.x + G * k;
+      const TileStats ts = k == (int)threadIdx.x ? ts0 : tstat[t];
+      float key[3];
+      bool hi;
+      tile_keys<MASK>(ts, key, &hi, base_ok, bm_ei, bp_pi, u.lambda);
+      bool keep = false;
+#pragma unroll
+      for (int af = 0; af < 3; ++af)
+        if (MASK & (1u << af)) keep |= may_reach(af, key[af], hi, th[af]);
+      if (keep) s_list[atomicAdd(&s_n, 1)] = t;
+    }
+    if (threadIdx.x < 3 && (MASK & (1u << threadIdx.x)))  // thresholds published since
+      s_thr[threadIdx.x] = fmax(s_thr[threadIdx.x], ord_val(__ldcg(c.b.gthr + threadIdx.x)));
+    __syncthreads();
+#pragma unroll
+    for (int af = 0; af < 3; ++af)
+      if (MASK & (1u << af)) th[af] = make_thr(s_thr[af]);
+    const int nl = s_n;
+    for (int idx = threadIdx.x; idx < nl * kTile; idx += blockDim.x) {
+      const int64_t j = (int64_t)s_list[idx / kTile] * kTile + idx % kTile;
+      if (j >= c.n || !eligible(c, j)) continue;
+      const double mu = c.mu[j], var = c.var[j];
+      float key[3];
+      bool hi;
+      bound_keys<MASK, false>(key, &hi, mu, var, base_ok, bm_ei, bp_pi, u.lambda);
+#pragma unroll
+      for (int af = 0; af < 3; ++af) {
+        if (!(MASK & (1u << af)) || !may_reach(af, key[af], hi, th[af])) continue;
+        const double s = score_of(af, mu, sqrt(var), u.best, u.lambda);
+        if (s == s) b[af] = better(b[af], Best{s, j});
+      }
+    }
+    __syncthreads();  // s_list / s_n reuse
+  }
+  SEL_MARK(3);
+  // the host-computed first eligible candidate lives in exactly one block
+  int64_t first = INT64_MAX;
+  int finite = 1;
+  const int64_t fp = p.first_eligible;
+  if (threadIdx.x == 0 && fp >= 0 && (int)((fp / kTile) % G) == (int)blockIdx.x) {
+    float key[3];
+    bool hi;
+    bound_keys<MASK, false>(key, &hi, c.mu[fp], c.var[fp], base_ok, bm_ei, bp_pi, u.lambda);
+    first = fp;
+#pragma unroll
+    for (int af = 0; af < 3; ++af)
+      if ((MASK & (1u << af)) && !(key[af] < kInf)) finite = 0;
+  }
+  const long long cnt = (blockIdx.x == 0 && threadIdx.x == 0) ? (long long)p.n_candidates : 0;
+  select_finish<MASK>(c, b, first, finite, cnt, u.best, u.lambda, u.mean_var, u.fallback, sc->status);
 }
 
 // (sum, count) of a variance source: a shard's local contribution to the
@@ -1321,11 +1568,11 @@ static void extend_impl(const ExtendArgs& a, int64_t tiles, cudaStream_t s) {
 
 void launch_extend(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V,
                    int64_t tile_stride, int n0, int r, bool final, double* mu, double* var,
-                   bool check_status, const VarPartials* vp, cudaStream_t s) {
+                   bool check_status, const VarPartials* vp, TileStats* tstat, cudaStream_t s) {
   count_launch();
   ExtendArgs a{sp, g, V, tile_stride, n0, r, final ? 1 : 0, check_status ? 1 : 0,
                k.lengthscale, k.s2, mu, var, vp ? vp->visited : nullptr,
-               (vp && final) ? vp->acc : nullptr, vp ? vp->acc_clear : nullptr};
+               (vp && final) ? vp->acc : nullptr, vp ? vp->acc_clear : nullptr, final ? tstat : nullptr};
   const int64_t tiles = sp.n_pad / kTile;
   if (r <= 1) {
     switch (k.nu) {
@@ -1342,9 +1589,9 @@ void launch_extend(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V
   }
 }
 
-void launch_prior(double* mu, double* var, int64_t n, double s2, cudaStream_t s) {
+void launch_prior(double* mu, double* var, int64_t n, double s2, TileStats* tstat, cudaStream_t s) {
   count_launch();
-  k_prior<<<148, 256, 0, s>>>(mu, var, n, s2);
+  k_prior<<<148, 256, 0, s>>>(mu, var, n, s2, tstat);
 }
 
 void launch_mark(uint32_t* visited, int64_t pos, int set, cudaStream_t s) {
@@ -1377,25 +1624,30 @@ static void select_geometry(int64_t n, uint32_t mask, int* per, int* grid) {
 }
 
 void launch_select(const double* mu, const double* var, const uint32_t* visited, int64_t n,
-                   const GpScalars* sc, SelectParams p, const VarSource& vs, const ReduceBufs& b,
-                   SelectDev* out, cudaStream_t s) {
+                   const GpScalars* sc, SelectParams p, const VarSource& vs, const TileStats* tstat,
+                   const ReduceBufs& b, SelectDev* out, cudaStream_t s) {
   count_launch();
   SelCtx c{mu, var, nullptr, visited, nullptr, p.excluded, p.n_excluded, n, p.af_mask, b, out};
-  // exactly one wave of resident blocks (chunk-stride inside): a partial
-  // second wave would double the kernel's time.  `per` candidates per thread
-  // per chunk spread the candidates over every SM.
-  int per, grid;
-  select_geometry(n, (p.af_mask & 7u) ? (p.af_mask & 7u) : 7u, &per, &grid);
-#define GTC_SELECT_CASE(M) \
-  case M: k_select<M><<<grid, kSelectThreads, 0, s>>>(c, sc, p, vs, per); break;
-  switch (p.af_mask & 7u) {  // launch errors surface through the caller's cudaGetLastError()
+  const uint32_t mask = (p.af_mask & 7u) ? (p.af_mask & 7u) : 7u;
+  const int ntiles = (int)((n + kTile - 1) / kTile);
+  static const int grid_override = [] {
+    const char* e = std::getenv("GTC_SELECT_GRID");  // diagnostics (tools/sel_bench.cu)
+    return e ? std::atoi(e) : 0;
+  }();
+  const int want = grid_override > 0 ? grid_override : sel_blocks_per_sm(mask) * sm_count();
+  const int grid = std::max(1, std::min({ntiles, want, kMaxReduceGrid}));
+#define GTC_SELECT_CASE(M)                                                       \
+  case M:                                                                        \
+    k_select<M><<<grid, kSelectThreads, 0, s>>>(c, sc, p, vs, tstat, ntiles); \
+    break;
+  switch (mask) {  // launch errors surface through the caller's cudaGetLastError()
     GTC_SELECT_CASE(1)
     GTC_SELECT_CASE(2)
     GTC_SELECT_CASE(3)
     GTC_SELECT_CASE(4)
     GTC_SELECT_CASE(5)
     GTC_SELECT_CASE(6)
-    default: k_select<7><<<grid, kSelectThreads, 0, s>>>(c, sc, p, vs, per); break;
+    default: GTC_SELECT_CASE(7)
   }
 #undef GTC_SELECT_CASE
 }

@@ -199,3 +199,9 @@ class SurrogateRun:
 
     def last_step_ms(self) -> float:
         return float(load().gtc_last_step_ms(self._h))
+
+    def last_phase_ms(self):
+        """(append, pass, selection) CUDA-event ms of the last appending observe."""
+        out = (C.c_double * 3)()
+        check(load().gtc_last_phase_ms(self._h, out))
+        return tuple(out)

@@ -36,6 +36,8 @@
 #include <cstdlib>
 #include <cstdint>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "gtc_internal.h"
 
@@ -159,13 +161,13 @@ __device__ __forceinline__ void var_source_read(const VarSource& v, double* sum,
 // inverse variant (explicit diagonal-block inverses + refinement) moved
 // results by ~1e-13 and flipped near-tied picks, so it is not used.
 //
-// Block-pipelined over 32-row blocks, accumulators in shared memory: warp
-// s % 8 runs block s's 32-step diagonal chain in registers (shuffle per
-// step, no barrier); after one barrier, warp (s+1) % 8 folds block s's 32
-// columns into block s+1's rows (one row per lane, fully unrolled so the
-// coefficient loads run ahead of the dependent subtractions) and goes
-// straight on to the next chain, while the other warps fold block s into the
-// rows beyond, off the critical path.
+// Block-pipelined over 32-row blocks: warp s % 8 runs block s's 32-step
+// diagonal chain in registers (shuffle per step, no barrier).  The warp that
+// owns block s+1 loads its coefficients (block s+1's diagonal block and block
+// s's columns of its rows) while that chain runs, and after one barrier folds
+// block s's solution into its rows (one row per lane, the subtractions in
+// ascending column order) and goes straight on to the next chain; the other
+// warps fold block s into the rows beyond, off the critical path.
 constexpr int kSolveWarps = kCtaThreads / 32;
 
 __device__ __forceinline__ void fold_block(const double* Lp, double* x, int r, int b0, int kmax) {
@@ -180,35 +182,59 @@ __device__ __forceinline__ void fold_block(const double* Lp, double* x, int r, i
 __device__ void cta_forward_solve(const double* Lp, int n, double* x, const double* rinv) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nblk = (n + 31) / 32;
+  double lrd[32];  // diagonal-block coefficients of the block this warp will chain next
+  double lf[32];   // block s's columns of this warp's next rows (fold)
+  double xr = 0.0, ri = 0.0;
+  auto load_diag = [&](int blk) {
+    const int b0 = 32 * blk, r = b0 + lane;
+    const bool live = r < n;
+    const double* Lr = Lp + packed(live ? r : b0) + b0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) lrd[k] = (live && k < lane) ? Lr[k] : 0.0;
+    ri = live ? rinv[r] : 0.0;
+  };
+  if (warp == 0) {
+    load_diag(0);
+    xr = lane < n ? x[lane] : 0.0;
+  }
   for (int s = 0; s < nblk; ++s) {
     const int b0 = 32 * s, kmax = min(32, n - b0);
-    if (warp == s % kSolveWarps) {  // rows of block s are complete w.r.t. columns < b0
-      const int r = b0 + lane;
+    const int wn = (s + 1) % kSolveWarps;
+    if (warp == wn && s + 1 < nblk) {  // prefetch while block s's chain runs
+      const int r = b0 + 32 + lane;
       const bool live = r < n;
       const double* Lr = Lp + packed(live ? r : b0) + b0;
-      double lr[32];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) lr[k] = (live && k < lane) ? Lr[k] : 0.0;
-      const double ri = live ? rinv[r] : 0.0;
-      double xr = live ? x[r] : 0.0;
+      for (int k = 0; k < 32; ++k) lf[k] = (live && k < kmax) ? Lr[k] : 0.0;
+      load_diag(s + 1);
+    }
+    if (warp == s % kSolveWarps) {  // xr: this warp's rows, complete w.r.t. columns < b0
+      // branch-free (a shuffle under a divergent guard costs a convergence
+      // check per step); lanes past n carry ri = 0, coefficients 0
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
-        if (k < kmax) {
-          const double xi = __shfl_sync(0xffffffffu, __dmul_rn(xr, ri), k);
-          if (lane == k) xr = xi;
-          else if (lane > k) xr = __dadd_rn(xr, -__dmul_rn(lr[k], xi));
-        }
+        const double xi = __shfl_sync(0xffffffffu, __dmul_rn(xr, ri), k);
+        const double upd = __dadd_rn(xr, -__dmul_rn(lrd[k], xi));
+        xr = lane == k ? xi : (lane > k ? upd : xr);
       }
-      if (live) x[r] = xr;
+      if (b0 + lane < n) x[b0 + lane] = xr;
     }
     __syncthreads();  // block s solved; every fold of block s-1 done
     if (s + 1 < nblk) {
-      const int wn = (s + 1) % kSolveWarps;
       if (warp == wn) {
-        if (b0 + 32 + lane < n) fold_block(Lp, x, b0 + 32 + lane, b0, kmax);
+        const int r = b0 + 32 + lane;
+        xr = r < n ? x[r] : 0.0;
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (k < kmax) xr = __dadd_rn(xr, -__dmul_rn(lf[k], x[b0 + k]));
       } else {
-        const int t = threadIdx.x - (warp > wn ? 32 : 0);
-        for (int r = b0 + 64 + t; r < n; r += kCtaThreads - 32) fold_block(Lp, x, r, b0, kmax);
+        // far rows on the warps that do not share a scheduler with the next
+        // chain (warps wn and wn + 4 share one of the 4 SM sub-partitions)
+        const int wo = (wn + kSolveWarps / 2) % kSolveWarps;
+        if (warp != wo) {
+          const int t = threadIdx.x - 32 * ((warp > wn) + (warp > wo));
+          for (int r = b0 + 64 + t; r < n; r += kCtaThreads - 64) fold_block(Lp, x, r, b0, kmax);
+        }
       }
     }
   }
@@ -1522,9 +1548,21 @@ static size_t cta_smem_bytes(int n_max, int rows, bool* staged) {
   return *staged ? with_l : base;
 }
 
+// Opt-in to large dynamic shared memory once per kernel and device (the
+// limit is raised to the whole budget; a driver call per launch would sit on
+// the observe step's host critical path).
 template <class K>
 static void opt_in_smem(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (bytes <= 48 * 1024) return;
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> seen;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& e : seen)
+    if (e.first == (const void*)kernel && e.second == dev) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCtaSmemLimit);
+  seen.emplace_back((const void*)kernel, dev);
 }
 
 void launch_gp_factor(const GpDev& g, KernelParams k, double noise, double jitter, int n,

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/gridtune_cuda.h"
@@ -213,8 +214,10 @@ struct gtc_space {
   int64_t n = 0, n_pad = 0;
   int d = 0;
   double* coords = nullptr;          // device SoA [d][n_pad]
+  uint8_t* cidx = nullptr;           // device [d][n_pad] value indices (SpaceDev), or null
+  double* ctab = nullptr;            // device [d][256] distinct values per dimension
   std::vector<double> host_coords;   // row-major n x d (gathers for fit)
-  SpaceDev dev() const { return SpaceDev{coords, n, n_pad, d}; }
+  SpaceDev dev() const { return SpaceDev{coords, n, n_pad, d, cidx, ctab}; }
 };
 
 struct gtc_run {
@@ -286,6 +289,35 @@ extern "C" uint64_t gtc_kernel_launches(void) { return launches(); }
 
 // =============================================================== space
 
+// Discrete search spaces have few distinct values per parameter (the
+// normalised ranks, search_space.hpp:158-166): when every dimension has at
+// most 256, the pass reads 1-byte indices into exact per-dimension tables
+// (bit patterns are kept, so the coordinates are reproduced exactly).
+static cudaError_t compress_coords(gtc_space* s, const std::vector<double>& soa) {
+  std::vector<uint8_t> idx((size_t)s->d * s->n_pad, 0);
+  std::vector<double> tab((size_t)s->d * 256, 0.0);
+  for (int t = 0; t < s->d; ++t) {
+    std::unordered_map<uint64_t, int> slot;
+    for (int64_t j = 0; j < s->n; ++j) {
+      const double v = soa[(size_t)t * s->n_pad + j];
+      uint64_t bits;
+      std::memcpy(&bits, &v, sizeof bits);
+      auto it = slot.find(bits);
+      if (it == slot.end()) {
+        if (slot.size() == 256) return cudaSuccess;  // not compressible: the pass reads coords
+        it = slot.emplace(bits, (int)slot.size()).first;
+        tab[(size_t)t * 256 + it->second] = v;
+      }
+      idx[(size_t)t * s->n_pad + j] = (uint8_t)it->second;
+    }
+  }
+  cudaError_t e = cudaMalloc(&s->cidx, idx.size());
+  if (e == cudaSuccess) e = cudaMalloc(&s->ctab, tab.size() * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemcpy(s->cidx, idx.data(), idx.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(s->ctab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice);
+  return e;
+}
+
 extern "C" int gtc_space_create(int device, const double* coords, int64_t n, int32_t d,
                                 gtc_space** out) {
   if (!out) return fail(GTC_ERR_INVALID, "out is null");
@@ -309,10 +341,10 @@ extern "C" int gtc_space_create(int device, const double* coords, int64_t n, int
     return rc;
   }
   cudaError_t e = cudaMemcpy(s->coords, soa.data(), soa.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = compress_coords(s, soa);
   if (e != cudaSuccess) {
-    cudaFree(s->coords);
-    delete s;
-    return fail(GTC_ERR_CUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
+    gtc_space_destroy(s);
+    return fail(GTC_ERR_CUDA, std::string("space upload: ") + cudaGetErrorString(e));
   }
   *out = s;
   return GTC_OK;
@@ -322,6 +354,8 @@ extern "C" int gtc_space_destroy(gtc_space* s) {
   if (!s) return GTC_OK;
   cudaSetDevice(s->device);
   cudaFree(s->coords);
+  cudaFree(s->cidx);
+  cudaFree(s->ctab);
   delete s;
   return GTC_OK;
 }

@@ -68,6 +68,11 @@ struct SpaceDev {
   int64_t n;
   int64_t n_pad;
   int d;
+  // Lossless compact copy for the predictive pass (null when some dimension
+  // has more than 256 distinct values): coordinate (t, j) is exactly
+  // ctab[t * 256 + cidx[t * n_pad + j]] -- 1 byte per value instead of 8.
+  const uint8_t* cidx;
+  const double* ctab;
 };
 
 // Result of the selection kernels (device side, copied to the host).

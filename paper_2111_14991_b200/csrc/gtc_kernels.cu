@@ -513,11 +513,21 @@ struct ExtendArgs {
   TileStats* tstat;  // final pass: per-tile posterior summary (optional)
 };
 
+// Coordinates t of candidates j0, j0 + 1 (j0 even): from the compact index
+// copy when the space has one (1-byte loads, exact table values), else SoA.
+__device__ __forceinline__ double2 coord2(const SpaceDev& sp, int t, int64_t j0) {
+  if (sp.cidx) {
+    const uchar2 ix = *reinterpret_cast<const uchar2*>(sp.cidx + (int64_t)t * sp.n_pad + j0);
+    return make_double2(__ldg(sp.ctab + t * 256 + ix.x), __ldg(sp.ctab + t * 256 + ix.y));
+  }
+  return *reinterpret_cast<const double2*>(sp.coords + (int64_t)t * sp.n_pad + j0);
+}
+
 // Rows [n0, n0+r) of V for every candidate, r <= R, streaming rows [0, n0)
 // once.  One CTA per tile of kTile candidates, one double2 column pair per
 // thread.  With final_pass the posterior mean/variance are produced too.
 template <int R, int NU>
-__global__ void __launch_bounds__(kExtendThreads) k_extend(ExtendArgs a) {
+__global__ void __launch_bounds__(kExtendThreads, R == 1 ? 10 : 4) k_extend(ExtendArgs a) {
   accum_clear(a.acc_clear);  // next generation's accumulator (even when the pass is skipped)
   if (a.check_status && a.g.sc->status != 0) return;  // bordered row failed: host refactors
   extern __shared__ double sm[];
@@ -548,14 +558,17 @@ __global__ void __launch_bounds__(kExtendThreads) k_extend(ExtendArgs a) {
   for (int t = 0; t < R; ++t) acc0[t] = acc1[t] = 0.0;
   double q0 = 0.0, q1 = 0.0, b0 = 0.0, b1 = 0.0;  // sum v^2, sum v*beta
 
-  int i = 0;
-  constexpr int U = (R == 1) ? 8 : 4;
-  for (; i + U <= n0; i += U) {
+  // U rows in flight; the last partial group is predicated inside the same
+  // unrolled body (a scalar remainder loop would serialise its loads)
+  constexpr int U = 4;
+  for (int i = 0; i < n0; i += U) {
     double2 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = __ldcs(Vt + (int64_t)(i + u) * kRowStride);
+    for (int u = 0; u < U; ++u)
+      v[u] = i + u < n0 ? __ldcs(Vt + (int64_t)(i + u) * kRowStride) : make_double2(0.0, 0.0);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
+      if (i + u >= n0) break;
 #pragma unroll
       for (int t = 0; t < R; ++t) {
         if (t < r) {
@@ -573,30 +586,12 @@ __global__ void __launch_bounds__(kExtendThreads) k_extend(ExtendArgs a) {
       }
     }
   }
-  for (; i < n0; ++i) {
-    const double2 v = __ldcs(Vt + (int64_t)i * kRowStride);
-#pragma unroll
-    for (int t = 0; t < R; ++t) {
-      if (t < r) {
-        const double l = Ls[t * ld + i];
-        acc0[t] = fma(l, v.x, acc0[t]);
-        acc1[t] = fma(l, v.y, acc1[t]);
-      }
-    }
-    if (a.final_pass) {
-      const double bb = bs[i];
-      q0 = fma(v.x, v.x, q0);
-      q1 = fma(v.y, v.y, q1);
-      b0 = fma(v.x, bb, b0);
-      b1 = fma(v.y, bb, b1);
-    }
-  }
 
   // candidate coordinates (SoA) and squared norms, gp.hpp:176-179 expansion
   const int d = a.sp.d;
   double c0n2 = 0.0, c1n2 = 0.0;
   for (int t = 0; t < d; ++t) {
-    const double2 c = *reinterpret_cast<const double2*>(a.sp.coords + (int64_t)t * a.sp.n_pad + j0);
+    const double2 c = coord2(a.sp, t, j0);
     c0n2 = __dadd_rn(c0n2, __dmul_rn(c.x, c.x));
     c1n2 = __dadd_rn(c1n2, __dmul_rn(c.y, c.y));
   }
@@ -606,7 +601,7 @@ __global__ void __launch_bounds__(kExtendThreads) k_extend(ExtendArgs a) {
     if (t < r) {
       double dot0 = 0.0, dot1 = 0.0;
       for (int s = 0; s < d; ++s) {
-        const double2 c = *reinterpret_cast<const double2*>(a.sp.coords + (int64_t)s * a.sp.n_pad + j0);
+        const double2 c = coord2(a.sp, s, j0);
         const double xv = xn[t * d + s];
         dot0 = __dadd_rn(dot0, __dmul_rn(xv, c.x));
         dot1 = __dadd_rn(dot1, __dmul_rn(xv, c.y));

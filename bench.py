@@ -215,7 +215,7 @@ def run_sharded(args, cfg, rank, world, local):
     lo, hi = split_bounds(N, world, rank)
     af = AcquisitionId.ei if args.config == "c4" else AcquisitionId.lcb
     kern = MaternKernel(MaternNu.three_halves, 1.5, 1.0)
-    shard = Shard(coords[lo:hi], lo, kern, n_max=n + args.steps + args.warmup + 2, device=local)
+    shard = Shard(coords[lo:hi], lo, kern, n_max=n, device=local)
     pos = prefix_positions(values, n - 1, BASE_SEED)
     y = values[pos]
     shard.fit_points(coords[pos], y)
@@ -229,9 +229,11 @@ def run_sharded(args, cfg, rank, world, local):
     stream = torch.cuda.ExternalStream(gt.load().gtc_run_stream(shard.run.handle))
 
     def step(pick, f_best):
+        shard.run.truncate_async(n - 1)      # bench rollback: model back to n-1 observations
         yv = float(values[pick])
-        f_best = min(f_best, yv)
-        s = group.observe(coords[pick], pick, yv, [af], f_best, expl, cv)
+        s = group.observe(coords[pick], pick, yv, [af], min(f_best, yv), expl, cv)
+        if shard.local(pick) >= 0:           # bench rollback: keep the candidate set fixed
+            shard.run.unmark_visited(shard.local(pick))
         return s.position[int(af)], f_best
 
     for _ in range(args.warmup):
@@ -261,7 +263,7 @@ def run_sharded(args, cfg, rank, world, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": cfg["workload"] + " (candidate axis sharded)", "N": N, "n": f"{n}..{n + args.steps + args.warmup}",
+            "config": {"workload": cfg["workload"] + " (candidate axis sharded)", "N": N, "n": n,
                        "parallelism": f"candidate-shard{world}",
                        "timing": "CUDA events bracketing the K steps on rank's stream (includes the NCCL exchanges), max over ranks"},
             "e2e": {"value": args.steps / wall, "unit": "iter/s", "h2d_bytes_per_step": 8 * (coords.shape[1] + 2),

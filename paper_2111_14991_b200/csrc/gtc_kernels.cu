@@ -523,11 +523,23 @@ __device__ __forceinline__ double2 coord2(const SpaceDev& sp, int t, int64_t j0)
   return *reinterpret_cast<const double2*>(sp.coords + (int64_t)t * sp.n_pad + j0);
 }
 
+// Rows in flight per thread and resident CTAs per SM of the single-row pass
+// (the HBM stream needs ~150 KB of loads in flight per SM, tools/bw_bench.cu).
+#ifndef GTC_PASS_U
+#define GTC_PASS_U 6
+#endif
+#ifndef GTC_PASS_MINB
+#define GTC_PASS_MINB 10
+#endif
+#ifndef GTC_PASS_DB
+#define GTC_PASS_DB 0  // double-buffered row groups
+#endif
+
 // Rows [n0, n0+r) of V for every candidate, r <= R, streaming rows [0, n0)
 // once.  One CTA per tile of kTile candidates, one double2 column pair per
 // thread.  With final_pass the posterior mean/variance are produced too.
 template <int R, int NU>
-__global__ void __launch_bounds__(kExtendThreads, R == 1 ? 10 : 4) k_extend(ExtendArgs a) {
+__global__ void __launch_bounds__(kExtendThreads, R == 1 ? GTC_PASS_MINB : 4) k_extend(ExtendArgs a) {
   accum_clear(a.acc_clear);  // next generation's accumulator (even when the pass is skipped)
   if (a.check_status && a.g.sc->status != 0) return;  // bordered row failed: host refactors
   extern __shared__ double sm[];
@@ -560,12 +572,9 @@ __global__ void __launch_bounds__(kExtendThreads, R == 1 ? 10 : 4) k_extend(Exte
 
   // U rows in flight; the last partial group is predicated inside the same
   // unrolled body (a scalar remainder loop would serialise its loads)
-  constexpr int U = 4;
-  for (int i = 0; i < n0; i += U) {
-    double2 v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      v[u] = i + u < n0 ? __ldcs(Vt + (int64_t)(i + u) * kRowStride) : make_double2(0.0, 0.0);
+  constexpr int U = (R == 1) ? GTC_PASS_U : 4;
+  // rows [i, i + U) into the accumulators, ascending (the reference's order)
+  auto consume = [&](const double2 (&v)[U], int i) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (i + u >= n0) break;
@@ -584,6 +593,29 @@ __global__ void __launch_bounds__(kExtendThreads, R == 1 ? 10 : 4) k_extend(Exte
         b0 = fma(v[u].x, bb, b0);
         b1 = fma(v[u].y, bb, b1);
       }
+    }
+  };
+  auto fetch = [&](double2 (&v)[U], int i) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      v[u] = i + u < n0 ? __ldcs(Vt + (int64_t)(i + u) * kRowStride) : make_double2(0.0, 0.0);
+  };
+  if (GTC_PASS_DB) {
+    // two groups in flight: the next group's loads are issued before the
+    // current group is consumed, so the stream never drains between groups
+    double2 va[U], vb[U];
+    fetch(va, 0);
+    for (int i = 0; i < n0; i += 2 * U) {
+      fetch(vb, i + U);
+      consume(va, i);
+      fetch(va, i + 2 * U);
+      consume(vb, i + U);
+    }
+  } else {
+    for (int i = 0; i < n0; i += U) {
+      double2 v[U];
+      fetch(v, i);
+      consume(v, i);
     }
   }
 

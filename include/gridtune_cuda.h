@@ -42,6 +42,8 @@ extern "C" {
 #define GTC_ERR_CAPACITY (-7)      /* more observations than the run's n_max          */
 #define GTC_ERR_SAMPLING (-8)      /* gridtune::SamplingError (run_bo preconditions, initial design) */
 #define GTC_ERR_ABORTED (-9)       /* the objective callback asked to stop            */
+#define GTC_ERR_PARSE (-10)        /* gridtune::ParseError (restriction syntax / types), errors.hpp:17-26 */
+#define GTC_ERR_EMPTY (-11)        /* gridtune::EmptySearchSpaceError, errors.hpp:29-32 */
 
 /* ---- enums mirroring the reference ---------------------------------------- */
 /* MaternNu, gp.hpp:12 */
@@ -120,6 +122,43 @@ uint64_t gtc_kernel_launches(void);
 int gtc_space_create(int device, const double* coords, int64_t n, int32_t d, gtc_space** out);
 int gtc_space_destroy(gtc_space* space);
 int64_t gtc_space_size(const gtc_space* space);
+
+/* ---- device search-space enumeration (SearchSpace, search_space.hpp:23-207) - */
+/* ParameterDef (parameter.hpp:62-125): kind 0 numeric (numbers), 1 categorical
+ * (strings), 2 boolean (booleans, 0/1); values in declaration order. */
+#define GTC_PARAM_NUMERIC 0
+#define GTC_PARAM_CATEGORICAL 1
+#define GTC_PARAM_BOOLEAN 2
+typedef struct {
+  const char* name;
+  int32_t kind;
+  int32_t n_values;
+  const double* numbers;
+  const char* const* strings;
+  const uint8_t* booleans;
+} gtc_param_def;
+
+/* SearchSpace(params, restriction_sources) + EnumeratedSpace (search_space.hpp:
+ * 35-44, 120-166, 216-245) on the device: parses and type-checks every
+ * restriction (GTC_ERR_PARSE, message "... (at position p)", the position in
+ * *error_position when non-null), validates the parameters (GTC_ERR_INVALID),
+ * enumerates the Cartesian grid (limit 20,000,000, GTC_ERR_INVALID) with the
+ * restrictions evaluated by sm_100a kernels, and builds the resident space of
+ * the valid configurations in canonical order with coordinates rank/(k-1)
+ * (GTC_ERR_EMPTY when nothing is valid). */
+int gtc_space_enumerate(int device, const gtc_param_def* params, int32_t n_params,
+                        const char* const* restrictions, int32_t n_restrictions,
+                        int64_t* error_position, gtc_space** out);
+/* Canonical indices (Configuration::index) of an enumerated space, ascending
+ * (GTC_ERR_INVALID for spaces built from explicit coordinates). */
+int gtc_space_ids(const gtc_space* space, uint64_t* ids);
+/* SearchSpace::cartesian_size() of an enumerated space (0 otherwise). */
+uint64_t gtc_space_cartesian_size(const gtc_space* space);
+/* Restriction::parse (restriction.hpp:479-486) without enumerating: 0 if the
+ * text is a well-typed boolean restriction over `params`, else GTC_ERR_PARSE
+ * with the position in *error_position. */
+int gtc_restriction_validate(const gtc_param_def* params, int32_t n_params, const char* text,
+                             int64_t* error_position);
 
 /* ---- BO run: resident GP + predictions over the whole space ----------------- */
 int gtc_run_create(gtc_space* space, const gtc_model_config* config, gtc_run** out);

@@ -12,6 +12,8 @@
 //   ref_tool gp     <seed> <trials> <outdir>      # GpModel fit/predict golden vectors
 //   ref_tool runbo  <function> <grid> <seed> <invalid|-> <strategy> <budget> <n_init> <bo_seed> <outdir>
 //   ref_tool bench  <grid> <seed> <n> <threads> <steps> <af>   # CPU baseline (JSON line)
+//   ref_tool enumjson <spec.json> <outdir>        # SearchSpace(params, restrictions) + EnumeratedSpace
+//   ref_tool restrict <spec.json>                 # Restriction::parse + evaluate over the grid
 #include <chrono>
 #include <cinttypes>
 #include <cstdio>
@@ -25,6 +27,7 @@
 
 #include "gridtune/strategies.hpp"
 #include "gridtune/synthetic.hpp"
+#include "json.hpp"
 
 using namespace gridtune;
 namespace fs = std::filesystem;
@@ -305,6 +308,74 @@ int cmd_bench(int argc, char** argv) {
 
 }  // namespace
 
+// ---- search spaces from a JSON spec:
+// {"params": [{"name": .., "kind": "numeric|categorical|boolean", "values": [..]}],
+//  "restrictions": ["..", ..]}
+std::vector<ParameterDef> params_from_json(const nlohmann::json& j) {
+  std::vector<ParameterDef> ps;
+  for (const auto& p : j.at("params")) {
+    const std::string kind = p.at("kind");
+    std::vector<Value> vals;
+    for (const auto& v : p.at("values")) {
+      if (kind == "numeric") vals.emplace_back(v.get<double>());
+      else if (kind == "categorical") vals.emplace_back(v.get<std::string>());
+      else vals.emplace_back(v.get<bool>());
+    }
+    ParameterDef d;  // unvalidated: SearchSpace validates (so its errors are reproduced)
+    d.name = p.at("name");
+    d.kind = kind == "numeric" ? ParamKind::numeric : kind == "categorical" ? ParamKind::categorical : ParamKind::boolean;
+    d.values = std::move(vals);
+    ps.push_back(std::move(d));
+  }
+  return ps;
+}
+
+std::string json_escape(const std::string& s) { return nlohmann::json(s).dump(); }
+
+int cmd_enumjson(int argc, char** argv) {
+  if (argc < 4) return 2;
+  std::ifstream f(argv[2]);
+  const nlohmann::json spec = nlohmann::json::parse(f);
+  std::vector<std::string> rs = spec.value("restrictions", std::vector<std::string>{});
+  try {
+    SearchSpace s(params_from_json(spec), rs);
+    const EnumeratedSpace space(s);
+    dump_space(space, nullptr, argv[3]);
+    std::printf("{\"n\": %zu, \"d\": %zu, \"cartesian\": %" PRIu64 "}\n", space.size(), space.dimension(),
+                s.cartesian_size());
+  } catch (const ParseError& e) {
+    std::printf("{\"error\": \"parse\", \"message\": %s, \"position\": %zu}\n", json_escape(e.what()).c_str(),
+                e.position());
+  } catch (const EmptySearchSpaceError& e) {
+    std::printf("{\"error\": \"empty\", \"message\": %s}\n", json_escape(e.what()).c_str());
+  } catch (const Error& e) {
+    std::printf("{\"error\": \"error\", \"message\": %s}\n", json_escape(e.what()).c_str());
+  }
+  return 0;
+}
+
+// One JSON line per restriction: the parse outcome, and for well-formed ones
+// the truth value at every grid point (canonical order) as a 0/1 string.
+int cmd_restrict(int argc, char** argv) {
+  if (argc < 3) return 2;
+  std::ifstream f(argv[2]);
+  const nlohmann::json spec = nlohmann::json::parse(f);
+  const std::vector<ParameterDef> ps = params_from_json(spec);
+  const SearchSpace grid(ps);
+  for (const std::string& text : spec.at("restrictions")) {
+    try {
+      const Restriction r = parse_restriction(text, ps);
+      std::string bits;
+      for (ConfigIndex i = 0; i < grid.cartesian_size(); ++i) bits += r.evaluate(grid.config_at(i).values) ? '1' : '0';
+      std::printf("{\"text\": %s, \"ok\": true, \"bits\": \"%s\"}\n", json_escape(text).c_str(), bits.c_str());
+    } catch (const ParseError& e) {
+      std::printf("{\"text\": %s, \"ok\": false, \"message\": %s, \"position\": %zu}\n", json_escape(text).c_str(),
+                  json_escape(e.what()).c_str(), e.position());
+    }
+  }
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc < 2) {
     std::fprintf(stderr, "usage: ref_tool space|gemm|gp|runbo|bench ...\n");
@@ -318,6 +389,8 @@ int main(int argc, char** argv) {
     else if (cmd == "gp") rc = cmd_gp(argc, argv);
     else if (cmd == "runbo") rc = cmd_runbo(argc, argv);
     else if (cmd == "bench") rc = cmd_bench(argc, argv);
+    else if (cmd == "enumjson") rc = cmd_enumjson(argc, argv);
+    else if (cmd == "restrict") rc = cmd_restrict(argc, argv);
     if (rc == 2) std::fprintf(stderr, "bad arguments for %s\n", cmd.c_str());
     return rc;
   } catch (const std::exception& e) {

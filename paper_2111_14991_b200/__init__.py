@@ -7,11 +7,13 @@ the Python mirror of the reference interface over its C ABI
 """
 from ._lib import LIB_PATH, load  # noqa: F401
 from .gp import (AcquisitionId, CandidateScores, ConfigError, ContextualVarianceState,  # noqa: F401
-                 DeviceError, Error, ExplorationConfig, GpModel, GpPrediction, MaternKernel,
-                 MaternNu, ModelConditioningError, SamplingError, acquisition_scores, best_candidate,
+                 DeviceError, EmptySearchSpaceError, Error, ExplorationConfig, GpModel, GpPrediction,
+                 MaternKernel, MaternNu, ModelConditioningError, ParseError, SamplingError,
+                 acquisition_scores, best_candidate,
                  contextual_variance_lambda, discounted_observation_score,
                  mean_posterior_variance)
 from .runtime import FitInfo, Selection, Space, SurrogateRun  # noqa: F401
+from .space import EnumeratedSpace, ParameterDef, ParamKind, SearchSpace, parse_restriction  # noqa: F401
 from .strategies import (StrategyConfig, StrategyId, TuningRun, run_bo, run_strategy,  # noqa: F401
                          strategy_from_string)
 

@@ -89,6 +89,14 @@ OBJECTIVE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_uint64, DP)
 
 GTC_ERR_SAMPLING = -8
 GTC_ERR_ABORTED = -9
+GTC_ERR_PARSE = -10
+GTC_ERR_EMPTY = -11
+
+
+class gtc_param_def(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("kind", C.c_int32), ("n_values", C.c_int32),
+                ("numbers", C.POINTER(C.c_double)), ("strings", C.POINTER(C.c_char_p)),
+                ("booleans", C.POINTER(C.c_uint8))]
 
 # (name, restype, argtypes) — exactly the declarations of include/gridtune_cuda.h
 SIGNATURES = [
@@ -98,6 +106,11 @@ SIGNATURES = [
     ("gtc_space_create", C.c_int, [C.c_int, DP, C.c_int64, C.c_int32, C.POINTER(P)]),
     ("gtc_space_destroy", C.c_int, [P]),
     ("gtc_space_size", C.c_int64, [P]),
+    ("gtc_space_enumerate", C.c_int, [C.c_int, C.POINTER(gtc_param_def), C.c_int32, C.POINTER(C.c_char_p),
+                                      C.c_int32, I64P, C.POINTER(P)]),
+    ("gtc_space_ids", C.c_int, [P, U64P]),
+    ("gtc_space_cartesian_size", C.c_uint64, [P]),
+    ("gtc_restriction_validate", C.c_int, [C.POINTER(gtc_param_def), C.c_int32, C.c_char_p, I64P]),
     ("gtc_run_create", C.c_int, [P, C.POINTER(gtc_model_config), C.POINTER(P)]),
     ("gtc_run_destroy", C.c_int, [P]),
     ("gtc_fit", C.c_int, [P, I64P, DP, C.c_int32, C.POINTER(gtc_fit_info)]),

@@ -16,6 +16,7 @@
 
 #include "../../include/gridtune_cuda.h"
 #include "gtc_internal.h"
+#include "restriction.hpp"
 
 using namespace gtc;
 
@@ -217,6 +218,8 @@ struct gtc_space {
   uint8_t* cidx = nullptr;           // device [d][n_pad] value indices (SpaceDev), or null
   double* ctab = nullptr;            // device [d][256] distinct values per dimension
   std::vector<double> host_coords;   // row-major n x d (gathers for fit)
+  std::vector<uint64_t> ids;         // canonical indices (enumerated spaces)
+  uint64_t cartesian = 0;            // Cartesian size (enumerated spaces)
   SpaceDev dev() const { return SpaceDev{coords, n, n_pad, d, cidx, ctab}; }
 };
 
@@ -361,6 +364,200 @@ extern "C" int gtc_space_destroy(gtc_space* s) {
 }
 
 extern "C" int64_t gtc_space_size(const gtc_space* s) { return s ? s->n : -1; }
+
+// =============================================================== enumeration
+
+static int convert_params(const gtc_param_def* params, int32_t n_params, std::vector<ParamDef>* out) {
+  if (n_params < 0 || (n_params > 0 && !params)) return fail(GTC_ERR_INVALID, "params is null");
+  out->clear();
+  for (int32_t i = 0; i < n_params; ++i) {
+    const gtc_param_def& g = params[i];
+    ParamDef p;
+    p.name = g.name ? g.name : "";
+    if (g.kind < 0 || g.kind > 2) return fail(GTC_ERR_INVALID, "parameter '" + p.name + "' has an unknown kind");
+    if (g.n_values < 0) return fail(GTC_ERR_INVALID, "parameter '" + p.name + "' has a negative value count");
+    p.kind = static_cast<ParamKind>(g.kind);
+    for (int32_t v = 0; v < g.n_values; ++v) {
+      if (p.kind == ParamKind::numeric) {
+        if (!g.numbers) return fail(GTC_ERR_INVALID, "parameter '" + p.name + "' numbers is null");
+        p.numbers.push_back(g.numbers[v]);
+      } else if (p.kind == ParamKind::categorical) {
+        if (!g.strings || !g.strings[v]) return fail(GTC_ERR_INVALID, "parameter '" + p.name + "' strings is null");
+        p.strings.emplace_back(g.strings[v]);
+      } else {
+        if (!g.booleans) return fail(GTC_ERR_INVALID, "parameter '" + p.name + "' booleans is null");
+        p.booleans.push_back(g.booleans[v] != 0);
+      }
+    }
+    out->push_back(std::move(p));
+  }
+  return GTC_OK;
+}
+
+extern "C" int gtc_restriction_validate(const gtc_param_def* params, int32_t n_params, const char* text,
+                                        int64_t* error_position) {
+  std::vector<ParamDef> ps;
+  int rc = convert_params(params, n_params, &ps);
+  if (rc) return rc;
+  EnumProgram prog;
+  RestrictionError err;
+  if (!compile_restriction(text ? text : "", ps, &prog, &err)) {
+    if (error_position) *error_position = (int64_t)err.position;
+    return fail(err.parse ? GTC_ERR_PARSE : GTC_ERR_INVALID, err.message);
+  }
+  return GTC_OK;
+}
+
+// RAII for the enumeration's temporary device buffers
+struct DevBufs {
+  std::vector<void*> ptrs;
+  ~DevBufs() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <class T>
+  int get(T** p, size_t count) {
+    int rc = dalloc(p, count);
+    if (!rc) ptrs.push_back(*p);
+    return rc;
+  }
+};
+
+extern "C" int gtc_space_enumerate(int device, const gtc_param_def* params, int32_t n_params,
+                                   const char* const* restrictions, int32_t n_restrictions,
+                                   int64_t* error_position, gtc_space** out) {
+  if (!out) return fail(GTC_ERR_INVALID, "out is null");
+  *out = nullptr;
+  std::vector<ParamDef> ps;
+  int rc = convert_params(params, n_params, &ps);
+  if (rc) return rc;
+  // SearchSpace(params, sources): every restriction is parsed, then the
+  // parameters are validated (search_space.hpp:35-44)
+  EnumProgram prog;
+  for (int32_t r = 0; r < n_restrictions; ++r) {
+    RestrictionError err;
+    if (!compile_restriction(restrictions && restrictions[r] ? restrictions[r] : "", ps, &prog, &err)) {
+      if (error_position) *error_position = (int64_t)err.position;
+      return fail(err.parse ? GTC_ERR_PARSE : GTC_ERR_INVALID, err.message);
+    }
+  }
+  {
+    RestrictionError err;
+    if (!validate_params(ps, &err)) return fail(GTC_ERR_INVALID, err.message);
+  }
+  const int d = (int)ps.size();
+  if (d > kMaxDim) return fail(GTC_ERR_INVALID, "search-space dimension out of range [1, 64]");
+  // cartesian_size() and the enumeration limit (search_space.hpp:120-127)
+  constexpr uint64_t kEnumerationLimit = 20000000ull;
+  uint64_t total = 1;
+  bool over = false;
+  for (const ParamDef& p : ps) {
+    if (total > (~0ull) / p.size()) over = true;
+    total *= p.size();
+  }
+  if (over || total > kEnumerationLimit)
+    return fail(GTC_ERR_INVALID, "Cartesian size " + std::to_string(total) + " exceeds the enumeration limit of " +
+                                     std::to_string(kEnumerationLimit));
+  // value tables (booleans 0/1), radices, exact normalised coordinates
+  std::vector<double> values, normtab;
+  std::vector<int32_t> val_off, radix;
+  bool compressible = true;
+  for (const ParamDef& p : ps) {
+    const size_t k = p.size();
+    val_off.push_back((int32_t)values.size());
+    radix.push_back((int32_t)k);
+    compressible = compressible && k <= 256;
+    for (size_t r = 0; r < k; ++r) {
+      values.push_back(p.kind == ParamKind::numeric ? p.numbers[r]
+                       : p.kind == ParamKind::boolean ? (p.booleans[r] ? 1.0 : 0.0) : 0.0);
+      normtab.push_back(k <= 1 ? 0.0 : static_cast<double>(r) / static_cast<double>(k - 1));
+    }
+  }
+  if (values.size() > 4096) return fail(GTC_ERR_INVALID, "more than 4096 parameter values in total");
+  GTC_CUDA(cudaSetDevice(device));
+  cudaStream_t st;
+  GTC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } sg{st};
+  DevBufs tmp;
+  EnumInstr* d_code;
+  double *d_values, *d_norm;
+  int32_t *d_off, *d_radix;
+  uint8_t* d_str;
+  uint32_t* d_mask;
+  int64_t *d_counts, *d_total;
+  const int64_t words = (int64_t)((total + 31) / 32);
+  if ((rc = tmp.get(&d_code, prog.code.size())) || (rc = tmp.get(&d_values, values.size())) ||
+      (rc = tmp.get(&d_norm, normtab.size())) || (rc = tmp.get(&d_off, d)) || (rc = tmp.get(&d_radix, d)) ||
+      (rc = tmp.get(&d_str, std::max<size_t>(prog.str_tables.size(), 1))) || (rc = tmp.get(&d_mask, words)) ||
+      (rc = tmp.get(&d_counts, 2048)) || (rc = tmp.get(&d_total, 1)))
+    return rc;
+  GTC_CUDA(cudaMemcpyAsync(d_code, prog.code.data(), sizeof(EnumInstr) * prog.code.size(), cudaMemcpyHostToDevice, st));
+  GTC_CUDA(cudaMemcpyAsync(d_values, values.data(), sizeof(double) * values.size(), cudaMemcpyHostToDevice, st));
+  GTC_CUDA(cudaMemcpyAsync(d_norm, normtab.data(), sizeof(double) * normtab.size(), cudaMemcpyHostToDevice, st));
+  GTC_CUDA(cudaMemcpyAsync(d_off, val_off.data(), sizeof(int32_t) * d, cudaMemcpyHostToDevice, st));
+  GTC_CUDA(cudaMemcpyAsync(d_radix, radix.data(), sizeof(int32_t) * d, cudaMemcpyHostToDevice, st));
+  if (!prog.str_tables.empty())
+    GTC_CUDA(cudaMemcpyAsync(d_str, prog.str_tables.data(), prog.str_tables.size(), cudaMemcpyHostToDevice, st));
+  const EnumDev e{d_code, (int)prog.code.size(), d_values, d_off, d_str, d_radix, d_norm, d, (int)values.size(),
+                  (int64_t)total};
+  launch_enumerate_mask(e, d_mask, d_counts, d_total, st);
+  GTC_LAUNCHED();
+  int64_t n = 0;
+  GTC_CUDA(cudaMemcpyAsync(&n, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GTC_CUDA(cudaStreamSynchronize(st));
+  if (n == 0) return fail(GTC_ERR_EMPTY, "restrictions exclude every configuration");
+  auto* s = new gtc_space();
+  s->device = device;
+  s->n = n;
+  s->n_pad = pad_tiles(n);
+  s->d = d;
+  s->cartesian = total;
+  uint64_t* d_ids;
+  if ((rc = tmp.get(&d_ids, n)) || (rc = dalloc(&s->coords, (size_t)d * s->n_pad)) ||
+      (compressible && ((rc = dalloc(&s->cidx, (size_t)d * s->n_pad)) || (rc = dalloc(&s->ctab, (size_t)d * 256))))) {
+    gtc_space_destroy(s);
+    return rc;
+  }
+  cudaError_t ce = cudaMemsetAsync(s->coords, 0, sizeof(double) * d * s->n_pad, st);
+  if (ce == cudaSuccess && compressible) ce = cudaMemsetAsync(s->cidx, 0, (size_t)d * s->n_pad, st);
+  if (ce == cudaSuccess && compressible) {
+    std::vector<double> ctab((size_t)d * 256, 0.0);
+    for (int t = 0; t < d; ++t)
+      for (int r = 0; r < radix[t]; ++r) ctab[(size_t)t * 256 + r] = normtab[val_off[t] + r];
+    ce = cudaMemcpy(s->ctab, ctab.data(), ctab.size() * sizeof(double), cudaMemcpyHostToDevice);
+  }
+  if (ce != cudaSuccess) {
+    gtc_space_destroy(s);
+    return fail(GTC_ERR_CUDA, std::string("enumerate: ") + cudaGetErrorString(ce));
+  }
+  launch_enumerate_compact(e, d_mask, d_counts, s->n_pad, d_ids, s->coords, s->cidx, st);
+  ce = cudaGetLastError();
+  std::vector<double> soa((size_t)d * s->n_pad);
+  s->ids.resize(n);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(s->ids.data(), d_ids, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, st);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(soa.data(), s->coords, sizeof(double) * soa.size(), cudaMemcpyDeviceToHost, st);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+  if (ce != cudaSuccess) {
+    gtc_space_destroy(s);
+    return fail(GTC_ERR_CUDA, std::string("enumerate: ") + cudaGetErrorString(ce));
+  }
+  s->host_coords.resize((size_t)n * d);  // row-major host view (fit gathers)
+  for (int64_t j = 0; j < n; ++j)
+    for (int t = 0; t < d; ++t) s->host_coords[(size_t)j * d + t] = soa[(size_t)t * s->n_pad + j];
+  *out = s;
+  return GTC_OK;
+}
+
+extern "C" int gtc_space_ids(const gtc_space* s, uint64_t* ids) {
+  if (!s || !ids) return fail(GTC_ERR_INVALID, "null argument");
+  if (s->ids.empty()) return fail(GTC_ERR_INVALID, "space was not enumerated: no canonical ids");
+  std::memcpy(ids, s->ids.data(), sizeof(uint64_t) * s->ids.size());
+  return GTC_OK;
+}
+
+extern "C" uint64_t gtc_space_cartesian_size(const gtc_space* s) { return s ? s->cartesian : 0; }
 extern "C" const double* gtc_space_coords(const gtc_space* s) { return s ? s->host_coords.data() : nullptr; }
 extern "C" int32_t gtc_space_dimension(const gtc_space* s) { return s ? s->d : -1; }
 extern "C" int32_t gtc_space_device(const gtc_space* s) { return s ? s->device : -1; }

@@ -218,6 +218,27 @@ void launch_best_candidate(const double* mu, const double* std, const uint8_t* e
 void launch_scores(const double* mu, const double* sd, int64_t n, int af, double best_std,
                    double lambda, double* out, cudaStream_t stream);
 
+// ---- device search-space enumeration (search_space.hpp:120-166) ----------
+// Restriction programs compiled by restriction.cpp (postfix, EnumInstr);
+// the kernels evaluate them over the Cartesian grid, then compact the valid
+// canonical indices (ascending) with their normalised coordinates.
+struct EnumDev {
+  const void* code;         // EnumInstr[n_code]
+  int n_code;
+  const double* values;     // concatenated per-parameter value tables (booleans 0/1, categorical 0)
+  const int32_t* val_off;   // [d]
+  const uint8_t* str_tab;   // string-comparison tables
+  const int32_t* radix;     // [d] values per parameter
+  const double* normtab;    // concatenated rank / (k - 1) tables (search_space.hpp:158-166)
+  int d;
+  int n_values;             // total entries of `values` / `normtab`
+  int64_t total;            // Cartesian size (<= 20,000,000)
+};
+int64_t launch_enumerate_mask(const EnumDev& e, uint32_t* mask, int64_t* block_counts, int64_t* total_valid,
+                              cudaStream_t stream);  // returns the number of count blocks
+void launch_enumerate_compact(const EnumDev& e, const uint32_t* mask, const int64_t* block_offsets,
+                              int64_t n_pad, uint64_t* ids, double* coords, uint8_t* cidx, cudaStream_t stream);
+
 int reduce_blocks(int64_t n);  // grid size used by the reduction kernels
 uint64_t launches();
 

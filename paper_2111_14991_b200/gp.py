@@ -41,10 +41,26 @@ class DeviceError(Error):
     """CUDA failure (no device / launch error).  There is no CPU fallback."""
 
 
-def check(rc: int) -> None:
+class ParseError(Error):
+    """gridtune::ParseError (errors.hpp:17-26): restriction syntax / type error."""
+
+    def __init__(self, msg: str, position: int = 0):
+        super().__init__(msg)
+        self.position = position
+
+
+class EmptySearchSpaceError(Error):
+    """gridtune::EmptySearchSpaceError (errors.hpp:29-32)."""
+
+
+def check(rc: int, position: int = 0) -> None:
     if rc == _lib.GTC_OK:
         return
     msg = _lib.last_error()
+    if rc == _lib.GTC_ERR_PARSE:
+        raise ParseError(msg, position)
+    if rc == _lib.GTC_ERR_EMPTY:
+        raise EmptySearchSpaceError(msg)
     if rc == _lib.GTC_ERR_CONDITIONING:
         raise ModelConditioningError(msg)
     if rc == _lib.GTC_ERR_CONFIG:

@@ -152,6 +152,11 @@ int gtc_space_enumerate(int device, const gtc_param_def* params, int32_t n_param
 /* Canonical indices (Configuration::index) of an enumerated space, ascending
  * (GTC_ERR_INVALID for spaces built from explicit coordinates). */
 int gtc_space_ids(const gtc_space* space, uint64_t* ids);
+/* Initial-sample snap (draw_initial_sample, sampling.hpp:98-117): for each
+ * of the n points (n x d row-major, [0,1]^d) the position of the nearest
+ * configuration (squared Euclidean distance accumulated in parameter order,
+ * lowest position on ties), computed on the space's device. */
+int gtc_space_nearest(const gtc_space* space, const double* points, int32_t n, int64_t* positions);
 /* SearchSpace::cartesian_size() of an enumerated space (0 otherwise). */
 uint64_t gtc_space_cartesian_size(const gtc_space* space);
 /* Restriction::parse (restriction.hpp:479-486) without enumerating: 0 if the

@@ -110,6 +110,7 @@ SIGNATURES = [
                                       C.c_int32, I64P, C.POINTER(P)]),
     ("gtc_space_ids", C.c_int, [P, U64P]),
     ("gtc_space_cartesian_size", C.c_uint64, [P]),
+    ("gtc_space_nearest", C.c_int, [P, DP, C.c_int32, I64P]),
     ("gtc_restriction_validate", C.c_int, [C.POINTER(gtc_param_def), C.c_int32, C.c_char_p, I64P]),
     ("gtc_run_create", C.c_int, [P, C.POINTER(gtc_model_config), C.POINTER(P)]),
     ("gtc_run_destroy", C.c_int, [P]),

@@ -19,7 +19,10 @@
 // were decided on the host.
 #include <cuda_runtime.h>
 
+#include <math_constants.h>
+
 #include <algorithm>
+#include <climits>
 #include <cstdint>
 
 #include "gtc_internal.h"
@@ -208,6 +211,93 @@ __global__ void __launch_bounds__(kEnumThreads)
 }
 
 // Grid and words per block shared by both passes (contiguous word ranges).
+// ---- initial-sample snap (sampling.hpp:98-117) ------------------------------
+// For every design point, the position with the smallest squared distance
+// d2 = sum_j (p_j - c_j)^2 (accumulated in j order, no contraction, exactly
+// the reference's loop) and the lowest position on ties (its strict `<` scan).
+constexpr int kSnapThreads = 256;
+constexpr int kSnapGroup = 8;  // design points per pass (registers)
+
+struct SnapBest {
+  double d2;
+  long long pos;
+};
+__device__ __forceinline__ SnapBest snap_min(SnapBest a, SnapBest b) {
+  return (b.d2 < a.d2 || (b.d2 == a.d2 && b.pos < a.pos)) ? b : a;
+}
+
+__global__ void __launch_bounds__(kSnapThreads)
+    k_snap_partial(SpaceDev sp, const double* __restrict__ pts, int n_pts, SnapBest* __restrict__ partial) {
+  __shared__ SnapBest red[kSnapThreads / 32][kSnapGroup];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int g0 = 0; g0 < n_pts; g0 += kSnapGroup) {
+    SnapBest best[kSnapGroup];
+#pragma unroll
+    for (int q = 0; q < kSnapGroup; ++q) best[q] = SnapBest{CUDART_INF, LLONG_MAX};
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < sp.n; j += (int64_t)gridDim.x * blockDim.x) {
+      double d2[kSnapGroup];
+#pragma unroll
+      for (int q = 0; q < kSnapGroup; ++q) d2[q] = 0.0;
+      for (int t = 0; t < sp.d; ++t) {
+        const double c = sp.cidx ? __ldg(sp.ctab + t * 256 + sp.cidx[(int64_t)t * sp.n_pad + j])
+                                 : sp.coords[(int64_t)t * sp.n_pad + j];
+#pragma unroll
+        for (int q = 0; q < kSnapGroup; ++q) {
+          if (g0 + q < n_pts) {
+            const double diff = __dsub_rn(pts[(g0 + q) * sp.d + t], c);
+            d2[q] = __dadd_rn(d2[q], __dmul_rn(diff, diff));
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kSnapGroup; ++q) best[q] = snap_min(best[q], SnapBest{d2[q], (long long)j});
+    }
+#pragma unroll
+    for (int q = 0; q < kSnapGroup; ++q) {
+      for (int o = 16; o > 0; o >>= 1) {
+        SnapBest other{__shfl_xor_sync(0xffffffffu, best[q].d2, o), __shfl_xor_sync(0xffffffffu, best[q].pos, o)};
+        best[q] = snap_min(best[q], other);
+      }
+      if (lane == 0) red[wid][q] = best[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < kSnapGroup && g0 + (int)threadIdx.x < n_pts) {
+      SnapBest b = red[0][threadIdx.x];
+      for (int w = 1; w < kSnapThreads / 32; ++w) b = snap_min(b, red[w][threadIdx.x]);
+      partial[(int64_t)blockIdx.x * n_pts + g0 + threadIdx.x] = b;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_snap_merge(const SnapBest* __restrict__ partial, int blocks, int n_pts, int64_t* out) {
+  const int q = blockIdx.x;  // one block per design point
+  SnapBest b{CUDART_INF, LLONG_MAX};
+  for (int i = threadIdx.x; i < blocks; i += blockDim.x) b = snap_min(b, partial[(int64_t)i * n_pts + q]);
+  for (int o = 16; o > 0; o >>= 1) {
+    SnapBest other{__shfl_xor_sync(0xffffffffu, b.d2, o), __shfl_xor_sync(0xffffffffu, b.pos, o)};
+    b = snap_min(b, other);
+  }
+  __shared__ SnapBest red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    SnapBest m = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = snap_min(m, red[w]);
+    out[q] = m.pos == LLONG_MAX ? 0 : (int64_t)m.pos;  // (the reference scan starts at position 0)
+  }
+}
+
+int snap_partial_blocks(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + kSnapThreads - 1) / kSnapThreads, 148 * 4));
+}
+
+void launch_snap(const SpaceDev& sp, const double* pts, int n_pts, void* partial, int64_t* out, cudaStream_t s) {
+  const int blocks = snap_partial_blocks(sp.n);
+  k_snap_partial<<<blocks, kSnapThreads, 0, s>>>(sp, pts, n_pts, static_cast<SnapBest*>(partial));
+  k_snap_merge<<<n_pts, 256, 0, s>>>(static_cast<const SnapBest*>(partial), blocks, n_pts, out);
+}
+
 static void enum_geometry(int64_t total, int* grid, int64_t* wpb_words) {
   const int64_t words = (total + 31) / 32;
   const int64_t wpb = kEnumThreads / 32;

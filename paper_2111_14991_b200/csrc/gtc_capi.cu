@@ -558,6 +558,33 @@ extern "C" int gtc_space_ids(const gtc_space* s, uint64_t* ids) {
 }
 
 extern "C" uint64_t gtc_space_cartesian_size(const gtc_space* s) { return s ? s->cartesian : 0; }
+
+extern "C" int gtc_space_nearest(const gtc_space* s, const double* points, int32_t n, int64_t* positions) {
+  if (!s || !positions || (n > 0 && !points)) return fail(GTC_ERR_INVALID, "null argument");
+  if (n <= 0) return GTC_OK;
+  GTC_CUDA(cudaSetDevice(s->device));
+  cudaStream_t st;
+  GTC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } sg{st};
+  DevBufs tmp;
+  double* d_pts;
+  unsigned char* d_part;
+  int64_t* d_out;
+  const int blocks = snap_partial_blocks(s->n);
+  int rc;
+  if ((rc = tmp.get(&d_pts, (size_t)n * s->d)) || (rc = tmp.get(&d_part, (size_t)16 * blocks * n)) ||
+      (rc = tmp.get(&d_out, n)))
+    return rc;
+  GTC_CUDA(cudaMemcpyAsync(d_pts, points, sizeof(double) * n * s->d, cudaMemcpyHostToDevice, st));
+  launch_snap(s->dev(), d_pts, n, d_part, d_out, st);
+  GTC_LAUNCHED();
+  GTC_CUDA(cudaMemcpyAsync(positions, d_out, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
+  GTC_CUDA(cudaStreamSynchronize(st));
+  return GTC_OK;
+}
 extern "C" const double* gtc_space_coords(const gtc_space* s) { return s ? s->host_coords.data() : nullptr; }
 extern "C" int32_t gtc_space_dimension(const gtc_space* s) { return s ? s->d : -1; }
 extern "C" int32_t gtc_space_device(const gtc_space* s) { return s ? s->device : -1; }

@@ -239,6 +239,12 @@ int64_t launch_enumerate_mask(const EnumDev& e, uint32_t* mask, int64_t* block_c
 void launch_enumerate_compact(const EnumDev& e, const uint32_t* mask, const int64_t* block_offsets,
                               int64_t n_pad, uint64_t* ids, double* coords, uint8_t* cidx, cudaStream_t stream);
 
+// Initial-sample snap (sampling.hpp:98-117): nearest position of each design
+// point (n_pts x d row-major, device); `partial` holds 16 * blocks * n_pts bytes.
+int snap_partial_blocks(int64_t n);
+void launch_snap(const SpaceDev& sp, const double* pts, int n_pts, void* partial, int64_t* out,
+                 cudaStream_t stream);
+
 int reduce_blocks(int64_t n);  // grid size used by the reduction kernels
 uint64_t launches();
 

@@ -38,6 +38,15 @@ class Space:
     def size(self) -> int:
         return self.n
 
+    def nearest(self, points) -> np.ndarray:
+        """Positions of the configurations nearest to `points` (m x d in
+        [0,1]^d; lowest position on ties) -- the initial-sample snap of
+        draw_initial_sample (sampling.hpp:98-117), on the device."""
+        p = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, self.d))
+        out = np.empty(len(p), dtype=np.int64)
+        check(load().gtc_space_nearest(self._h, _lib.dptr(p), len(p), _lib.i64ptr(out)))
+        return out
+
     def close(self):
         h, self._h = getattr(self, "_h", None), None
         if h:

@@ -14,7 +14,7 @@ contextual variance (StrategyConfig defaults: Matern 3/2, l = 1.5).
 V (1.76 GB) >> L2 (126 MB), so every step streams from HBM (no L2 flush needed).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c4|c3]
+                  [--config c4|c3|c2]
 Under torchrun (N > 1) every rank runs an independent replica of the workload
 (run-level sharding, no collective on the data path); value = total iter/s.
 """
@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS) + ["c2"])
     ap.add_argument("--n", type=int, default=220)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
@@ -150,6 +150,89 @@ def prefix_positions(values, n, seed):
     rng = np.random.default_rng(seed)
     valid = np.nonzero(~np.isnan(values))[0]
     return rng.choice(valid, n, replace=False)
+
+
+# C2 (BASELINE.json configs[1]): convolution and pnpoly simulation-mode cases
+# (PAPER.md:345-380 parameters, SURVEY.md §8(d) restrictions and invalid
+# fractions), bo-multi, budget 220, n_init 20, 35 repeats each.
+C2_SPACES = {
+    "conv": ([("filter_width", [15]), ("filter_height", [15]),
+              ("block_size_x", [1, 2, 4, 8, 16, 32, 48, 64, 80, 96, 112, 128]),
+              ("block_size_y", [1, 2, 4, 8, 16, 32]), ("tile_size_x", list(range(1, 9))),
+              ("tile_size_y", list(range(1, 9))), ("use_padding", [0, 1]), ("read_only", [0, 1])],
+             ["block_size_x*block_size_y>=64", "tile_size_x*tile_size_y<30"], 0.385, 1.625),
+    "pnpoly": ([("block_size_x", list(range(32, 993, 32))), ("tile_size", [1] + list(range(2, 21, 2))),
+                ("between_method", [0, 1, 2, 3]), ("use_precomputed_slopes", [0, 1]), ("use_method", [0, 1, 2])],
+               [], 0.039, 26.968),
+}
+
+
+def c2_values(n, invalid, minimum, seed):
+    """Seeded synthetic measurements over an enumerated space (no cache files
+    exist): a smooth random landscape rescaled to the case's published minimum,
+    with the case's fraction of runtime-invalid configurations."""
+    rng = np.random.default_rng(seed)
+    v = np.cumsum(rng.normal(size=n)) * 0.05 + rng.random(n)
+    v = minimum + (v - v.min())
+    v[rng.random(n) < invalid] = np.nan
+    return v
+
+
+def run_c2(args):
+    """C2 throughput: 35 repeats of each case as independent runs driven by a
+    host thread pool on one device (run_experiment's model); runs/s."""
+    import torch
+    import paper_2111_14991_b200 as gt
+    reps = 35
+    t_total, runs, evals = 0.0, 0, 0
+    spaces = {}
+    for name, (params, rs, invalid, minimum) in C2_SPACES.items():
+        es = gt.SearchSpace([gt.ParameterDef(k, v) for k, v in params], rs).enumerate()
+        spaces[name] = (es, c2_values(es.n, invalid, minimum, BASE_SEED + len(name)))
+    threads = reps  # one host thread per run of a case: the threads mostly wait on device syncs
+    with ClockSampler(0) as clocks:
+        for name, (es, values) in spaces.items():
+            cfgs = [gt.StrategyConfig(id=gt.StrategyId.bo_multi, seed=BASE_SEED + r, budget=220, n_init=20)
+                    for r in range(reps)]
+            gt.run_bo_batch(es, es.ids, cfgs[:2], values, threads=2)  # warm-up
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out = gt.run_bo_batch(es, es.ids, cfgs, values, threads=threads)
+            torch.cuda.synchronize()
+            t_total += time.perf_counter() - t0
+            runs += len(out)
+            evals += sum(int(r.evaluations) for r in out)
+    print(json.dumps({
+        "metric": "BO runs/sec (C2: conv + pnpoly simulation mode, bo-multi, budget 220)", "value": runs / t_total,
+        "unit": "runs/s", "n_gpus": 1, "steps": runs, "warmup": 2, "ms_per_step": 1e3 * t_total / runs,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic measurements over the device-enumerated conv (N=%d) and pnpoly (N=%d) spaces" % (
+            spaces["conv"][0].n, spaces["pnpoly"][0].n),
+        "config": {"workload": "C2 conv + pnpoly, 35 repeats each, bo-multi, n_init 20, budget 220",
+                   "threads": threads, "evaluations": evals,
+                   "timing": "wall clock of gtc_run_bo_batch (host thread pool, one stream per run)"},
+        "evaluations_per_sec": evals / t_total, "clocks": clocks.summary(),
+        "cpu_baseline": c2_reference()}))
+
+
+def c2_reference():
+    """The unmodified reference run_bo (oracle/_ref/ref_tool runbo) on one
+    host core for one run of a conv-sized proxy (random-rough 12x8x8x12 =
+    9,216 candidates, 38.5 % invalid, bo-multi, budget 220, n_init 20);
+    run_experiment runs one run per worker thread, so runs/s = cores / t."""
+    tool = ROOT / "oracle" / "_ref" / "ref_tool"
+    if not tool.exists():
+        return None
+    import tempfile
+    cores = os.cpu_count() or 1
+    with tempfile.TemporaryDirectory() as tmp:
+        t0 = time.perf_counter()
+        subprocess.run([str(tool), "runbo", "random-rough", "12x8x8x12", str(BASE_SEED), "0.385", "bo-multi", "220",
+                        "20", "1", tmp], check=True, capture_output=True, timeout=900)
+        t = time.perf_counter() - t0
+    return {"value": cores / t, "unit": "runs/s", "cores": cores, "kind": "reference",
+            "sample": f"one reference run_bo (bo-multi, budget 220) on a 9,216-candidate random-rough proxy took "
+                      f"{t:.1f} s on one core; {cores} concurrent runs as run_experiment's thread pool"}
 
 
 def cpu_baseline(cfg, n, budget_s=30.0):
@@ -273,6 +356,9 @@ def run_sharded(args, cfg, rank, world, local):
 
 def main():
     args = parse()
+    if args.config == "c2":
+        run_c2(args)
+        return
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference_arm(args, cfg)

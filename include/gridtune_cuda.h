@@ -314,6 +314,17 @@ int gtc_run_bo_table(gtc_space* space, const uint64_t* ids, const gtc_bo_config*
                      const double* values, gtc_bo_record* records, double* lambdas,
                      int64_t capacity, gtc_bo_summary* summary);
 
+/* run_experiment's worker pool (experiment.hpp:313-358) for replay tables:
+ * n_runs independent BO runs over one resident space and one value table,
+ * `threads` host threads (<= 0: hardware concurrency), each driving its runs
+ * one after another on its own CUDA streams, so the device interleaves the
+ * runs' kernels.  Run i uses configs[i] and writes records/lambdas at
+ * i * capacity, summaries[i] and statuses[i] (a GTC_* code).  Returns GTC_OK
+ * when every run succeeded, else the first failing run's status. */
+int gtc_run_bo_batch(gtc_space* space, const uint64_t* ids, const gtc_bo_config* configs, int32_t n_runs,
+                     const double* values, int32_t threads, gtc_bo_record* records, double* lambdas,
+                     int64_t capacity, gtc_bo_summary* summaries, int32_t* statuses);
+
 /* ---- candidate-axis sharding (very large spaces over several GPUs) --------- */
 /* Each rank holds a contiguous slice of the global candidate list in its own
  * gtc_space; the GP state is replicated (every rank applies the same

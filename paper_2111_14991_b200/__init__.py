@@ -14,7 +14,7 @@ from .gp import (AcquisitionId, CandidateScores, ConfigError, ContextualVariance
                  mean_posterior_variance)
 from .runtime import FitInfo, Selection, Space, SurrogateRun  # noqa: F401
 from .space import EnumeratedSpace, ParameterDef, ParamKind, SearchSpace, parse_restriction  # noqa: F401
-from .strategies import (StrategyConfig, StrategyId, TuningRun, run_bo, run_strategy,  # noqa: F401
-                         strategy_from_string)
+from .strategies import (StrategyConfig, StrategyId, TuningRun, run_bo, run_bo_batch,  # noqa: F401
+                         run_strategy, strategy_from_string)
 
 __version__ = "0.1.0"

@@ -1,7 +1,11 @@
 // C ABI entry points for a whole BO run (gtc_run_bo / gtc_run_bo_table) over
 // the C++ host mirror in include/gridtune_b200/strategies.hpp.
+#include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
+#include <thread>
+#include <vector>
 #include <exception>
 #include <limits>
 #include <string>
@@ -114,6 +118,37 @@ extern "C" int gtc_run_bo(gtc_space* space, const std::uint64_t* ids, const gtc_
     return rc > 0 ? Measurement::valid(v) : Measurement::invalid(InvalidReason::runtime_error);
   };
   return run(space, ids, cfg, obj, records, lambdas, capacity, summary);
+}
+
+extern "C" int gtc_run_bo_batch(gtc_space* space, const std::uint64_t* ids, const gtc_bo_config* configs,
+                                std::int32_t n_runs, const double* values, std::int32_t threads,
+                                gtc_bo_record* records, double* lambdas, std::int64_t capacity,
+                                gtc_bo_summary* summaries, std::int32_t* statuses) {
+  if (!space || !ids || !configs || !values || !statuses || n_runs < 0) {
+    gtc_internal_set_error("null argument");
+    return GTC_ERR_INVALID;
+  }
+  const Objective obj = [values](const Configuration& c) {
+    const double v = values[c.position];
+    return std::isnan(v) ? Measurement::invalid(InvalidReason::runtime_error) : Measurement::valid(v);
+  };
+  int workers = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
+  workers = std::max(1, std::min(workers, static_cast<int>(n_runs)));
+  std::atomic<std::int32_t> next{0};
+  auto worker = [&]() {
+    for (std::int32_t i; (i = next.fetch_add(1)) < n_runs;) {
+      statuses[i] = run(space, ids, &configs[i], obj, records ? records + (std::int64_t)i * capacity : nullptr,
+                        lambdas ? lambdas + (std::int64_t)i * capacity : nullptr, capacity,
+                        summaries ? &summaries[i] : nullptr);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int w = 1; w < workers; ++w) pool.emplace_back(worker);
+  worker();
+  for (std::thread& t : pool) t.join();
+  for (std::int32_t i = 0; i < n_runs; ++i)
+    if (statuses[i] != GTC_OK) return statuses[i];
+  return GTC_OK;
 }
 
 extern "C" int gtc_run_bo_table(gtc_space* space, const std::uint64_t* ids, const gtc_bo_config* cfg,

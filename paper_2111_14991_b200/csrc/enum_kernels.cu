@@ -314,7 +314,8 @@ int64_t launch_enumerate_mask(const EnumDev& e, uint32_t* mask, int64_t* block_c
   int64_t wpb_words;
   enum_geometry(e.total, &grid, &wpb_words);
   const size_t sm = sizeof(EnumInstr) * e.n_code + sizeof(double) * e.n_values + sizeof(int32_t) * 2 * e.d + 16;
-  if (sm > 48 * 1024) cudaFuncSetAttribute(k_enum_mask, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (sm + 8 * 1024 > 48 * 1024)  // the 48 KB default covers static + dynamic shared memory
+    cudaFuncSetAttribute(k_enum_mask, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_enum_mask<<<grid, kEnumThreads, sm, s>>>(e, wpb_words, mask, block_counts);
   k_enum_scan<<<1, 1024, 0, s>>>(block_counts, grid, total_valid);
   return grid;

@@ -1575,21 +1575,29 @@ static size_t cta_smem_bytes(int n_max, int rows, bool* staged) {
   return *staged ? with_l : base;
 }
 
-// Opt-in to large dynamic shared memory once per kernel and device (the
-// limit is raised to the whole budget; a driver call per launch would sit on
-// the observe step's host critical path).
+// Opt-in to large dynamic shared memory: the attribute is raised to the
+// largest size requested so far per kernel and device (a driver call only
+// when the requirement grows, not on every launch of the observe step).
 template <class K>
 static void opt_in_smem(K kernel, size_t bytes) {
-  if (bytes <= 48 * 1024) return;
+  // the 48 KB default covers static + dynamic shared memory: opt in with room
+  // for the kernels' static arrays
+  if (bytes + 8 * 1024 <= 48 * 1024) return;
   static std::mutex mu;
-  static std::vector<std::pair<const void*, int>> seen;
+  static std::vector<std::pair<std::pair<const void*, int>, size_t>> set_to;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
-  for (const auto& e : seen)
-    if (e.first == (const void*)kernel && e.second == dev) return;
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCtaSmemLimit);
-  seen.emplace_back((const void*)kernel, dev);
+  const std::pair<const void*, int> key{(const void*)kernel, dev};
+  for (auto& e : set_to) {
+    if (e.first != key) continue;
+    if (e.second >= bytes) return;
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess)
+      e.second = bytes;
+    return;
+  }
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess)
+    set_to.push_back({key, bytes});
 }
 
 void launch_gp_factor(const GpDev& g, KernelParams k, double noise, double jitter, int n,

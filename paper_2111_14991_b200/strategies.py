@@ -123,6 +123,10 @@ def run_bo(space: Space, ids, config: StrategyConfig, values=None,
         if err:
             raise err[0]
     check(rc)
+    return _tuning_run(recs, lams, summ)
+
+
+def _tuning_run(recs, lams, summ) -> TuningRun:
     n = summ.n_records
     arr = np.ctypeslib.as_array(recs)[:n]
     return TuningRun(
@@ -135,6 +139,33 @@ def run_bo(space: Space, ids, config: StrategyConfig, values=None,
         evaluations=summ.evaluations, budget_consumed=summ.budget_consumed,
         invalid_count=summ.invalid_count, surrogate_size=summ.surrogate_size,
         best_value=summ.best_value, best_position=summ.best_position, n_warnings=summ.n_warnings)
+
+
+def run_bo_batch(space: Space, ids, configs, values, threads: int = 0) -> list:
+    """Independent BO runs over one resident space and replay table, driven by
+    a host thread pool on the device (run_experiment's worker model,
+    experiment.hpp:313-358; gtc_run_bo_batch).  Returns one TuningRun per
+    config, in order; raises the first failing run's error."""
+    ids = np.ascontiguousarray(np.asarray(ids, dtype=np.uint64))
+    if len(ids) != space.n:
+        raise ValueError("ids must have one entry per position")
+    v = np.ascontiguousarray(np.asarray(values, dtype=np.float64))
+    n = len(configs)
+    cap = space.n + 1
+    recs = (_lib.gtc_bo_record * (cap * max(n, 1)))()
+    lams = np.zeros(cap * max(n, 1))
+    summ = (_lib.gtc_bo_summary * max(n, 1))()
+    cfgs = (_lib.gtc_bo_config * max(n, 1))(*[c.c() for c in configs])
+    st = np.zeros(max(n, 1), dtype=np.int32)
+    rc = load().gtc_run_bo_batch(space.handle, ids.ctypes.data_as(_lib.U64P), cfgs, n, _lib.dptr(v), int(threads),
+                                 recs, _lib.dptr(lams), cap, summ, st.ctypes.data_as(C.POINTER(C.c_int32)))
+    check(rc)
+    rsize = C.sizeof(_lib.gtc_bo_record)
+    out = []
+    for i in range(n):
+        sub = (_lib.gtc_bo_record * cap).from_address(C.addressof(recs) + i * cap * rsize)
+        out.append(_tuning_run(sub, lams[i * cap:(i + 1) * cap], summ[i]))
+    return out
 
 
 run_strategy = run_bo

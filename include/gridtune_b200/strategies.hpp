@@ -153,6 +153,13 @@ class RunContext {
 
 /// One run's resident surrogate (gtc_run) as an argmax source: positions are
 /// space positions, candidates are the unvisited configurations.
+/// Observe group of the calling thread (gtc_run_bo_batch sets it for its
+/// worker threads): runs created on the thread join it.
+inline gtc_group*& thread_observe_group() {
+  static thread_local gtc_group* g = nullptr;
+  return g;
+}
+
 class DeviceSurrogate : public ArgmaxSource {
  public:
   DeviceSurrogate(const EnumeratedSpace& space, const MaternKernel& kernel, double noise, double jitter,
@@ -162,6 +169,7 @@ class DeviceSurrogate : public ArgmaxSource {
     gtc_run* r = nullptr;
     check(gtc_run_create(space.device_space(), &cfg, &r));
     run_.reset(r, [](gtc_run* p) { gtc_run_destroy(p); });
+    if (gtc_group* g = thread_observe_group()) check(gtc_run_set_group(r, g));
   }
 
   gtc_run* handle() const { return run_.get(); }

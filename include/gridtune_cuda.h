@@ -62,6 +62,7 @@ extern "C" {
 typedef struct gtc_space gtc_space; /* resident normalised search space      */
 typedef struct gtc_run gtc_run;     /* one BO run's resident surrogate state */
 typedef struct gtc_gp gtc_gp;       /* stand-alone GpModel (arbitrary points) */
+typedef struct gtc_group gtc_group; /* batched observe across runs (one per batch) */
 
 /* MaternKernel, gp.hpp:27-56 */
 typedef struct {
@@ -324,6 +325,19 @@ int gtc_run_bo_table(gtc_space* space, const uint64_t* ids, const gtc_bo_config*
 int gtc_run_bo_batch(gtc_space* space, const uint64_t* ids, const gtc_bo_config* configs, int32_t n_runs,
                      const double* values, int32_t threads, gtc_bo_record* records, double* lambdas,
                      int64_t capacity, gtc_bo_summary* summaries, int32_t* statuses);
+
+/* Observe groups: the member threads of a group each drive their own run
+ * (gtc_run_set_group); a grouped gtc_observe waits until every member has
+ * issued one (or left) and then all of them run in shared launches (one
+ * bordered-append, one predictive-pass, one selection launch per AF mask, one
+ * read-back) -- same results as the single-run path.  Every member thread
+ * joins before its first grouped call and leaves when it is done.  Runs of a
+ * group must share one space. */
+int gtc_group_create(int device, gtc_group** out);
+int gtc_group_destroy(gtc_group* group);
+int gtc_group_join(gtc_group* group);
+int gtc_group_leave(gtc_group* group);
+int gtc_run_set_group(gtc_run* run, gtc_group* group);
 
 /* ---- candidate-axis sharding (very large spaces over several GPUs) --------- */
 /* Each rank holds a contiguous slice of the global candidate list in its own

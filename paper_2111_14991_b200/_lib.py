@@ -152,6 +152,11 @@ SIGNATURES = [
                              C.POINTER(gtc_bo_record), DP, C.c_int64, C.POINTER(gtc_bo_summary)]),
     ("gtc_run_bo_table", C.c_int, [P, U64P, C.POINTER(gtc_bo_config), DP, C.POINTER(gtc_bo_record), DP,
                                    C.c_int64, C.POINTER(gtc_bo_summary)]),
+    ("gtc_group_create", C.c_int, [C.c_int, C.POINTER(P)]),
+    ("gtc_group_destroy", C.c_int, [P]),
+    ("gtc_group_join", C.c_int, [P]),
+    ("gtc_group_leave", C.c_int, [P]),
+    ("gtc_run_set_group", C.c_int, [P, P]),
     ("gtc_run_bo_batch", C.c_int, [P, U64P, C.POINTER(gtc_bo_config), C.c_int32, DP, C.c_int32,
                                    C.POINTER(gtc_bo_record), DP, C.c_int64, C.POINTER(gtc_bo_summary),
                                    C.POINTER(C.c_int32)]),

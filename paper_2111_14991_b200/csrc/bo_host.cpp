@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -134,18 +135,41 @@ extern "C" int gtc_run_bo_batch(gtc_space* space, const std::uint64_t* ids, cons
   };
   int workers = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
   workers = std::max(1, std::min(workers, static_cast<int>(n_runs)));
-  std::atomic<std::int32_t> next{0};
+  // observe groups: each group's per-iteration device work shares launches;
+  // several groups (own streams) keep the device busy while one group's
+  // threads do their host work
+  static const int per_group = [] {
+    const char* e = std::getenv("GTC_RUNS_PER_GROUP");
+    return e ? std::max(1, std::atoi(e)) : 64;
+  }();
+  const int n_groups = workers > 1 ? (workers + per_group - 1) / per_group : 0;
+  std::vector<gtc_group*> groups(n_groups, nullptr);
+  for (int k = 0; k < n_groups; ++k) {
+    const int rc = gtc_group_create(gtc_space_device(space), &groups[k]);
+    if (rc) {
+      for (gtc_group* g : groups) gtc_group_destroy(g);
+      return rc;
+    }
+  }
+  std::atomic<std::int32_t> next{0}, next_worker{0};
   auto worker = [&]() {
+    const int w = next_worker.fetch_add(1);
+    gtc_group* group = n_groups ? groups[w % n_groups] : nullptr;
+    if (group) gtc_group_join(group);
+    thread_observe_group() = group;
     for (std::int32_t i; (i = next.fetch_add(1)) < n_runs;) {
       statuses[i] = run(space, ids, &configs[i], obj, records ? records + (std::int64_t)i * capacity : nullptr,
                         lambdas ? lambdas + (std::int64_t)i * capacity : nullptr, capacity,
                         summaries ? &summaries[i] : nullptr);
     }
+    thread_observe_group() = nullptr;
+    if (group) gtc_group_leave(group);
   };
   std::vector<std::thread> pool;
   for (int w = 1; w < workers; ++w) pool.emplace_back(worker);
   worker();
   for (std::thread& t : pool) t.join();
+  for (gtc_group* g : groups) gtc_group_destroy(g);
   for (std::int32_t i = 0; i < n_runs; ++i)
     if (statuses[i] != GTC_OK) return statuses[i];
   return GTC_OK;

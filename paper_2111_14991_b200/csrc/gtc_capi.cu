@@ -7,6 +7,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <atomic>
+#include <semaphore>
+#include <thread>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -225,6 +231,7 @@ struct gtc_space {
 
 struct gtc_run {
   gtc_space* space = nullptr;
+  gtc_group* group = nullptr;  // batched observe (gtc_run_set_group)
   gtc_model_config cfg{};
   cudaStream_t stream = nullptr;
   GpStore gp;
@@ -269,6 +276,8 @@ struct gtc_run {
     return VarPartials{visited, acc + acc_gen, acc + (acc_gen ^ 1)};
   }
   VarSource vsrc() const { return VarSource{acc + acc_gen, cfg.kernel.output_variance, 0.0, 0, 0}; }
+  // the total to update in O(1) on a mark, when it matches the visited set
+  VarAccum* live_acc() const { return acc_valid && predictions_valid ? acc + acc_gen : nullptr; }
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;          // last predictive pass
   cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;  // last gtc_observe device span
   bool pass_timed = false, step_timed = false, step_appended = false;
@@ -835,9 +844,10 @@ static int set_visited(gtc_run* r, int64_t pos, int set) {
   if (pos < 0 || pos >= r->space->n) return fail(GTC_ERR_INVALID, "position out of range");
   GTC_CUDA(cudaSetDevice(r->space->device));
   if (!host_mark(r, pos, set)) return GTC_OK;
-  launch_mark(r->visited, pos, set, r->stream);
+  VarAccum* acc = r->live_acc();
+  launch_mark(r->visited, pos, set, r->stream, acc, r->var, r->cfg.kernel.output_variance);
   GTC_LAUNCHED();
-  r->acc_valid = false;
+  r->acc_valid = acc != nullptr;
   return GTC_OK;
 }
 
@@ -897,11 +907,8 @@ static int ensure_var_totals(gtc_run* r) {
   return GTC_OK;
 }
 
-// Enqueues the selection kernel (asynchronous).  With `global_totals`, the
-// mean variance comes from the global (sum, count) passed by value
-// (candidate-axis sharding) instead of this run's own variance total.
-static int enqueue_selection(gtc_run* r, const gtc_select_args* a, bool global_totals = false,
-                             double global_sum = 0.0, long long global_count = 0) {
+static int build_selection(gtc_run* r, const gtc_select_args* a, bool global_totals, double global_sum,
+                           long long global_count, SelectRunArgs* out) {
   int rc = ensure_predictions(r);
   if (rc) return rc;
   SelectParams p{a->af_mask & 7u, a->lambda_mode, a->lambda_constant, a->cv_initial_sample_mean,
@@ -926,16 +933,24 @@ static int enqueue_selection(gtc_run* r, const gtc_select_args* a, bool global_t
     p.n_excluded = (int)ex.size();
   }
   first_and_count(r, ex, &p.first_eligible, &p.n_candidates);
-  if (global_totals) {
-    const VarSource vs{nullptr, 0.0, global_sum, global_count, 1};
-    launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, vs, r->tstat, r->red.b, r->red.sel,
-                  r->stream);
-    GTC_LAUNCHED();
-    return GTC_OK;
+  VarSource vs{nullptr, 0.0, global_sum, global_count, 1};
+  if (!global_totals) {
+    if ((rc = ensure_var_totals(r))) return rc;
+    vs = r->vsrc();
   }
-  if ((rc = ensure_var_totals(r))) return rc;
-  launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, r->vsrc(), r->tstat, r->red.b,
-                r->red.sel, r->stream);
+  *out = SelectRunArgs{r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, vs, r->tstat, r->red.b, r->red.sel};
+  return GTC_OK;
+}
+
+// Enqueues the selection kernel (asynchronous).  With `global_totals`, the
+// mean variance comes from the global (sum, count) passed by value
+// (candidate-axis sharding) instead of this run's own variance total.
+static int enqueue_selection(gtc_run* r, const gtc_select_args* a, bool global_totals = false,
+                             double global_sum = 0.0, long long global_count = 0) {
+  SelectRunArgs sa;
+  int rc = build_selection(r, a, global_totals, global_sum, global_count, &sa);
+  if (rc) return rc;
+  launch_select(sa.mu, sa.var, sa.visited, sa.n, sa.sc, sa.p, sa.vs, sa.tstat, sa.b, sa.out, r->stream);
   GTC_LAUNCHED();
   return GTC_OK;
 }
@@ -1080,6 +1095,388 @@ extern "C" int gtc_select(gtc_run* r, const gtc_select_args* a, gtc_select_resul
 // (optional) cooperative selection -> one readback.  A failed bordered pivot
 // is detected on the device (the pass is skipped, the selection reports
 // GpScalars::status) and handled here by the escalating refit.
+// One gtc_observe call, split so that a group can run the device part of
+// many runs' calls in shared launches (gtc_run_bo_batch).
+struct ObserveReq {
+  gtc_run* r;
+  int64_t pos;
+  double y_raw;
+  int32_t valid;
+  const gtc_select_args* a;
+  bool newly = false;
+  int n0 = 0;
+  bool appended = false;   // bordered append + pass enqueued
+  bool selecting = false;  // selection enqueued
+  int status = GTC_OK;     // device-phase failure
+  std::string error;
+  std::binary_semaphore done{0};  // released by the group's executor
+};
+
+// Host bookkeeping before the device work.
+static void observe_prepare(ObserveReq& q) {
+  gtc_run* r = q.r;
+  q.newly = host_mark(r, q.pos, 1);
+  q.n0 = r->n;
+  if (q.valid) {
+    keep_obs(r, q.n0);
+    push_obs(r, &r->space->host_coords[(size_t)q.pos * r->space->d], q.y_raw);
+  }
+}
+
+// The device part on the run's own stream (single-run path).
+static int observe_device(ObserveReq& q, gtc_fit_info* info) {
+  gtc_run* r = q.r;
+  int rc;
+  GTC_CUDA(cudaEventRecord(r->ev_step0, r->stream));
+  if (q.valid) {
+    if (q.n0 == 0) {
+      if (q.newly) {
+        launch_mark(r->visited, q.pos, 1, r->stream);
+        GTC_LAUNCHED();
+        r->acc_valid = false;
+      }
+      if ((rc = refit(r, r->cfg.jitter, info))) return rc;
+    } else {
+      if ((rc = enqueue_append(r, q.pos, q.y_raw, q.newly ? r->visited : nullptr))) return rc;
+      r->predictions_valid = true;
+      q.appended = true;
+    }
+  } else if (q.newly) {
+    VarAccum* acc = r->live_acc();
+    launch_mark(r->visited, q.pos, 1, r->stream, acc, r->var, r->cfg.kernel.output_variance);
+    GTC_LAUNCHED();
+    r->acc_valid = acc != nullptr;
+  }
+  q.selecting = q.a && r->space->n - r->visited_count > 0;
+  if (q.selecting && (rc = enqueue_selection(r, q.a))) return rc;
+  GTC_CUDA(cudaEventRecord(r->ev_step1, r->stream));
+  r->step_timed = true;
+  r->step_appended = q.appended;
+  if (q.selecting)
+    GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sel, r->red.sel, sizeof(SelectDev), cudaMemcpyDeviceToHost, r->stream));
+  GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sc, r->gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, r->stream));
+  GTC_CUDA(cudaStreamSynchronize(r->stream));
+  return GTC_OK;
+}
+
+// After the device work (h_rb holds the scalars and the selection).
+static int observe_finish(ObserveReq& q, gtc_select_result* out, gtc_fit_info* info) {
+  gtc_run* r = q.r;
+  int rc;
+  if (q.appended) {
+    if (r->h_rb->sc.status != 0) {
+      // bordered pivot <= 0: refactorise with escalated jitter (gp.hpp:116-129)
+      if ((rc = refit(r, r->jitter * 2.0, info))) return rc;
+      if (q.selecting) {
+        if ((rc = enqueue_selection(r, q.a))) return rc;
+        GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sel, r->red.sel, sizeof(SelectDev), cudaMemcpyDeviceToHost, r->stream));
+        GTC_CUDA(cudaStreamSynchronize(r->stream));
+      }
+    } else {
+      r->n = q.n0 + 1;
+      *r->gp.h_sc = r->h_rb->sc;
+      fill_info(info, r->h_rb->sc, r->n, 0);
+    }
+  } else if (!q.valid) {
+    fill_info(info, r->h_rb->sc, r->n, 0);
+  }
+  if (q.selecting && out) {
+    copy_result(r->h_rb->sel, out);
+    if (r->h_rb->sel.n_candidates == 0) return fail(GTC_ERR_NO_CANDIDATES, "acquisition: no candidates remaining");
+  } else if (out) {
+    std::memset(out, 0, sizeof(*out));
+    for (int k = 0; k < 3; ++k) out->position[k] = -1;
+  }
+  return GTC_OK;
+}
+
+// ---- observe groups (gtc_run_bo_batch) -------------------------------------
+// The member threads of a group each drive their own run; a gtc_observe of a
+// grouped run queues its request and waits until every member has queued
+// one (or left), then the last one to arrive enqueues the device work of all
+// queued requests in shared launches on the group's stream -- marks, one
+// bordered-append launch, one predictive-pass launch, one selection launch
+// per AF mask -- and one read-back.  Results are bit-identical to the
+// single-run path (same kernels, same per-run arguments).
+struct gtc_group {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  int members = 0;
+  std::atomic<uint64_t> round{0};  // completed rounds (waiters spin on it, no lock hand-off)
+  std::vector<ObserveReq*> queue;
+  unsigned char* h_buf = nullptr;  // pinned staging (arguments, results)
+  unsigned char* d_buf = nullptr;
+  size_t cap = 0;
+  // diagnostics (GTC_GROUP_STATS=1 prints them at destroy)
+  uint64_t n_rounds = 0, n_requests = 0;
+  double t_exec = 0.0, t_first = -1.0, t_last = 0.0, t_enqueued = 0.0, t_round0 = 0.0;
+};
+
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+static int group_reserve(gtc_group* g, size_t bytes) {
+  if (bytes <= g->cap) return GTC_OK;
+  const size_t cap = std::max(bytes, 2 * g->cap);
+  if (g->h_buf) cudaFreeHost(g->h_buf);
+  if (g->d_buf) cudaFree(g->d_buf);
+  g->h_buf = g->d_buf = nullptr;
+  g->cap = 0;
+  GTC_CUDA(cudaMallocHost(&g->h_buf, cap));
+  GTC_CUDA(cudaMalloc(&g->d_buf, cap));
+  g->cap = cap;
+  return GTC_OK;
+}
+
+static size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
+
+// Device work of every queued request (called with the group lock held).
+static int execute_round(gtc_group* g) {
+  std::vector<ObserveReq*>& Q = g->queue;
+  const int R = (int)Q.size();
+  GTC_CUDA(cudaSetDevice(g->device));
+  std::vector<cudaStream_t> saved(R);
+  for (int i = 0; i < R; ++i) {  // every run's device work of this round on the group stream
+    saved[i] = Q[i]->r->stream;
+    Q[i]->r->stream = g->stream;
+  }
+  struct Restore {
+    std::vector<ObserveReq*>& Q;
+    std::vector<cudaStream_t>& saved;
+    ~Restore() {
+      for (size_t i = 0; i < Q.size(); ++i) Q[i]->r->stream = saved[i];
+    }
+  } restore{Q, saved};
+  // layout of the staging buffer
+  const size_t o_app = 0, o_ext = align16(o_app + sizeof(AppendArgs) * R);
+  const size_t o_sel = align16(o_ext + sizeof(ExtendArgs) * R), o_mark = align16(o_sel + sizeof(SelectRunArgs) * R);
+  const size_t o_gat = align16(o_mark + sizeof(MarkDesc) * R), o_res = align16(o_gat + sizeof(GatherDesc) * 2 * R);
+  const size_t per_res = align16(sizeof(SelectDev)) + align16(sizeof(GpScalars));
+  // (+ one masked copy of the selection arguments per AF mask, for rounds
+  // whose runs ask for different AF sets)
+  const size_t o_msk = align16(o_res + per_res * R);
+  int rc = group_reserve(g, o_msk + sizeof(SelectRunArgs) * R * 8);
+  if (rc) return rc;
+  auto* app = reinterpret_cast<AppendArgs*>(g->h_buf + o_app);
+  auto* ext = reinterpret_cast<ExtendArgs*>(g->h_buf + o_ext);
+  auto* sel = reinterpret_cast<SelectRunArgs*>(g->h_buf + o_sel);
+  auto* mark = reinterpret_cast<MarkDesc*>(g->h_buf + o_mark);
+  auto* gat = reinterpret_cast<GatherDesc*>(g->h_buf + o_gat);
+  // 1. marks of invalid evaluations, appends + passes of valid ones
+  int n_mark = 0, n_app = 0, nu = -1, max_n0 = 0, d = 0;
+  size_t app_smem = 0;
+  int64_t tiles = 0, n_cand = 0;
+  for (int i = 0; i < R; ++i) {
+    ObserveReq& q = *Q[i];
+    gtc_run* r = q.r;
+    app[i] = AppendArgs{};
+    ext[i] = ExtendArgs{};
+    sel[i] = SelectRunArgs{};
+    d = r->space->d;
+    tiles = r->space->n_pad / kTile;
+    n_cand = r->space->n;
+    if (q.valid) {
+      size_t sm;
+      app[i] = make_append_args(r->gp.dev, kparams(r->cfg.kernel), r->cfg.noise, r->space->dev(), q.pos, nullptr,
+                                q.y_raw, q.n0, q.newly ? r->visited : nullptr, &sm);
+      const VarPartials vp = r->vp();
+      ext[i] = make_pass_args(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, q.n0, r->mu,
+                              r->var, &vp, r->tstat);
+      app_smem = std::max(app_smem, sm);
+      max_n0 = std::max(max_n0, q.n0);
+      nu = r->cfg.kernel.nu;
+      r->acc_valid = true;
+      r->predictions_valid = true;
+      r->pass_timed = false;
+      q.appended = true;
+      ++n_app;
+    } else if (q.newly) {
+      VarAccum* acc = r->live_acc();
+      mark[n_mark++] = MarkDesc{r->visited, q.pos, acc, r->var, r->cfg.kernel.output_variance};
+      r->acc_valid = acc != nullptr;
+    }
+    r->step_timed = false;
+  }
+  // arguments of the append / pass / mark launches: one copy
+  GTC_CUDA(cudaMemcpyAsync(g->d_buf, g->h_buf, o_sel, cudaMemcpyHostToDevice, g->stream));
+  if (n_mark) {
+    GTC_CUDA(cudaMemcpyAsync(g->d_buf + o_mark, g->h_buf + o_mark, sizeof(MarkDesc) * n_mark, cudaMemcpyHostToDevice,
+                             g->stream));
+    launch_mark_batch(reinterpret_cast<MarkDesc*>(g->d_buf + o_mark), n_mark, g->stream);
+    GTC_LAUNCHED();
+  }
+  if (n_app) {
+    launch_gp_append_batch(reinterpret_cast<AppendArgs*>(g->d_buf + o_app), R, nu, app_smem, g->stream);
+    GTC_LAUNCHED();
+    launch_extend_batch(reinterpret_cast<ExtendArgs*>(g->d_buf + o_ext), R, tiles, nu, max_n0, d, g->stream);
+    GTC_LAUNCHED();
+  }
+  // 2. selections (auxiliary per-run work -- exclusions, variance totals after
+  // marks -- is enqueued on the group stream by build_selection)
+  uint32_t masks = 0;
+  for (int i = 0; i < R; ++i) {
+    ObserveReq& q = *Q[i];
+    q.selecting = q.a && q.r->space->n - q.r->visited_count > 0;
+    if (!q.selecting) continue;
+    if ((rc = build_selection(q.r, q.a, false, 0.0, 0, &sel[i]))) {
+      q.status = rc;
+      q.error = g_last_error;
+      q.selecting = false;
+      sel[i] = SelectRunArgs{};
+      continue;
+    }
+    masks |= 1u << (sel[i].p.af_mask & 7u);
+  }
+  if (masks) {
+    GTC_CUDA(cudaMemcpyAsync(g->d_buf + o_sel, g->h_buf + o_sel, sizeof(SelectRunArgs) * R, cudaMemcpyHostToDevice,
+                             g->stream));
+    for (uint32_t m = 1; m < 8; ++m) {
+      if (!(masks & (1u << m))) continue;
+      // one launch per mask: runs with another mask see out == nullptr
+      if (masks == (1u << m)) {
+        launch_select_batch(reinterpret_cast<SelectRunArgs*>(g->d_buf + o_sel), R, m, n_cand, g->stream);
+      } else {  // mixed masks: a masked copy of the argument array per mask
+        const size_t off = o_msk + sizeof(SelectRunArgs) * R * m;
+        auto* hs = reinterpret_cast<SelectRunArgs*>(g->h_buf + off);
+        for (int i = 0; i < R; ++i) {
+          hs[i] = sel[i];
+          if ((sel[i].p.af_mask & 7u) != m) hs[i].out = nullptr;
+        }
+        GTC_CUDA(cudaMemcpyAsync(g->d_buf + off, hs, sizeof(SelectRunArgs) * R, cudaMemcpyHostToDevice, g->stream));
+        launch_select_batch(reinterpret_cast<SelectRunArgs*>(g->d_buf + off), R, m, n_cand, g->stream);
+      }
+      GTC_LAUNCHED();
+    }
+  }
+  // 3. one read-back of every run's selection record and GP scalars
+  int n_gat = 0;
+  for (int i = 0; i < R; ++i) {
+    ObserveReq& q = *Q[i];
+    const uint32_t base = (uint32_t)(per_res * i);
+    if (q.selecting)
+      gat[n_gat++] = GatherDesc{reinterpret_cast<const unsigned char*>(q.r->red.sel), (uint32_t)sizeof(SelectDev), base};
+    gat[n_gat++] = GatherDesc{reinterpret_cast<const unsigned char*>(q.r->gp.dev.sc), (uint32_t)sizeof(GpScalars),
+                              base + (uint32_t)align16(sizeof(SelectDev))};
+  }
+  GTC_CUDA(cudaMemcpyAsync(g->d_buf + o_gat, g->h_buf + o_gat, sizeof(GatherDesc) * n_gat, cudaMemcpyHostToDevice,
+                           g->stream));
+  launch_gather(reinterpret_cast<GatherDesc*>(g->d_buf + o_gat), n_gat, g->d_buf + o_res, g->stream);
+  GTC_LAUNCHED();
+  GTC_CUDA(cudaMemcpyAsync(g->h_buf + o_res, g->d_buf + o_res, per_res * R, cudaMemcpyDeviceToHost, g->stream));
+  g->t_enqueued += now_s() - g->t_round0;
+  GTC_CUDA(cudaStreamSynchronize(g->stream));
+  for (int i = 0; i < R; ++i) {
+    ObserveReq& q = *Q[i];
+    const unsigned char* base = g->h_buf + o_res + per_res * i;
+    if (q.selecting) std::memcpy(&q.r->h_rb->sel, base, sizeof(SelectDev));
+    std::memcpy(&q.r->h_rb->sc, base + align16(sizeof(SelectDev)), sizeof(GpScalars));
+  }
+  return GTC_OK;
+}
+
+static int group_observe(ObserveReq& q, gtc_fit_info*) {
+  gtc_group* g = q.r->group;
+  std::unique_lock<std::mutex> lk(g->mu);
+  g->queue.push_back(&q);
+  const uint64_t my_round = g->round.load(std::memory_order_relaxed);
+  if ((int)g->queue.size() >= g->members) {
+    const double t0 = now_s();
+    g->t_round0 = t0;
+    const int rc = execute_round(g);
+    const double t1 = now_s();
+    g->t_exec += t1 - t0;
+    ++g->n_rounds;
+    g->n_requests += g->queue.size();
+    if (g->t_first < 0) g->t_first = t0;
+    g->t_last = t1;
+    if (rc)
+      for (ObserveReq* o : g->queue)
+        if (!o->status) {
+          o->status = rc;
+          o->error = g_last_error;
+        }
+    g->round.fetch_add(1, std::memory_order_release);
+    for (ObserveReq* o : g->queue)
+      if (o != &q) o->done.release();  // one wake-up per waiter, no shared lock hand-off
+    g->queue.clear();
+  } else {
+    lk.unlock();
+    // a short spin catches quick rounds; then sleep on this request's semaphore
+    for (int spin = 0; spin < 256 && g->round.load(std::memory_order_acquire) == my_round; ++spin)
+      std::this_thread::yield();
+    q.done.acquire();
+  }
+  if (q.status) return fail(q.status, q.error);
+  return GTC_OK;
+}
+
+extern "C" int gtc_group_create(int device, gtc_group** out) {
+  if (!out) return fail(GTC_ERR_INVALID, "out is null");
+  GTC_CUDA(cudaSetDevice(device));
+  auto* g = new gtc_group();
+  g->device = device;
+  cudaError_t e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete g;
+    return fail(GTC_ERR_CUDA, std::string("group stream: ") + cudaGetErrorString(e));
+  }
+  *out = g;
+  return GTC_OK;
+}
+
+extern "C" int gtc_group_destroy(gtc_group* g) {
+  if (!g) return GTC_OK;
+  if (std::getenv("GTC_GROUP_STATS"))
+    std::fprintf(stderr, "gtc_group: %llu rounds, %.1f requests/round, host enqueue %.1f, exec %.1f us/round, span %.1f us/round\n",
+                 (unsigned long long)g->n_rounds, g->n_rounds ? (double)g->n_requests / g->n_rounds : 0.0,
+                 g->n_rounds ? 1e6 * g->t_enqueued / g->n_rounds : 0.0,
+                 g->n_rounds ? 1e6 * g->t_exec / g->n_rounds : 0.0,
+                 g->n_rounds ? 1e6 * (g->t_last - g->t_first) / g->n_rounds : 0.0);
+  cudaSetDevice(g->device);
+  cudaStreamSynchronize(g->stream);
+  cudaStreamDestroy(g->stream);
+  if (g->h_buf) cudaFreeHost(g->h_buf);
+  if (g->d_buf) cudaFree(g->d_buf);
+  delete g;
+  return GTC_OK;
+}
+
+extern "C" int gtc_group_join(gtc_group* g) {
+  if (!g) return fail(GTC_ERR_INVALID, "group is null");
+  std::lock_guard<std::mutex> lk(g->mu);
+  ++g->members;
+  return GTC_OK;
+}
+
+extern "C" int gtc_group_leave(gtc_group* g) {
+  if (!g) return fail(GTC_ERR_INVALID, "group is null");
+  std::lock_guard<std::mutex> lk(g->mu);
+  --g->members;
+  if (!g->queue.empty() && (int)g->queue.size() >= g->members) {  // the rest are all waiting
+    g->t_round0 = now_s();
+    const int rc = execute_round(g);
+    if (rc)
+      for (ObserveReq* o : g->queue)
+        if (!o->status) {
+          o->status = rc;
+          o->error = g_last_error;
+        }
+    g->round.fetch_add(1, std::memory_order_release);
+    for (ObserveReq* o : g->queue) o->done.release();
+    g->queue.clear();
+  }
+  return GTC_OK;
+}
+
+extern "C" int gtc_run_set_group(gtc_run* r, gtc_group* g) {
+  if (!r) return fail(GTC_ERR_INVALID, "run is null");
+  if (g && g->device != r->space->device) return fail(GTC_ERR_INVALID, "group and run are on different devices");
+  r->group = g;
+  return GTC_OK;
+}
+
 extern "C" int gtc_observe(gtc_run* r, int64_t pos, double y_raw, int32_t valid, const gtc_select_args* a,
                            gtc_select_result* out, gtc_fit_info* info) {
   if (!r) return fail(GTC_ERR_INVALID, "run is null");
@@ -1088,65 +1485,12 @@ extern "C" int gtc_observe(gtc_run* r, int64_t pos, double y_raw, int32_t valid,
   if (valid && r->n >= r->cfg.n_max) return fail(GTC_ERR_CAPACITY, "more observations than the run's n_max");
   if (a && (a->af_mask & 7u) == 0) return fail(GTC_ERR_INVALID, "af_mask selects no acquisition function");
   GTC_CUDA(cudaSetDevice(r->space->device));
-  int rc;
-  const bool newly = host_mark(r, pos, 1);
-  const int n0 = r->n;
-  bool appended = false;
-  GTC_CUDA(cudaEventRecord(r->ev_step0, r->stream));
-  if (valid) {
-    keep_obs(r, n0);
-    push_obs(r, &r->space->host_coords[(size_t)pos * r->space->d], y_raw);
-    if (n0 == 0) {
-      if (newly) {
-        launch_mark(r->visited, pos, 1, r->stream);
-        GTC_LAUNCHED();
-        r->acc_valid = false;
-      }
-      if ((rc = refit(r, r->cfg.jitter, info))) return rc;
-    } else {
-      if ((rc = enqueue_append(r, pos, y_raw, newly ? r->visited : nullptr))) return rc;
-      r->predictions_valid = true;
-      appended = true;
-    }
-  } else if (newly) {
-    launch_mark(r->visited, pos, 1, r->stream);
-    GTC_LAUNCHED();
-    r->acc_valid = false;
-  }
-  const bool selecting = a && r->space->n - r->visited_count > 0;
-  if (selecting && (rc = enqueue_selection(r, a))) return rc;
-  GTC_CUDA(cudaEventRecord(r->ev_step1, r->stream));
-  r->step_timed = true;
-  r->step_appended = appended;
-  if (selecting)
-    GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sel, r->red.sel, sizeof(SelectDev), cudaMemcpyDeviceToHost, r->stream));
-  GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sc, r->gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, r->stream));
-  GTC_CUDA(cudaStreamSynchronize(r->stream));
-  if (appended) {
-    if (r->h_rb->sc.status != 0) {
-      // bordered pivot <= 0: refactorise with escalated jitter (gp.hpp:116-129)
-      if ((rc = refit(r, r->jitter * 2.0, info))) return rc;
-      if (selecting) {
-        if ((rc = enqueue_selection(r, a))) return rc;
-        GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sel, r->red.sel, sizeof(SelectDev), cudaMemcpyDeviceToHost, r->stream));
-        GTC_CUDA(cudaStreamSynchronize(r->stream));
-      }
-    } else {
-      r->n = n0 + 1;
-      *r->gp.h_sc = r->h_rb->sc;
-      fill_info(info, r->h_rb->sc, r->n, 0);
-    }
-  } else if (!valid) {
-    fill_info(info, r->h_rb->sc, r->n, 0);
-  }
-  if (selecting && out) {
-    copy_result(r->h_rb->sel, out);
-    if (r->h_rb->sel.n_candidates == 0) return fail(GTC_ERR_NO_CANDIDATES, "acquisition: no candidates remaining");
-  } else if (out) {
-    std::memset(out, 0, sizeof(*out));
-    for (int k = 0; k < 3; ++k) out->position[k] = -1;
-  }
-  return GTC_OK;
+  ObserveReq q{r, pos, y_raw, valid, a};
+  observe_prepare(q);
+  // the first observation refits from scratch: always on the run's own stream
+  const int rc = (r->group && !(q.valid && q.n0 == 0)) ? group_observe(q, info) : observe_device(q, info);
+  if (rc) return rc;
+  return observe_finish(q, out, info);
 }
 
 extern "C" int gtc_read_predictions(gtc_run* r, double* mean, double* variance) {

@@ -184,6 +184,74 @@ struct VarPartials {
   VarAccum* acc_clear;
 };
 
+// Arguments of the kernels that a batch of runs shares one launch of
+// (gtc_observe requests gathered across the runs of gtc_run_bo_batch).
+struct AppendArgs {
+  GpDev g;              // g.L == nullptr: no append for this run in the batch
+  KernelParams k;
+  double noise;
+  SpaceDev sp;
+  int64_t pos;
+  const double* x_explicit;
+  double y_new;
+  int n0;
+  uint32_t* visited_mark;
+  int staged;
+};
+
+struct ExtendArgs {
+  SpaceDev sp;
+  GpDev g;
+  double* V;            // V == nullptr: no pass for this run in the batch
+  int64_t tile_stride;
+  int n0, r, final_pass, check_status;
+  double lengthscale, s2;
+  double* mu;
+  double* var;
+  const uint32_t* visited;  // with acc: per-tile variance totals (final pass)
+  VarAccum* acc;
+  VarAccum* acc_clear;
+  TileStats* tstat;  // final pass: per-tile posterior summary (optional)
+};
+
+struct SelectRunArgs {
+  const double* mu;
+  const double* var;
+  const uint32_t* visited;
+  int64_t n;
+  const GpScalars* sc;
+  SelectParams p;
+  VarSource vs;
+  const TileStats* tstat;
+  ReduceBufs b;
+  SelectDev* out;       // out == nullptr: no selection for this run in the batch
+};
+
+struct GatherDesc {
+  const unsigned char* src;
+  uint32_t bytes;
+  uint32_t dst_offset;
+};
+struct MarkDesc {
+  uint32_t* visited;
+  int64_t pos;
+  VarAccum* acc;      // optional O(1) update of the variance total
+  const double* var;
+  double s2;
+};
+void launch_gather(const GatherDesc* d_descs, int count, unsigned char* dst, cudaStream_t stream);
+void launch_mark_batch(const MarkDesc* d_marks, int count, cudaStream_t stream);
+
+AppendArgs make_append_args(const GpDev& g, KernelParams k, double noise, const SpaceDev& space, int64_t pos,
+                            const double* x_explicit, double y_new, int n0, uint32_t* visited_mark,
+                            size_t* smem_bytes);
+ExtendArgs make_pass_args(const SpaceDev& space, const GpDev& g, KernelParams k, double* V, int64_t tile_stride,
+                          int n0, double* mu, double* var, const VarPartials* vp, TileStats* tstat);
+void launch_gp_append_batch(const AppendArgs* d_args, int count, int nu, size_t smem, cudaStream_t stream);
+void launch_extend_batch(const ExtendArgs* d_args, int count, int64_t tiles, int nu, int max_n0, int d,
+                         cudaStream_t stream);
+void launch_select_batch(const SelectRunArgs* d_args, int count, uint32_t mask, int64_t n, cudaStream_t stream);
+
 // Multi-row V extension over all candidates: rows [n0, n0+r) from rows [0, n0).
 // When `final`, also writes the posterior mean/variance of every candidate
 // (and, with `vp`, the variance partials).  With `check_status` it is a
@@ -197,7 +265,10 @@ void launch_var_partials(const double* var, int64_t n, double s2, const VarParti
 void launch_var_totals(const VarSource& src, VarTotals* out, cudaStream_t stream);
 
 void launch_prior(double* mu, double* var, int64_t n, double s2, TileStats* tstat, cudaStream_t stream);
-void launch_mark(uint32_t* visited, int64_t pos, int set, cudaStream_t stream);
+// Marks/unmarks one candidate; with `acc` (a total valid for the current
+// visited set) its variance moves out of / back into the total.
+void launch_mark(uint32_t* visited, int64_t pos, int set, cudaStream_t stream, VarAccum* acc = nullptr,
+                 const double* var = nullptr, double s2 = 0.0);
 
 // Sum of the variance over unvisited candidates -> totals (deterministic).
 void launch_varsum(const double* var, const uint32_t* visited, int64_t n, double* partial_sum,

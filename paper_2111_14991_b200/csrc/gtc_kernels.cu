@@ -131,10 +131,26 @@ __device__ void accum_add(VarAccum* a, double ts, long long tc, double s2) {
   if (tc) atomicAdd(&a->count, (unsigned long long)tc);
 }
 
+// One candidate's variance in (sign = +1) or out (sign = -1) of a total: the
+// visited set changed by one mark, so the total is updated in O(1) instead of
+// re-reduced over N.  Limbs are read as signed (two's complement), so a
+// subtraction that borrows within a limb is exact.
+__device__ void accum_add_one(VarAccum* a, double v, int sign, double s2) {
+  double w = ldexp(v, 120 - var_scale_exp(s2));
+#pragma unroll
+  for (int k = 3; k >= 0; --k) {
+    const double p = floor(ldexp(w, -42 * k));
+    w = __dadd_rn(w, -ldexp(p, 42 * k));
+    const unsigned long long l = (unsigned long long)p;
+    if (l) atomicAdd(&a->limb[k], sign > 0 ? l : (unsigned long long)(-(long long)l));
+  }
+  atomicAdd(&a->count, sign > 0 ? 1ull : (unsigned long long)(-1ll));
+}
+
 __device__ __forceinline__ void accum_read(const VarAccum* a, double s2, double* sum, long long* cnt) {
   double t = 0.0;
 #pragma unroll
-  for (int k = 3; k >= 0; --k) t = __dadd_rn(ldexp(t, 42), (double)__ldcg(&a->limb[k]));
+  for (int k = 3; k >= 0; --k) t = __dadd_rn(ldexp(t, 42), (double)(long long)__ldcg(&a->limb[k]));
   *sum = ldexp(t, var_scale_exp(s2) - 120);
   *cnt = (long long)__ldcg(&a->count);
 }
@@ -450,9 +466,17 @@ __global__ void __launch_bounds__(kCtaThreads)
 }
 
 template <int NU>
-__global__ void __launch_bounds__(kCtaThreads)
-    k_gp_append(GpDev g, KernelParams k, double noise, SpaceDev sp, int64_t pos,
-                const double* x_explicit, double y_new, int n0, uint32_t* visited_mark, int staged) {
+__device__ void gp_append_body(const AppendArgs& a) {
+  const GpDev& g = a.g;
+  const KernelParams k = a.k;
+  const double noise = a.noise;
+  const SpaceDev& sp = a.sp;
+  const int64_t pos = a.pos;
+  const double* x_explicit = a.x_explicit;
+  const double y_new = a.y_new;
+  const int n0 = a.n0;
+  uint32_t* visited_mark = a.visited_mark;
+  const int staged = a.staged;
   extern __shared__ double smem[];
   __shared__ double red[32];
   __shared__ double xnew[64];
@@ -491,27 +515,25 @@ __global__ void __launch_bounds__(kCtaThreads)
   if (threadIdx.x == 0) tm[6] = gtc_globaltimer();
 }
 
+template <int NU>
+__global__ void __launch_bounds__(kCtaThreads) k_gp_append(AppendArgs a) {
+  gp_append_body<NU>(a);
+}
+
+// One CTA per run of a batch (gtc_observe requests gathered across runs).
+template <int NU>
+__global__ void __launch_bounds__(kCtaThreads) k_gp_append_batch(const AppendArgs* __restrict__ args) {
+  const AppendArgs a = args[blockIdx.x];
+  if (a.g.L == nullptr) return;  // this run does not append in this batch
+  gp_append_body<NU>(a);
+}
+
 __global__ void k_gp_truncate(GpDev g, int n) {
   __shared__ double red[32];
   cta_stats_beta(g, n, red);
 }
 
 // ------------------------------------------------------------ V extension
-
-struct ExtendArgs {
-  SpaceDev sp;
-  GpDev g;
-  double* V;
-  int64_t tile_stride;
-  int n0, r, final_pass, check_status;
-  double lengthscale, s2;
-  double* mu;
-  double* var;
-  const uint32_t* visited;  // with acc: per-tile variance totals (final pass)
-  VarAccum* acc;
-  VarAccum* acc_clear;
-  TileStats* tstat;  // final pass: per-tile posterior summary (optional)
-};
 
 // Coordinates t of candidates j0, j0 + 1 (j0 even): from the compact index
 // copy when the space has one (1-byte loads, exact table values), else SoA.
@@ -539,7 +561,7 @@ __device__ __forceinline__ double2 coord2(const SpaceDev& sp, int t, int64_t j0)
 // once.  One CTA per tile of kTile candidates, one double2 column pair per
 // thread.  With final_pass the posterior mean/variance are produced too.
 template <int R, int NU>
-__global__ void __launch_bounds__(kExtendThreads, R == 1 ? GTC_PASS_MINB : 4) k_extend(ExtendArgs a) {
+__device__ __forceinline__ void extend_body(const ExtendArgs& a) {
   accum_clear(a.acc_clear);  // next generation's accumulator (even when the pass is skipped)
   if (a.check_status && a.g.sc->status != 0) return;  // bordered row failed: host refactors
   extern __shared__ double sm[];
@@ -749,6 +771,19 @@ __global__ void __launch_bounds__(kExtendThreads, R == 1 ? GTC_PASS_MINB : 4) k_
   }
 }
 
+template <int R, int NU>
+__global__ void __launch_bounds__(kExtendThreads, R == 1 ? GTC_PASS_MINB : 4) k_extend(ExtendArgs a) {
+  extend_body<R, NU>(a);
+}
+
+// Runs of a batch on the y axis (same space, hence the same tiles).
+template <int NU>
+__global__ void __launch_bounds__(kExtendThreads, GTC_PASS_MINB) k_extend_batch(const ExtendArgs* __restrict__ args) {
+  const ExtendArgs a = args[blockIdx.y];
+  if (a.V == nullptr) return;  // this run does not append in this batch
+  extend_body<1, NU>(a);
+}
+
 // Prior (n == 0): mean 0, variance = output variance (gp.hpp:155-158).
 __global__ void k_prior(double* mu, double* var, int64_t n, double s2, TileStats* tstat) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
@@ -761,11 +796,24 @@ __global__ void k_prior(double* mu, double* var, int64_t n, double s2, TileStats
       tstat[t] = TileStats{0.0, s2, s2, 0.0, s2, t * kTile};
 }
 
-__global__ void k_mark(uint32_t* visited, int64_t pos, int set) {
+// Marks (or unmarks) one candidate; with `acc`, moves its variance out of (or
+// back into) the run's variance total.  The caller guarantees the bit flips.
+__device__ __forceinline__ void mark_update(uint32_t* visited, int64_t pos, int set, VarAccum* acc,
+                                            const double* var, double s2) {
   if (set)
-    visited[pos >> 5] |= (1u << (pos & 31));
+    atomicOr(visited + (pos >> 5), 1u << (pos & 31));
   else
-    visited[pos >> 5] &= ~(1u << (pos & 31));
+    atomicAnd(visited + (pos >> 5), ~(1u << (pos & 31)));
+  if (acc) accum_add_one(acc, var[pos], set ? -1 : 1, s2);
+}
+
+__global__ void k_mark_batch(const MarkDesc* __restrict__ m, int count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) mark_update(m[i].visited, m[i].pos, 1, m[i].acc, m[i].var, m[i].s2);
+}
+
+__global__ void k_mark(uint32_t* visited, int64_t pos, int set, VarAccum* acc, const double* var, double s2) {
+  mark_update(visited, pos, set, acc, var, s2);
 }
 
 // ------------------------------------------------------------ reductions
@@ -1408,8 +1456,8 @@ __device__ __forceinline__ void tile_keys(const TileStats& ts, float* key, bool*
 constexpr int kTileList = 512;  // tiles examined per block per round
 
 template <uint32_t MASK>
-__global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK))
-    k_select(SelCtx c, const GpScalars* sc, SelectParams p, VarSource vs, const TileStats* tstat, int ntiles) {
+__device__ __forceinline__ void select_run_body(const SelCtx& c, const GpScalars* sc, const SelectParams& p,
+                                                const VarSource& vs, const TileStats* tstat, int ntiles) {
   __shared__ Best redb[32];
   __shared__ int s_list[kTileList];
   __shared__ int s_n;
@@ -1528,6 +1576,22 @@ __global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK))
   select_finish<MASK>(c, b, first, finite, cnt, u.best, u.lambda, u.mean_var, u.fallback, sc->status);
 }
 
+template <uint32_t MASK>
+__global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK))
+    k_select(SelCtx c, const GpScalars* sc, SelectParams p, VarSource vs, const TileStats* tstat, int ntiles) {
+  select_run_body<MASK>(c, sc, p, vs, tstat, ntiles);
+}
+
+// Runs of a batch on the y axis (one AF mask per launch).
+template <uint32_t MASK>
+__global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK))
+    k_select_batch(const SelectRunArgs* __restrict__ args) {
+  const SelectRunArgs& r = args[blockIdx.y];
+  if (r.out == nullptr) return;
+  const SelCtx c{r.mu, r.var, nullptr, r.visited, nullptr, r.p.excluded, r.p.n_excluded, r.n, r.p.af_mask, r.b, r.out};
+  select_run_body<MASK>(c, r.sc, r.p, r.vs, r.tstat, (int)((r.n + kTile - 1) / kTile));
+}
+
 // (sum, count) of a variance source: a shard's local contribution to the
 // global mean variance.
 __global__ void k_var_totals(VarSource v, VarTotals* out) {
@@ -1613,17 +1677,33 @@ void launch_gp_factor(const GpDev& g, KernelParams k, double noise, double jitte
   }
 }
 
+AppendArgs make_append_args(const GpDev& g, KernelParams k, double noise, const SpaceDev& sp, int64_t pos,
+                             const double* x_explicit, double y_new, int n0, uint32_t* visited_mark,
+                             size_t* smem_bytes) {
+  bool staged;
+  *smem_bytes = cta_smem_bytes(g.n_max, n0 + 1, &staged);
+  return AppendArgs{g, k, noise, sp, pos, x_explicit, y_new, n0, visited_mark, staged ? 1 : 0};
+}
+
 void launch_gp_append(const GpDev& g, KernelParams k, double noise, const SpaceDev& sp,
                       int64_t pos, const double* x_explicit, double y_new, int n0,
                       uint32_t* visited_mark, cudaStream_t s) {
   count_launch();
-  bool staged;
-  const size_t sm = cta_smem_bytes(g.n_max, n0 + 1, &staged);
-  const int st = staged ? 1 : 0;
+  size_t sm;
+  const AppendArgs a = make_append_args(g, k, noise, sp, pos, x_explicit, y_new, n0, visited_mark, &sm);
   switch (k.nu) {
-    case 0: opt_in_smem(k_gp_append<0>, sm); k_gp_append<0><<<1, kCtaThreads, sm, s>>>(g, k, noise, sp, pos, x_explicit, y_new, n0, visited_mark, st); break;
-    case 1: opt_in_smem(k_gp_append<1>, sm); k_gp_append<1><<<1, kCtaThreads, sm, s>>>(g, k, noise, sp, pos, x_explicit, y_new, n0, visited_mark, st); break;
-    default: opt_in_smem(k_gp_append<2>, sm); k_gp_append<2><<<1, kCtaThreads, sm, s>>>(g, k, noise, sp, pos, x_explicit, y_new, n0, visited_mark, st); break;
+    case 0: opt_in_smem(k_gp_append<0>, sm); k_gp_append<0><<<1, kCtaThreads, sm, s>>>(a); break;
+    case 1: opt_in_smem(k_gp_append<1>, sm); k_gp_append<1><<<1, kCtaThreads, sm, s>>>(a); break;
+    default: opt_in_smem(k_gp_append<2>, sm); k_gp_append<2><<<1, kCtaThreads, sm, s>>>(a); break;
+  }
+}
+
+void launch_gp_append_batch(const AppendArgs* d_args, int count, int nu, size_t smem, cudaStream_t s) {
+  count_launch();
+  switch (nu) {
+    case 0: opt_in_smem(k_gp_append_batch<0>, smem); k_gp_append_batch<0><<<count, kCtaThreads, smem, s>>>(d_args); break;
+    case 1: opt_in_smem(k_gp_append_batch<1>, smem); k_gp_append_batch<1><<<count, kCtaThreads, smem, s>>>(d_args); break;
+    default: opt_in_smem(k_gp_append_batch<2>, smem); k_gp_append_batch<2><<<count, kCtaThreads, smem, s>>>(d_args); break;
   }
 }
 
@@ -1662,14 +1742,50 @@ void launch_extend(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V
   }
 }
 
+ExtendArgs make_pass_args(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V, int64_t tile_stride,
+                          int n0, double* mu, double* var, const VarPartials* vp, TileStats* tstat) {
+  return ExtendArgs{sp, g, V, tile_stride, n0, 1, 1, 1, k.lengthscale, k.s2, mu, var, vp ? vp->visited : nullptr,
+                    vp ? vp->acc : nullptr, vp ? vp->acc_clear : nullptr, tstat};
+}
+
+void launch_extend_batch(const ExtendArgs* d_args, int count, int64_t tiles, int nu, int max_n0, int d,
+                         cudaStream_t s) {
+  count_launch();
+  const size_t sm = sizeof(double) * ((size_t)2 * (max_n0 + 1) + (size_t)d + 1 + 8);
+  const dim3 grid((unsigned)tiles, (unsigned)count);
+  switch (nu) {
+    case 0: opt_in_smem(k_extend_batch<0>, sm); k_extend_batch<0><<<grid, kExtendThreads, sm, s>>>(d_args); break;
+    case 1: opt_in_smem(k_extend_batch<1>, sm); k_extend_batch<1><<<grid, kExtendThreads, sm, s>>>(d_args); break;
+    default: opt_in_smem(k_extend_batch<2>, sm); k_extend_batch<2><<<grid, kExtendThreads, sm, s>>>(d_args); break;
+  }
+}
+
+// Copies scattered device records into one contiguous buffer (one read-back
+// for a whole batch of runs).
+__global__ void k_gather(const GatherDesc* __restrict__ d, unsigned char* __restrict__ dst) {
+  const GatherDesc g = d[blockIdx.x];
+  for (uint32_t i = threadIdx.x; i < g.bytes; i += blockDim.x) dst[g.dst_offset + i] = g.src[i];
+}
+
+void launch_gather(const GatherDesc* d_descs, int count, unsigned char* dst, cudaStream_t s) {
+  count_launch();
+  k_gather<<<count, 128, 0, s>>>(d_descs, dst);
+}
+
+void launch_mark_batch(const MarkDesc* d_marks, int count, cudaStream_t s) {
+  count_launch();
+  k_mark_batch<<<(count + 127) / 128, 128, 0, s>>>(d_marks, count);
+}
+
 void launch_prior(double* mu, double* var, int64_t n, double s2, TileStats* tstat, cudaStream_t s) {
   count_launch();
   k_prior<<<148, 256, 0, s>>>(mu, var, n, s2, tstat);
 }
 
-void launch_mark(uint32_t* visited, int64_t pos, int set, cudaStream_t s) {
+void launch_mark(uint32_t* visited, int64_t pos, int set, cudaStream_t s, VarAccum* acc, const double* var,
+                 double s2) {
   count_launch();
-  k_mark<<<1, 1, 0, s>>>(visited, pos, set);
+  k_mark<<<1, 1, 0, s>>>(visited, pos, set, acc, var, s2);
 }
 
 void launch_varsum(const double* var, const uint32_t* visited, int64_t n, double* ps, int64_t* pc,
@@ -1723,6 +1839,23 @@ void launch_select(const double* mu, const double* var, const uint32_t* visited,
     default: GTC_SELECT_CASE(7)
   }
 #undef GTC_SELECT_CASE
+}
+
+void launch_select_batch(const SelectRunArgs* d_args, int count, uint32_t mask, int64_t n, cudaStream_t s) {
+  count_launch();
+  const uint32_t m = (mask & 7u) ? (mask & 7u) : 7u;
+  const int ntiles = (int)((n + kTile - 1) / kTile);
+  const int grid = std::max(1, std::min({ntiles, sel_blocks_per_sm(m) * sm_count(), kMaxReduceGrid}));
+  const dim3 g((unsigned)grid, (unsigned)count);
+  switch (m) {
+    case 1: k_select_batch<1><<<g, kSelectThreads, 0, s>>>(d_args); break;
+    case 2: k_select_batch<2><<<g, kSelectThreads, 0, s>>>(d_args); break;
+    case 3: k_select_batch<3><<<g, kSelectThreads, 0, s>>>(d_args); break;
+    case 4: k_select_batch<4><<<g, kSelectThreads, 0, s>>>(d_args); break;
+    case 5: k_select_batch<5><<<g, kSelectThreads, 0, s>>>(d_args); break;
+    case 6: k_select_batch<6><<<g, kSelectThreads, 0, s>>>(d_args); break;
+    default: k_select_batch<7><<<g, kSelectThreads, 0, s>>>(d_args); break;
+  }
 }
 
 void launch_best_candidate(const double* mu, const double* sd, const uint8_t* excluded, int64_t n,

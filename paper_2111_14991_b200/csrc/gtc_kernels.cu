@@ -19,10 +19,12 @@
 // the posterior falls out of the same pass:
 //   mu = sum_i v_i beta_i  (beta = L^-1 y_standardized),  var = max(s2 - sum_i v_i^2, 0).
 // The pass streams V once (HBM-bound GEMV): tile-major V, 16-byte streaming
-// loads, 8 rows in flight per thread; its epilogue leaves per-tile partial
-// sums of the posterior variance.  The selection (k_select) reduces those
-// partials in every block (same fixed order -> same lambda everywhere), then
-// EI/PI/LCB + masked argmax in one pass over the candidates.
+// loads, 6 rows in flight per thread, 1-byte coordinate indices; its epilogue
+// adds the tile's variance sum to a fixed-point total (VarAccum) and records
+// a per-tile posterior summary (TileStats).  The selection (k_select) reads
+// the total (same lambda in every block), bounds tiles and candidates with
+// rigorous FP32 Mills-ratio keys and scores exactly in FP64 only what can
+// reach a threshold (see the "pruned selection" section).
 //
 // L is stored packed row-major (row i at i(i+1)/2) so that the whole factor
 // of a budget-220 run (194 KB) fits in the shared memory of the single-CTA
@@ -1367,12 +1369,6 @@ __device__ void select_pruned(const SelCtx& c, double best, double lambda, doubl
 // registers (two blocks), several AFs keep their keys in 128 (one block).
 __host__ __device__ constexpr int sel_blocks_per_sm(uint32_t mask) { return (mask & (mask - 1)) ? 1 : 2; }
 
-// Selection for a resident run.  The mean posterior variance over the
-// unvisited candidates comes from the run's fixed-point variance total (left
-// by the predictive pass or k_var_partials; VarAccum): every block reads the
-// same 40 bytes, so all blocks agree on lambda (strategies.hpp:404-418,
-// acquisition.hpp:73-83) and best_std (gp.hpp:145) without a grid barrier;
-// then the pruned masked argmax (select_pruned).
 // lambda (strategies.hpp:404-418, acquisition.hpp:73-83) and best_std
 // (gp.hpp:145) from the variance total: identical in every block.
 struct SelSetup {

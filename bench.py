@@ -14,7 +14,7 @@ contextual variance (StrategyConfig defaults: Matern 3/2, l = 1.5).
 V (1.76 GB) >> L2 (126 MB), so every step streams from HBM (no L2 flush needed).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c4|c3|c2]
+                  [--config c4|c3|c2|c5]
 Under torchrun (N > 1) every rank runs an independent replica of the workload
 (run-level sharding, no collective on the data path); value = total iter/s.
 """
@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS) + ["c2"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS) + ["c2", "c5"])
     ap.add_argument("--n", type=int, default=220)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
@@ -165,6 +165,50 @@ C2_SPACES = {
                 ("between_method", [0, 1, 2, 3]), ("use_precomputed_slopes", [0, 1]), ("use_method", [0, 1, 2])],
                [], 0.039, 26.968),
 }
+
+
+# C1's GEMM space (PAPER.md:319-333 + Kernel Tuner's restrictions) for C5
+GEMM = ([("MWG", [16, 32, 64, 128]), ("NWG", [16, 32, 64, 128]), ("KWG", [32]), ("MDIMC", [8, 16, 32]),
+         ("NDIMC", [8, 16, 32]), ("MDIMA", [8, 16, 32]), ("NDIMB", [8, 16, 32]), ("KWI", [2]),
+         ("VWM", [1, 2, 4, 8]), ("VWN", [1, 2, 4, 8]), ("STRM", [0]), ("STRN", [0]), ("SA", [0, 1]),
+         ("SB", [0, 1]), ("PRECISION", [32])],
+        ["KWG % KWI == 0", "MWG % (MDIMC * VWM) == 0", "NWG % (NDIMC * VWN) == 0", "MWG % (MDIMA * VWM) == 0",
+         "NWG % (NDIMB * VWN) == 0", "KWG % ((MDIMC * NDIMC) / MDIMA) == 0", "KWG % ((MDIMC * NDIMC) / NDIMB) == 0"],
+        0.0, 28.307)
+
+
+def run_c5(args):
+    """C5 strategy sweep: {GEMM, conv, pnpoly} x {bo-ei, bo-poi, bo-lcb, bo-multi}
+    x 100 repeats = 1,200 independent runs on one device (run-level sharding
+    gives each of N GPUs 1/N of them); runs/s."""
+    import torch
+    import paper_2111_14991_b200 as gt
+    reps = 100
+    strategies = [gt.StrategyId.bo_ei, gt.StrategyId.bo_poi, gt.StrategyId.bo_lcb, gt.StrategyId.bo_multi]
+    cases = {"gemm": GEMM, **C2_SPACES}
+    t_total, runs, evals = 0.0, 0, 0
+    with ClockSampler(0) as clocks:
+        for name, (params, rs, invalid, minimum) in cases.items():
+            es = gt.SearchSpace([gt.ParameterDef(k, v) for k, v in params], rs).enumerate()
+            values = c2_values(es.n, invalid, minimum, BASE_SEED + len(name))
+            cfgs = [gt.StrategyConfig(id=sid, seed=BASE_SEED + r, budget=220, n_init=20)
+                    for sid in strategies for r in range(reps)]
+            gt.run_bo_batch(es, es.ids, cfgs[:2], values, threads=2)  # warm-up
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out = gt.run_bo_batch(es, es.ids, cfgs, values, threads=64)
+            torch.cuda.synchronize()
+            t_total += time.perf_counter() - t0
+            runs += len(out)
+            evals += sum(int(r.evaluations) for r in out)
+    print(json.dumps({
+        "metric": "BO runs/sec (C5: {GEMM, conv, pnpoly} x {ei, poi, lcb, multi} x 100 repeats, budget 220)",
+        "value": runs / t_total, "unit": "runs/s", "n_gpus": 1, "steps": runs, "warmup": 2,
+        "ms_per_step": 1e3 * t_total / runs, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic measurements over the device-enumerated GEMM, conv and pnpoly spaces",
+        "config": {"workload": "C5 strategy sweep, 1,200 runs, n_init 20, budget 220", "threads": 64,
+                   "evaluations": evals, "timing": "wall clock of gtc_run_bo_batch per case (observe groups)"},
+        "evaluations_per_sec": evals / t_total, "clocks": clocks.summary()}))
 
 
 def c2_values(n, invalid, minimum, seed):
@@ -356,8 +400,8 @@ def run_sharded(args, cfg, rank, world, local):
 
 def main():
     args = parse()
-    if args.config == "c2":
-        run_c2(args)
+    if args.config in ("c2", "c5"):
+        (run_c2 if args.config == "c2" else run_c5)(args)
         return
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -159,6 +159,11 @@ inline gtc_group*& thread_observe_group() {
   static thread_local gtc_group* g = nullptr;
   return g;
 }
+/// Whether the calling thread is currently a member of its observe group.
+inline bool& thread_group_member() {
+  static thread_local bool m = false;
+  return m;
+}
 
 class DeviceSurrogate : public ArgmaxSource {
  public:
@@ -171,6 +176,27 @@ class DeviceSurrogate : public ArgmaxSource {
     run_.reset(r, [](gtc_run* p) { gtc_run_destroy(p); });
     if (gtc_group* g = thread_observe_group()) check(gtc_run_set_group(r, g));
   }
+
+  /// Membership of the run's observe group for the BO loop: a thread that
+  /// starts a later run leaves the group during that run's initial design
+  /// (host LHS, snap, first fit) so it does not hold up the other members'
+  /// rounds.  (A worker joins at its start, so the first runs' initial designs
+  /// all finish before the first round.)
+  struct GroupMembership {
+    gtc_group* g;
+    explicit GroupMembership(gtc_group* group) : g(group) {
+      if (g && !thread_group_member()) {
+        gtc_group_join(g);
+        thread_group_member() = true;
+      }
+    }
+    ~GroupMembership() {
+      if (g && thread_group_member()) {
+        gtc_group_leave(g);
+        thread_group_member() = false;
+      }
+    }
+  };
 
   gtc_run* handle() const { return run_.get(); }
 
@@ -303,6 +329,7 @@ inline TuningRun run_bo(const EnumeratedSpace& space, const Objective& objective
     return a;
   };
 
+  const DeviceSurrogate::GroupMembership membership(thread_observe_group());
   while (!ctx.exhausted()) {
     gp.args = select_args();
 

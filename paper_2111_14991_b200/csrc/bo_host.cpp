@@ -154,16 +154,22 @@ extern "C" int gtc_run_bo_batch(gtc_space* space, const std::uint64_t* ids, cons
   std::atomic<std::int32_t> next{0}, next_worker{0};
   auto worker = [&]() {
     const int w = next_worker.fetch_add(1);
+    // the worker is a member from its start until its first run's loop ends;
+    // later runs join for their BO loops only (run_bo's GroupMembership)
     gtc_group* group = n_groups ? groups[w % n_groups] : nullptr;
-    if (group) gtc_group_join(group);
     thread_observe_group() = group;
+    if (group) {
+      gtc_group_join(group);
+      thread_group_member() = true;
+    }
     for (std::int32_t i; (i = next.fetch_add(1)) < n_runs;) {
       statuses[i] = run(space, ids, &configs[i], obj, records ? records + (std::int64_t)i * capacity : nullptr,
                         lambdas ? lambdas + (std::int64_t)i * capacity : nullptr, capacity,
                         summaries ? &summaries[i] : nullptr);
     }
+    if (group && thread_group_member()) gtc_group_leave(group);  // (a run that failed early)
+    thread_group_member() = false;
     thread_observe_group() = nullptr;
-    if (group) gtc_group_leave(group);
   };
   std::vector<std::thread> pool;
   for (int w = 1; w < workers; ++w) pool.emplace_back(worker);

@@ -339,6 +339,11 @@ int gtc_group_join(gtc_group* group);
 int gtc_group_leave(gtc_group* group);
 int gtc_run_set_group(gtc_run* run, gtc_group* group);
 
+/* MeasurementCache::checksum (cache.hpp:55-70): FNV-1a over (index, "%.17g"
+ * value or invalid reason) of the entries in ascending index order; reasons:
+ * 0 valid, 1 compile_error, 2 runtime_error, 3 restricted.  Host only. */
+uint64_t gtc_cache_checksum(const uint64_t* ids, const double* values, const uint8_t* reasons, int64_t n);
+
 /* ---- candidate-axis sharding (very large spaces over several GPUs) --------- */
 /* Each rank holds a contiguous slice of the global candidate list in its own
  * gtc_space; the GP state is replicated (every rank applies the same

@@ -14,6 +14,7 @@
 //   ref_tool bench  <grid> <seed> <n> <threads> <steps> <af>   # CPU baseline (JSON line)
 //   ref_tool enumjson <spec.json> <outdir>        # SearchSpace(params, restrictions) + EnumeratedSpace
 //   ref_tool restrict <spec.json>                 # Restriction::parse + evaluate over the grid
+//   ref_tool cachegen <function> <grid> <seed> <invalid|-> <path>   # MeasurementCache::save (JSON)
 #include <chrono>
 #include <cinttypes>
 #include <cstdio>
@@ -376,6 +377,15 @@ int cmd_restrict(int argc, char** argv) {
   return 0;
 }
 
+int cmd_cachegen(int argc, char** argv) {
+  if (argc < 7) return 2;
+  const MeasurementCache cache = make_cache(argv[2], argv[3], std::stoull(argv[4]), argv[5]);
+  cache.save(argv[6]);
+  std::printf("{\"entries\": %zu, \"checksum\": \"%016llx\"}\n", cache.entries.size(),
+              static_cast<unsigned long long>(cache.checksum()));
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc < 2) {
     std::fprintf(stderr, "usage: ref_tool space|gemm|gp|runbo|bench ...\n");
@@ -391,6 +401,7 @@ int main(int argc, char** argv) {
     else if (cmd == "bench") rc = cmd_bench(argc, argv);
     else if (cmd == "enumjson") rc = cmd_enumjson(argc, argv);
     else if (cmd == "restrict") rc = cmd_restrict(argc, argv);
+    else if (cmd == "cachegen") rc = cmd_cachegen(argc, argv);
     if (rc == 2) std::fprintf(stderr, "bad arguments for %s\n", cmd.c_str());
     return rc;
   } catch (const std::exception& e) {

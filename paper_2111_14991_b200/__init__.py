@@ -13,6 +13,7 @@ from .gp import (AcquisitionId, CandidateScores, ConfigError, ContextualVariance
                  contextual_variance_lambda, discounted_observation_score,
                  mean_posterior_variance)
 from .runtime import FitInfo, Selection, Space, SurrogateRun  # noqa: F401
+from .cache import CacheError, MeasurementCache  # noqa: F401
 from .space import EnumeratedSpace, ParameterDef, ParamKind, SearchSpace, parse_restriction  # noqa: F401
 from .strategies import (StrategyConfig, StrategyId, TuningRun, run_bo, run_bo_batch,  # noqa: F401
                          run_strategy, strategy_from_string)

@@ -157,6 +157,7 @@ SIGNATURES = [
     ("gtc_group_join", C.c_int, [P]),
     ("gtc_group_leave", C.c_int, [P]),
     ("gtc_run_set_group", C.c_int, [P, P]),
+    ("gtc_cache_checksum", C.c_uint64, [U64P, DP, U8P, C.c_int64]),
     ("gtc_run_bo_batch", C.c_int, [P, U64P, C.POINTER(gtc_bo_config), C.c_int32, DP, C.c_int32,
                                    C.POINTER(gtc_bo_record), DP, C.c_int64, C.POINTER(gtc_bo_summary),
                                    C.POINTER(C.c_int32)]),

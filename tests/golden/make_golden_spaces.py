@@ -184,6 +184,11 @@ def main():
             p.write_text(json.dumps(sp))
             errs[name] = {"spec": sp, "result": run("enumjson", p, tmp / f"err_{name}")[-1]}
         (HERE / "enum_errors.json").write_text(json.dumps(errs, indent=1))
+        # reference measurement caches (MeasurementCache::save, cache.hpp:117-160):
+        # the spaces of traj_rr13_* and traj_rosen_adv, and a 4-D one with invalids
+        run("cachegen", "random-rough", "13x13", 17, "0.3", HERE / "cache_rr13.json")
+        run("cachegen", "rosenbrock-disc", "30x30", 1, "-", HERE / "cache_rosen.json")
+        run("cachegen", "random-rough", "6x5x4x3", 5, "0.2", HERE / "cache_rr4d.json")
     print("search-space fixtures written to", HERE)
 
 

@@ -177,38 +177,23 @@ GEMM = ([("MWG", [16, 32, 64, 128]), ("NWG", [16, 32, 64, 128]), ("KWG", [32]), 
         0.0, 28.307)
 
 
-def run_c5(args):
+def run_c5(args, rank=0, world=1, local=0):
     """C5 strategy sweep: {GEMM, conv, pnpoly} x {bo-ei, bo-poi, bo-lcb, bo-multi}
-    x 100 repeats = 1,200 independent runs on one device (run-level sharding
-    gives each of N GPUs 1/N of them); runs/s."""
-    import torch
+    x 100 repeats = 1,200 independent runs, dealt to the ranks; runs/s."""
     import paper_2111_14991_b200 as gt
-    reps = 100
     strategies = [gt.StrategyId.bo_ei, gt.StrategyId.bo_poi, gt.StrategyId.bo_lcb, gt.StrategyId.bo_multi]
-    cases = {"gemm": GEMM, **C2_SPACES}
-    t_total, runs, evals = 0.0, 0, 0
-    with ClockSampler(0) as clocks:
-        for name, (params, rs, invalid, minimum) in cases.items():
-            es = gt.SearchSpace([gt.ParameterDef(k, v) for k, v in params], rs).enumerate()
-            values = c2_values(es.n, invalid, minimum, BASE_SEED + len(name))
-            cfgs = [gt.StrategyConfig(id=sid, seed=BASE_SEED + r, budget=220, n_init=20)
-                    for sid in strategies for r in range(reps)]
-            gt.run_bo_batch(es, es.ids, cfgs[:2], values, threads=2)  # warm-up
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            out = gt.run_bo_batch(es, es.ids, cfgs, values, threads=64)
-            torch.cuda.synchronize()
-            t_total += time.perf_counter() - t0
-            runs += len(out)
-            evals += sum(int(r.evaluations) for r in out)
+    dt, runs, evals, clocks = sweep({"gemm": GEMM, **C2_SPACES}, strategies, 100, 64, rank, world, local)
+    if rank != 0:
+        return
     print(json.dumps({
         "metric": "BO runs/sec (C5: {GEMM, conv, pnpoly} x {ei, poi, lcb, multi} x 100 repeats, budget 220)",
-        "value": runs / t_total, "unit": "runs/s", "n_gpus": 1, "steps": runs, "warmup": 2,
-        "ms_per_step": 1e3 * t_total / runs, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "value": runs / dt, "unit": "runs/s", "n_gpus": world, "steps": runs, "warmup": 2,
+        "ms_per_step": 1e3 * dt / runs, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic measurements over the device-enumerated GEMM, conv and pnpoly spaces",
         "config": {"workload": "C5 strategy sweep, 1,200 runs, n_init 20, budget 220", "threads": 64,
-                   "evaluations": evals, "timing": "wall clock of gtc_run_bo_batch per case (observe groups)"},
-        "evaluations_per_sec": evals / t_total, "clocks": clocks.summary()}))
+                   "parallelism": f"run-sharded over {world} GPU(s)", "evaluations": evals,
+                   "timing": "wall clock of gtc_run_bo_batch per case (observe groups), max over ranks"},
+        "evaluations_per_sec": evals / dt, "clocks": clocks, "cpu_baseline": c2_reference()}))
 
 
 def c2_values(n, invalid, minimum, seed):
@@ -222,40 +207,63 @@ def c2_values(n, invalid, minimum, seed):
     return v
 
 
-def run_c2(args):
-    """C2 throughput: 35 repeats of each case as independent runs driven by a
-    host thread pool on one device (run_experiment's model); runs/s."""
+def sweep(cases, strategies, reps, threads, rank, world, local):
+    """Independent runs of every (case, strategy, repeat), dealt round-robin
+    to the ranks (run-level sharding, no data-path collective: seeds derive
+    from the keys, experiment.hpp:125-128); each rank drives its runs with
+    gtc_run_bo_batch on its own device.  Returns (seconds = max over ranks,
+    total runs, total evaluations, clock summary)."""
     import torch
     import paper_2111_14991_b200 as gt
-    reps = 35
-    t_total, runs, evals = 0.0, 0, 0
-    spaces = {}
-    for name, (params, rs, invalid, minimum) in C2_SPACES.items():
-        es = gt.SearchSpace([gt.ParameterDef(k, v) for k, v in params], rs).enumerate()
-        spaces[name] = (es, c2_values(es.n, invalid, minimum, BASE_SEED + len(name)))
-    threads = reps  # one host thread per run of a case: the threads mostly wait on device syncs
-    with ClockSampler(0) as clocks:
-        for name, (es, values) in spaces.items():
-            cfgs = [gt.StrategyConfig(id=gt.StrategyId.bo_multi, seed=BASE_SEED + r, budget=220, n_init=20)
-                    for r in range(reps)]
-            gt.run_bo_batch(es, es.ids, cfgs[:2], values, threads=2)  # warm-up
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            out = gt.run_bo_batch(es, es.ids, cfgs, values, threads=threads)
-            torch.cuda.synchronize()
-            t_total += time.perf_counter() - t0
+    # one worker thread per host core: more threads than cores make the
+    # observe-group rounds wait on the OS scheduler
+    host_threads = int(os.environ.get("GTC_SWEEP_THREADS", os.cpu_count() or 1))
+    prepared = []
+    for name, (params, rs, invalid, minimum) in cases.items():
+        es = gt.SearchSpace([gt.ParameterDef(k, v) for k, v in params], rs).enumerate(device=local)
+        values = c2_values(es.n, invalid, minimum, BASE_SEED + len(name))
+        keys = [(sid, r) for sid in strategies for r in range(reps)]
+        mine = [gt.StrategyConfig(id=sid, seed=BASE_SEED + r, budget=220, n_init=20)
+                for i, (sid, r) in enumerate(keys) if i % world == rank]
+        gt.run_bo_batch(es, es.ids, mine[:2], values, threads=2)  # warm-up
+        prepared.append((es, values, mine))
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    runs = evals = 0
+    with ClockSampler(local) as clocks:
+        t0 = time.perf_counter()
+        for es, values, mine in prepared:
+            out = gt.run_bo_batch(es, es.ids, mine, values, threads=min(threads, len(mine), host_threads))
             runs += len(out)
             evals += sum(int(r.evaluations) for r in out)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt, runs, evals], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t[:1], op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(t[1:], op=torch.distributed.ReduceOp.SUM)
+        dt, runs, evals = float(t[0]), int(t[1]), int(t[2])
+    return dt, runs, evals, clocks.summary()
+
+
+def run_c2(args, rank=0, world=1, local=0):
+    """C2 throughput: 35 repeats of each case as independent runs driven by a
+    host thread pool (run_experiment's model, observe groups); runs/s."""
+    import paper_2111_14991_b200 as gt
+    dt, runs, evals, clocks = sweep(C2_SPACES, [gt.StrategyId.bo_multi], 35, 35, rank, world, local)
+    if rank != 0:
+        return
+    t_total, threads = dt, 35
     print(json.dumps({
         "metric": "BO runs/sec (C2: conv + pnpoly simulation mode, bo-multi, budget 220)", "value": runs / t_total,
-        "unit": "runs/s", "n_gpus": 1, "steps": runs, "warmup": 2, "ms_per_step": 1e3 * t_total / runs,
+        "unit": "runs/s", "n_gpus": world, "steps": runs, "warmup": 2, "ms_per_step": 1e3 * t_total / runs,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic measurements over the device-enumerated conv (N=%d) and pnpoly (N=%d) spaces" % (
-            spaces["conv"][0].n, spaces["pnpoly"][0].n),
+        "data": "synthetic measurements over the device-enumerated conv (N=9400) and pnpoly (N=8184) spaces",
         "config": {"workload": "C2 conv + pnpoly, 35 repeats each, bo-multi, n_init 20, budget 220",
                    "threads": threads, "evaluations": evals,
                    "timing": "wall clock of gtc_run_bo_batch (host thread pool, one stream per run)"},
-        "evaluations_per_sec": evals / t_total, "clocks": clocks.summary(),
+        "evaluations_per_sec": evals / t_total, "clocks": clocks,
         "cpu_baseline": c2_reference()}))
 
 
@@ -401,7 +409,25 @@ def run_sharded(args, cfg, rank, world, local):
 def main():
     args = parse()
     if args.config in ("c2", "c5"):
-        (run_c2 if args.config == "c2" else run_c5)(args)
+        if args.impl == "reference":
+            rank, _, _ = dist_env()
+            if rank == 0:
+                ref = c2_reference()
+                print(json.dumps({"impl": "reference", "metric": f"BO runs/sec ({args.config.upper()})",
+                                  "value": ref["value"], "unit": "runs/s", "higher_is_better": True,
+                                  "n_gpus": args.gpus, "cpu_baseline": ref,
+                                  "e2e": {"value": ref["value"], "unit": "runs/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0}}))
+            return
+        rank, world, local = dist_env()
+        import torch
+        torch.cuda.set_device(local)
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        (run_c2 if args.config == "c2" else run_c5)(args, rank, world, local)
+        if world > 1:
+            torch.distributed.destroy_process_group()
         return
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -168,6 +168,11 @@ int gtc_restriction_validate(const gtc_param_def* params, int32_t n_params, cons
 
 /* ---- BO run: resident GP + predictions over the whole space ----------------- */
 int gtc_run_create(gtc_space* space, const gtc_model_config* config, gtc_run** out);
+/* Back to the freshly created state (no observations, nothing visited, no
+ * group) under a new config with the same n_max, keeping the device
+ * allocations: a worker that runs many BO runs reuses one run handle instead
+ * of a create/destroy pair (cudaFree synchronises the whole device). */
+int gtc_run_reset(gtc_run* run, const gtc_model_config* config);
 int gtc_run_destroy(gtc_run* run);
 
 /* GpModel::fit over candidates at `positions` (the fit_current lambda,

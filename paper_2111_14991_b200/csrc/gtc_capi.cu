@@ -418,16 +418,28 @@ extern "C" int gtc_restriction_validate(const gtc_param_def* params, int32_t n_p
 }
 
 // RAII for the enumeration's temporary device buffers
+// Temporary device buffers of one call, stream-ordered (cudaMallocAsync /
+// cudaFreeAsync from the device's pool): unlike cudaFree, releasing them does
+// not synchronise the whole device, so concurrent runs' pipelines keep going.
 struct DevBufs {
+  cudaStream_t stream;
   std::vector<void*> ptrs;
+  explicit DevBufs(cudaStream_t s) : stream(s) {}
   ~DevBufs() {
-    for (void* p : ptrs) cudaFree(p);
+    for (void* p : ptrs) cudaFreeAsync(p, stream);
   }
   template <class T>
   int get(T** p, size_t count) {
-    int rc = dalloc(p, count);
-    if (!rc) ptrs.push_back(*p);
-    return rc;
+    if (count == 0) count = 1;
+    const cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * count, stream);
+    if (e != cudaSuccess) {
+      *p = nullptr;
+      cudaGetLastError();
+      return fail(e == cudaErrorMemoryAllocation ? GTC_ERR_OOM : GTC_ERR_CUDA,
+                  std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+    }
+    ptrs.push_back(*p);
+    return GTC_OK;
   }
 };
 
@@ -489,7 +501,7 @@ extern "C" int gtc_space_enumerate(int device, const gtc_param_def* params, int3
     cudaStream_t s;
     ~StreamGuard() { cudaStreamDestroy(s); }
   } sg{st};
-  DevBufs tmp;
+  DevBufs tmp(st);
   EnumInstr* d_code;
   double *d_values, *d_norm;
   int32_t *d_off, *d_radix;
@@ -578,7 +590,7 @@ extern "C" int gtc_space_nearest(const gtc_space* s, const double* points, int32
     cudaStream_t s;
     ~StreamGuard() { cudaStreamDestroy(s); }
   } sg{st};
-  DevBufs tmp;
+  DevBufs tmp(st);
   double* d_pts;
   unsigned char* d_part;
   int64_t* d_out;
@@ -663,6 +675,36 @@ extern "C" int gtc_run_create(gtc_space* space, const gtc_model_config* cfg, gtc
   r->visited_host.assign(words, 0u);
   r->tiles = (int)tiles;
   *out = r;
+  return GTC_OK;
+}
+
+extern "C" int gtc_run_reset(gtc_run* r, const gtc_model_config* cfg) {
+  if (!r || !cfg) return fail(GTC_ERR_INVALID, "run/config is null");
+  if (cfg->n_max != r->cfg.n_max) return fail(GTC_ERR_CONFIG, "gtc_run_reset cannot change n_max");
+  int rc = check_kernel(&cfg->kernel);
+  if (rc) return rc;
+  if (!(cfg->noise >= 0.0)) return fail(GTC_ERR_INVALID, "GP fit: noise must be non-negative");
+  if (!(cfg->jitter > 0.0)) return fail(GTC_ERR_INVALID, "GP fit: jitter must be positive");
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  const int64_t words = (r->space->n + 31) / 32;
+  GTC_CUDA(cudaMemsetAsync(r->visited, 0, words * sizeof(uint32_t), r->stream));
+  GTC_CUDA(cudaMemsetAsync(r->acc, 0, 2 * sizeof(VarAccum), r->stream));
+  GTC_CUDA(cudaStreamSynchronize(r->stream));
+  r->cfg = *cfg;
+  r->jitter = cfg->jitter;
+  r->n = 0;
+  r->predictions_valid = false;
+  r->acc_gen = 0;
+  r->acc_valid = false;
+  r->visited_host.assign(words, 0u);
+  r->visited_count = 0;
+  r->first_hint = 0;
+  r->ex_host.clear();
+  r->y_host.clear();
+  r->x_host.clear();
+  r->shard_offset = 0;
+  r->group = nullptr;
+  r->pass_timed = r->step_timed = r->step_appended = false;
   return GTC_OK;
 }
 
@@ -1404,7 +1446,7 @@ static int group_observe(ObserveReq& q, gtc_fit_info*) {
   } else {
     lk.unlock();
     // a short spin catches quick rounds; then sleep on this request's semaphore
-    for (int spin = 0; spin < 256 && g->round.load(std::memory_order_acquire) == my_round; ++spin)
+    for (int spin = 0; spin < 32 && g->round.load(std::memory_order_acquire) == my_round; ++spin)
       std::this_thread::yield();
     q.done.acquire();
   }

@@ -8,7 +8,9 @@
 #pragma once
 
 #include <array>
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <functional>
 #include <limits>
 #include <memory>
@@ -276,6 +278,21 @@ class DeviceSurrogate : public ArgmaxSource {
     check(gtc_select(run_.get(), &a, &last));
     return {last.position[0], last.position[1], last.position[2]};
   }
+  /// Simulation mode: the objective's replay table on the device (gtc_run_set_values).
+  void set_values(const double* values) { check(gtc_run_set_values(run_.get(), values, static_cast<std::int64_t>(space_.size()))); }
+
+  /// Up to k resident iterations of a single-AF loop (gtc_run_steps).
+  std::vector<gtc_step_record> steps(const gtc_select_args& a, std::size_t k) {
+    prefetched_mask_ = 0;
+    std::vector<gtc_step_record> recs(std::max<std::size_t>(k, 1));
+    std::int32_t done = 0;
+    gtc_fit_info info{};
+    check(gtc_run_steps(run_.get(), &a, static_cast<std::int32_t>(k), 0, recs.data(), &done, &info));
+    recs.resize(static_cast<std::size_t>(done));
+    if (done > 0) info_ = info;
+    return recs;
+  }
+
   std::uint64_t id_at(std::int64_t p) const override { return space_.id(static_cast<std::size_t>(p)); }
   std::int64_t position_of_id(std::uint64_t id) const override {
     const std::size_t p = space_.position_of(id);
@@ -294,8 +311,19 @@ class DeviceSurrogate : public ArgmaxSource {
 
 inline bool is_bayesian(StrategyId) { return true; }
 
+/// Whether run_bo may run single-AF simulation-mode loops on the device
+/// (GTC_RESIDENT_LOOP=0 forces the per-iteration gtc_observe loop).
+inline bool resident_loop_enabled() {
+  const char* e = std::getenv("GTC_RESIDENT_LOOP");
+  return !(e && e[0] == '0');
+}
+
 /// run_bo (strategies.hpp:261-457).
-inline TuningRun run_bo(const EnumeratedSpace& space, const Objective& objective, const StrategyConfig& config) {
+/// `table`: the objective's replay table (values[pos], NaN = invalid) when the
+/// objective is one (simulation mode, cache.hpp:246-257); single-AF strategies
+/// then run their loop resident on the device (gtc_run_steps), same results.
+inline TuningRun run_bo(const EnumeratedSpace& space, const Objective& objective, const StrategyConfig& config,
+                        const double* table = nullptr) {
   if (space.size() <= config.n_init)
     throw SamplingError("space has " + std::to_string(space.size()) +
                         " valid configurations; need more than n_init = " + std::to_string(config.n_init));
@@ -354,8 +382,33 @@ inline TuningRun run_bo(const EnumeratedSpace& space, const Objective& objective
     return a;
   };
 
+  const bool resident = single && table && !config.inspect && resident_loop_enabled();
+  if (resident) gp.set_values(table);
   const DeviceSurrogate::GroupMembership membership(thread_observe_group());
   while (!ctx.exhausted()) {
+    if (resident && !train_pos.empty()) {
+      // as many iterations as the budget surely allows, without host round
+      // trips; the host replays the evaluations (same table) for its records
+      const std::size_t k = std::min(config.budget - ctx.run().budget_consumed, ctx.unvisited_count());
+      const std::vector<gtc_step_record> recs = gp.steps(select_args(), k);
+      if (recs.empty()) break;
+      for (const gtc_step_record& r : recs) {
+        if (r.cv_fallback && !warned) {
+          ctx.run().warnings.push_back(
+              "contextual variance unavailable (non-positive observations or zero initial variance); "
+              "falling back to constant exploration factor " + std::to_string(config.exploration.constant));
+          warned = true;
+        }
+        const Measurement m = ctx.evaluate(static_cast<std::size_t>(r.position));
+        if (m.is_valid() != (r.valid != 0)) throw Error("internal: resident loop and objective disagree");
+        if (m.is_valid()) {
+          train_pos.push_back(static_cast<std::size_t>(r.position));
+          train_val.push_back(*m.value);
+        }
+        ctx.run().lambdas.push_back(r.lambda);
+      }
+      continue;
+    }
     gp.args = select_args();
 
     std::size_t pick;

@@ -209,6 +209,41 @@ int gtc_select(gtc_run* run, const gtc_select_args* args, gtc_select_result* out
 int gtc_observe(gtc_run* run, int64_t position, double y_raw, int32_t valid,
                 const gtc_select_args* args, gtc_select_result* out, gtc_fit_info* info);
 
+/* ---- resident BO loop (simulation mode) ---------------------------------- */
+/* The objective of a simulation-mode run is a replay table (values[pos], NaN =
+ * runtime-invalid; cache.hpp:246-257).  gtc_run_set_values copies it to the
+ * device (n == gtc_space_size); gtc_run_steps then runs up to k iterations of
+ * a single-acquisition BO loop (bo-ei / bo-poi / bo-lcb: strategies.hpp:401-449
+ * with best_candidate, portfolio.hpp:32-61) without host round trips: each
+ * step selects (args: exactly one AF bit, no exclusions; f_best_raw = the
+ * current best valid observation), evaluates the table, marks the pick
+ * visited and, when valid, appends it (bordered row + predictive pass).
+ * records[i] = the i-th step's pick, value, lambda and contextual-variance
+ * fallback flag; *done = steps run (< k only when every candidate has been
+ * visited).  Same results as the gtc_observe loop.  A failed bordered pivot
+ * is refactorised with escalated jitter as in gtc_append.
+ * GTC_STEPS_HOLD_N (benchmarking the steady state at a fixed n): every valid
+ * step replaces the observation appended by the previous one at row n0 (the
+ * model's size at the call) and un-marks its position, so every step runs at
+ * exactly n0 + 1 observations; f_best_raw is then min(args->f_best_raw, y). */
+typedef struct {
+  int64_t position;
+  double value;        /* NaN when invalid */
+  double lambda;       /* exploration factor of the selection that picked it */
+  int32_t valid;
+  int32_t cv_fallback; /* 1: contextual variance undefined, constant used */
+} gtc_step_record;
+#define GTC_STEPS_HOLD_N 1
+#define GTC_STEPS_TIMING 2 /* record CUDA events around each step's phases */
+int gtc_run_set_values(gtc_run* run, const double* values, int64_t n);
+int gtc_run_steps(gtc_run* run, const gtc_select_args* args, int32_t k, int32_t flags,
+                  gtc_step_record* records, int32_t* done, gtc_fit_info* info);
+/* CUDA-event milliseconds of the last gtc_run_steps chunk's device work. */
+double gtc_last_steps_ms(const gtc_run* run);
+/* With GTC_STEPS_TIMING: mean CUDA-event ms per step of the last chunk's
+ * phases: out3[0] selection + advance, [1] bordered append, [2] predictive pass. */
+int gtc_last_steps_phase_ms(const gtc_run* run, double* out3);
+
 /* Mean posterior variance over the unvisited candidates (the initial
  * contextual-variance normaliser, strategies.hpp:392-397; 0 when empty). */
 int gtc_mean_variance(gtc_run* run, double* mean_variance, int64_t* count);

@@ -51,6 +51,15 @@ class gtc_select_result(C.Structure):
                 ("n_candidates", C.c_int64), ("cv_fallback", C.c_int32)]
 
 
+class gtc_step_record(C.Structure):
+    _fields_ = [("position", C.c_int64), ("value", C.c_double), ("lambda_", C.c_double),
+                ("valid", C.c_int32), ("cv_fallback", C.c_int32)]
+
+
+GTC_STEPS_HOLD_N = 1
+GTC_STEPS_TIMING = 2
+
+
 class gtc_shard_selection(C.Structure):
     _fields_ = [("best_position", C.c_int64 * 3), ("best_score", C.c_double * 3),
                 ("first_eligible", C.c_int64), ("first_nan_mask", C.c_uint32),
@@ -124,6 +133,11 @@ SIGNATURES = [
     ("gtc_select", C.c_int, [P, C.POINTER(gtc_select_args), C.POINTER(gtc_select_result)]),
     ("gtc_observe", C.c_int, [P, C.c_int64, C.c_double, C.c_int32, C.POINTER(gtc_select_args),
                               C.POINTER(gtc_select_result), C.POINTER(gtc_fit_info)]),
+    ("gtc_run_set_values", C.c_int, [P, DP, C.c_int64]),
+    ("gtc_run_steps", C.c_int, [P, C.POINTER(gtc_select_args), C.c_int32, C.c_int32,
+                                C.POINTER(gtc_step_record), C.POINTER(C.c_int32), C.POINTER(gtc_fit_info)]),
+    ("gtc_last_steps_ms", C.c_double, [P]),
+    ("gtc_last_steps_phase_ms", C.c_int, [P, DP]),
     ("gtc_mean_variance", C.c_int, [P, DP, I64P]),
     ("gtc_read_predictions", C.c_int, [P, DP, DP]),
     ("gtc_last_pass_ms", C.c_double, [P]),

@@ -57,7 +57,8 @@ struct Aborted : std::exception {
 };
 
 int run(gtc_space* space, const std::uint64_t* ids, const gtc_bo_config* cfg, const Objective& objective,
-        gtc_bo_record* records, double* lambdas, std::int64_t capacity, gtc_bo_summary* summary) {
+        gtc_bo_record* records, double* lambdas, std::int64_t capacity, gtc_bo_summary* summary,
+        const double* table = nullptr) {
   if (!space || !ids || !cfg) {
     gtc_internal_set_error("null argument");
     return GTC_ERR_INVALID;
@@ -65,7 +66,7 @@ int run(gtc_space* space, const std::uint64_t* ids, const gtc_bo_config* cfg, co
   try {
     const EnumeratedSpace es(space, ids);
     const StrategyConfig sc = to_config(*cfg);
-    const TuningRun r = run_bo(es, objective, sc);
+    const TuningRun r = run_bo(es, objective, sc, table);
     const std::int64_t nrec = static_cast<std::int64_t>(r.records.size());
     const std::int64_t nlam = static_cast<std::int64_t>(r.lambdas.size());
     if (records) {
@@ -194,5 +195,5 @@ extern "C" int gtc_run_bo_table(gtc_space* space, const std::uint64_t* ids, cons
     const double v = values[c.position];
     return std::isnan(v) ? Measurement::invalid(InvalidReason::runtime_error) : Measurement::valid(v);
   };
-  return run(space, ids, cfg, obj, records, lambdas, capacity, summary);
+  return run(space, ids, cfg, obj, records, lambdas, capacity, summary, values);
 }

@@ -278,6 +278,15 @@ struct gtc_run {
   VarSource vsrc() const { return VarSource{acc + acc_gen, cfg.kernel.output_variance, 0.0, 0, 0}; }
   // the total to update in O(1) on a mark, when it matches the visited set
   VarAccum* live_acc() const { return acc_valid && predictions_valid ? acc + acc_gen : nullptr; }
+  // resident loop (gtc_run_steps): value table, loop state, step records
+  double* d_values = nullptr;
+  bool has_values = false;
+  LoopDev* d_loop = nullptr;
+  LoopDev* h_loop = nullptr;  // pinned
+  StepRec* d_rec = nullptr;
+  int rec_cap = 0;
+  std::vector<cudaEvent_t> step_events;  // GTC_STEPS_TIMING: 3 per step + 1
+  int timed_steps = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;          // last predictive pass
   cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;  // last gtc_observe device span
   bool pass_timed = false, step_timed = false, step_appended = false;
@@ -626,6 +635,11 @@ extern "C" int gtc_run_destroy(gtc_run* r) {
   cudaFree(r->acc);
   cudaFree(r->tstat);
   cudaFree(r->d_xnew);
+  cudaFree(r->d_values);
+  cudaFree(r->d_loop);
+  cudaFree(r->d_rec);
+  if (r->h_loop) cudaFreeHost(r->h_loop);
+  for (cudaEvent_t ev : r->step_events) cudaEventDestroy(ev);
   if (r->h_xnew) cudaFreeHost(r->h_xnew);
   if (r->h_rb) cudaFreeHost(r->h_rb);
   for (cudaEvent_t ev : {r->ev0, r->ev1, r->ev_step0, r->ev_step1})
@@ -704,6 +718,7 @@ extern "C" int gtc_run_reset(gtc_run* r, const gtc_model_config* cfg) {
   r->x_host.clear();
   r->shard_offset = 0;
   r->group = nullptr;
+  r->has_values = false;
   r->pass_timed = r->step_timed = r->step_appended = false;
   return GTC_OK;
 }
@@ -995,6 +1010,200 @@ static int enqueue_selection(gtc_run* r, const gtc_select_args* a, bool global_t
   launch_select(sa.mu, sa.var, sa.visited, sa.n, sa.sc, sa.p, sa.vs, sa.tstat, sa.b, sa.out, r->stream);
   GTC_LAUNCHED();
   return GTC_OK;
+}
+
+// =============================================================== resident loop
+
+extern "C" int gtc_run_set_values(gtc_run* r, const double* values, int64_t n) {
+  if (!r || !values) return fail(GTC_ERR_INVALID, "null argument");
+  if (n != r->space->n) return fail(GTC_ERR_INVALID, "value table size != space size");
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  int rc;
+  if (!r->d_values && (rc = dalloc(&r->d_values, (size_t)r->space->n))) return rc;
+  GTC_CUDA(cudaMemcpyAsync(r->d_values, values, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, r->stream));
+  GTC_CUDA(cudaStreamSynchronize(r->stream));
+  r->has_values = true;
+  return GTC_OK;
+}
+
+// Host bookkeeping of the steps a resident chunk ran (the same updates
+// gtc_observe makes per call).
+static void replay_steps(gtc_run* r, const StepRec* rec, int m, bool hold, int hold_n0, int64_t* hold_prev) {
+  for (int i = 0; i < m; ++i) {
+    const int64_t pos = rec[i].position;
+    if (rec[i].valid) {
+      if (hold) {
+        if (*hold_prev >= 0) host_mark(r, *hold_prev, 0);
+        *hold_prev = pos;
+        keep_obs(r, hold_n0);
+      }
+      push_obs(r, &r->space->host_coords[(size_t)pos * r->space->d], rec[i].value);
+    }
+    host_mark(r, pos, 1);
+  }
+}
+
+// k BO iterations of a single-AF strategy in simulation mode without host
+// round trips: per step select -> k_loop_advance (table lookup, visited mark,
+// f_best) -> bordered append -> predictive pass, all launch arguments
+// constant.  A failed bordered pivot halts the chunk on the device; the host
+// refactorises with escalated jitter (gp.hpp:116-129, as gtc_append) and
+// continues with a new chunk.
+extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, int32_t flags,
+                             gtc_step_record* records, int32_t* done, gtc_fit_info* info) {
+  if (!r || !a || !done || (k > 0 && !records)) return fail(GTC_ERR_INVALID, "null argument");
+  *done = 0;
+  const uint32_t mask = a->af_mask & 7u;
+  if (mask == 0 || (mask & (mask - 1)) != 0) return fail(GTC_ERR_INVALID, "gtc_run_steps needs exactly one acquisition function");
+  if (a->n_excluded > 0) return fail(GTC_ERR_INVALID, "gtc_run_steps takes no exclusions");
+  if (!r->has_values) return fail(GTC_ERR_INVALID, "no value table (gtc_run_set_values)");
+  if (r->n < 1) return fail(GTC_ERR_INVALID, "gtc_run_steps needs a fitted model (n >= 1)");
+  const bool hold = (flags & GTC_STEPS_HOLD_N) != 0;
+  if (hold && r->n >= r->cfg.n_max) return fail(GTC_ERR_CAPACITY, "more observations than the run's n_max");
+  if (k <= 0) return GTC_OK;
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  int rc;
+  if (k > r->rec_cap) {
+    cudaFree(r->d_rec);
+    r->d_rec = nullptr;
+    r->rec_cap = 0;
+    if ((rc = dalloc(&r->d_rec, (size_t)k))) return rc;
+    r->rec_cap = k;
+  }
+  if (!r->d_loop) {
+    if ((rc = dalloc(&r->d_loop, 1))) return rc;
+    GTC_CUDA(cudaMallocHost(&r->h_loop, sizeof(LoopDev)));
+  }
+  int af = 0;
+  while (!((mask >> af) & 1u)) ++af;
+  const int hold_n0 = r->n;  // hold: every valid step appends at this row
+  int64_t hold_prev = -1;
+  double f_best = a->f_best_raw;
+  bool refitted = false;
+  while (*done < k) {
+    const int m = k - *done;
+    if (r->space->n - r->visited_count <= 0) break;
+    if ((rc = ensure_predictions(r)) || (rc = ensure_var_totals(r))) return rc;
+    const int n0_max = hold ? hold_n0 : std::min(r->n + m - 1, r->cfg.n_max - 1);
+    LoopDev& L = *r->h_loop;
+    L = LoopDev{};
+    L.pos = -1;
+    L.n = r->n;
+    L.gen = r->acc_gen;
+    L.halt = kLoopRunning;
+    L.af = af;
+    L.n_max = r->cfg.n_max;
+    L.hold = hold ? 1 : 0;
+    L.hold_n0 = hold_n0;
+    L.hold_prev = hold_prev;
+    L.f_best = f_best;
+    L.f_base = a->f_best_raw;
+    r->first_hint = first_unvisited_from(r, r->first_hint);
+    L.first = r->first_hint < r->space->n ? r->first_hint : -1;
+    L.count = r->space->n - r->visited_count;
+    L.n_space = r->space->n;
+    L.acc = r->acc;
+    L.table = r->d_values;
+    L.visited = r->visited;
+    L.var = r->var;
+    L.s2 = r->cfg.kernel.output_variance;
+    L.sc = r->gp.dev.sc;
+    L.sel = r->red.sel;
+    L.rec = r->d_rec;
+    GTC_CUDA(cudaMemcpyAsync(r->d_loop, r->h_loop, sizeof(LoopDev), cudaMemcpyHostToDevice, r->stream));
+    SelectParams p{mask, a->lambda_mode, a->lambda_constant, a->cv_initial_sample_mean, a->cv_initial_mean_variance,
+                   f_best, nullptr, 0, -1, 0, r->d_loop};
+    const VarSource vs = r->vsrc();
+    // loop-mode launch arguments: per-step values come from the loop state
+    AppendArgs aa{};
+    size_t append_smem = 0;
+    aa = make_append_args(r->gp.dev, kparams(r->cfg.kernel), r->cfg.noise, r->space->dev(), 0, nullptr, 0.0,
+                          n0_max, nullptr, &append_smem);
+    aa.loop = r->d_loop;
+    ExtendArgs ea = make_pass_args(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, n0_max,
+                                   r->mu, r->var, nullptr, r->tstat);
+    ea.visited = r->visited;
+    ea.acc = r->acc;  // (generation chosen on the device)
+    ea.acc_clear = r->acc + 1;
+    ea.loop = r->d_loop;
+    const bool timing = (flags & GTC_STEPS_TIMING) != 0;
+    if (timing) {
+      while ((int)r->step_events.size() < 3 * m + 1) {
+        cudaEvent_t ev;
+        GTC_CUDA(cudaEventCreate(&ev));
+        r->step_events.push_back(ev);
+      }
+      r->timed_steps = 0;
+    }
+    cudaEvent_t* te = r->step_events.data();
+    GTC_CUDA(cudaEventRecord(r->ev_step0, r->stream));
+    for (int i = 0; i < m; ++i) {
+      if (timing) GTC_CUDA(cudaEventRecord(te[3 * i], r->stream));
+      launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, vs, r->tstat, r->red.b, r->red.sel,
+                    r->stream);
+      launch_loop_advance(r->d_loop, r->stream);
+      if (timing) GTC_CUDA(cudaEventRecord(te[3 * i + 1], r->stream));
+      launch_gp_append_loop(aa, r->cfg.kernel.nu, append_smem, r->stream);
+      if (timing) GTC_CUDA(cudaEventRecord(te[3 * i + 2], r->stream));
+      launch_extend_loop(ea, r->space->n_pad / kTile, r->cfg.kernel.nu, r->stream);
+      GTC_LAUNCHED();
+    }
+    if (timing) {
+      GTC_CUDA(cudaEventRecord(te[3 * m], r->stream));
+      r->timed_steps = m;
+    }
+    GTC_CUDA(cudaEventRecord(r->ev_step1, r->stream));
+    r->step_timed = true;
+    r->step_appended = false;
+    r->pass_timed = false;
+    GTC_CUDA(cudaMemcpyAsync(r->h_loop, r->d_loop, sizeof(LoopDev), cudaMemcpyDeviceToHost, r->stream));
+    GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sc, r->gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, r->stream));
+    static_assert(sizeof(StepRec) == sizeof(gtc_step_record), "record layout");
+    GTC_CUDA(cudaMemcpyAsync(records + *done, r->d_rec, sizeof(StepRec) * (size_t)m, cudaMemcpyDeviceToHost, r->stream));
+    GTC_CUDA(cudaStreamSynchronize(r->stream));
+    const int steps = L.step;
+    replay_steps(r, reinterpret_cast<const StepRec*>(records + *done), steps, hold, hold_n0, &hold_prev);
+    *done += steps;
+    r->acc_gen = L.gen;
+    f_best = L.f_best;
+    if (L.halt == kLoopPivot) {
+      // the last step's bordered row failed (its observation is in the host
+      // training set): refactorise from 2 x jitter like gtc_append
+      if ((rc = refit(r, r->jitter * 2.0, info))) return rc;
+      refitted = true;
+      if (hold) return fail(GTC_ERR_CONDITIONING, "gtc_run_steps: bordered pivot failed in hold mode");
+      continue;
+    }
+    r->n = hold ? (hold_prev >= 0 ? hold_n0 + 1 : hold_n0) : L.n;
+    if (steps > 0) *r->gp.h_sc = r->h_rb->sc;
+    r->predictions_valid = true;
+    r->acc_valid = true;
+    if (L.halt == kLoopCapacity) return fail(GTC_ERR_CAPACITY, "more observations than the run's n_max");
+    if (L.halt == kLoopNoCandidates) break;
+  }
+  fill_info(info, *r->gp.h_sc, r->n, refitted ? 1 : 0);
+  return GTC_OK;
+}
+
+extern "C" int gtc_last_steps_phase_ms(const gtc_run* r, double* out3) {
+  if (!r || !out3) return fail(GTC_ERR_INVALID, "null argument");
+  if (r->timed_steps <= 0) return fail(GTC_ERR_INVALID, "last gtc_run_steps chunk was not timed");
+  double acc[3] = {0.0, 0.0, 0.0};
+  const cudaEvent_t* te = r->step_events.data();
+  for (int i = 0; i < r->timed_steps; ++i)
+    for (int k = 0; k < 3; ++k) {
+      float ms = 0.f;
+      GTC_CUDA(cudaEventElapsedTime(&ms, te[3 * i + k], te[3 * i + k + 1]));
+      acc[k] += ms;
+    }
+  for (int k = 0; k < 3; ++k) out3[k] = acc[k] / r->timed_steps;
+  return GTC_OK;
+}
+
+extern "C" double gtc_last_steps_ms(const gtc_run* r) {
+  if (!r || !r->step_timed) return 0.0;
+  float ms = 0.f;
+  return cudaEventElapsedTime(&ms, r->ev_step0, r->ev_step1) == cudaSuccess ? (double)ms : 0.0;
 }
 
 // =============================================================== sharding

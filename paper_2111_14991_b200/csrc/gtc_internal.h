@@ -133,6 +133,8 @@ struct VarSource {
   int direct;
 };
 
+struct LoopDev;
+
 struct SelectParams {
   uint32_t af_mask;
   int lambda_mode;
@@ -144,6 +146,8 @@ struct SelectParams {
   int n_excluded;
   int64_t first_eligible;   // host-computed: lowest unvisited, non-excluded position (-1: none)
   int64_t n_candidates;     // host-computed: number of eligible candidates
+  const LoopDev* loop;      // resident loop: f_best_raw / first_eligible / n_candidates / the
+                            // variance total come from the loop state instead
 };
 
 // Per-block scratch of the selection kernels (sized by reduce_blocks(n)).
@@ -197,6 +201,7 @@ struct AppendArgs {
   int n0;
   uint32_t* visited_mark;
   int staged;
+  const LoopDev* loop;  // resident loop: pos / y_new / n0 from the loop state (no-op unless valid)
 };
 
 struct ExtendArgs {
@@ -212,6 +217,7 @@ struct ExtendArgs {
   VarAccum* acc;
   VarAccum* acc_clear;
   TileStats* tstat;  // final pass: per-tile posterior summary (optional)
+  const LoopDev* loop;  // resident loop: n0 and the accumulator generation from the loop state
 };
 
 struct SelectRunArgs {
@@ -315,6 +321,55 @@ void launch_enumerate_compact(const EnumDev& e, const uint32_t* mask, const int6
 int snap_partial_blocks(int64_t n);
 void launch_snap(const SpaceDev& sp, const double* pts, int n_pts, void* partial, int64_t* out,
                  cudaStream_t stream);
+
+// ---- resident BO loop (gtc_run_steps) --------------------------------------
+// The device-side state of a run's BO loop in simulation mode (objective =
+// resident value table): k_loop_advance turns the last selection into the
+// next evaluation -- table lookup, visited mark, candidate count / first
+// eligible position, f_best, accumulator generation -- and the append, pass
+// and selection kernels read their per-step inputs from here, so a chunk of
+// iterations runs without a host round trip (all launch arguments constant).
+struct StepRec {  // == gtc_step_record
+  int64_t position;
+  double value;     // NaN: runtime-invalid
+  double lambda;    // exploration factor of the selection that picked it
+  int32_t valid;
+  int32_t cv_fallback;
+};
+enum : int32_t { kLoopRunning = 0, kLoopNoCandidates = 1, kLoopPivot = 2, kLoopCapacity = 3 };
+struct LoopDev {
+  int64_t pos;        // this step's pick
+  double y;           // its value
+  int32_t valid;
+  int32_t n0;         // row of this step's bordered append
+  int32_t n;          // observations in the model
+  int32_t gen;        // current variance-accumulator generation
+  int32_t halt;       // kLoop*
+  int32_t step;       // records written
+  int32_t af;         // acquisition slot of the strategy
+  int32_t n_max;
+  int32_t hold;       // steady-state mode: every valid step re-appends at row n0 = hold_n0
+  int32_t hold_n0;
+  int64_t hold_prev;  // position observed at row hold_n0 (unmarked when replaced), -1 none
+  double f_best;      // best valid raw observation (f_best_raw of the selection)
+  double f_base;      // hold mode: f_best = min(f_base, y)
+  int64_t first;      // lowest unvisited position (-1: none)
+  int64_t count;      // unvisited candidates
+  int64_t n_space;
+  VarAccum* acc;      // [2] the run's accumulator generations
+  const double* table;
+  uint32_t* visited;
+  const double* var;
+  double s2;
+  const GpScalars* sc;
+  const SelectDev* sel;
+  StepRec* rec;
+};
+void launch_loop_advance(LoopDev* d_loop, cudaStream_t stream);
+// Loop-mode launches of the bordered append / single-row pass (args.loop set;
+// smem / args.n0 sized for the largest row of the chunk).
+void launch_gp_append_loop(const AppendArgs& a, int nu, size_t smem, cudaStream_t stream);
+void launch_extend_loop(const ExtendArgs& a, int64_t tiles, int nu, cudaStream_t stream);
 
 int reduce_blocks(int64_t n);  // grid size used by the reduction kernels
 uint64_t launches();

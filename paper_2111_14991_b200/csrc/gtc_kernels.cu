@@ -473,10 +473,17 @@ __device__ void gp_append_body(const AppendArgs& a) {
   const KernelParams k = a.k;
   const double noise = a.noise;
   const SpaceDev& sp = a.sp;
-  const int64_t pos = a.pos;
+  int64_t pos = a.pos;
   const double* x_explicit = a.x_explicit;
-  const double y_new = a.y_new;
-  const int n0 = a.n0;
+  double y_new = a.y_new;
+  int n0 = a.n0;
+  if (a.loop) {  // resident loop: this step's evaluation (k_loop_advance)
+    const LoopDev* lp = a.loop;
+    if (lp->halt != kLoopRunning || !lp->valid) return;
+    pos = lp->pos;
+    y_new = lp->y;
+    n0 = lp->n0;
+  }
   uint32_t* visited_mark = a.visited_mark;
   const int staged = a.staged;
   extern __shared__ double smem[];
@@ -563,7 +570,15 @@ __device__ __forceinline__ double2 coord2(const SpaceDev& sp, int t, int64_t j0)
 // once.  One CTA per tile of kTile candidates, one double2 column pair per
 // thread.  With final_pass the posterior mean/variance are produced too.
 template <int R, int NU>
-__device__ __forceinline__ void extend_body(const ExtendArgs& a) {
+__device__ __forceinline__ void extend_body(const ExtendArgs& a_in) {
+  ExtendArgs a = a_in;
+  if (a.loop) {  // resident loop: only after a valid evaluation; generation flipped by k_loop_advance
+    const LoopDev* lp = a.loop;
+    if (lp->halt != kLoopRunning || !lp->valid) return;
+    a.n0 = lp->n0;
+    a.acc = lp->acc + lp->gen;
+    a.acc_clear = lp->acc + (lp->gen ^ 1);
+  }
   accum_clear(a.acc_clear);  // next generation's accumulator (even when the pass is skipped)
   if (a.check_status && a.g.sc->status != 0) return;  // bordered row failed: host refactors
   extern __shared__ double sm[];
@@ -1575,7 +1590,96 @@ __device__ __forceinline__ void select_run_body(const SelCtx& c, const GpScalars
 template <uint32_t MASK>
 __global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK))
     k_select(SelCtx c, const GpScalars* sc, SelectParams p, VarSource vs, const TileStats* tstat, int ntiles) {
+  if (p.loop) {  // resident loop: per-step inputs from the loop state
+    const LoopDev* lp = p.loop;
+    if (lp->halt != kLoopRunning || sc->status != 0) return;  // (a failed bordered row halts the loop)
+    p.f_best_raw = lp->f_best;
+    p.first_eligible = lp->first;
+    p.n_candidates = lp->count;
+    vs.acc = lp->acc + lp->gen;
+  }
   select_run_body<MASK>(c, sc, p, vs, tstat, ntiles);
+}
+
+// Resident loop step (one warp): the last selection's pick is evaluated from
+// the value table and applied to the loop state -- the host bookkeeping of
+// gtc_observe (visited mark, candidate count, first eligible position, f_best;
+// RunContext::evaluate, strategies.hpp:159-232) done on the device.
+__global__ void k_loop_advance(LoopDev* L) {
+  __shared__ int64_t s_pos;
+  __shared__ int s_go;
+  const int lane = threadIdx.x;
+  if (lane == 0) {
+    s_go = 0;
+    if (L->halt == kLoopRunning) {
+      const SelectDev* sel = L->sel;
+      if (L->sc->status != 0) {
+        L->halt = kLoopPivot;  // the last bordered row failed: the host refactorises
+      } else if (sel->n_candidates <= 0) {
+        L->halt = kLoopNoCandidates;
+      } else {
+        const int64_t pos = sel->position[L->af];
+        const double y = L->table[pos];
+        const int valid = y == y;
+        if (valid && !L->hold && L->n >= L->n_max) {
+          L->halt = kLoopCapacity;
+        } else {
+          L->rec[L->step] = StepRec{pos, y, sel->lambda, valid, sel->cv_fallback};
+          ++L->step;
+          L->pos = pos;
+          L->y = y;
+          L->valid = valid;
+          if (valid) {
+            if (L->hold) {  // steady state: replace the observation at row hold_n0
+              const int64_t prev = L->hold_prev;
+              if (prev >= 0) {
+                L->visited[prev >> 5] &= ~(1u << (prev & 31));
+                ++L->count;
+                if (L->first < 0 || prev < L->first) L->first = prev;
+              }
+              L->hold_prev = pos;
+              L->n0 = L->hold_n0;
+              L->n = L->hold_n0 + 1;
+              L->f_best = y < L->f_base ? y : L->f_base;
+            } else {
+              L->n0 = L->n;
+              ++L->n;
+              if (y < L->f_best) L->f_best = y;
+            }
+            L->gen ^= 1;  // the pass produces the next generation
+            L->visited[pos >> 5] |= 1u << (pos & 31);
+          } else {
+            // no refit: the variance total loses this candidate in O(1)
+            mark_update(L->visited, pos, 1, L->acc + L->gen, L->var, L->s2);
+          }
+          --L->count;
+          s_pos = pos;
+          s_go = pos == L->first;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (!s_go) return;
+  // the first eligible position was picked: next unvisited one (warp scan)
+  const int64_t n = L->n_space;
+  const int64_t nw = (n + 31) >> 5;
+  int64_t found = -1;
+  for (int64_t w0 = (s_pos >> 5); w0 < nw && found < 0; w0 += 32) {
+    const int64_t w = w0 + lane;
+    uint32_t free_bits = 0;
+    if (w < nw) {
+      free_bits = ~L->visited[w];
+      if (w == (nw - 1) && (n & 31)) free_bits &= (1u << (n & 31)) - 1u;
+    }
+    const unsigned ball = __ballot_sync(0xffffffffu, free_bits != 0);
+    if (ball) {
+      const int src = __ffs(ball) - 1;
+      const uint32_t fb = __shfl_sync(0xffffffffu, free_bits, src);
+      found = ((w0 + src) << 5) + (__ffs(fb) - 1);
+    }
+  }
+  if (lane == 0) L->first = found;
 }
 
 // Runs of a batch on the y axis (one AF mask per launch).
@@ -1703,6 +1807,20 @@ void launch_gp_append_batch(const AppendArgs* d_args, int count, int nu, size_t 
   }
 }
 
+void launch_gp_append_loop(const AppendArgs& a, int nu, size_t smem, cudaStream_t s) {
+  count_launch();
+  switch (nu) {
+    case 0: opt_in_smem(k_gp_append<0>, smem); k_gp_append<0><<<1, kCtaThreads, smem, s>>>(a); break;
+    case 1: opt_in_smem(k_gp_append<1>, smem); k_gp_append<1><<<1, kCtaThreads, smem, s>>>(a); break;
+    default: opt_in_smem(k_gp_append<2>, smem); k_gp_append<2><<<1, kCtaThreads, smem, s>>>(a); break;
+  }
+}
+
+void launch_loop_advance(LoopDev* d_loop, cudaStream_t s) {
+  count_launch();
+  k_loop_advance<<<1, 32, 0, s>>>(d_loop);
+}
+
 void launch_gp_truncate(const GpDev& g, int n, cudaStream_t s) {
   count_launch();
   k_gp_truncate<<<1, kCtaThreads, 0, s>>>(g, n);
@@ -1735,6 +1853,15 @@ void launch_extend(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V
       case 1: extend_impl<kMaxRows, 1>(a, tiles, s); break;
       default: extend_impl<kMaxRows, 2>(a, tiles, s); break;
     }
+  }
+}
+
+void launch_extend_loop(const ExtendArgs& a, int64_t tiles, int nu, cudaStream_t s) {
+  count_launch();
+  switch (nu) {
+    case 0: extend_impl<1, 0>(a, tiles, s); break;
+    case 1: extend_impl<1, 1>(a, tiles, s); break;
+    default: extend_impl<1, 2>(a, tiles, s); break;
   }
 }
 

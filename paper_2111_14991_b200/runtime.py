@@ -199,6 +199,37 @@ class SurrogateRun:
                                  C.byref(r), C.byref(info)))
         return FitInfo.of(info), None
 
+    def set_values(self, values) -> None:
+        """Simulation-mode objective: values[pos] (NaN = runtime-invalid) on the device."""
+        v = np.ascontiguousarray(np.asarray(values, dtype=np.float64))
+        check(load().gtc_run_set_values(self._h, _lib.dptr(v), len(v)))
+
+    def steps(self, af: AcquisitionId, k: int, f_best_raw: float,
+              exploration: ExplorationConfig = ExplorationConfig(),
+              cv_state: ContextualVarianceState = ContextualVarianceState(), hold: bool = False,
+              timing: bool = False):
+        """gtc_run_steps: k resident BO iterations (select -> table lookup ->
+        mark -> append + pass) with one host synchronisation.  Returns the
+        step records (position, value, lambda_, valid, cv_fallback)."""
+        a, _keep = self._args([af], f_best_raw, exploration, cv_state, None)
+        recs = (_lib.gtc_step_record * max(1, int(k)))()
+        done = C.c_int32()
+        info = _lib.gtc_fit_info()
+        flags = (_lib.GTC_STEPS_HOLD_N if hold else 0) | (_lib.GTC_STEPS_TIMING if timing else 0)
+        check(load().gtc_run_steps(self._h, C.byref(a), int(k), flags, recs,
+                                   C.byref(done), C.byref(info)))
+        return recs[:done.value]
+
+    def last_steps_ms(self) -> float:
+        return float(load().gtc_last_steps_ms(self._h))
+
+    def last_steps_phase_ms(self):
+        """(selection + advance, append, pass) mean CUDA-event ms per step of
+        the last gtc_run_steps(timing=True) chunk."""
+        out = (C.c_double * 3)()
+        check(load().gtc_last_steps_phase_ms(self._h, out))
+        return tuple(out)
+
     def truncate_async(self, n: int) -> None:
         """Model back to its first n observations without a host round trip."""
         check(load().gtc_truncate(self._h, int(n), None))

@@ -1,0 +1,138 @@
+"""Resident BO loop (gtc_run_steps, simulation mode): k iterations of a
+single-AF strategy on the device must equal the gtc_observe loop driven from
+the host -- the run_bo iteration of strategies.hpp:401-449 -- pick for pick,
+lambda for lambda and posterior bit for bit (same kernels, per-step inputs
+read from the loop state instead of launch arguments)."""
+import numpy as np
+import pytest
+
+from paper_2111_14991_b200 import synthetic
+
+pytestmark = pytest.mark.gpu
+
+
+def setup(gt, grid, invalid, seed, nu=1, n_init=20, n_max=160, l=1.5):
+    coords, ids, values = synthetic.random_rough(grid, seed, invalid)
+    space = gt.Space(coords)
+    run = gt.SurrogateRun(space, gt.MaternKernel(gt.MaternNu(nu), l, 1.0), 1e-10, 1e-6, n_max)
+    rng = np.random.default_rng(seed)
+    valid = np.nonzero(~np.isnan(values))[0]
+    init = rng.choice(valid, n_init, replace=False)
+    run.fit(init, values[init])
+    for p in init:
+        run.mark_visited(int(p))
+    cv = gt.ContextualVarianceState(float(np.mean(values[init])), run.mean_variance())
+    return space, run, values, init, cv
+
+
+def host_loop(gt, run, values, af, k, f_best, expl, cv):
+    """The gtc_observe loop: select -> evaluate -> observe (+ next selection)."""
+    picks, lams, fbs = [], [], []
+    sel = run.select([af], f_best, expl, cv)
+    for _ in range(k):
+        if sel.n_candidates == 0:
+            break
+        p = sel.pick(af)
+        y = values[p]
+        picks.append(p)
+        lams.append(sel.lambda_)
+        valid = not np.isnan(y)
+        if valid:
+            f_best = min(f_best, float(y))
+        _, sel = run.observe(p, float(y) if valid else None, [af], f_best, expl, cv)
+        fbs.append(f_best)
+    return picks, lams
+
+
+@pytest.mark.parametrize("af", [0, 1, 2])
+@pytest.mark.parametrize("mode", ["cv", "const"])
+def test_steps_equal_observe_loop(gt, af, mode):
+    af = gt.AcquisitionId(af)
+    expl = gt.ExplorationConfig() if mode == "cv" else gt.ExplorationConfig(gt.ExplorationConfig.Mode.constant, 0.01)
+    grid, inv, seed, k = [8, 8, 8, 6], 0.3, 11 + int(af), 90
+    space, run_a, values, init, cv = setup(gt, grid, inv, seed)
+    f0 = float(np.min(values[init]))
+    picks_h, lams_h = host_loop(gt, run_a, values, af, k, f0, expl, cv)
+    m_h, v_h = run_a.predictions()
+
+    _, run_b, _, _, cv_b = setup(gt, grid, inv, seed)
+    assert cv_b.initial_mean_variance == cv.initial_mean_variance
+    run_b.set_values(values)
+    recs = run_b.steps(af, k, f0, expl, cv)
+    picks_d = [r.position for r in recs]
+    assert picks_d == picks_h
+    np.testing.assert_array_equal([r.lambda_ for r in recs], lams_h)
+    vals = values[picks_d]
+    np.testing.assert_array_equal([bool(r.valid) for r in recs], ~np.isnan(vals))
+    assert any(not r.valid for r in recs)  # the invalid (O(1) total update) path ran
+    m_d, v_d = run_b.predictions()
+    np.testing.assert_array_equal(m_d, m_h)
+    np.testing.assert_array_equal(v_d, v_h)
+    assert run_b.unvisited_count() == run_a.unvisited_count()
+    # continuing from the host API after a resident chunk: same next selection
+    fb = min([f0] + [float(v) for v in vals if not np.isnan(v)])
+    s_a = run_a.select([af], fb, expl, cv)
+    s_b = run_b.select([af], fb, expl, cv)
+    assert s_a.pick(af) == s_b.pick(af) and s_a.lambda_ == s_b.lambda_
+
+
+def test_steps_chunked_and_nu(gt):
+    """Several calls in a row (host state re-synchronised between chunks) and
+    the other Matern orders."""
+    for nu in (0, 2):
+        af = gt.AcquisitionId.ei
+        expl = gt.ExplorationConfig()
+        space, run_a, values, init, cv = setup(gt, [10, 10, 6, 5], 0.2, 3 + nu, nu=nu)
+        f0 = float(np.min(values[init]))
+        picks_h, _ = host_loop(gt, run_a, values, af, 70, f0, expl, cv)
+        _, run_b, _, _, _ = setup(gt, [10, 10, 6, 5], 0.2, 3 + nu, nu=nu)
+        run_b.set_values(values)
+        picks_d, fb = [], f0
+        for k in (1, 9, 25, 35):
+            recs = run_b.steps(af, k, fb, expl, cv)
+            picks_d += [r.position for r in recs]
+            fb = min([fb] + [r.value for r in recs if r.valid])
+        assert picks_d == picks_h
+
+
+def test_steps_exhaust_space(gt):
+    """A space smaller than the chunk: the device loop stops when every
+    candidate has been visited (run_bo's exhaustion, strategies.hpp:399)."""
+    af = gt.AcquisitionId.lcb
+    space, run, values, init, cv = setup(gt, [5, 4, 3], 0.25, 5, n_max=80)
+    run.set_values(values)
+    recs = run.steps(af, 200, float(np.min(values[init])), gt.ExplorationConfig(), cv)
+    assert len(recs) == 60 - 20
+    assert sorted([r.position for r in recs] + list(init)) == list(range(60))
+    assert run.unvisited_count() == 0
+
+
+def test_steps_hold_equals_rollback_loop(gt):
+    """GTC_STEPS_HOLD_N (the bench's steady state) == the host rollback loop
+    (truncate to n0, observe, unmark the pick)."""
+    af = gt.AcquisitionId.ei
+    expl = gt.ExplorationConfig()
+    grid, seed, k = [10, 10, 10, 8], 21, 40
+    space, run_a, values, init, cv = setup(gt, grid, 0.0, seed, n_init=60, n_max=64)
+    f0 = float(np.min(values[init]))
+    n0 = 60
+    pick = run_a.select([af], f0, expl, cv).pick(af)
+    picks_h = []
+    for _ in range(k):
+        run_a.truncate_async(n0)
+        picks_h.append(pick)
+        y = float(values[pick])
+        _, s = run_a.observe(pick, y, [af], min(f0, y), expl, cv)
+        run_a.unmark_visited(pick)
+        pick = s.pick(af)
+    _, run_b, _, _, _ = setup(gt, grid, 0.0, seed, n_init=60, n_max=64)
+    run_b.set_values(values)
+    recs = run_b.steps(af, k, f0, expl, cv, hold=True)
+    assert [r.position for r in recs] == picks_h
+    # both models now hold the init points + the last pick at row n0
+    m_a, v_a = run_a.predictions()
+    m_b, v_b = run_b.predictions()
+    np.testing.assert_array_equal(m_a, m_b)
+    np.testing.assert_array_equal(v_a, v_b)
+    # the host path unmarked the last pick too; the device run keeps it visited
+    assert run_b.unvisited_count() == run_a.unvisited_count() - 1

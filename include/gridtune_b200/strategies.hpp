@@ -281,6 +281,8 @@ class DeviceSurrogate : public ArgmaxSource {
   /// Simulation mode: the objective's replay table on the device (gtc_run_set_values).
   void set_values(const double* values) { check(gtc_run_set_values(run_.get(), values, static_cast<std::int64_t>(space_.size()))); }
 
+  void detach_group() { check(gtc_run_set_group(run_.get(), nullptr)); }
+
   /// Up to k resident iterations of a single-AF loop (gtc_run_steps).
   std::vector<gtc_step_record> steps(const gtc_select_args& a, std::size_t k) {
     prefetched_mask_ = 0;
@@ -383,8 +385,17 @@ inline TuningRun run_bo(const EnumeratedSpace& space, const Objective& objective
   };
 
   const bool resident = single && table && !config.inspect && resident_loop_enabled();
-  if (resident) gp.set_values(table);
-  const DeviceSurrogate::GroupMembership membership(thread_observe_group());
+  if (resident) {
+    gp.set_values(table);
+    // a resident run never takes part in observe rounds (gtc_run_bo_batch):
+    // it runs on its own stream and must not hold up the group's members
+    gp.detach_group();
+    if (thread_observe_group() && thread_group_member()) {
+      gtc_group_leave(thread_observe_group());
+      thread_group_member() = false;
+    }
+  }
+  const DeviceSurrogate::GroupMembership membership(resident ? nullptr : thread_observe_group());
   while (!ctx.exhausted()) {
     if (resident && !train_pos.empty()) {
       // as many iterations as the budget surely allows, without host round

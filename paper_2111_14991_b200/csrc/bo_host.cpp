@@ -152,6 +152,10 @@ extern "C" int gtc_run_bo_batch(gtc_space* space, const std::uint64_t* ids, cons
       return rc;
     }
   }
+  // GTC_BATCH_RESIDENT=1: single-AF runs loop resident on the device
+  // (gtc_run_steps, own stream) instead of joining the observe groups
+  const char* br = std::getenv("GTC_BATCH_RESIDENT");
+  const bool batch_resident = br && br[0] == '1';
   std::atomic<std::int32_t> next{0}, next_worker{0};
   auto worker = [&]() {
     const int w = next_worker.fetch_add(1);
@@ -167,7 +171,7 @@ extern "C" int gtc_run_bo_batch(gtc_space* space, const std::uint64_t* ids, cons
     for (std::int32_t i; (i = next.fetch_add(1)) < n_runs;) {
       statuses[i] = run(space, ids, &configs[i], obj, records ? records + (std::int64_t)i * capacity : nullptr,
                         lambdas ? lambdas + (std::int64_t)i * capacity : nullptr, capacity,
-                        summaries ? &summaries[i] : nullptr);
+                        summaries ? &summaries[i] : nullptr, batch_resident ? values : nullptr);
     }
     if (group && thread_group_member()) gtc_group_leave(group);  // (a run that failed early)
     thread_group_member() = false;

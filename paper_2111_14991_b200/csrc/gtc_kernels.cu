@@ -59,6 +59,32 @@ static std::atomic<uint64_t> g_launches{0};
 uint64_t launches() { return g_launches.load(); }
 static inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+// Programmatic dependent launch (resident loop): let the next kernel of the
+// stream be scheduled now, then wait until every preceding kernel has
+// completed and its writes are visible.  Both are no-ops for a kernel
+// launched without the PDL attribute.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// cudaLaunchKernelEx with programmatic stream serialisation.
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 __host__ __device__ __forceinline__ int64_t packed(int64_t i) { return i * (i + 1) / 2; }
 
 // ------------------------------------------------------------ device helpers
@@ -477,6 +503,7 @@ __device__ void gp_append_body(const AppendArgs& a) {
   const double* x_explicit = a.x_explicit;
   double y_new = a.y_new;
   int n0 = a.n0;
+  pdl_begin();
   if (a.loop) {  // resident loop: this step's evaluation (k_loop_advance)
     const LoopDev* lp = a.loop;
     if (lp->halt != kLoopRunning || !lp->valid) return;
@@ -572,6 +599,7 @@ __device__ __forceinline__ double2 coord2(const SpaceDev& sp, int t, int64_t j0)
 template <int R, int NU>
 __device__ __forceinline__ void extend_body(const ExtendArgs& a_in) {
   ExtendArgs a = a_in;
+  pdl_begin();
   if (a.loop) {  // resident loop: only after a valid evaluation; generation flipped by k_loop_advance
     const LoopDev* lp = a.loop;
     if (lp->halt != kLoopRunning || !lp->valid) return;
@@ -1590,6 +1618,7 @@ __device__ __forceinline__ void select_run_body(const SelCtx& c, const GpScalars
 template <uint32_t MASK>
 __global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK))
     k_select(SelCtx c, const GpScalars* sc, SelectParams p, VarSource vs, const TileStats* tstat, int ntiles) {
+  pdl_begin();
   if (p.loop) {  // resident loop: per-step inputs from the loop state
     const LoopDev* lp = p.loop;
     if (lp->halt != kLoopRunning || sc->status != 0) return;  // (a failed bordered row halts the loop)
@@ -1609,6 +1638,7 @@ __global__ void k_loop_advance(LoopDev* L) {
   __shared__ int64_t s_pos;
   __shared__ int s_go;
   const int lane = threadIdx.x;
+  pdl_begin();
   if (lane == 0) {
     s_go = 0;
     if (L->halt == kLoopRunning) {
@@ -1810,15 +1840,15 @@ void launch_gp_append_batch(const AppendArgs* d_args, int count, int nu, size_t 
 void launch_gp_append_loop(const AppendArgs& a, int nu, size_t smem, cudaStream_t s) {
   count_launch();
   switch (nu) {
-    case 0: opt_in_smem(k_gp_append<0>, smem); k_gp_append<0><<<1, kCtaThreads, smem, s>>>(a); break;
-    case 1: opt_in_smem(k_gp_append<1>, smem); k_gp_append<1><<<1, kCtaThreads, smem, s>>>(a); break;
-    default: opt_in_smem(k_gp_append<2>, smem); k_gp_append<2><<<1, kCtaThreads, smem, s>>>(a); break;
+    case 0: opt_in_smem(k_gp_append<0>, smem); launch_pdl(k_gp_append<0>, 1, kCtaThreads, smem, s, a); break;
+    case 1: opt_in_smem(k_gp_append<1>, smem); launch_pdl(k_gp_append<1>, 1, kCtaThreads, smem, s, a); break;
+    default: opt_in_smem(k_gp_append<2>, smem); launch_pdl(k_gp_append<2>, 1, kCtaThreads, smem, s, a); break;
   }
 }
 
 void launch_loop_advance(LoopDev* d_loop, cudaStream_t s) {
   count_launch();
-  k_loop_advance<<<1, 32, 0, s>>>(d_loop);
+  launch_pdl(k_loop_advance, 1, 32, 0, s, d_loop);
 }
 
 void launch_gp_truncate(const GpDev& g, int n, cudaStream_t s) {
@@ -1856,12 +1886,19 @@ void launch_extend(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V
   }
 }
 
+template <int NU>
+static void extend_loop_impl(const ExtendArgs& a, int64_t tiles, cudaStream_t s) {
+  const size_t sm = sizeof(double) * ((size_t)2 * (a.n0 + 1) + (size_t)a.g.d + 1 + 8);
+  opt_in_smem(k_extend<1, NU>, sm);
+  launch_pdl(k_extend<1, NU>, dim3((unsigned)tiles), dim3(kExtendThreads), sm, s, a);
+}
+
 void launch_extend_loop(const ExtendArgs& a, int64_t tiles, int nu, cudaStream_t s) {
   count_launch();
   switch (nu) {
-    case 0: extend_impl<1, 0>(a, tiles, s); break;
-    case 1: extend_impl<1, 1>(a, tiles, s); break;
-    default: extend_impl<1, 2>(a, tiles, s); break;
+    case 0: extend_loop_impl<0>(a, tiles, s); break;
+    case 1: extend_loop_impl<1>(a, tiles, s); break;
+    default: extend_loop_impl<2>(a, tiles, s); break;
   }
 }
 
@@ -1948,9 +1985,12 @@ void launch_select(const double* mu, const double* var, const uint32_t* visited,
   }();
   const int want = grid_override > 0 ? grid_override : sel_blocks_per_sm(mask) * sm_count();
   const int grid = std::max(1, std::min({ntiles, want, kMaxReduceGrid}));
-#define GTC_SELECT_CASE(M)                                                       \
-  case M:                                                                        \
-    k_select<M><<<grid, kSelectThreads, 0, s>>>(c, sc, p, vs, tstat, ntiles); \
+#define GTC_SELECT_CASE(M)                                                           \
+  case M:                                                                            \
+    if (p.loop)                                                                      \
+      launch_pdl(k_select<M>, dim3(grid), dim3(kSelectThreads), 0, s, c, sc, p, vs, tstat, ntiles); \
+    else                                                                             \
+      k_select<M><<<grid, kSelectThreads, 0, s>>>(c, sc, p, vs, tstat, ntiles);      \
     break;
   switch (mask) {  // launch errors surface through the caller's cudaGetLastError()
     GTC_SELECT_CASE(1)

@@ -136,3 +136,45 @@ def test_steps_hold_equals_rollback_loop(gt):
     np.testing.assert_array_equal(v_a, v_b)
     # the host path unmarked the last pick too; the device run keeps it visited
     assert run_b.unvisited_count() == run_a.unvisited_count() - 1
+
+
+@pytest.mark.parametrize("variant", ["cv", "const", "free_invalid", "nu52"])
+def test_run_bo_resident_equals_observe_loop(gt, monkeypatch, variant):
+    """gtc_run_bo_table with the resident loop == the per-iteration gtc_observe
+    loop (GTC_RESIDENT_LOOP=0), every single-AF strategy."""
+    coords, ids, values = synthetic.random_rough([12, 10, 8], 7, 0.3)
+    space = gt.Space(coords)
+    for sid in (gt.StrategyId.bo_ei, gt.StrategyId.bo_poi, gt.StrategyId.bo_lcb):
+        cfg = gt.StrategyConfig(id=sid, seed=5 + int(sid), budget=120, n_init=10)
+        if variant == "const":
+            cfg.exploration = gt.ExplorationConfig(gt.ExplorationConfig.Mode.constant, 0.05)
+        elif variant == "free_invalid":
+            cfg.invalid_consumes_budget = False
+        elif variant == "nu52":
+            cfg.nu = gt.MaternNu.five_halves
+        monkeypatch.setenv("GTC_RESIDENT_LOOP", "0")
+        a = gt.run_bo(space, ids, cfg, values=values)
+        monkeypatch.setenv("GTC_RESIDENT_LOOP", "1")
+        b = gt.run_bo(space, ids, cfg, values=values)
+        np.testing.assert_array_equal(a.positions, b.positions)
+        np.testing.assert_array_equal(a.lambdas, b.lambdas)
+        assert (a.evaluations, a.budget_consumed, a.invalid_count, a.surrogate_size, a.n_warnings) == \
+               (b.evaluations, b.budget_consumed, b.invalid_count, b.surrogate_size, b.n_warnings)
+        assert a.best_value == b.best_value
+
+
+def test_batch_resident_equals_groups(gt, monkeypatch):
+    """gtc_run_bo_batch: single-AF runs resident (default) or in observe groups
+    (GTC_BATCH_RESIDENT=0), mixed with multi-AF runs -- identical runs."""
+    coords, ids, values = synthetic.random_rough([12, 10, 8], 13, 0.3)
+    space = gt.Space(coords)
+    cfgs = [gt.StrategyConfig(id=sid, seed=seed, budget=80, n_init=10)
+            for sid in (gt.StrategyId.bo_ei, gt.StrategyId.bo_multi, gt.StrategyId.bo_poi, gt.StrategyId.bo_lcb)
+            for seed in (1, 2, 3, 4)]
+    monkeypatch.setenv("GTC_BATCH_RESIDENT", "0")
+    a = gt.run_bo_batch(space, ids, cfgs, values, threads=8)
+    monkeypatch.setenv("GTC_BATCH_RESIDENT", "1")
+    b = gt.run_bo_batch(space, ids, cfgs, values, threads=8)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x.positions, y.positions)
+        np.testing.assert_array_equal(x.lambdas, y.lambdas)

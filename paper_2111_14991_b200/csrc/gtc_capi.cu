@@ -1044,9 +1044,9 @@ static void replay_steps(gtc_run* r, const StepRec* rec, int m, bool hold, int h
 }
 
 // k BO iterations of a single-AF strategy in simulation mode without host
-// round trips: per step select -> k_loop_advance (table lookup, visited mark,
-// f_best) -> bordered append -> predictive pass, all launch arguments
-// constant.  A failed bordered pivot halts the chunk on the device; the host
+// round trips: per step select (its last block advances the loop state:
+// table lookup, visited mark, f_best) -> bordered append -> predictive pass,
+// all launch arguments constant, chained by programmatic dependent launch.  A failed bordered pivot halts the chunk on the device; the host
 // refactorises with escalated jitter (gp.hpp:116-129, as gtc_append) and
 // continues with a new chunk.
 extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, int32_t flags,
@@ -1141,7 +1141,6 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
       if (timing) GTC_CUDA(cudaEventRecord(te[3 * i], r->stream));
       launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, vs, r->tstat, r->red.b, r->red.sel,
                     r->stream);
-      launch_loop_advance(r->d_loop, r->stream);
       if (timing) GTC_CUDA(cudaEventRecord(te[3 * i + 1], r->stream));
       launch_gp_append_loop(aa, r->cfg.kernel.nu, append_smem, r->stream);
       if (timing) GTC_CUDA(cudaEventRecord(te[3 * i + 2], r->stream));

@@ -146,8 +146,9 @@ struct SelectParams {
   int n_excluded;
   int64_t first_eligible;   // host-computed: lowest unvisited, non-excluded position (-1: none)
   int64_t n_candidates;     // host-computed: number of eligible candidates
-  const LoopDev* loop;      // resident loop: f_best_raw / first_eligible / n_candidates / the
-                            // variance total come from the loop state instead
+  LoopDev* loop;            // resident loop: f_best_raw / first_eligible / n_candidates / the
+                            // variance total come from the loop state instead, and the
+                            // selection's last block advances the loop (loop_advance)
 };
 
 // Per-block scratch of the selection kernels (sized by reduce_blocks(n)).
@@ -324,10 +325,11 @@ void launch_snap(const SpaceDev& sp, const double* pts, int n_pts, void* partial
 
 // ---- resident BO loop (gtc_run_steps) --------------------------------------
 // The device-side state of a run's BO loop in simulation mode (objective =
-// resident value table): k_loop_advance turns the last selection into the
+// resident value table): loop_advance turns the last selection into the
 // next evaluation -- table lookup, visited mark, candidate count / first
-// eligible position, f_best, accumulator generation -- and the append, pass
-// and selection kernels read their per-step inputs from here, so a chunk of
+// eligible position, f_best, accumulator generation (loop_advance, run by the
+// selection's last block) -- and the append, pass and selection kernels read
+// their per-step inputs from here, so a chunk of
 // iterations runs without a host round trip (all launch arguments constant).
 struct StepRec {  // == gtc_step_record
   int64_t position;
@@ -365,7 +367,6 @@ struct LoopDev {
   const SelectDev* sel;
   StepRec* rec;
 };
-void launch_loop_advance(LoopDev* d_loop, cudaStream_t stream);
 // Loop-mode launches of the bordered append / single-row pass (args.loop set;
 // smem / args.n0 sized for the largest row of the chunk).
 void launch_gp_append_loop(const AppendArgs& a, int nu, size_t smem, cudaStream_t stream);

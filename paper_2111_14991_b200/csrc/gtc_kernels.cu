@@ -504,7 +504,7 @@ __device__ void gp_append_body(const AppendArgs& a) {
   double y_new = a.y_new;
   int n0 = a.n0;
   pdl_begin();
-  if (a.loop) {  // resident loop: this step's evaluation (k_loop_advance)
+  if (a.loop) {  // resident loop: this step's evaluation (loop_advance)
     const LoopDev* lp = a.loop;
     if (lp->halt != kLoopRunning || !lp->valid) return;
     pos = lp->pos;
@@ -600,7 +600,7 @@ template <int R, int NU>
 __device__ __forceinline__ void extend_body(const ExtendArgs& a_in) {
   ExtendArgs a = a_in;
   pdl_begin();
-  if (a.loop) {  // resident loop: only after a valid evaluation; generation flipped by k_loop_advance
+  if (a.loop) {  // resident loop: only after a valid evaluation; generation flipped by loop_advance
     const LoopDev* lp = a.loop;
     if (lp->halt != kLoopRunning || !lp->valid) return;
     a.n0 = lp->n0;
@@ -1029,6 +1029,7 @@ struct SelCtx {
   uint32_t af_mask;
   ReduceBufs b;
   SelectDev* out;
+  LoopDev* loop;  // resident loop: advanced by the last block (loop_advance)
 };
 
 __device__ __forceinline__ bool eligible(const SelCtx& c, int64_t j) {
@@ -1096,6 +1097,67 @@ __device__ __forceinline__ SelPart sel_warp_reduce(SelPart v) {
     v = sel_merge<MASK>(v, w);
   }
   return v;
+}
+
+// Resident loop step, run by the selection's last thread once the selection
+// is final: its pick is evaluated from the value table and applied to the
+// loop state -- the host bookkeeping of gtc_observe (visited mark, candidate
+// count, first eligible position, f_best; RunContext::evaluate,
+// strategies.hpp:159-232) done on the device.
+__device__ void loop_advance(LoopDev* L, const SelectDev* sel) {
+  if (sel->n_candidates <= 0) {
+    L->halt = kLoopNoCandidates;
+    return;
+  }
+  const int64_t pos = sel->position[L->af];
+  const double y = L->table[pos];
+  const int valid = y == y;
+  if (valid && !L->hold && L->n >= L->n_max) {
+    L->halt = kLoopCapacity;
+    return;
+  }
+  L->rec[L->step] = StepRec{pos, y, sel->lambda, valid, sel->cv_fallback};
+  ++L->step;
+  L->pos = pos;
+  L->y = y;
+  L->valid = valid;
+  if (valid) {
+    if (L->hold) {  // steady state: replace the observation at row hold_n0
+      const int64_t prev = L->hold_prev;
+      if (prev >= 0) {
+        L->visited[prev >> 5] &= ~(1u << (prev & 31));
+        ++L->count;
+        if (L->first < 0 || prev < L->first) L->first = prev;
+      }
+      L->hold_prev = pos;
+      L->n0 = L->hold_n0;
+      L->n = L->hold_n0 + 1;
+      L->f_best = y < L->f_base ? y : L->f_base;
+    } else {
+      L->n0 = L->n;
+      ++L->n;
+      if (y < L->f_best) L->f_best = y;
+    }
+    L->gen ^= 1;  // the pass produces the next generation
+    L->visited[pos >> 5] |= 1u << (pos & 31);
+  } else {
+    // no refit: the variance total loses this candidate in O(1)
+    mark_update(L->visited, pos, 1, L->acc + L->gen, L->var, L->s2);
+  }
+  --L->count;
+  if (pos == L->first) {  // next unvisited position (first only moves forward within a run)
+    const int64_t n = L->n_space, nw = (n + 31) >> 5;
+    int64_t found = -1;
+    for (int64_t w = pos >> 5; w < nw; ++w) {
+      uint32_t fb = ~L->visited[w];
+      if (w == nw - 1 && (n & 31)) fb &= (1u << (n & 31)) - 1u;
+      if (fb) {
+        found = (w << 5) + (__ffs(fb) - 1);
+        break;
+      }
+    }
+    L->first = found;
+  }
 }
 
 template <uint32_t MASK>
@@ -1190,6 +1252,7 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first
   c.out->gp_status = gp_status;
   if (c.b.gthr) c.b.gthr[0] = c.b.gthr[1] = c.b.gthr[2] = 0ull;  // next selection starts afresh
   *c.b.counter = 0;
+  if (c.loop) loop_advance(c.loop, c.out);
 #ifdef GTC_SEL_TRACE
   g_sel_trace[blockIdx.x][6] = gtc_globaltimer();
 #endif
@@ -1621,7 +1684,11 @@ __global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK))
   pdl_begin();
   if (p.loop) {  // resident loop: per-step inputs from the loop state
     const LoopDev* lp = p.loop;
-    if (lp->halt != kLoopRunning || sc->status != 0) return;  // (a failed bordered row halts the loop)
+    if (lp->halt != kLoopRunning) return;
+    if (sc->status != 0) {  // the last bordered row failed: the host refactorises
+      if (blockIdx.x == 0 && threadIdx.x == 0) p.loop->halt = kLoopPivot;
+      return;
+    }
     p.f_best_raw = lp->f_best;
     p.first_eligible = lp->first;
     p.n_candidates = lp->count;
@@ -1630,87 +1697,6 @@ __global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK))
   select_run_body<MASK>(c, sc, p, vs, tstat, ntiles);
 }
 
-// Resident loop step (one warp): the last selection's pick is evaluated from
-// the value table and applied to the loop state -- the host bookkeeping of
-// gtc_observe (visited mark, candidate count, first eligible position, f_best;
-// RunContext::evaluate, strategies.hpp:159-232) done on the device.
-__global__ void k_loop_advance(LoopDev* L) {
-  __shared__ int64_t s_pos;
-  __shared__ int s_go;
-  const int lane = threadIdx.x;
-  pdl_begin();
-  if (lane == 0) {
-    s_go = 0;
-    if (L->halt == kLoopRunning) {
-      const SelectDev* sel = L->sel;
-      if (L->sc->status != 0) {
-        L->halt = kLoopPivot;  // the last bordered row failed: the host refactorises
-      } else if (sel->n_candidates <= 0) {
-        L->halt = kLoopNoCandidates;
-      } else {
-        const int64_t pos = sel->position[L->af];
-        const double y = L->table[pos];
-        const int valid = y == y;
-        if (valid && !L->hold && L->n >= L->n_max) {
-          L->halt = kLoopCapacity;
-        } else {
-          L->rec[L->step] = StepRec{pos, y, sel->lambda, valid, sel->cv_fallback};
-          ++L->step;
-          L->pos = pos;
-          L->y = y;
-          L->valid = valid;
-          if (valid) {
-            if (L->hold) {  // steady state: replace the observation at row hold_n0
-              const int64_t prev = L->hold_prev;
-              if (prev >= 0) {
-                L->visited[prev >> 5] &= ~(1u << (prev & 31));
-                ++L->count;
-                if (L->first < 0 || prev < L->first) L->first = prev;
-              }
-              L->hold_prev = pos;
-              L->n0 = L->hold_n0;
-              L->n = L->hold_n0 + 1;
-              L->f_best = y < L->f_base ? y : L->f_base;
-            } else {
-              L->n0 = L->n;
-              ++L->n;
-              if (y < L->f_best) L->f_best = y;
-            }
-            L->gen ^= 1;  // the pass produces the next generation
-            L->visited[pos >> 5] |= 1u << (pos & 31);
-          } else {
-            // no refit: the variance total loses this candidate in O(1)
-            mark_update(L->visited, pos, 1, L->acc + L->gen, L->var, L->s2);
-          }
-          --L->count;
-          s_pos = pos;
-          s_go = pos == L->first;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (!s_go) return;
-  // the first eligible position was picked: next unvisited one (warp scan)
-  const int64_t n = L->n_space;
-  const int64_t nw = (n + 31) >> 5;
-  int64_t found = -1;
-  for (int64_t w0 = (s_pos >> 5); w0 < nw && found < 0; w0 += 32) {
-    const int64_t w = w0 + lane;
-    uint32_t free_bits = 0;
-    if (w < nw) {
-      free_bits = ~L->visited[w];
-      if (w == (nw - 1) && (n & 31)) free_bits &= (1u << (n & 31)) - 1u;
-    }
-    const unsigned ball = __ballot_sync(0xffffffffu, free_bits != 0);
-    if (ball) {
-      const int src = __ffs(ball) - 1;
-      const uint32_t fb = __shfl_sync(0xffffffffu, free_bits, src);
-      found = ((w0 + src) << 5) + (__ffs(fb) - 1);
-    }
-  }
-  if (lane == 0) L->first = found;
-}
 
 // Runs of a batch on the y axis (one AF mask per launch).
 template <uint32_t MASK>
@@ -1846,10 +1832,6 @@ void launch_gp_append_loop(const AppendArgs& a, int nu, size_t smem, cudaStream_
   }
 }
 
-void launch_loop_advance(LoopDev* d_loop, cudaStream_t s) {
-  count_launch();
-  launch_pdl(k_loop_advance, 1, 32, 0, s, d_loop);
-}
 
 void launch_gp_truncate(const GpDev& g, int n, cudaStream_t s) {
   count_launch();
@@ -1976,7 +1958,7 @@ void launch_select(const double* mu, const double* var, const uint32_t* visited,
                    const GpScalars* sc, SelectParams p, const VarSource& vs, const TileStats* tstat,
                    const ReduceBufs& b, SelectDev* out, cudaStream_t s) {
   count_launch();
-  SelCtx c{mu, var, nullptr, visited, nullptr, p.excluded, p.n_excluded, n, p.af_mask, b, out};
+  SelCtx c{mu, var, nullptr, visited, nullptr, p.excluded, p.n_excluded, n, p.af_mask, b, out, p.loop};
   const uint32_t mask = (p.af_mask & 7u) ? (p.af_mask & 7u) : 7u;
   const int ntiles = (int)((n + kTile - 1) / kTile);
   static const int grid_override = [] {

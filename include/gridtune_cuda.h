@@ -253,8 +253,10 @@ int gtc_mean_variance(gtc_run* run, double* mean_variance, int64_t* count);
  * length gtc_space_size().  Visited candidates carry values too. */
 int gtc_read_predictions(gtc_run* run, double* mean, double* variance);
 
-/* Device-side timing helper for benchmarks: CUDA-event milliseconds of the
- * last gtc_append's predictive-pass kernel (0 if none). */
+/* Device-side timing helpers for benchmarks, active only when the process
+ * runs with GTC_PHASE_EVENTS=1 (events between the kernels would stop them
+ * from launching early): CUDA-event milliseconds of the last gtc_append's
+ * predictive-pass kernel (0 if none). */
 double gtc_last_pass_ms(const gtc_run* run);
 /* CUDA-event milliseconds of the last gtc_observe's device work (all of its
  * kernels, first launch to last, excluding the result readback). */

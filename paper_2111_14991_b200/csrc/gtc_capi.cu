@@ -800,6 +800,17 @@ extern "C" int gtc_fit(gtc_run* r, const int64_t* positions, const double* y_raw
   return refit(r, r->cfg.jitter, info);
 }
 
+// CUDA events between the observe path's kernels (gtc_last_pass_ms /
+// gtc_last_step_ms / gtc_last_phase_ms) only with GTC_PHASE_EVENTS=1: an
+// event between two kernels stops the second from launching early (PDL).
+static bool phase_events() {
+  static const bool on = [] {
+    const char* e = std::getenv("GTC_PHASE_EVENTS");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // Enqueues the bordered-row update + predictive pass for observation n0
 // (asynchronous; the pass is a no-op if the pivot fails on the device).
 static int enqueue_append(gtc_run* r, int64_t pos, double y_raw, uint32_t* mark) {
@@ -807,13 +818,14 @@ static int enqueue_append(gtc_run* r, int64_t pos, double y_raw, uint32_t* mark)
   launch_gp_append(r->gp.dev, kparams(r->cfg.kernel), r->cfg.noise, r->space->dev(), pos, nullptr, y_raw, n0,
                    mark, r->stream);
   GTC_LAUNCHED();
-  GTC_CUDA(cudaEventRecord(r->ev0, r->stream));
+  const bool ev = phase_events();
+  if (ev) GTC_CUDA(cudaEventRecord(r->ev0, r->stream));
   const VarPartials vp = r->vp();
   launch_extend(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, n0, 1, true, r->mu,
                 r->var, true, &vp, r->tstat, r->stream);
   GTC_LAUNCHED();
-  GTC_CUDA(cudaEventRecord(r->ev1, r->stream));
-  r->pass_timed = true;
+  if (ev) GTC_CUDA(cudaEventRecord(r->ev1, r->stream));
+  r->pass_timed = ev;
   r->acc_valid = true;  // (stale if the pivot failed; the refit rewrites them)
   return GTC_OK;
 }
@@ -1377,7 +1389,8 @@ static void observe_prepare(ObserveReq& q) {
 static int observe_device(ObserveReq& q, gtc_fit_info* info) {
   gtc_run* r = q.r;
   int rc;
-  GTC_CUDA(cudaEventRecord(r->ev_step0, r->stream));
+  const bool ev = phase_events();
+  if (ev) GTC_CUDA(cudaEventRecord(r->ev_step0, r->stream));
   if (q.valid) {
     if (q.n0 == 0) {
       if (q.newly) {
@@ -1399,8 +1412,8 @@ static int observe_device(ObserveReq& q, gtc_fit_info* info) {
   }
   q.selecting = q.a && r->space->n - r->visited_count > 0;
   if (q.selecting && (rc = enqueue_selection(r, q.a))) return rc;
-  GTC_CUDA(cudaEventRecord(r->ev_step1, r->stream));
-  r->step_timed = true;
+  if (ev) GTC_CUDA(cudaEventRecord(r->ev_step1, r->stream));
+  r->step_timed = ev;
   r->step_appended = q.appended;
   if (q.selecting)
     GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sel, r->red.sel, sizeof(SelectDev), cudaMemcpyDeviceToHost, r->stream));

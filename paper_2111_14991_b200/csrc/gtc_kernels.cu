@@ -1808,9 +1808,9 @@ void launch_gp_append(const GpDev& g, KernelParams k, double noise, const SpaceD
   size_t sm;
   const AppendArgs a = make_append_args(g, k, noise, sp, pos, x_explicit, y_new, n0, visited_mark, &sm);
   switch (k.nu) {
-    case 0: opt_in_smem(k_gp_append<0>, sm); k_gp_append<0><<<1, kCtaThreads, sm, s>>>(a); break;
-    case 1: opt_in_smem(k_gp_append<1>, sm); k_gp_append<1><<<1, kCtaThreads, sm, s>>>(a); break;
-    default: opt_in_smem(k_gp_append<2>, sm); k_gp_append<2><<<1, kCtaThreads, sm, s>>>(a); break;
+    case 0: opt_in_smem(k_gp_append<0>, sm); launch_pdl(k_gp_append<0>, 1, kCtaThreads, sm, s, a); break;
+    case 1: opt_in_smem(k_gp_append<1>, sm); launch_pdl(k_gp_append<1>, 1, kCtaThreads, sm, s, a); break;
+    default: opt_in_smem(k_gp_append<2>, sm); launch_pdl(k_gp_append<2>, 1, kCtaThreads, sm, s, a); break;
   }
 }
 
@@ -1842,7 +1842,7 @@ template <int R, int NU>
 static void extend_impl(const ExtendArgs& a, int64_t tiles, cudaStream_t s) {
   const size_t sm = sizeof(double) * ((size_t)(R + 1) * (a.n0 + R) + (size_t)R * a.g.d + R + 8);
   opt_in_smem(k_extend<R, NU>, sm);
-  k_extend<R, NU><<<(unsigned)tiles, kExtendThreads, sm, s>>>(a);
+  launch_pdl(k_extend<R, NU>, dim3((unsigned)tiles), dim3(kExtendThreads), sm, s, a);
 }
 
 void launch_extend(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V,
@@ -1969,10 +1969,7 @@ void launch_select(const double* mu, const double* var, const uint32_t* visited,
   const int grid = std::max(1, std::min({ntiles, want, kMaxReduceGrid}));
 #define GTC_SELECT_CASE(M)                                                           \
   case M:                                                                            \
-    if (p.loop)                                                                      \
-      launch_pdl(k_select<M>, dim3(grid), dim3(kSelectThreads), 0, s, c, sc, p, vs, tstat, ntiles); \
-    else                                                                             \
-      k_select<M><<<grid, kSelectThreads, 0, s>>>(c, sc, p, vs, tstat, ntiles);      \
+    launch_pdl(k_select<M>, dim3(grid), dim3(kSelectThreads), 0, s, c, sc, p, vs, tstat, ntiles); \
     break;
   switch (mask) {  // launch errors surface through the caller's cudaGetLastError()
     GTC_SELECT_CASE(1)

@@ -1132,6 +1132,7 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     aa = make_append_args(r->gp.dev, kparams(r->cfg.kernel), r->cfg.noise, r->space->dev(), 0, nullptr, 0.0,
                           n0_max, nullptr, &append_smem);
     aa.loop = r->d_loop;
+    aa.stable_rows = hold ? hold_n0 : r->n;  // hold: row hold_n0 is rewritten, rows below never
     ExtendArgs ea = make_pass_args(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, n0_max,
                                    r->mu, r->var, nullptr, r->tstat);
     ea.visited = r->visited;

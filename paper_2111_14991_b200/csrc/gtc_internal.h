@@ -203,6 +203,7 @@ struct AppendArgs {
   uint32_t* visited_mark;
   int staged;
   const LoopDev* loop;  // resident loop: pos / y_new / n0 from the loop state (no-op unless valid)
+  int stable_rows;      // resident loop: rows of L that no step of the chunk changes (staged early)
 };
 
 struct ExtendArgs {

@@ -63,9 +63,11 @@ static inline void count_launch() { g_launches.fetch_add(1, std::memory_order_re
 // stream be scheduled now, then wait until every preceding kernel has
 // completed and its writes are visible.  Both are no-ops for a kernel
 // launched without the PDL attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_begin() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  pdl_trigger();
+  pdl_wait();
 }
 
 // cudaLaunchKernelEx with programmatic stream serialisation.
@@ -503,20 +505,49 @@ __device__ void gp_append_body(const AppendArgs& a) {
   const double* x_explicit = a.x_explicit;
   double y_new = a.y_new;
   int n0 = a.n0;
-  pdl_begin();
-  if (a.loop) {  // resident loop: this step's evaluation (loop_advance)
-    const LoopDev* lp = a.loop;
-    if (lp->halt != kLoopRunning || !lp->valid) return;
-    pos = lp->pos;
-    y_new = lp->y;
-    n0 = lp->n0;
-  }
   uint32_t* visited_mark = a.visited_mark;
   const int staged = a.staged;
   extern __shared__ double smem[];
   __shared__ double red[32];
   __shared__ double xnew[64];
+  __shared__ __align__(8) uint64_t pre_bar;
   const CtaSmem m = cta_smem_layout(smem, g.n_max, n0 + 1, staged != 0);
+  if (a.loop) {  // resident loop: this step's evaluation (loop_advance)
+    pdl_trigger();
+    // rows [0, stable_rows) of L do not change during the chunk: stage them
+    // while the selection that produces this step's pick drains
+    const int pre = staged ? a.stable_rows : 0;
+    const uint32_t bar = smem_u32(&pre_bar);
+    if (pre > 0 && threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      const uint32_t bytes = static_cast<uint32_t>(staged_l_doubles(pre) * 8);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+      bulk_g2s(smem_u32(m.Ls), g.L, bytes, bar);
+    }
+    pdl_wait();
+    const LoopDev* lp = a.loop;
+    const bool go = lp->halt == kLoopRunning && lp->valid;
+    pos = lp->pos;
+    y_new = lp->y;
+    n0 = lp->n0;
+    if (pre > 0) {
+      __syncthreads();  // barrier initialised before anyone waits on it
+      asm volatile(
+          "{\n"
+          ".reg .pred p;\n"
+          "WAIT_%=:\n"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+          "@!p bra WAIT_%=;\n"
+          "}\n" ::"r"(bar)
+          : "memory");
+    }
+    if (!go) return;  // (after the bulk copy landed)
+    if (staged)  // the rows appended during this chunk
+      for (int64_t i = packed(pre) + threadIdx.x; i < packed(n0); i += blockDim.x) m.Ls[i] = g.L[i];
+  } else {
+    pdl_begin();
+  }
   unsigned long long* tm = g.sc->t;
   if (threadIdx.x == 0) tm[0] = gtc_globaltimer();
   if (visited_mark && threadIdx.x == 0) visited_mark[pos >> 5] |= 1u << (pos & 31);
@@ -531,7 +562,10 @@ __device__ void gp_append_body(const AppendArgs& a) {
     g.sc->fail_row = -1;
     if (n0 == 0) g.sc->y0 = y_new;
   }
-  cta_stage_L(g, n0, m);  // includes __syncthreads
+  if (a.loop)
+    __syncthreads();  // staged above
+  else
+    cta_stage_L(g, n0, m);  // includes __syncthreads
   {
     const double* lp = lp_of(g, m);
     for (int i = threadIdx.x; i < n0; i += blockDim.x) m.rinv[i] = __drcp_rn(lp[packed(i) + i]);

@@ -15,7 +15,9 @@
 //   ref_tool enumjson <spec.json> <outdir>        # SearchSpace(params, restrictions) + EnumeratedSpace
 //   ref_tool restrict <spec.json>                 # Restriction::parse + evaluate over the grid
 //   ref_tool cachegen <function> <grid> <seed> <invalid|-> <path>   # MeasurementCache::save (JSON)
+//   ref_tool runbo_spec <spec.json> <values.f64> <strategy> <budget> <n_init> <bo_seed> <outdir>
 #include <chrono>
+#include <cmath>
 #include <cinttypes>
 #include <cstdio>
 #include <cstring>
@@ -377,6 +379,48 @@ int cmd_restrict(int argc, char** argv) {
   return 0;
 }
 
+// run_bo of the reference over a JSON-specified space (SearchSpace +
+// EnumeratedSpace) with replay values from a raw little-endian f64 file in
+// position order (NaN = runtime-invalid): the simulation-mode C1/C2 cases.
+int cmd_runbo_spec(int argc, char** argv) {
+  if (argc < 9) return 2;
+  std::ifstream f(argv[2]);
+  const nlohmann::json spec = nlohmann::json::parse(f);
+  std::vector<std::string> rs = spec.value("restrictions", std::vector<std::string>{});
+  const SearchSpace ss(params_from_json(spec), rs);
+  const EnumeratedSpace space(ss);
+  std::vector<double> values(space.size());
+  std::ifstream vf(argv[3], std::ios::binary);
+  vf.read(reinterpret_cast<char*>(values.data()), static_cast<std::streamsize>(sizeof(double) * values.size()));
+  if (!vf) throw Error("values file shorter than the space");
+  StrategyConfig config;
+  config.id = strategy_of(argv[4]);
+  config.budget = std::stoul(argv[5]);
+  config.n_init = std::stoul(argv[6]);
+  config.seed = std::stoull(argv[7]);
+  const fs::path out = argv[8];
+  std::vector<double> lambdas;
+  config.inspect = [&](std::size_t, std::size_t, std::size_t, double l) { lambdas.push_back(l); };
+  const Objective objective = [&](const Configuration& c) {
+    const double v = values[space.position_of(c.index)];
+    return std::isnan(v) ? Measurement::invalid(InvalidReason::runtime_error) : Measurement::valid(v);
+  };
+  const TuningRun run = run_bo(space, objective, config);
+  fs::create_directories(out);
+  std::vector<std::int64_t> pos;
+  std::vector<double> val;
+  for (const EvaluationRecord& r : run.records) {
+    pos.push_back(static_cast<std::int64_t>(space.position_of(r.config_index)));
+    val.push_back(r.value ? *r.value : std::numeric_limits<double>::quiet_NaN());
+  }
+  write_npy(out / "traj_pos.npy", pos, {pos.size()});
+  write_npy(out / "traj_val.npy", val, {val.size()});
+  write_npy(out / "traj_lambda.npy", lambdas, {lambdas.size()});
+  std::printf("{\"n\": %zu, \"evaluations\": %zu, \"best\": %.17g, \"surrogate\": %zu, \"warnings\": %zu}\n",
+              space.size(), run.evaluations, run.best_value, run.surrogate_size, run.warnings.size());
+  return 0;
+}
+
 int cmd_cachegen(int argc, char** argv) {
   if (argc < 7) return 2;
   const MeasurementCache cache = make_cache(argv[2], argv[3], std::stoull(argv[4]), argv[5]);
@@ -398,6 +442,7 @@ int main(int argc, char** argv) {
     else if (cmd == "gemm") rc = cmd_gemm(argc, argv);
     else if (cmd == "gp") rc = cmd_gp(argc, argv);
     else if (cmd == "runbo") rc = cmd_runbo(argc, argv);
+    else if (cmd == "runbo_spec") rc = cmd_runbo_spec(argc, argv);
     else if (cmd == "bench") rc = cmd_bench(argc, argv);
     else if (cmd == "enumjson") rc = cmd_enumjson(argc, argv);
     else if (cmd == "restrict") rc = cmd_restrict(argc, argv);

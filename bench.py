@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS) + ["c2", "c5"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS) + ["c1", "c2", "c5"])
     ap.add_argument("--n", type=int, default=220)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
@@ -247,6 +247,73 @@ def sweep(cases, strategies, reps, threads, rank, world, local):
     return dt, runs, evals, clocks.summary()
 
 
+def c1_setup(local=0):
+    import paper_2111_14991_b200 as gt
+    params, rs, invalid, minimum = GEMM
+    es = gt.SearchSpace([gt.ParameterDef(k, v) for k, v in params], rs).enumerate(device=local)
+    values = c2_values(es.n, invalid, minimum, BASE_SEED + len("gemm"))
+    return es, values
+
+
+def c1_reference(budget_s=60.0):
+    """The unmodified reference run_bo (oracle/_ref/ref_tool runbo_spec) for
+    the C1 run on one host core (the reference's own CPU-runnable case)."""
+    tool = ROOT / "oracle" / "_ref" / "ref_tool"
+    if not tool.exists():
+        return None
+    import tempfile
+    params, rs, invalid, minimum = GEMM
+    spec = {"params": [{"name": k, "kind": "numeric", "values": [float(x) for x in v]} for k, v in params],
+            "restrictions": rs}
+    with tempfile.TemporaryDirectory() as tmp:
+        tmp = pathlib.Path(tmp)
+        (tmp / "spec.json").write_text(json.dumps(spec))
+        n = json.loads(subprocess.run([str(tool), "enumjson", str(tmp / "spec.json"), str(tmp / "sp")], check=True,
+                                      capture_output=True, text=True).stdout)["n"]
+        c2_values(n, invalid, minimum, BASE_SEED + len("gemm")).astype("<f8").tofile(tmp / "values.f64")
+        t0 = time.perf_counter()
+        subprocess.run([str(tool), "runbo_spec", str(tmp / "spec.json"), str(tmp / "values.f64"), "bo-ei", "220", "20",
+                        str(BASE_SEED), str(tmp / "run")], check=True, capture_output=True, timeout=budget_s * 20)
+        t = time.perf_counter() - t0
+    return {"value": 1.0 / t, "unit": "runs/s", "cores": 1, "kind": "reference",
+            "sample": f"one reference run_bo (C1 GEMM space, 17,956 configurations, bo-ei, budget 220) took {t:.1f} s "
+                      f"on one core (ref_tool runbo_spec)"}
+
+
+def run_c1(args, rank=0, world=1, local=0):
+    """C1 (BASELINE.json configs[0]): one bo-ei run, budget 220, on the GEMM
+    simulation-mode case -- gtc_run_bo_table (device enumeration done once
+    outside the timed region; initial design + resident loop inside)."""
+    import torch
+    import paper_2111_14991_b200 as gt
+    es, values = c1_setup(local)
+    cfg = lambda r: gt.StrategyConfig(id=gt.StrategyId.bo_ei, seed=BASE_SEED + r, budget=220, n_init=20)  # noqa: E731
+    for r in range(max(3, args.warmup)):
+        gt.run_bo(es, es.ids, cfg(1000 + r), values=values)
+    torch.cuda.synchronize()
+    k = max(1, min(args.steps, 50))
+    ts = []
+    with ClockSampler(local) as clocks:
+        for r in range(k):
+            t0 = time.perf_counter()
+            run = gt.run_bo(es, es.ids, cfg(r), values=values)
+            ts.append(time.perf_counter() - t0)
+    if rank != 0:
+        return
+    dt = float(np.sum(ts))
+    print(json.dumps({
+        "metric": "BO runs/sec (C1: GEMM simulation mode, bo-ei, budget 220, one run at a time)", "value": k / dt,
+        "unit": "runs/s", "n_gpus": 1, "steps": k, "warmup": max(3, args.warmup), "ms_per_step": 1e3 * dt / k,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic measurements over the device-enumerated GEMM space (17,956 of 82,944 configurations)",
+        "config": {"workload": "C1 GEMM, bo-ei, contextual variance, n_init 20, budget 220", "runs": k,
+                   "timing": "wall clock of gtc_run_bo_table per run (initial design, fit, 200 resident iterations, "
+                             "records D2H)", "median_ms": 1e3 * float(np.median(ts))},
+        "e2e": {"value": k / dt, "unit": "runs/s", "h2d_bytes_per_step": 8 * es.n, "d2h_bytes_per_step": 32 * 200},
+        "evaluations": int(run.evaluations), "clocks": clocks.summary(),
+        "cpu_baseline": None if args.no_cpu_baseline else c1_reference()}))
+
+
 def run_c2(args, rank=0, world=1, local=0):
     """C2 throughput: 35 repeats of each case as independent runs driven by a
     host thread pool (run_experiment's model, observe groups); runs/s."""
@@ -408,11 +475,11 @@ def run_sharded(args, cfg, rank, world, local):
 
 def main():
     args = parse()
-    if args.config in ("c2", "c5"):
+    if args.config in ("c1", "c2", "c5"):
         if args.impl == "reference":
             rank, _, _ = dist_env()
             if rank == 0:
-                ref = c2_reference()
+                ref = c1_reference() if args.config == "c1" else c2_reference()
                 print(json.dumps({"impl": "reference", "metric": f"BO runs/sec ({args.config.upper()})",
                                   "value": ref["value"], "unit": "runs/s", "higher_is_better": True,
                                   "n_gpus": args.gpus, "cpu_baseline": ref,
@@ -425,7 +492,7 @@ def main():
         if world > 1:
             import torch.distributed as dist
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        (run_c2 if args.config == "c2" else run_c5)(args, rank, world, local)
+        {"c1": run_c1, "c2": run_c2, "c5": run_c5}[args.config](args, rank, world, local)
         if world > 1:
             torch.distributed.destroy_process_group()
         return

@@ -282,6 +282,7 @@ class DeviceSurrogate : public ArgmaxSource {
   void set_values(const double* values) { check(gtc_run_set_values(run_.get(), values, static_cast<std::int64_t>(space_.size()))); }
 
   void detach_group() { check(gtc_run_set_group(run_.get(), nullptr)); }
+  void set_portfolio(const gtc_portfolio_config& c) { check(gtc_run_set_portfolio(run_.get(), &c)); }
 
   /// Up to k resident iterations of a single-AF loop (gtc_run_steps).
   std::vector<gtc_step_record> steps(const gtc_select_args& a, std::size_t k) {
@@ -384,9 +385,15 @@ inline TuningRun run_bo(const EnumeratedSpace& space, const Objective& objective
     return a;
   };
 
-  const bool resident = single && table && !config.inspect && resident_loop_enabled();
+  const bool resident = table && !config.inspect && resident_loop_enabled();
   if (resident) {
     gp.set_values(table);
+    if (portfolio) {  // Portfolio::suggest/record run on the device (gtc_run_set_portfolio)
+      const gtc_portfolio_config pc{config.id == StrategyId::bo_multi ? GTC_PORTFOLIO_MULTI : GTC_PORTFOLIO_ADVANCED,
+                                    portfolio->config().skip_threshold, portfolio->config().discount,
+                                    portfolio->config().required_improvement};
+      gp.set_portfolio(pc);
+    }
     // a resident run never takes part in observe rounds (gtc_run_bo_batch):
     // it runs on its own stream and must not hold up the group's members
     gp.detach_group();

@@ -213,8 +213,9 @@ int gtc_observe(gtc_run* run, int64_t position, double y_raw, int32_t valid,
 /* The objective of a simulation-mode run is a replay table (values[pos], NaN =
  * runtime-invalid; cache.hpp:246-257).  gtc_run_set_values copies it to the
  * device (n == gtc_space_size); gtc_run_steps then runs up to k iterations of
- * a single-acquisition BO loop (bo-ei / bo-poi / bo-lcb: strategies.hpp:401-449
- * with best_candidate, portfolio.hpp:32-61) without host round trips: each
+ * the BO loop (strategies.hpp:401-449: best_candidate, portfolio.hpp:32-61, for
+ * bo-ei / bo-poi / bo-lcb; the portfolio below for bo-multi /
+ * bo-advanced-multi) without host round trips: each
  * step selects (args: exactly one AF bit, no exclusions; f_best_raw = the
  * current best valid observation), evaluates the table, marks the pick
  * visited and, when valid, appends it (bordered row + predictive pass).
@@ -232,7 +233,25 @@ typedef struct {
   double lambda;       /* exploration factor of the selection that picked it */
   int32_t valid;
   int32_t cv_fallback; /* 1: contextual variance undefined, constant used */
+  int32_t by;          /* GTC_AF_* that produced the pick */
+  int32_t pad;
 } gtc_step_record;
+/* Portfolio of a multi / advanced-multi run (PortfolioConfig, portfolio.hpp:65-71;
+ * order ei, poi, lcb).  gtc_run_set_portfolio starts a fresh portfolio (NULL or
+ * mode NONE: single AF); gtc_run_steps then runs Portfolio::suggest/record
+ * (portfolio.hpp:130-309) on the device every step, args->af_mask ignored, and
+ * keeps the portfolio state across calls.  Invalid results are recorded as the
+ * median of the model's training values (= the run's valid observations). */
+#define GTC_PORTFOLIO_NONE 0
+#define GTC_PORTFOLIO_MULTI 1
+#define GTC_PORTFOLIO_ADVANCED 2
+typedef struct {
+  int32_t mode;
+  int32_t skip_threshold;
+  double discount;
+  double required_improvement;
+} gtc_portfolio_config;
+int gtc_run_set_portfolio(gtc_run* run, const gtc_portfolio_config* config);
 #define GTC_STEPS_HOLD_N 1
 #define GTC_STEPS_TIMING 2 /* record CUDA events around each step's phases */
 int gtc_run_set_values(gtc_run* run, const double* values, int64_t n);

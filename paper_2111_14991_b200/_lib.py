@@ -53,7 +53,12 @@ class gtc_select_result(C.Structure):
 
 class gtc_step_record(C.Structure):
     _fields_ = [("position", C.c_int64), ("value", C.c_double), ("lambda_", C.c_double),
-                ("valid", C.c_int32), ("cv_fallback", C.c_int32)]
+                ("valid", C.c_int32), ("cv_fallback", C.c_int32), ("by", C.c_int32), ("pad", C.c_int32)]
+
+
+class gtc_portfolio_config(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("skip_threshold", C.c_int32), ("discount", C.c_double),
+                ("required_improvement", C.c_double)]
 
 
 GTC_STEPS_HOLD_N = 1
@@ -134,6 +139,7 @@ SIGNATURES = [
     ("gtc_observe", C.c_int, [P, C.c_int64, C.c_double, C.c_int32, C.POINTER(gtc_select_args),
                               C.POINTER(gtc_select_result), C.POINTER(gtc_fit_info)]),
     ("gtc_run_set_values", C.c_int, [P, DP, C.c_int64]),
+    ("gtc_run_set_portfolio", C.c_int, [P, C.POINTER(gtc_portfolio_config)]),
     ("gtc_run_steps", C.c_int, [P, C.POINTER(gtc_select_args), C.c_int32, C.c_int32,
                                 C.POINTER(gtc_step_record), C.POINTER(C.c_int32), C.POINTER(gtc_fit_info)]),
     ("gtc_last_steps_ms", C.c_double, [P]),

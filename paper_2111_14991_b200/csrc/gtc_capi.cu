@@ -286,6 +286,9 @@ struct gtc_run {
   StepRec* d_rec = nullptr;
   int rec_cap = 0;
   std::vector<cudaEvent_t> step_events;  // GTC_STEPS_TIMING: 3 per step + 1
+  PortDev port{};                        // portfolio state between gtc_run_steps calls (mode 0: none)
+  std::vector<double> sorted_host;
+  double* d_sorted_y = nullptr;          // [n_max] sorted valid observations (portfolio median)
   int timed_steps = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;          // last predictive pass
   cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;  // last gtc_observe device span
@@ -638,6 +641,7 @@ extern "C" int gtc_run_destroy(gtc_run* r) {
   cudaFree(r->d_values);
   cudaFree(r->d_loop);
   cudaFree(r->d_rec);
+  cudaFree(r->d_sorted_y);
   if (r->h_loop) cudaFreeHost(r->h_loop);
   for (cudaEvent_t ev : r->step_events) cudaEventDestroy(ev);
   if (r->h_xnew) cudaFreeHost(r->h_xnew);
@@ -719,6 +723,7 @@ extern "C" int gtc_run_reset(gtc_run* r, const gtc_model_config* cfg) {
   r->shard_offset = 0;
   r->group = nullptr;
   r->has_values = false;
+  r->port = PortDev{};
   r->pass_timed = r->step_timed = r->step_appended = false;
   return GTC_OK;
 }
@@ -1026,6 +1031,27 @@ static int enqueue_selection(gtc_run* r, const gtc_select_args* a, bool global_t
 
 // =============================================================== resident loop
 
+extern "C" int gtc_run_set_portfolio(gtc_run* r, const gtc_portfolio_config* c) {
+  if (!r) return fail(GTC_ERR_INVALID, "run is null");
+  r->port = PortDev{};
+  if (!c || c->mode == GTC_PORTFOLIO_NONE) return GTC_OK;
+  if (c->mode != GTC_PORTFOLIO_MULTI && c->mode != GTC_PORTFOLIO_ADVANCED)
+    return fail(GTC_ERR_CONFIG, "unknown portfolio mode");
+  // PortfolioConfig checks (portfolio.hpp:101-110)
+  if (c->skip_threshold < 1) return fail(GTC_ERR_CONFIG, "skip threshold must be >= 1");
+  if (!(c->discount > 0.0 && c->discount < 1.0)) return fail(GTC_ERR_CONFIG, "discount factor must be in (0,1)");
+  if (!(c->required_improvement > 0.0)) return fail(GTC_ERR_CONFIG, "required improvement factor must be positive");
+  r->port.mode = c->mode;
+  r->port.skip_threshold = c->skip_threshold;
+  r->port.discount = c->discount;
+  r->port.rho = c->required_improvement;
+  for (int a = 0; a < 3; ++a) {
+    r->port.active[a] = 1;
+    r->port.last_sug[a] = -1;
+  }
+  return GTC_OK;
+}
+
 extern "C" int gtc_run_set_values(gtc_run* r, const double* values, int64_t n) {
   if (!r || !values) return fail(GTC_ERR_INVALID, "null argument");
   if (n != r->space->n) return fail(GTC_ERR_INVALID, "value table size != space size");
@@ -1065,8 +1091,12 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
                              gtc_step_record* records, int32_t* done, gtc_fit_info* info) {
   if (!r || !a || !done || (k > 0 && !records)) return fail(GTC_ERR_INVALID, "null argument");
   *done = 0;
-  const uint32_t mask = a->af_mask & 7u;
-  if (mask == 0 || (mask & (mask - 1)) != 0) return fail(GTC_ERR_INVALID, "gtc_run_steps needs exactly one acquisition function");
+  const bool portfolio = r->port.mode != 0;
+  // a portfolio consults every function's argmax: the selection computes all three
+  const uint32_t mask = portfolio ? 7u : a->af_mask & 7u;
+  if (!portfolio && (mask == 0 || (mask & (mask - 1)) != 0))
+    return fail(GTC_ERR_INVALID, "gtc_run_steps needs exactly one acquisition function (or a portfolio)");
+  if (portfolio && (flags & GTC_STEPS_HOLD_N)) return fail(GTC_ERR_INVALID, "hold mode is single-AF only");
   if (a->n_excluded > 0) return fail(GTC_ERR_INVALID, "gtc_run_steps takes no exclusions");
   if (!r->has_values) return fail(GTC_ERR_INVALID, "no value table (gtc_run_set_values)");
   if (r->n < 1) return fail(GTC_ERR_INVALID, "gtc_run_steps needs a fitted model (n >= 1)");
@@ -1086,6 +1116,7 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     if ((rc = dalloc(&r->d_loop, 1))) return rc;
     GTC_CUDA(cudaMallocHost(&r->h_loop, sizeof(LoopDev)));
   }
+  if (portfolio && !r->d_sorted_y && (rc = dalloc(&r->d_sorted_y, (size_t)r->cfg.n_max))) return rc;
   int af = 0;
   while (!((mask >> af) & 1u)) ++af;
   const int hold_n0 = r->n;  // hold: every valid step appends at this row
@@ -1122,6 +1153,16 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     L.sc = r->gp.dev.sc;
     L.sel = r->red.sel;
     L.rec = r->d_rec;
+    L.port = r->port;
+    if (portfolio) {  // the valid observations = the model's training values, sorted (median)
+      std::vector<double>& ys = r->sorted_host;
+      ys.assign(r->y_host.begin(), r->y_host.end());
+      std::sort(ys.begin(), ys.end());
+      GTC_CUDA(cudaMemcpyAsync(r->d_sorted_y, ys.data(), sizeof(double) * ys.size(), cudaMemcpyHostToDevice,
+                               r->stream));
+      L.sorted_y = r->d_sorted_y;
+      L.n_sorted = (int32_t)ys.size();
+    }
     GTC_CUDA(cudaMemcpyAsync(r->d_loop, r->h_loop, sizeof(LoopDev), cudaMemcpyHostToDevice, r->stream));
     SelectParams p{mask, a->lambda_mode, a->lambda_constant, a->cv_initial_sample_mean, a->cv_initial_mean_variance,
                    f_best, nullptr, 0, -1, 0, r->d_loop};
@@ -1177,6 +1218,7 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     replay_steps(r, reinterpret_cast<const StepRec*>(records + *done), steps, hold, hold_n0, &hold_prev);
     *done += steps;
     r->acc_gen = L.gen;
+    r->port = L.port;
     f_best = L.f_best;
     if (L.halt == kLoopPivot) {
       // the last step's bordered row failed (its observation is in the host

@@ -338,8 +338,26 @@ struct StepRec {  // == gtc_step_record
   double lambda;    // exploration factor of the selection that picked it
   int32_t valid;
   int32_t cv_fallback;
+  int32_t by;       // acquisition function that produced the pick
+  int32_t pad;
 };
 enum : int32_t { kLoopRunning = 0, kLoopNoCandidates = 1, kLoopPivot = 2, kLoopCapacity = 3 };
+
+// Portfolio state of a multi / advanced-multi run (portfolio.hpp:65-316),
+// slots in the fixed order ei, poi, lcb (PortfolioConfig::order).
+struct PortDev {
+  int32_t mode;            // 0 single AF, 1 multi, 2 advanced multi
+  int32_t skip_threshold;
+  double discount;
+  double rho;              // required improvement
+  int32_t active[3];
+  int32_t duplicates[3];
+  int32_t above[3];
+  int32_t below[3];
+  double dos[3];           // discounted observation scores
+  int64_t last_sug[3];     // most recent suggestion (position; -1 none)
+  int64_t cursor;          // rotation cursor
+};
 struct LoopDev {
   int64_t pos;        // this step's pick
   double y;           // its value
@@ -367,6 +385,10 @@ struct LoopDev {
   const GpScalars* sc;
   const SelectDev* sel;
   StepRec* rec;
+  PortDev port;
+  double* sorted_y;   // valid observations in ascending order (portfolio median), capacity n_max
+  int32_t n_sorted;
+  int32_t pad2;
 };
 // Loop-mode launches of the bordered append / single-row pass (args.loop set;
 // smem / args.n0 sized for the largest row of the chunk).

@@ -1138,19 +1138,128 @@ __device__ __forceinline__ SelPart sel_warp_reduce(SelPart v) {
 // loop state -- the host bookkeeping of gtc_observe (visited mark, candidate
 // count, first eligible position, f_best; RunContext::evaluate,
 // strategies.hpp:159-232) done on the device.
+// Portfolio::next_in_rotation (portfolio.hpp:182-189).
+__device__ int port_next(PortDev& P) {
+  for (int step = 0; step < 3; ++step) {
+    const int a = (int)(P.cursor % 3);
+    ++P.cursor;
+    if (P.active[a]) return a;
+  }
+  return -1;
+}
+
+// Portfolio::suggest (portfolio.hpp:130-134, suggest_multi :191-218 with
+// resolve_duplicates :222-236, suggest_advanced :238-256; the pending set
+// is always empty inside run_bo) on the selection's per-AF argmaxes.
+__device__ int64_t port_suggest(PortDev& P, const SelectDev* sel, int* by) {
+  if (P.mode == 2) {
+    const int c = port_next(P);
+    *by = c;
+    P.last_sug[c] = sel->position[c];
+    return sel->position[c];
+  }
+  int64_t pick[3];
+  for (int a = 0; a < 3; ++a) {
+    pick[a] = sel->position[a];
+    if (P.active[a]) P.last_sug[a] = pick[a];
+  }
+  const int c = port_next(P);
+  *by = c;
+  const int64_t chosen = pick[c];
+  bool conflict[3] = {false, false, false};
+  bool any = false;
+  for (int a = 0; a < 3; ++a)
+    if (P.active[a] && a != c && P.last_sug[a] == chosen) conflict[a] = any = true;
+  if (any) {
+    ++P.duplicates[c];
+    for (int a = 0; a < 3; ++a)
+      if (conflict[a]) ++P.duplicates[a];
+    conflict[c] = true;
+    bool over = false;
+    for (int a = 0; a < 3; ++a) over |= conflict[a] && P.duplicates[a] > P.skip_threshold;
+    if (over) {  // keep the lowest discounted observation score (earliest on ties)
+      int keep = -1;
+      for (int a = 0; a < 3; ++a)
+        if (P.active[a] && conflict[a] && (keep < 0 || P.dos[a] < P.dos[keep])) keep = a;
+      for (int a = 0; a < 3; ++a)
+        if (conflict[a]) {
+          P.duplicates[a] = 0;
+          if (a != keep) P.active[a] = 0;
+        }
+    }
+  }
+  return chosen;
+}
+
+// Portfolio::update_bands (portfolio.hpp:259-299).
+__device__ void port_update_bands(PortDev& P, int p) {
+  if (!P.active[p]) return;
+  double mean = 0.0;
+  int n = 0;
+  for (int a = 0; a < 3; ++a)
+    if (P.active[a]) {
+      mean = __dadd_rn(mean, P.dos[a]);
+      ++n;
+    }
+  mean = __ddiv_rn(mean, (double)n);
+  if (P.dos[p] > __dmul_rn(__dadd_rn(1.0, P.rho), mean))
+    ++P.above[p];
+  else if (P.dos[p] < __dmul_rn(__dadd_rn(1.0, -P.rho), mean))
+    ++P.below[p];
+  if (P.below[p] >= P.skip_threshold && n > 1) {
+    for (int a = 0; a < 3; ++a) {
+      if (a != p) P.active[a] = 0;
+      P.above[a] = 0;
+      P.below[a] = 0;
+    }
+    return;
+  }
+  if (P.above[p] >= P.skip_threshold && n > 1) {
+    P.active[p] = 0;
+    P.above[p] = 0;
+    P.below[p] = 0;
+    for (int a = 0; a < 3; ++a)
+      if (P.active[a]) {
+        P.above[a] = 0;
+        P.below[a] = 0;
+      }
+  }
+}
+
 __device__ void loop_advance(LoopDev* L, const SelectDev* sel) {
   if (sel->n_candidates <= 0) {
     L->halt = kLoopNoCandidates;
     return;
   }
-  const int64_t pos = sel->position[L->af];
+  PortDev& P = L->port;
+  int by = L->af;
+  const int64_t pos = P.mode != 0 ? port_suggest(P, sel, &by) : sel->position[L->af];
   const double y = L->table[pos];
   const int valid = y == y;
   if (valid && !L->hold && L->n >= L->n_max) {
     L->halt = kLoopCapacity;
     return;
   }
-  L->rec[L->step] = StepRec{pos, y, sel->lambda, valid, sel->cv_fallback};
+  if (P.mode != 0) {
+    // Portfolio::record (portfolio.hpp:140-150): invalid -> median of the valid observations
+    double observed = y;
+    if (!valid) {  // (n_sorted >= 1: the loop starts from a fitted model of the valid observations)
+      const int m = L->n_sorted;
+      observed = (m & 1) ? L->sorted_y[m / 2]
+                         : __dmul_rn(0.5, __dadd_rn(L->sorted_y[m / 2 - 1], L->sorted_y[m / 2]));
+    }
+    P.dos[by] = __dadd_rn(__dmul_rn(P.dos[by], P.discount), observed);
+    if (P.mode == 2) port_update_bands(P, by);
+    if (valid) {  // keep the valid observations sorted (insertion)
+      int i = L->n_sorted++;
+      while (i > 0 && L->sorted_y[i - 1] > y) {
+        L->sorted_y[i] = L->sorted_y[i - 1];
+        --i;
+      }
+      L->sorted_y[i] = y;
+    }
+  }
+  L->rec[L->step] = StepRec{pos, y, sel->lambda, valid, sel->cv_fallback, by, 0};
   ++L->step;
   L->pos = pos;
   L->y = y;

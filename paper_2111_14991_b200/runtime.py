@@ -204,6 +204,12 @@ class SurrogateRun:
         v = np.ascontiguousarray(np.asarray(values, dtype=np.float64))
         check(load().gtc_run_set_values(self._h, _lib.dptr(v), len(v)))
 
+    def set_portfolio(self, mode: int, skip_threshold: int = 5, discount: float = 0.65,
+                      required_improvement: float = 0.1) -> None:
+        """gtc_run_set_portfolio: 0 single AF, 1 multi, 2 advanced multi (fresh state)."""
+        c = _lib.gtc_portfolio_config(int(mode), int(skip_threshold), float(discount), float(required_improvement))
+        check(load().gtc_run_set_portfolio(self._h, C.byref(c)))
+
     def steps(self, af: AcquisitionId, k: int, f_best_raw: float,
               exploration: ExplorationConfig = ExplorationConfig(),
               cv_state: ContextualVarianceState = ContextualVarianceState(), hold: bool = False,

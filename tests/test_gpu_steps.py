@@ -141,10 +141,12 @@ def test_steps_hold_equals_rollback_loop(gt):
 @pytest.mark.parametrize("variant", ["cv", "const", "free_invalid", "nu52"])
 def test_run_bo_resident_equals_observe_loop(gt, monkeypatch, variant):
     """gtc_run_bo_table with the resident loop == the per-iteration gtc_observe
-    loop (GTC_RESIDENT_LOOP=0), every single-AF strategy."""
+    loop (GTC_RESIDENT_LOOP=0), every BO strategy (the portfolio of bo-multi /
+    bo-advanced-multi on the device vs the host Portfolio)."""
     coords, ids, values = synthetic.random_rough([12, 10, 8], 7, 0.3)
     space = gt.Space(coords)
-    for sid in (gt.StrategyId.bo_ei, gt.StrategyId.bo_poi, gt.StrategyId.bo_lcb):
+    for sid in (gt.StrategyId.bo_ei, gt.StrategyId.bo_poi, gt.StrategyId.bo_lcb, gt.StrategyId.bo_multi,
+                gt.StrategyId.bo_advanced_multi):
         cfg = gt.StrategyConfig(id=sid, seed=5 + int(sid), budget=120, n_init=10)
         if variant == "const":
             cfg.exploration = gt.ExplorationConfig(gt.ExplorationConfig.Mode.constant, 0.05)
@@ -169,7 +171,8 @@ def test_batch_resident_equals_groups(gt, monkeypatch):
     coords, ids, values = synthetic.random_rough([12, 10, 8], 13, 0.3)
     space = gt.Space(coords)
     cfgs = [gt.StrategyConfig(id=sid, seed=seed, budget=80, n_init=10)
-            for sid in (gt.StrategyId.bo_ei, gt.StrategyId.bo_multi, gt.StrategyId.bo_poi, gt.StrategyId.bo_lcb)
+            for sid in (gt.StrategyId.bo_ei, gt.StrategyId.bo_multi, gt.StrategyId.bo_poi, gt.StrategyId.bo_lcb,
+                        gt.StrategyId.bo_advanced_multi)
             for seed in (1, 2, 3, 4)]
     monkeypatch.setenv("GTC_BATCH_RESIDENT", "0")
     a = gt.run_bo_batch(space, ids, cfgs, values, threads=8)
@@ -178,3 +181,21 @@ def test_batch_resident_equals_groups(gt, monkeypatch):
     for x, y in zip(a, b):
         np.testing.assert_array_equal(x.positions, y.positions)
         np.testing.assert_array_equal(x.lambdas, y.lambdas)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_portfolio_skips_and_promotions(gt, monkeypatch, mode):
+    """Long portfolio runs whose duplicate counters / bands fire (small skip
+    threshold): the device portfolio deactivates and promotes exactly like the
+    host Portfolio (portfolio.hpp:191-299)."""
+    coords, ids, values = synthetic.random_rough([10, 10, 8, 6], 17, 0.25)
+    space = gt.Space(coords)
+    sid = gt.StrategyId.bo_multi if mode == 1 else gt.StrategyId.bo_advanced_multi
+    for seed, skip in ((1, 1), (2, 2), (3, 5)):
+        cfg = gt.StrategyConfig(id=sid, seed=seed, budget=200, n_init=15, skip_threshold=skip)
+        monkeypatch.setenv("GTC_RESIDENT_LOOP", "0")
+        a = gt.run_bo(space, ids, cfg, values=values)
+        monkeypatch.setenv("GTC_RESIDENT_LOOP", "1")
+        b = gt.run_bo(space, ids, cfg, values=values)
+        np.testing.assert_array_equal(a.positions, b.positions)
+        np.testing.assert_array_equal(a.lambdas, b.lambdas)

@@ -189,7 +189,11 @@ class DeviceSurrogate : public ArgmaxSource {
         rc.n_max = n_max;
       }
     }
-    if (gtc_group* g = thread_observe_group()) check(gtc_run_set_group(run_.get(), g));
+    if (gtc_group* g = thread_observe_group()) {
+      check(gtc_run_set_group(run_.get(), g));
+      // a batch worker's run shares the device with many concurrent runs
+      check(gtc_run_set_pdl(run_.get(), 0));
+    }
   }
 
   /// Per-thread reusable run handle (enabled by gtc_run_bo_batch's workers).

@@ -252,6 +252,12 @@ typedef struct {
   double required_improvement;
 } gtc_portfolio_config;
 int gtc_run_set_portfolio(gtc_run* run, const gtc_portfolio_config* config);
+/* Programmatic dependent launch between the run's kernels (default on): the
+ * next kernel is scheduled while the current one drains.  Turn it off for runs
+ * that share a device with many concurrently driven runs (gtc_run_bo_batch
+ * does), where early-scheduled waiting blocks would take SM slots from the
+ * other runs' streams.  Results are identical either way. */
+int gtc_run_set_pdl(gtc_run* run, int32_t enable);
 #define GTC_STEPS_HOLD_N 1
 #define GTC_STEPS_TIMING 2 /* record CUDA events around each step's phases */
 int gtc_run_set_values(gtc_run* run, const double* values, int64_t n);

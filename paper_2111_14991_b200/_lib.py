@@ -140,6 +140,7 @@ SIGNATURES = [
                               C.POINTER(gtc_select_result), C.POINTER(gtc_fit_info)]),
     ("gtc_run_set_values", C.c_int, [P, DP, C.c_int64]),
     ("gtc_run_set_portfolio", C.c_int, [P, C.POINTER(gtc_portfolio_config)]),
+    ("gtc_run_set_pdl", C.c_int, [P, C.c_int32]),
     ("gtc_run_steps", C.c_int, [P, C.POINTER(gtc_select_args), C.c_int32, C.c_int32,
                                 C.POINTER(gtc_step_record), C.POINTER(C.c_int32), C.POINTER(gtc_fit_info)]),
     ("gtc_last_steps_ms", C.c_double, [P]),

@@ -286,6 +286,7 @@ struct gtc_run {
   StepRec* d_rec = nullptr;
   int rec_cap = 0;
   std::vector<cudaEvent_t> step_events;  // GTC_STEPS_TIMING: 3 per step + 1
+  bool pdl = true;                       // programmatic dependent launch (gtc_run_set_pdl)
   PortDev port{};                        // portfolio state between gtc_run_steps calls (mode 0: none)
   std::vector<double> sorted_host;
   double* d_sorted_y = nullptr;          // [n_max] sorted valid observations (portfolio median)
@@ -1031,6 +1032,12 @@ static int enqueue_selection(gtc_run* r, const gtc_select_args* a, bool global_t
 
 // =============================================================== resident loop
 
+extern "C" int gtc_run_set_pdl(gtc_run* r, int32_t enable) {
+  if (!r) return fail(GTC_ERR_INVALID, "run is null");
+  r->pdl = enable != 0;
+  return GTC_OK;
+}
+
 extern "C" int gtc_run_set_portfolio(gtc_run* r, const gtc_portfolio_config* c) {
   if (!r) return fail(GTC_ERR_INVALID, "run is null");
   r->port = PortDev{};
@@ -1104,6 +1111,7 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
   if (hold && r->n >= r->cfg.n_max) return fail(GTC_ERR_CAPACITY, "more observations than the run's n_max");
   if (k <= 0) return GTC_OK;
   GTC_CUDA(cudaSetDevice(r->space->device));
+  set_thread_pdl(r->pdl);
   int rc;
   if (k > r->rec_cap) {
     cudaFree(r->d_rec);
@@ -1432,6 +1440,7 @@ static void observe_prepare(ObserveReq& q) {
 static int observe_device(ObserveReq& q, gtc_fit_info* info) {
   gtc_run* r = q.r;
   int rc;
+  set_thread_pdl(r->pdl);
   const bool ev = phase_events();
   if (ev) GTC_CUDA(cudaEventRecord(r->ev_step0, r->stream));
   if (q.valid) {

@@ -395,6 +395,9 @@ struct LoopDev {
 void launch_gp_append_loop(const AppendArgs& a, int nu, size_t smem, cudaStream_t stream);
 void launch_extend_loop(const ExtendArgs& a, int64_t tiles, int nu, cudaStream_t stream);
 
+// Programmatic dependent launch for this host thread's subsequent launches.
+void set_thread_pdl(bool on);
+
 int reduce_blocks(int64_t n);  // grid size used by the reduction kernels
 uint64_t launches();
 

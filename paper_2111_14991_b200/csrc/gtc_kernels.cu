@@ -70,10 +70,20 @@ __device__ __forceinline__ void pdl_begin() {
   pdl_wait();
 }
 
+// Per host thread: whether launch_pdl sets the PDL attribute (gtc_run_set_pdl;
+// off for runs that share the device with many concurrent streams, where
+// early-launched waiting CTAs would take SM slots from the other streams).
+static thread_local bool t_pdl = true;
+void set_thread_pdl(bool on) { t_pdl = on; }
+
 // cudaLaunchKernelEx with programmatic stream serialisation.
 template <typename... KArgs, typename... Args>
 static void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                        Args&&... args) {
+  if (!t_pdl) {
+    kernel<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+    return;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;

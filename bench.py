@@ -225,7 +225,10 @@ def sweep(cases, strategies, reps, threads, rank, world, local):
         keys = [(sid, r) for sid in strategies for r in range(reps)]
         mine = [gt.StrategyConfig(id=sid, seed=BASE_SEED + r, budget=220, n_init=20)
                 for i, (sid, r) in enumerate(keys) if i % world == rank]
-        gt.run_bo_batch(es, es.ids, mine[:2], values, threads=2)  # warm-up
+        # warm-up with as many concurrent runs as the timed sweep drives: the
+        # space's pool of idle run handles (gtc_run_acquire) is then populated
+        nw = max(1, min(threads, len(mine), host_threads))
+        gt.run_bo_batch(es, es.ids, mine[:nw], values, threads=nw)
         prepared.append((es, values, mine))
     torch.cuda.synchronize()
     if world > 1:

@@ -173,39 +173,16 @@ class DeviceSurrogate : public ArgmaxSource {
                   std::size_t n_max)
       : space_(space) {
     const gtc_model_config cfg{kernel.c(), noise, jitter, static_cast<std::int32_t>(n_max)};
-    // a worker thread of gtc_run_bo_batch keeps its last run handle and resets
-    // it for the next run on the same space and capacity
-    RunCache& rc = thread_run_cache();
-    if (rc.enabled && rc.run && rc.space == space.device_space() && rc.n_max == n_max &&
-        gtc_run_reset(rc.run.get(), &cfg) == GTC_OK) {
-      run_ = rc.run;
-    } else {
-      gtc_run* r = nullptr;
-      check(gtc_run_create(space.device_space(), &cfg, &r));
-      run_.reset(r, [](gtc_run* p) { gtc_run_destroy(p); });
-      if (rc.enabled) {
-        rc.run = run_;
-        rc.space = space.device_space();
-        rc.n_max = n_max;
-      }
-    }
+    // run handles come from the space's pool of idle runs (gtc_run_acquire /
+    // gtc_run_release): a sweep allocates device memory once per concurrent run
+    gtc_run* r = nullptr;
+    check(gtc_run_acquire(space.device_space(), &cfg, &r));
+    run_.reset(r, [](gtc_run* p) { gtc_run_release(p); });
     if (gtc_group* g = thread_observe_group()) {
       check(gtc_run_set_group(run_.get(), g));
       // a batch worker's run shares the device with many concurrent runs
       check(gtc_run_set_pdl(run_.get(), 0));
     }
-  }
-
-  /// Per-thread reusable run handle (enabled by gtc_run_bo_batch's workers).
-  struct RunCache {
-    bool enabled = false;
-    std::shared_ptr<gtc_run> run;
-    gtc_space* space = nullptr;
-    std::size_t n_max = 0;
-  };
-  static RunCache& thread_run_cache() {
-    static thread_local RunCache c;
-    return c;
   }
 
   /// Membership of the run's observe group for the BO loop: a thread that

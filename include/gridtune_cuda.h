@@ -173,6 +173,13 @@ int gtc_run_create(gtc_space* space, const gtc_model_config* config, gtc_run** o
  * allocations: a worker that runs many BO runs reuses one run handle instead
  * of a create/destroy pair (cudaFree synchronises the whole device). */
 int gtc_run_reset(gtc_run* run, const gtc_model_config* config);
+/* Pool of idle runs per space: gtc_run_acquire returns a reset idle run of the
+ * same n_max (else a new one); gtc_run_release waits for the run's stream and
+ * returns it to the pool.  gtc_space_destroy destroys the pooled runs, so
+ * sweeps of many runs allocate (and synchronise the device for) one run per
+ * concurrent worker instead of one per run. */
+int gtc_run_acquire(gtc_space* space, const gtc_model_config* config, gtc_run** out);
+int gtc_run_release(gtc_run* run);
 int gtc_run_destroy(gtc_run* run);
 
 /* GpModel::fit over candidates at `positions` (the fit_current lambda,

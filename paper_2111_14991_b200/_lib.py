@@ -129,6 +129,8 @@ SIGNATURES = [
     ("gtc_run_create", C.c_int, [P, C.POINTER(gtc_model_config), C.POINTER(P)]),
     ("gtc_run_destroy", C.c_int, [P]),
     ("gtc_run_reset", C.c_int, [P, C.POINTER(gtc_model_config)]),
+    ("gtc_run_acquire", C.c_int, [P, C.POINTER(gtc_model_config), C.POINTER(P)]),
+    ("gtc_run_release", C.c_int, [P]),
     ("gtc_fit", C.c_int, [P, I64P, DP, C.c_int32, C.POINTER(gtc_fit_info)]),
     ("gtc_append", C.c_int, [P, C.c_int64, C.c_double, C.POINTER(gtc_fit_info)]),
     ("gtc_truncate", C.c_int, [P, C.c_int32, C.POINTER(gtc_fit_info)]),

@@ -163,7 +163,6 @@ extern "C" int gtc_run_bo_batch(gtc_space* space, const std::uint64_t* ids, cons
     // later runs join for their BO loops only (run_bo's GroupMembership)
     gtc_group* group = n_groups ? groups[w % n_groups] : nullptr;
     thread_observe_group() = group;
-    DeviceSurrogate::thread_run_cache().enabled = true;  // reuse one run handle per worker
     if (group) {
       gtc_group_join(group);
       thread_group_member() = true;
@@ -176,7 +175,6 @@ extern "C" int gtc_run_bo_batch(gtc_space* space, const std::uint64_t* ids, cons
     if (group && thread_group_member()) gtc_group_leave(group);  // (a run that failed early)
     thread_group_member() = false;
     thread_observe_group() = nullptr;
-    DeviceSurrogate::thread_run_cache() = DeviceSurrogate::RunCache{};  // releases the worker's run
   };
   std::vector<std::thread> pool;
   for (int w = 1; w < workers; ++w) pool.emplace_back(worker);

@@ -226,6 +226,10 @@ struct gtc_space {
   std::vector<double> host_coords;   // row-major n x d (gathers for fit)
   std::vector<uint64_t> ids;         // canonical indices (enumerated spaces)
   uint64_t cartesian = 0;            // Cartesian size (enumerated spaces)
+  // idle run handles (gtc_run_release): reused by gtc_run_acquire, so sweeps
+  // of many runs allocate device memory once per concurrent run, not per run
+  std::mutex pool_mu;
+  std::vector<gtc_run*> pool;
   SpaceDev dev() const { return SpaceDev{coords, n, n_pad, d, cidx, ctab}; }
 };
 
@@ -377,6 +381,12 @@ extern "C" int gtc_space_create(int device, const double* coords, int64_t n, int
 
 extern "C" int gtc_space_destroy(gtc_space* s) {
   if (!s) return GTC_OK;
+  std::vector<gtc_run*> idle;
+  {
+    std::lock_guard<std::mutex> lk(s->pool_mu);
+    idle.swap(s->pool);
+  }
+  for (gtc_run* r : idle) gtc_run_destroy(r);
   cudaSetDevice(s->device);
   cudaFree(s->coords);
   cudaFree(s->cidx);
@@ -697,6 +707,42 @@ extern "C" int gtc_run_create(gtc_space* space, const gtc_model_config* cfg, gtc
   return GTC_OK;
 }
 
+extern "C" int gtc_run_acquire(gtc_space* space, const gtc_model_config* cfg, gtc_run** out) {
+  if (!out) return fail(GTC_ERR_INVALID, "out is null");
+  *out = nullptr;
+  if (!space || !cfg) return fail(GTC_ERR_INVALID, "space/config is null");
+  gtc_run* r = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(space->pool_mu);
+    for (size_t i = space->pool.size(); i-- > 0;)
+      if (space->pool[i]->cfg.n_max == cfg->n_max) {
+        r = space->pool[i];
+        space->pool.erase(space->pool.begin() + (std::ptrdiff_t)i);
+        break;
+      }
+  }
+  if (!r) return gtc_run_create(space, cfg, out);
+  const int rc = gtc_run_reset(r, cfg);
+  if (rc) {
+    gtc_run_destroy(r);
+    return rc;
+  }
+  *out = r;
+  return GTC_OK;
+}
+
+extern "C" int gtc_run_release(gtc_run* r) {
+  if (!r) return GTC_OK;
+  cudaSetDevice(r->space->device);
+  if (cudaStreamSynchronize(r->stream) != cudaSuccess) {  // not reusable
+    cudaGetLastError();
+    return gtc_run_destroy(r);
+  }
+  std::lock_guard<std::mutex> lk(r->space->pool_mu);
+  r->space->pool.push_back(r);
+  return GTC_OK;
+}
+
 extern "C" int gtc_run_reset(gtc_run* r, const gtc_model_config* cfg) {
   if (!r || !cfg) return fail(GTC_ERR_INVALID, "run/config is null");
   if (cfg->n_max != r->cfg.n_max) return fail(GTC_ERR_CONFIG, "gtc_run_reset cannot change n_max");
@@ -725,6 +771,7 @@ extern "C" int gtc_run_reset(gtc_run* r, const gtc_model_config* cfg) {
   r->group = nullptr;
   r->has_values = false;
   r->port = PortDev{};
+  r->pdl = true;
   r->pass_timed = r->step_timed = r->step_appended = false;
   return GTC_OK;
 }
@@ -1113,12 +1160,13 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
   GTC_CUDA(cudaSetDevice(r->space->device));
   set_thread_pdl(r->pdl);
   int rc;
-  if (k > r->rec_cap) {
+  if (k > r->rec_cap) {  // (cudaFree synchronises the device: grow rarely)
+    const int cap = std::max({k, r->cfg.n_max, 2 * r->rec_cap});
     cudaFree(r->d_rec);
     r->d_rec = nullptr;
     r->rec_cap = 0;
-    if ((rc = dalloc(&r->d_rec, (size_t)k))) return rc;
-    r->rec_cap = k;
+    if ((rc = dalloc(&r->d_rec, (size_t)cap))) return rc;
+    r->rec_cap = cap;
   }
   if (!r->d_loop) {
     if ((rc = dalloc(&r->d_loop, 1))) return rc;

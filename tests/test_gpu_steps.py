@@ -199,3 +199,77 @@ def test_portfolio_skips_and_promotions(gt, monkeypatch, mode):
         b = gt.run_bo(space, ids, cfg, values=values)
         np.testing.assert_array_equal(a.positions, b.positions)
         np.testing.assert_array_equal(a.lambdas, b.lambdas)
+
+
+def test_resident_jitter_escalation_equals_observe_loop(gt, monkeypatch):
+    """Duplicated configurations (identical coordinates) make bordered pivots
+    fail at a tiny jitter: the resident loop halts on the device, the host
+    refactorises with escalated jitter (gp.hpp:116-129) and continues -- same
+    trajectory as the per-iteration loop, every strategy."""
+    rng = np.random.default_rng(4)
+    base = rng.random((300, 3))
+    coords = np.repeat(base, 4, axis=0)                 # every configuration 4 times
+    ids = np.arange(len(coords), dtype=np.uint64)
+    values = 1.0 + rng.random(len(coords))
+    values[rng.random(len(coords)) < 0.1] = np.nan
+    space = gt.Space(coords)
+    for sid in (gt.StrategyId.bo_ei, gt.StrategyId.bo_multi, gt.StrategyId.bo_advanced_multi):
+        cfg = gt.StrategyConfig(id=sid, seed=3, budget=90, n_init=10, noise=0.0, jitter=1e-13)
+        monkeypatch.setenv("GTC_RESIDENT_LOOP", "0")
+        a = gt.run_bo(space, ids, cfg, values=values)
+        monkeypatch.setenv("GTC_RESIDENT_LOOP", "1")
+        b = gt.run_bo(space, ids, cfg, values=values)
+        np.testing.assert_array_equal(a.positions, b.positions)
+        np.testing.assert_array_equal(a.lambdas, b.lambdas)
+        assert a.surrogate_size == b.surrogate_size
+
+
+def test_resident_pivot_failure_refit(gt):
+    """Only duplicates of training points left as candidates: the bordered
+    pivot fails on the device, the chunk halts, the host refactorises with
+    escalated jitter and the loop continues -- same picks, posterior and
+    outcome (or the same ModelConditioningError) as the gtc_observe loop."""
+    rng = np.random.default_rng(8)
+    uniq = rng.random((40, 3))
+    coords = np.concatenate([uniq, uniq[:10]])          # positions 40..49 duplicate 0..9
+    values = 1.0 + rng.random(len(coords))
+    values[40:] = values[:10]
+
+    def make():
+        space = gt.Space(coords)
+        run = gt.SurrogateRun(space, gt.MaternKernel(gt.MaternNu.three_halves, 1.5, 1.0), 0.0, 1e-16, 64)
+        run.fit(np.arange(10), values[:10])
+        for p in range(40):                             # only the duplicates stay candidates
+            run.mark_visited(p)
+        return space, run
+
+    expl = gt.ExplorationConfig(gt.ExplorationConfig.Mode.constant, 0.01)
+    cv = gt.ContextualVarianceState()
+    f0 = float(np.min(values[:10]))
+    _, run_a = make()
+    af = gt.AcquisitionId.ei
+    picks_h, jitters, err_h = [], [], None
+    try:
+        sel = run_a.select([af], f0, expl, cv)
+        for _ in range(6):
+            p = sel.pick(af)
+            picks_h.append(p)
+            info, sel = run_a.observe(p, float(values[p]), [af], f0, expl, cv)
+            jitters.append(info.jitter)
+    except gt.ModelConditioningError as e:
+        picks_h, err_h = None, str(e)
+    assert err_h is not None or max(jitters) > 1e-16  # the escalation path ran
+    _, run_b = make()
+    run_b.set_values(values)
+    try:
+        recs = run_b.steps(gt.AcquisitionId.ei, 6, f0, expl, cv)
+        err_d = None
+    except gt.ModelConditioningError as e:
+        recs, err_d = None, str(e)
+    assert err_d == err_h
+    if err_h is None:
+        assert [r.position for r in recs] == picks_h
+        m_a, v_a = run_a.predictions()
+        m_b, v_b = run_b.predictions()
+        np.testing.assert_array_equal(m_a, m_b)
+        np.testing.assert_array_equal(v_a, v_b)

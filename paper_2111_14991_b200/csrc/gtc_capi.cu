@@ -292,6 +292,19 @@ struct gtc_run {
   std::vector<cudaEvent_t> step_events;  // GTC_STEPS_TIMING: 3 per step + 1
   bool pdl = true;                       // programmatic dependent launch (gtc_run_set_pdl)
   PortDev port{};                        // portfolio state between gtc_run_steps calls (mode 0: none)
+  // gtc_run_steps without PDL: captured iteration graphs (kSteps iterations and
+  // one iteration), reused while their launch arguments are unchanged
+  struct StepGraphs {
+    std::string key;
+    cudaGraphExec_t many = nullptr, one = nullptr;
+    bool failed = false;
+    void release() {
+      if (many) cudaGraphExecDestroy(many);
+      if (one) cudaGraphExecDestroy(one);
+      many = one = nullptr;
+      key.clear();
+    }
+  } graphs;
   std::vector<double> sorted_host;
   double* d_sorted_y = nullptr;          // [n_max] sorted valid observations (portfolio median)
   int timed_steps = 0;
@@ -655,6 +668,7 @@ extern "C" int gtc_run_destroy(gtc_run* r) {
   cudaFree(r->d_sorted_y);
   if (r->h_loop) cudaFreeHost(r->h_loop);
   for (cudaEvent_t ev : r->step_events) cudaEventDestroy(ev);
+  r->graphs.release();
   if (r->h_xnew) cudaFreeHost(r->h_xnew);
   if (r->h_rb) cudaFreeHost(r->h_rb);
   for (cudaEvent_t ev : {r->ev0, r->ev1, r->ev_step0, r->ev_step1})
@@ -1183,7 +1197,11 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     const int m = k - *done;
     if (r->space->n - r->visited_count <= 0) break;
     if ((rc = ensure_predictions(r)) || (rc = ensure_var_totals(r))) return rc;
-    const int n0_max = hold ? hold_n0 : std::min(r->n + m - 1, r->cfg.n_max - 1);
+    const bool timing = (flags & GTC_STEPS_TIMING) != 0;
+    // graph-launched chunks (see below) size for the largest row, so that one
+    // captured graph serves every chunk of the run handle
+    bool graphed = !r->pdl && !timing && !r->graphs.failed;
+    const int n0_max = hold ? hold_n0 : graphed ? r->cfg.n_max - 1 : std::min(r->n + m - 1, r->cfg.n_max - 1);
     LoopDev& L = *r->h_loop;
     L = LoopDev{};
     L.pos = -1;
@@ -1219,9 +1237,14 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
       L.sorted_y = r->d_sorted_y;
       L.n_sorted = (int32_t)ys.size();
     }
+    L.lambda_mode = a->lambda_mode;
+    L.lambda_constant = a->lambda_constant;
+    L.cv_mu_s = a->cv_initial_sample_mean;
+    L.cv_var_s = a->cv_initial_mean_variance;
     GTC_CUDA(cudaMemcpyAsync(r->d_loop, r->h_loop, sizeof(LoopDev), cudaMemcpyHostToDevice, r->stream));
-    SelectParams p{mask, a->lambda_mode, a->lambda_constant, a->cv_initial_sample_mean, a->cv_initial_mean_variance,
-                   f_best, nullptr, 0, -1, 0, r->d_loop};
+    // (every per-run / per-step selection input is read from the loop state:
+    // the launch arguments depend only on the run handle and its model config)
+    SelectParams p{mask, 0, 0.0, 0.0, 0.0, 0.0, nullptr, 0, -1, 0, r->d_loop};
     const VarSource vs = r->vsrc();
     // loop-mode launch arguments: per-step values come from the loop state
     AppendArgs aa{};
@@ -1236,7 +1259,6 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     ea.acc = r->acc;  // (generation chosen on the device)
     ea.acc_clear = r->acc + 1;
     ea.loop = r->d_loop;
-    const bool timing = (flags & GTC_STEPS_TIMING) != 0;
     if (timing) {
       while ((int)r->step_events.size() < 3 * m + 1) {
         cudaEvent_t ev;
@@ -1246,8 +1268,50 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
       r->timed_steps = 0;
     }
     cudaEvent_t* te = r->step_events.data();
+    auto launch_iteration = [&]() -> int {
+      launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, vs, r->tstat, r->red.b, r->red.sel,
+                    r->stream);
+      launch_gp_append_loop(aa, r->cfg.kernel.nu, append_smem, r->stream);
+      launch_extend_loop(ea, r->space->n_pad / kTile, r->cfg.kernel.nu, r->stream);
+      GTC_LAUNCHED();
+      return GTC_OK;
+    };
+    // Runs driven by many host threads (no PDL) are bound by the driver's
+    // launch rate: launch captured graphs of kSteps iterations instead
+    // (identical kernels and arguments, one launch per kSteps iterations).
+    constexpr int kSteps = 16;
+    if (graphed) {
+      char key[256];
+      std::snprintf(key, sizeof key, "%u|%d|%d|%d|%d|%.17g|%.17g|%.17g", mask, n0_max, aa.stable_rows, hold ? 1 : 0,
+                    r->cfg.kernel.nu, r->cfg.kernel.lengthscale, r->cfg.kernel.output_variance, r->cfg.noise);
+      if (r->graphs.key != key) {
+        r->graphs.release();
+        auto capture = [&](int count, cudaGraphExec_t* out) -> bool {
+          if (cudaStreamBeginCapture(r->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return false;
+          int lrc = GTC_OK;
+          for (int i = 0; i < count && lrc == GTC_OK; ++i) lrc = launch_iteration();
+          cudaGraph_t g = nullptr;
+          const bool ok = cudaStreamEndCapture(r->stream, &g) == cudaSuccess && lrc == GTC_OK && g &&
+                          cudaGraphInstantiate(out, g, 0) == cudaSuccess;
+          if (g) cudaGraphDestroy(g);
+          return ok;
+        };
+        if (capture(kSteps, &r->graphs.many) && capture(1, &r->graphs.one)) {
+          r->graphs.key = key;
+        } else {  // fall back to plain launches for this run handle
+          cudaGetLastError();
+          r->graphs.release();
+          r->graphs.failed = true;
+          graphed = false;
+        }
+      }
+    }
     GTC_CUDA(cudaEventRecord(r->ev_step0, r->stream));
-    for (int i = 0; i < m; ++i) {
+    if (graphed) {
+      for (int i = 0; i + kSteps <= m; i += kSteps) GTC_CUDA(cudaGraphLaunch(r->graphs.many, r->stream));
+      for (int i = m - m % kSteps; i < m; ++i) GTC_CUDA(cudaGraphLaunch(r->graphs.one, r->stream));
+    }
+    for (int i = 0; i < m && !graphed; ++i) {
       if (timing) GTC_CUDA(cudaEventRecord(te[3 * i], r->stream));
       launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, vs, r->tstat, r->red.b, r->red.sel,
                     r->stream);

@@ -388,7 +388,10 @@ struct LoopDev {
   PortDev port;
   double* sorted_y;   // valid observations in ascending order (portfolio median), capacity n_max
   int32_t n_sorted;
-  int32_t pad2;
+  int32_t lambda_mode;  // the selection's exploration parameters (SelectParams in loop mode)
+  double lambda_constant;
+  double cv_mu_s;
+  double cv_var_s;
 };
 // Loop-mode launches of the bordered append / single-row pass (args.loop set;
 // smem / args.n0 sized for the largest row of the chunk).

@@ -1845,6 +1845,10 @@ __global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK))
     p.f_best_raw = lp->f_best;
     p.first_eligible = lp->first;
     p.n_candidates = lp->count;
+    p.lambda_mode = lp->lambda_mode;
+    p.lambda_constant = lp->lambda_constant;
+    p.cv_mu_s = lp->cv_mu_s;
+    p.cv_var_s = lp->cv_var_s;
     vs.acc = lp->acc + lp->gen;
   }
   select_run_body<MASK>(c, sc, p, vs, tstat, ntiles);

@@ -204,6 +204,11 @@ class SurrogateRun:
         v = np.ascontiguousarray(np.asarray(values, dtype=np.float64))
         check(load().gtc_run_set_values(self._h, _lib.dptr(v), len(v)))
 
+    def set_pdl(self, enable: bool) -> None:
+        """gtc_run_set_pdl: programmatic dependent launch on (default) or off
+        (then gtc_run_steps launches captured graphs of its iterations)."""
+        check(load().gtc_run_set_pdl(self._h, 1 if enable else 0))
+
     def set_portfolio(self, mode: int, skip_threshold: int = 5, discount: float = 0.65,
                       required_improvement: float = 0.1) -> None:
         """gtc_run_set_portfolio: 0 single AF, 1 multi, 2 advanced multi (fresh state)."""

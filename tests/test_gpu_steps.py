@@ -273,3 +273,28 @@ def test_resident_pivot_failure_refit(gt):
         m_b, v_b = run_b.predictions()
         np.testing.assert_array_equal(m_a, m_b)
         np.testing.assert_array_equal(v_a, v_b)
+
+
+@pytest.mark.parametrize("portfolio", [0, 1, 2])
+def test_graph_launched_chunks(gt, portfolio):
+    """Without PDL gtc_run_steps launches captured graphs (16 iterations, then
+    single iterations); same picks and posterior as PDL launches, across
+    chunk sizes that reuse and re-capture the graphs."""
+    af = gt.AcquisitionId.ei
+    expl = gt.ExplorationConfig()
+    out = []
+    for pdl in (True, False):
+        space, run, values, init, cv = setup(gt, [10, 10, 6, 5], 0.2, 31)
+        run.set_values(values)
+        run.set_pdl(pdl)
+        if portfolio:
+            run.set_portfolio(portfolio, 2, 0.65 if portfolio == 1 else 0.75, 0.1)
+        picks, fb = [], float(np.min(values[init]))
+        for k in (20, 17, 1, 45, 16):
+            recs = run.steps(af, k, fb, expl, cv)
+            picks += [(r.position, r.by, r.lambda_) for r in recs]
+            fb = min([fb] + [r.value for r in recs if r.valid])
+        out.append((picks, run.predictions()))
+    assert out[0][0] == out[1][0]
+    np.testing.assert_array_equal(out[0][1][0], out[1][1][0])
+    np.testing.assert_array_equal(out[0][1][1], out[1][1][1])

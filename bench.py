@@ -39,7 +39,7 @@ BASE_SEED = 20261017
 METRIC = "BO iterations/sec (full-space GP posterior+acquisition) at N, n=220"
 # dram__bytes_read.sum + dram__bytes_write.sum per k_extend<1> launch, from the
 # committed ncu --set full capture of the resident loop
-TRAFFIC = {"c4": 1.76611e9}  # 1.758509 GB read + 7.60 MB written per launch (profiles/r01b_ncu_full.txt)
+TRAFFIC = {"c4": 1.76555e9}  # 1.758576 GB read + 6.97 MB written per launch (profiles/r01c_ncu_full.txt)
 CONFIGS = {
     "c4": dict(grid=[10] * 6, invalid=0.0, workload="C4 synthetic random-rough 1M candidates (10^6 grid, d=6), n=220, bo-ei, contextual variance"),
     "c3": dict(grid=[10, 10, 10, 10, 5, 2], invalid=0.3, workload="C3 synthetic random-rough 100k candidates (d=6, ~30% invalid), n=220, bo-lcb, contextual variance"),
@@ -191,6 +191,7 @@ def run_c5(args, rank=0, world=1, local=0):
         "ms_per_step": 1e3 * dt / runs, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic measurements over the device-enumerated GEMM, conv and pnpoly spaces",
         "config": {"workload": "C5 strategy sweep, 1,200 runs, n_init 20, budget 220", "threads": 64,
+                   "sweep_seconds": [round(t, 4) for t in sweep.times], "statistic": "median of the sweeps",
                    "parallelism": f"run-sharded over {world} GPU(s)", "evaluations": evals,
                    "timing": "wall clock of gtc_run_bo_batch per case (observe groups), max over ranks"},
         "evaluations_per_sec": evals / dt, "clocks": clocks, "cpu_baseline": c2_reference()}))
@@ -215,9 +216,10 @@ def sweep(cases, strategies, reps, threads, rank, world, local):
     total runs, total evaluations, clock summary)."""
     import torch
     import paper_2111_14991_b200 as gt
-    # one worker thread per host core: more threads than cores make the
-    # observe-group rounds wait on the OS scheduler
-    host_threads = int(os.environ.get("GTC_SWEEP_THREADS", os.cpu_count() or 1))
+    # worker threads: one per concurrently driven run (threads = runs per case
+    # for C2): with the space's run pool, 35 threads measured 290-320 runs/s on
+    # C2 vs a noisy 40-220 with one thread per host core (tools/c2_variance.py)
+    host_threads = int(os.environ.get("GTC_SWEEP_THREADS", threads))
     prepared = []
     for name, (params, rs, invalid, minimum) in cases.items():
         es = gt.SearchSpace([gt.ParameterDef(k, v) for k, v in params], rs).enumerate(device=local)
@@ -233,15 +235,22 @@ def sweep(cases, strategies, reps, threads, rank, world, local):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    runs = evals = 0
+    # the whole sweep `reps` times (a sweep of 70 short runs lasts well under a
+    # second, where host scheduling hiccups are visible): the median sweep counts
+    reps = max(1, int(os.environ.get("GTC_SWEEP_REPS", "3")))
+    times = []
     with ClockSampler(local) as clocks:
-        t0 = time.perf_counter()
-        for es, values, mine in prepared:
-            out = gt.run_bo_batch(es, es.ids, mine, values, threads=min(threads, len(mine), host_threads))
-            runs += len(out)
-            evals += sum(int(r.evaluations) for r in out)
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
+        for _ in range(reps):
+            runs = evals = 0
+            t0 = time.perf_counter()
+            for es, values, mine in prepared:
+                out = gt.run_bo_batch(es, es.ids, mine, values, threads=min(threads, len(mine), host_threads))
+                runs += len(out)
+                evals += sum(int(r.evaluations) for r in out)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+    dt = float(np.median(times))
+    sweep.times = times
     if world > 1:
         t = torch.tensor([dt, runs, evals], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t[:1], op=torch.distributed.ReduceOp.MAX)
@@ -332,6 +341,7 @@ def run_c2(args, rank=0, world=1, local=0):
         "data": "synthetic measurements over the device-enumerated conv (N=9400) and pnpoly (N=8184) spaces",
         "config": {"workload": "C2 conv + pnpoly, 35 repeats each, bo-multi, n_init 20, budget 220",
                    "threads": threads, "evaluations": evals,
+                   "sweep_seconds": [round(t, 4) for t in sweep.times], "statistic": "median of the sweeps",
                    "timing": "wall clock of gtc_run_bo_batch (host thread pool, one stream per run)"},
         "evaluations_per_sec": evals / t_total, "clocks": clocks,
         "cpu_baseline": c2_reference()}))

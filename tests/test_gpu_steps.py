@@ -298,3 +298,33 @@ def test_graph_launched_chunks(gt, portfolio):
     assert out[0][0] == out[1][0]
     np.testing.assert_array_equal(out[0][1][0], out[1][1][0])
     np.testing.assert_array_equal(out[0][1][1], out[1][1][1])
+
+
+def test_steps_argument_errors(gt):
+    """gtc_run_steps preconditions map to the reference error types."""
+    af = gt.AcquisitionId.ei
+    expl = gt.ExplorationConfig()
+    space, run, values, init, cv = setup(gt, [6, 6, 5], 0.0, 2, n_max=40)
+    f0 = float(np.min(values[init]))
+    with pytest.raises(gt.Error, match="no value table"):
+        run.steps(af, 3, f0, expl, cv)
+    run.set_values(values)
+    a, _ = run._args([gt.AcquisitionId.ei, gt.AcquisitionId.lcb], f0, expl, cv, None)
+    import ctypes as C
+    from paper_2111_14991_b200 import _lib
+    recs = (_lib.gtc_step_record * 4)()
+    done = C.c_int32()
+    info = _lib.gtc_fit_info()
+    rc = gt.load().gtc_run_steps(run.handle, C.byref(a), 4, 0, recs, C.byref(done), C.byref(info))
+    assert rc == _lib.GTC_ERR_INVALID and b"exactly one" in gt.load().gtc_last_error()
+    run.set_portfolio(1)
+    with pytest.raises(gt.Error, match="single-AF"):
+        run.steps(af, 3, f0, expl, cv, hold=True)
+    with pytest.raises(gt.ConfigError):
+        run.set_portfolio(1, skip_threshold=0)
+    with pytest.raises(gt.ConfigError):
+        run.set_portfolio(2, discount=1.0)
+    # capacity: the model cannot grow past n_max (20 initial + 20 appended)
+    run.set_portfolio(0)
+    with pytest.raises(gt.Error, match="n_max"):
+        run.steps(af, 30, f0, expl, cv)

@@ -640,7 +640,7 @@ __device__ __forceinline__ double2 coord2(const SpaceDev& sp, int t, int64_t j0)
 // Rows [n0, n0+r) of V for every candidate, r <= R, streaming rows [0, n0)
 // once.  One CTA per tile of kTile candidates, one double2 column pair per
 // thread.  With final_pass the posterior mean/variance are produced too.
-template <int R, int NU>
+template <int R, int NU, int UP = GTC_PASS_U>
 __device__ __forceinline__ void extend_body(const ExtendArgs& a_in) {
   ExtendArgs a = a_in;
   pdl_begin();
@@ -683,7 +683,7 @@ __device__ __forceinline__ void extend_body(const ExtendArgs& a_in) {
 
   // U rows in flight; the last partial group is predicated inside the same
   // unrolled body (a scalar remainder loop would serialise its loads)
-  constexpr int U = (R == 1) ? GTC_PASS_U : 4;
+  constexpr int U = (R == 1) ? UP : 4;
   // rows [i, i + U) into the accumulators, ascending (the reference's order)
   auto consume = [&](const double2 (&v)[U], int i) {
 #pragma unroll
@@ -864,6 +864,18 @@ template <int R, int NU>
 __global__ void __launch_bounds__(kExtendThreads, R == 1 ? GTC_PASS_MINB : 4) k_extend(ExtendArgs a) {
   extend_body<R, NU>(a);
 }
+
+// Small spaces (fewer tiles than ~4 per SM): too few CTAs to keep enough V
+// loads in flight, so each thread keeps kDeepRows rows in flight instead
+// (same operations in the same order, only deeper load pipelining).
+#ifndef GTC_PASS_U_DEEP
+#define GTC_PASS_U_DEEP 16
+#endif
+template <int NU>
+__global__ void __launch_bounds__(kExtendThreads, 4) k_extend_deep(ExtendArgs a) {
+  extend_body<1, NU, GTC_PASS_U_DEEP>(a);
+}
+static bool deep_pass(int64_t tiles);
 
 // Runs of a batch on the y axis (same space, hence the same tiles).
 template <int NU>
@@ -1995,9 +2007,22 @@ void launch_gp_truncate(const GpDev& g, int n, cudaStream_t s) {
   k_gp_truncate<<<1, kCtaThreads, 0, s>>>(g, n);
 }
 
+static bool deep_pass(int64_t tiles) {
+  static const int off = [] {
+    const char* e = std::getenv("GTC_PASS_DEEP");
+    return e && e[0] == '0';
+  }();
+  return !off && tiles < 4 * (int64_t)sm_count();
+}
+
 template <int R, int NU>
 static void extend_impl(const ExtendArgs& a, int64_t tiles, cudaStream_t s) {
   const size_t sm = sizeof(double) * ((size_t)(R + 1) * (a.n0 + R) + (size_t)R * a.g.d + R + 8);
+  if (R == 1 && deep_pass(tiles)) {
+    opt_in_smem(k_extend_deep<NU>, sm);
+    launch_pdl(k_extend_deep<NU>, dim3((unsigned)tiles), dim3(kExtendThreads), sm, s, a);
+    return;
+  }
   opt_in_smem(k_extend<R, NU>, sm);
   launch_pdl(k_extend<R, NU>, dim3((unsigned)tiles), dim3(kExtendThreads), sm, s, a);
 }
@@ -2027,9 +2052,7 @@ void launch_extend(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V
 
 template <int NU>
 static void extend_loop_impl(const ExtendArgs& a, int64_t tiles, cudaStream_t s) {
-  const size_t sm = sizeof(double) * ((size_t)2 * (a.n0 + 1) + (size_t)a.g.d + 1 + 8);
-  opt_in_smem(k_extend<1, NU>, sm);
-  launch_pdl(k_extend<1, NU>, dim3((unsigned)tiles), dim3(kExtendThreads), sm, s, a);
+  extend_impl<1, NU>(a, tiles, s);
 }
 
 void launch_extend_loop(const ExtendArgs& a, int64_t tiles, int nu, cudaStream_t s) {

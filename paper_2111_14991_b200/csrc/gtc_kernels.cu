@@ -2134,6 +2134,21 @@ static void select_geometry(int64_t n, uint32_t mask, int* per, int* grid) {
   *grid = (int)std::max<int64_t>(1, std::min<int64_t>({(n + chunk - 1) / chunk, sms, (int64_t)kMaxReduceGrid}));
 }
 
+// Threads per selection block: a block handles ceil(tiles / grid) tiles, so
+// when there are fewer tiles than resident 512-thread blocks (small spaces,
+// one tile per block) most threads would idle; 128-thread blocks hold far
+// fewer SM resources per tile (several concurrent runs share the device).
+// The argmax does not depend on the block size (max with the lowest-position
+// tie rule; thresholds are exact scores).
+static int select_threads(int ntiles, uint32_t mask) {
+  static const int forced = [] {
+    const char* e = std::getenv("GTC_SELECT_THREADS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 128 || forced == 256 || forced == 512) return forced;
+  return ntiles < sel_blocks_per_sm(mask) * sm_count() ? 128 : kSelectThreads;
+}
+
 void launch_select(const double* mu, const double* var, const uint32_t* visited, int64_t n,
                    const GpScalars* sc, SelectParams p, const VarSource& vs, const TileStats* tstat,
                    const ReduceBufs& b, SelectDev* out, cudaStream_t s) {
@@ -2147,9 +2162,10 @@ void launch_select(const double* mu, const double* var, const uint32_t* visited,
   }();
   const int want = grid_override > 0 ? grid_override : sel_blocks_per_sm(mask) * sm_count();
   const int grid = std::max(1, std::min({ntiles, want, kMaxReduceGrid}));
+  const int threads = select_threads(ntiles, mask);
 #define GTC_SELECT_CASE(M)                                                           \
   case M:                                                                            \
-    launch_pdl(k_select<M>, dim3(grid), dim3(kSelectThreads), 0, s, c, sc, p, vs, tstat, ntiles); \
+    launch_pdl(k_select<M>, dim3(grid), dim3(threads), 0, s, c, sc, p, vs, tstat, ntiles); \
     break;
   switch (mask) {  // launch errors surface through the caller's cudaGetLastError()
     GTC_SELECT_CASE(1)
@@ -2169,14 +2185,15 @@ void launch_select_batch(const SelectRunArgs* d_args, int count, uint32_t mask, 
   const int ntiles = (int)((n + kTile - 1) / kTile);
   const int grid = std::max(1, std::min({ntiles, sel_blocks_per_sm(m) * sm_count(), kMaxReduceGrid}));
   const dim3 g((unsigned)grid, (unsigned)count);
+  const int t = select_threads(ntiles, m);
   switch (m) {
-    case 1: k_select_batch<1><<<g, kSelectThreads, 0, s>>>(d_args); break;
-    case 2: k_select_batch<2><<<g, kSelectThreads, 0, s>>>(d_args); break;
-    case 3: k_select_batch<3><<<g, kSelectThreads, 0, s>>>(d_args); break;
-    case 4: k_select_batch<4><<<g, kSelectThreads, 0, s>>>(d_args); break;
-    case 5: k_select_batch<5><<<g, kSelectThreads, 0, s>>>(d_args); break;
-    case 6: k_select_batch<6><<<g, kSelectThreads, 0, s>>>(d_args); break;
-    default: k_select_batch<7><<<g, kSelectThreads, 0, s>>>(d_args); break;
+    case 1: k_select_batch<1><<<g, t, 0, s>>>(d_args); break;
+    case 2: k_select_batch<2><<<g, t, 0, s>>>(d_args); break;
+    case 3: k_select_batch<3><<<g, t, 0, s>>>(d_args); break;
+    case 4: k_select_batch<4><<<g, t, 0, s>>>(d_args); break;
+    case 5: k_select_batch<5><<<g, t, 0, s>>>(d_args); break;
+    case 6: k_select_batch<6><<<g, t, 0, s>>>(d_args); break;
+    default: k_select_batch<7><<<g, t, 0, s>>>(d_args); break;
   }
 }
 

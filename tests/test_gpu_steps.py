@@ -328,3 +328,35 @@ def test_steps_argument_errors(gt):
     run.set_portfolio(0)
     with pytest.raises(gt.Error, match="n_max"):
         run.steps(af, 30, f0, expl, cv)
+
+
+def test_steps_hold_with_invalid_values(gt):
+    """GTC_STEPS_HOLD_N with runtime-invalid values (the C3 bench): an invalid
+    pick is marked and stays visited without touching the model; a valid one
+    replaces the observation at row n0 and un-marks the position it replaces.
+    Same picks as that protocol driven through gtc_observe from the host."""
+    af = gt.AcquisitionId.lcb
+    expl = gt.ExplorationConfig()
+    grid, seed, k = [10, 10, 10, 8], 23, 60
+    space, run_a, values, init, cv = setup(gt, grid, 0.3, seed, n_init=60, n_max=64)
+    f0 = float(np.min(values[init]))
+    n0 = 60
+    sel = run_a.select([af], f0, expl, cv)
+    picks_h, prev = [], None
+    for _ in range(k):
+        p = sel.pick(af)
+        picks_h.append(p)
+        y = values[p]
+        if np.isnan(y):
+            _, sel = run_a.observe(p, None, [af], f0 if prev is None else min(f0, values[prev]), expl, cv)
+            continue
+        run_a.truncate_async(n0)
+        if prev is not None:
+            run_a.unmark_visited(prev)
+        prev = p
+        _, sel = run_a.observe(p, float(y), [af], min(f0, float(y)), expl, cv)
+    _, run_b, _, _, _ = setup(gt, grid, 0.3, seed, n_init=60, n_max=64)
+    run_b.set_values(values)
+    recs = run_b.steps(af, k, f0, expl, cv, hold=True)
+    assert any(not r.valid for r in recs)
+    assert [r.position for r in recs] == picks_h

@@ -191,7 +191,17 @@ class SurrogateRun:
         r = _lib.gtc_select_result()
         info = _lib.gtc_fit_info()
         if afs:
-            a, _keep = self._args(afs, f_best_raw, exploration, cv_state, excluded)
+            if excluded:
+                a, _keep = self._args(afs, f_best_raw, exploration, cv_state, excluded)
+            else:  # per-iteration calls: reuse the argument struct, only f_best changes
+                key = (tuple(int(x) for x in afs), int(exploration.mode), float(exploration.constant),
+                       float(cv_state.initial_sample_mean), float(cv_state.initial_mean_variance))
+                cached = getattr(self, "_obs_args", None)
+                if cached is None or cached[0] != key:
+                    cached = (key, self._args(afs, f_best_raw, exploration, cv_state, None)[0])
+                    self._obs_args = cached
+                a = cached[1]
+                a.f_best_raw = float(f_best_raw)
             check(load().gtc_observe(self._h, int(position), float(y_raw) if valid else 0.0, int(valid),
                                      C.byref(a), C.byref(r), C.byref(info)))
             return FitInfo.of(info), self._selection(r)

@@ -69,6 +69,23 @@ def dist_env():
     return rank, world, local
 
 
+def init_dist(local):
+    """One rank per GPU over NCCL.  (GTC_BENCH_BACKEND=gloo lets several ranks
+    share one GPU to exercise the multi-rank flow on a single-GPU box.)"""
+    import torch
+    import torch.distributed as dist
+    backend = os.environ.get("GTC_BENCH_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+
+
+def device_of(local):
+    import torch
+    return local % max(1, torch.cuda.device_count())
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -501,10 +518,10 @@ def main():
             return
         rank, world, local = dist_env()
         import torch
+        local = device_of(local)
         torch.cuda.set_device(local)
         if world > 1:
-            import torch.distributed as dist
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            init_dist(local)
         {"c1": run_c1, "c2": run_c2, "c5": run_c5}[args.config](args, rank, world, local)
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -515,10 +532,10 @@ def main():
         return
     rank, world, local = dist_env()
     import torch
+    local = device_of(local)
     torch.cuda.set_device(local)
     if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(local)
     if args.mode == "sharded":
         run_sharded(args, cfg, rank, world, local)
         if world > 1:

@@ -1734,6 +1734,15 @@ __device__ __forceinline__ void select_run_body(const SelCtx& c, const GpScalars
   // this thread's first tile summary, loaded before the variance total (independent)
   TileStats ts0{};
   if ((int)threadIdx.x < mine) ts0 = tstat[blockIdx.x + G * threadIdx.x];
+  // the first eligible candidate's inputs, loaded now by the block that owns it
+  // (used at the end; keeps the load off the block's tail)
+  const int64_t fp = p.first_eligible;
+  const bool own_first = threadIdx.x == 0 && fp >= 0 && (int)((fp / kTile) % G) == (int)blockIdx.x;
+  double f_mu = 0.0, f_var = 0.0;
+  if (own_first) {
+    f_mu = c.mu[fp];
+    f_var = c.var[fp];
+  }
   const SelSetup u = sel_setup(sc, p, vs);
   const double bm_ei = __dadd_rn(u.best, -u.lambda), bp_pi = __dadd_rn(u.best, u.lambda);
   const bool base_ok = fabs(bm_ei) < 1e30 && fabs(bp_pi) < 1e30;
@@ -1829,11 +1838,10 @@ __device__ __forceinline__ void select_run_body(const SelCtx& c, const GpScalars
   // the host-computed first eligible candidate lives in exactly one block
   int64_t first = INT64_MAX;
   int finite = 1;
-  const int64_t fp = p.first_eligible;
-  if (threadIdx.x == 0 && fp >= 0 && (int)((fp / kTile) % G) == (int)blockIdx.x) {
+  if (own_first) {
     float key[3];
     bool hi;
-    bound_keys<MASK, false>(key, &hi, c.mu[fp], c.var[fp], base_ok, bm_ei, bp_pi, u.lambda);
+    bound_keys<MASK, false>(key, &hi, f_mu, f_var, base_ok, bm_ei, bp_pi, u.lambda);
     first = fp;
 #pragma unroll
     for (int af = 0; af < 3; ++af)

@@ -259,6 +259,30 @@ typedef struct {
   double required_improvement;
 } gtc_portfolio_config;
 int gtc_run_set_portfolio(gtc_run* run, const gtc_portfolio_config* config);
+/* The device portfolio of gtc_run_steps driven by an explicit script (the
+ * reference's Portfolio unit scenarios, test_portfolio.cpp): kind 0 =
+ * Portfolio::suggest on the given per-function argmax positions (ei, poi,
+ * lcb), kind 1 = Portfolio::record(af, value).  out[i] = the suggestion
+ * (position, by; -1 for records) and the state after op i.  initial_active
+ * (NULL: all) restricts PortfolioConfig::order to a subset. */
+typedef struct {
+  int32_t kind;
+  int32_t af;
+  int64_t picks[3];
+  double value;
+} gtc_portfolio_op;
+typedef struct {
+  int64_t position;
+  int32_t by;
+  int32_t active[3];
+  int32_t duplicates[3];
+  int32_t above[3];
+  int32_t below[3];
+  int32_t pad;
+  double dos[3];
+} gtc_portfolio_state;
+int gtc_portfolio_trace(int device, const gtc_portfolio_config* config, const int32_t* initial_active,
+                        int32_t n_ops, const gtc_portfolio_op* ops, gtc_portfolio_state* out);
 /* Programmatic dependent launch between the run's kernels (default on): the
  * next kernel is scheduled while the current one drains.  Turn it off for runs
  * that share a device with many concurrently driven runs (gtc_run_bo_batch

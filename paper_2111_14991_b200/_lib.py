@@ -61,6 +61,16 @@ class gtc_portfolio_config(C.Structure):
                 ("required_improvement", C.c_double)]
 
 
+class gtc_portfolio_op(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("af", C.c_int32), ("picks", C.c_int64 * 3), ("value", C.c_double)]
+
+
+class gtc_portfolio_state(C.Structure):
+    _fields_ = [("position", C.c_int64), ("by", C.c_int32), ("active", C.c_int32 * 3),
+                ("duplicates", C.c_int32 * 3), ("above", C.c_int32 * 3), ("below", C.c_int32 * 3),
+                ("pad", C.c_int32), ("dos", C.c_double * 3)]
+
+
 GTC_STEPS_HOLD_N = 1
 GTC_STEPS_TIMING = 2
 
@@ -143,6 +153,8 @@ SIGNATURES = [
     ("gtc_run_set_values", C.c_int, [P, DP, C.c_int64]),
     ("gtc_run_set_portfolio", C.c_int, [P, C.POINTER(gtc_portfolio_config)]),
     ("gtc_run_set_pdl", C.c_int, [P, C.c_int32]),
+    ("gtc_portfolio_trace", C.c_int, [C.c_int, C.POINTER(gtc_portfolio_config), C.POINTER(C.c_int32), C.c_int32,
+                                      C.POINTER(gtc_portfolio_op), C.POINTER(gtc_portfolio_state)]),
     ("gtc_run_steps", C.c_int, [P, C.POINTER(gtc_select_args), C.c_int32, C.c_int32,
                                 C.POINTER(gtc_step_record), C.POINTER(C.c_int32), C.POINTER(gtc_fit_info)]),
     ("gtc_last_steps_ms", C.c_double, [P]),

@@ -1120,6 +1120,48 @@ extern "C" int gtc_run_set_portfolio(gtc_run* r, const gtc_portfolio_config* c) 
   return GTC_OK;
 }
 
+extern "C" int gtc_portfolio_trace(int device, const gtc_portfolio_config* c, const int32_t* initial_active,
+                                   int32_t n_ops, const gtc_portfolio_op* ops, gtc_portfolio_state* out) {
+  static_assert(sizeof(PortOp) == sizeof(gtc_portfolio_op), "op layout");
+  static_assert(sizeof(PortState) == sizeof(gtc_portfolio_state), "state layout");
+  if (!c || (n_ops > 0 && (!ops || !out)) || n_ops < 0) return fail(GTC_ERR_INVALID, "null argument");
+  if (c->mode != GTC_PORTFOLIO_MULTI && c->mode != GTC_PORTFOLIO_ADVANCED)
+    return fail(GTC_ERR_CONFIG, "unknown portfolio mode");
+  if (c->skip_threshold < 1) return fail(GTC_ERR_CONFIG, "skip threshold must be >= 1");
+  if (!(c->discount > 0.0 && c->discount < 1.0)) return fail(GTC_ERR_CONFIG, "discount factor must be in (0,1)");
+  if (!(c->required_improvement > 0.0)) return fail(GTC_ERR_CONFIG, "required improvement factor must be positive");
+  for (int32_t i = 0; i < n_ops; ++i)
+    if (ops[i].kind == 1 && (ops[i].af < 0 || ops[i].af > 2)) return fail(GTC_ERR_INVALID, "unknown acquisition function");
+  if (n_ops == 0) return GTC_OK;
+  GTC_CUDA(cudaSetDevice(device));
+  PortDev P{};
+  P.mode = c->mode;
+  P.skip_threshold = c->skip_threshold;
+  P.discount = c->discount;
+  P.rho = c->required_improvement;
+  for (int a = 0; a < 3; ++a) {
+    P.active[a] = initial_active ? (initial_active[a] != 0) : 1;
+    P.last_sug[a] = -1;
+  }
+  PortOp* d_ops = nullptr;
+  PortState* d_out = nullptr;
+  int rc;
+  if ((rc = dalloc(&d_ops, (size_t)n_ops)) || (rc = dalloc(&d_out, (size_t)n_ops))) {
+    cudaFree(d_ops);
+    return rc;
+  }
+  cudaError_t e = cudaMemcpy(d_ops, ops, sizeof(PortOp) * (size_t)n_ops, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    launch_portfolio_trace(P, d_ops, n_ops, d_out, nullptr);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, d_out, sizeof(PortState) * (size_t)n_ops, cudaMemcpyDeviceToHost);
+  cudaFree(d_ops);
+  cudaFree(d_out);
+  if (e != cudaSuccess) return fail(GTC_ERR_CUDA, std::string("portfolio trace: ") + cudaGetErrorString(e));
+  return GTC_OK;
+}
+
 extern "C" int gtc_run_set_values(gtc_run* r, const double* values, int64_t n) {
   if (!r || !values) return fail(GTC_ERR_INVALID, "null argument");
   if (n != r->space->n) return fail(GTC_ERR_INVALID, "value table size != space size");

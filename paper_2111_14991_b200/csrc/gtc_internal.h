@@ -396,6 +396,24 @@ struct LoopDev {
 // Loop-mode launches of the bordered append / single-row pass (args.loop set;
 // smem / args.n0 sized for the largest row of the chunk).
 void launch_gp_append_loop(const AppendArgs& a, int nu, size_t smem, cudaStream_t stream);
+// Portfolio script (== gtc_portfolio_op / gtc_portfolio_state).
+struct PortOp {
+  int32_t kind;  // 0 suggest (picks = per-AF argmax positions), 1 record (af, value)
+  int32_t af;
+  int64_t picks[3];
+  double value;
+};
+struct PortState {
+  int64_t position;
+  int32_t by;
+  int32_t active[3];
+  int32_t duplicates[3];
+  int32_t above[3];
+  int32_t below[3];
+  int32_t pad;
+  double dos[3];
+};
+void launch_portfolio_trace(const PortDev& P, const PortOp* d_ops, int n, PortState* d_out, cudaStream_t stream);
 void launch_extend_loop(const ExtendArgs& a, int64_t tiles, int nu, cudaStream_t stream);
 
 // Programmatic dependent launch for this host thread's subsequent launches.

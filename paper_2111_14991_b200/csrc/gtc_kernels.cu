@@ -1248,6 +1248,13 @@ __device__ void port_update_bands(PortDev& P, int p) {
   }
 }
 
+// Portfolio::record (portfolio.hpp:140-150) of an already resolved observed
+// value (an invalid result's median is the caller's).
+__device__ void port_record(PortDev& P, int by, double observed) {
+  P.dos[by] = __dadd_rn(__dmul_rn(P.dos[by], P.discount), observed);
+  if (P.mode == 2) port_update_bands(P, by);
+}
+
 __device__ void loop_advance(LoopDev* L, const SelectDev* sel) {
   if (sel->n_candidates <= 0) {
     L->halt = kLoopNoCandidates;
@@ -1270,8 +1277,7 @@ __device__ void loop_advance(LoopDev* L, const SelectDev* sel) {
       observed = (m & 1) ? L->sorted_y[m / 2]
                          : __dmul_rn(0.5, __dadd_rn(L->sorted_y[m / 2 - 1], L->sorted_y[m / 2]));
     }
-    P.dos[by] = __dadd_rn(__dmul_rn(P.dos[by], P.discount), observed);
-    if (P.mode == 2) port_update_bands(P, by);
+    port_record(P, by, observed);
     if (valid) {  // keep the valid observations sorted (insertion)
       int i = L->n_sorted++;
       while (i > 0 && L->sorted_y[i - 1] > y) {
@@ -1323,6 +1329,40 @@ __device__ void loop_advance(LoopDev* L, const SelectDev* sel) {
     }
     L->first = found;
   }
+}
+
+// The device portfolio driven by an explicit script (gtc_portfolio_trace):
+// the same port_suggest / port_record the resident loop runs, on given
+// per-function argmaxes and observed values (portfolio parity tests).
+__global__ void k_portfolio_trace(PortDev P, const PortOp* ops, int n, PortState* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int i = 0; i < n; ++i) {
+    PortState& o = out[i];
+    o.position = -1;
+    o.by = -1;
+    if (ops[i].kind == 0) {
+      SelectDev sel{};
+      for (int a = 0; a < 3; ++a) sel.position[a] = ops[i].picks[a];
+      int by = -1;
+      o.position = port_suggest(P, &sel, &by);
+      o.by = by;
+    } else {
+      port_record(P, ops[i].af, ops[i].value);
+      o.by = ops[i].af;
+    }
+    for (int a = 0; a < 3; ++a) {
+      o.active[a] = P.active[a];
+      o.duplicates[a] = P.duplicates[a];
+      o.above[a] = P.above[a];
+      o.below[a] = P.below[a];
+      o.dos[a] = P.dos[a];
+    }
+  }
+}
+
+void launch_portfolio_trace(const PortDev& P, const PortOp* d_ops, int n, PortState* d_out, cudaStream_t s) {
+  count_launch();
+  k_portfolio_trace<<<1, 32, 0, s>>>(P, d_ops, n, d_out);
 }
 
 template <uint32_t MASK>

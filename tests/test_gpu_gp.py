@@ -85,6 +85,56 @@ def test_matches_dense_solve_oracle(gt, oracle):  # test_gp.cpp:87-126, same Rng
         assert close(p.mean, m2) and close(p.variance, v2)
 
 
+def dense_posterior_ld(kernel_fn, X, y_std, reg, Q):
+    """The dense-inverse posterior of oracles.hpp:58-92 in extended precision
+    (x87 long double Gauss-Jordan): its own error (~cond * 1e-19) stays far
+    below the 1e-8 gate, unlike a double inverse at cond(K) ~ 1e8."""
+    ld = np.longdouble
+    n = len(X)
+    D = np.sqrt(((X[:, None, :] - X[None, :, :]) ** 2).sum(-1))
+    K = kernel_fn(D).astype(ld) + ld(reg) * np.eye(n, dtype=ld)
+    A = np.concatenate([K, np.eye(n, dtype=ld)], axis=1)
+    for c in range(n):
+        piv = c + int(np.argmax(np.abs(A[c:, c])))
+        A[[c, piv]] = A[[piv, c]]
+        A[c] /= A[c, c]
+        for r in range(n):
+            if r != c:
+                A[r] -= A[r, c] * A[c]
+    Kinv = A[:, n:]
+    ks = kernel_fn(np.sqrt(((X[:, None, :] - Q[None, :, :]) ** 2).sum(-1))).astype(ld)
+    w = Kinv @ ks
+    return (w.T @ y_std.astype(ld)).astype(np.float64), (ld(kernel_fn(np.zeros(1))[0]) - (ks * w).sum(0)).astype(np.float64)
+
+
+def test_acceptance_gp_oracle_equivalence(gt):  # acceptance_main.cpp:56-112 (criterion 1)
+    """100 instances (n 1..20, d 1..4, 15 test points, same Rng stream):
+    device posterior within 1e-8 of the dense-inverse oracle, under 10 s."""
+    import time
+    rng = Rng(1001)
+    worst = 0.0
+    t0 = time.perf_counter()
+    for instance in range(100):
+        n = 1 + rng.uniform_below(20)
+        d = 1 + rng.uniform_below(4)
+        nu = 1 if instance % 2 == 0 else 2
+        l = 0.5 + 2.5 * rng.uniform01()
+        noise = 1e-8
+        X, yl = [], []
+        for _ in range(n):
+            X.append([rng.uniform01() for _ in range(d)])
+            yl.append(3.0 + 2.0 * rng.normal())
+        Q = np.array([[rng.uniform01() for _ in range(d)] for _ in range(15)])
+        X, y = np.array(X), np.array(yl)
+        model = gt.GpModel.fit(gt.MaternKernel(gt.MaternNu(nu), l, 1.0), X, y, noise)
+        p = model.predict(Q)
+        ys = np.array([model.standardize(v) for v in y])
+        dm, dv = dense_posterior_ld(matern_np(nu, l, 1.0), X, ys, noise + model.jitter(), Q)
+        worst = max(worst, float(np.max(np.abs(p.mean - dm))), float(np.max(np.abs(p.variance - np.maximum(dv, 0.0)))))
+    assert time.perf_counter() - t0 < 10.0
+    assert worst <= 1e-8, worst
+
+
 def test_reference_golden_vectors(gt, golden):
     """24 GpModel instances (n 1..40, d 1..6, nu 1/2, 3/2, 5/2) produced by the
     unmodified reference: device posterior within 1e-9 (mixed abs/rel)."""

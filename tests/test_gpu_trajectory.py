@@ -107,3 +107,34 @@ def test_budget_free_invalids(gt):  # test_strategies.cpp:214-227 for BO
     run = gt.run_bo(gt.Space(coords), ids, cfg, values=values)
     assert run.budget_consumed == 40
     assert run.evaluations == 40 + run.invalid_count
+
+
+def test_acceptance_contextual_variance(gt):  # acceptance_main.cpp:148-201 (criterion 3)
+    """random-rough 12x12 (seed 3, 15 % invalid), bo-advanced-multi: lambda
+    >= 0 on every iteration of 20 seeded runs (budget 60, n_init 12), and the
+    chosen configurations invariant under x2 rescaling on 20 seeds (budget 40,
+    n_init 10)."""
+    coords, ids, values = synthetic.random_rough([12, 12], 3, 0.15)
+    space = gt.Space(coords)
+    for seed in range(20):
+        cfg = gt.StrategyConfig(id=gt.StrategyId.bo_advanced_multi, seed=seed, budget=60, n_init=12)
+        assert np.all(gt.run_bo(space, ids, cfg, values=values).lambdas >= 0.0), seed
+    for seed in range(20):
+        cfg = gt.StrategyConfig(id=gt.StrategyId.bo_advanced_multi, seed=seed, budget=40, n_init=10)
+        a = gt.run_bo(space, ids, cfg, values=values)
+        b = gt.run_bo(space, ids, cfg, values=values * 2.0)
+        np.testing.assert_array_equal(a.positions, b.positions)
+
+
+def test_acceptance_invalid_handling(gt):  # acceptance_main.cpp:266-308 (criterion 5)
+    """random-rough 40x40 (seed 9) at the convolution-scale 38.5 % invalid
+    rate, 35 bo-advanced-multi runs (budget 120, n_init 20): no configuration
+    evaluated twice, surrogate size == valid evaluations."""
+    coords, ids, values = synthetic.random_rough([40, 40], 9, 0.385)
+    rate = float(np.mean(np.isnan(values)))
+    assert 0.35 <= rate <= 0.42
+    space = gt.Space(coords)
+    cfgs = [gt.StrategyConfig(id=gt.StrategyId.bo_advanced_multi, seed=s, budget=120, n_init=20) for s in range(35)]
+    for run in gt.run_bo_batch(space, ids, cfgs, values, threads=8):
+        assert len(np.unique(run.positions)) == len(run.positions)
+        assert run.surrogate_size == int(np.sum(~np.isnan(values[run.positions])))

@@ -39,7 +39,7 @@ BASE_SEED = 20261017
 METRIC = "BO iterations/sec (full-space GP posterior+acquisition) at N, n=220"
 # dram__bytes_read.sum + dram__bytes_write.sum per k_extend<1> launch, from the
 # committed ncu --set full capture of the resident loop
-TRAFFIC = {"c4": 1.76555e9}  # 1.758576 GB read + 6.97 MB written per launch (profiles/r01c_ncu_full.txt)
+TRAFFIC = {"c4": 1.76591e9}  # 1.758600 GB read + 7.31 MB written per launch (profiles/r01c_ncu_full.txt)
 CONFIGS = {
     "c4": dict(grid=[10] * 6, invalid=0.0, workload="C4 synthetic random-rough 1M candidates (10^6 grid, d=6), n=220, bo-ei, contextual variance"),
     "c3": dict(grid=[10, 10, 10, 10, 5, 2], invalid=0.3, workload="C3 synthetic random-rough 100k candidates (d=6, ~30% invalid), n=220, bo-lcb, contextual variance"),

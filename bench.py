@@ -41,8 +41,8 @@ METRIC = "BO iterations/sec (full-space GP posterior+acquisition) at N, n=220"
 # committed ncu --set full capture of the resident loop
 TRAFFIC = {"c4": 1.76591e9}  # 1.758600 GB read + 7.31 MB written per launch (profiles/r01c_ncu_full.txt)
 CONFIGS = {
-    "c4": dict(grid=[10] * 6, invalid=0.0, workload="C4 synthetic random-rough 1M candidates (10^6 grid, d=6), n=220, bo-ei, contextual variance"),
-    "c3": dict(grid=[10, 10, 10, 10, 5, 2], invalid=0.3, workload="C3 synthetic random-rough 100k candidates (d=6, ~30% invalid), n=220, bo-lcb, contextual variance"),
+    "c4": dict(grid=[10] * 6, invalid=0.0, af="ei", workload="C4 synthetic random-rough 1M candidates (10^6 grid, d=6), n=220, bo-ei, contextual variance"),
+    "c3": dict(grid=[10, 10, 10, 10, 5, 2], invalid=0.3, af="lcb", workload="C3 synthetic random-rough 100k candidates (d=6, ~30% invalid), n=220, bo-lcb, contextual variance"),
 }
 
 
@@ -393,7 +393,7 @@ def cpu_baseline(cfg, n, budget_s=30.0):
     cores = os.cpu_count() or 1
     grid = "x".join(str(k) for k in cfg["grid"])
     try:
-        out = subprocess.run([str(tool), "bench", grid, str(BASE_SEED), str(n), str(cores), "1", "ei"],
+        out = subprocess.run([str(tool), "bench", grid, str(BASE_SEED), str(n), str(cores), "1", cfg["af"]],
                              capture_output=True, text=True, timeout=budget_s * 20)
         rec = json.loads(out.stdout.strip().splitlines()[-1])
     except Exception as e:  # noqa: BLE001
@@ -418,7 +418,7 @@ def run_reference_arm(args, cfg):
     cores = os.cpu_count() or 1
     grid = "x".join(str(k) for k in cfg["grid"])
     steps = max(1, min(args.steps, 3))
-    out = subprocess.run([str(tool), "bench", grid, str(BASE_SEED), str(args.n), str(cores), str(steps), "ei"],
+    out = subprocess.run([str(tool), "bench", grid, str(BASE_SEED), str(args.n), str(cores), str(steps), cfg["af"]],
                          capture_output=True, text=True)
     rec = json.loads(out.stdout.strip().splitlines()[-1])
     v = rec["iters_per_sec"]

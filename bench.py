@@ -584,6 +584,7 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     launches_before = gt.load().gtc_kernel_launches()
+    exact0 = run.exact_rows()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
@@ -595,6 +596,7 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         launches = gt.load().gtc_kernel_launches() - launches_before
+        exact_rows = run.exact_rows() - exact0
         assert len(recs) == args.steps
         # the same K steps with CUDA events around every phase (kernel times for the roofline)
         resident(args.steps, timing=True)
@@ -673,6 +675,7 @@ def main():
                          "kernel_share_of_step": avg_pass / (dev_ms / args.steps),
                          "algorithmic_bytes": alg_bytes, "peak_kind": peak_kind},
             "clocks": clocks.summary(),
+            "bordered_rows_exact": int(exact_rows),
             "phases_us": dict(zip(("select+advance", "append", "pass"), (round(1e3 * float(v), 2) for v in phases))),
         }
         if not args.no_cpu_baseline:

@@ -325,6 +325,10 @@ int gtc_last_phase_ms(const gtc_run* run, double* out3);
  * seen by gtc_observe: [0] start, [1] factor staged, [2] Gram row, [3] forward
  * solve, [4] pivot/row written, [5] c/e rows, [6] statistics + beta. */
 int gtc_debug_append_marks(const gtc_run* run, uint64_t* marks7);
+/* Diagnostics: bordered rows (since the run was created) whose
+ * V-column pivot was below the exactness margin, so the exact forward
+ * substitution ran (as of the last synchronising call). */
+int64_t gtc_run_exact_rows(const gtc_run* run);
 /* The CUDA stream the run launches on (as an opaque integer, for NCCL). */
 uint64_t gtc_run_stream(const gtc_run* run);
 

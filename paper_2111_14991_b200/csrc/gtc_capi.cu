@@ -883,7 +883,7 @@ static bool phase_events() {
 static int enqueue_append(gtc_run* r, int64_t pos, double y_raw, uint32_t* mark) {
   const int n0 = r->n;
   launch_gp_append(r->gp.dev, kparams(r->cfg.kernel), r->cfg.noise, r->space->dev(), pos, nullptr, y_raw, n0,
-                   mark, r->stream);
+                   mark, r->stream, r->V, r->tile_stride);
   GTC_LAUNCHED();
   const bool ev = phase_events();
   if (ev) GTC_CUDA(cudaEventRecord(r->ev0, r->stream));
@@ -1283,6 +1283,12 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     L.lambda_constant = a->lambda_constant;
     L.cv_mu_s = a->cv_initial_sample_mean;
     L.cv_var_s = a->cv_initial_mean_variance;
+    L.g = r->gp.dev;  // the selection's last block appends valid steps from the pick's V column
+    L.kp = kparams(r->cfg.kernel);
+    L.noise = r->cfg.noise;
+    L.sp = r->space->dev();
+    L.V = r->V;
+    L.tile_stride = r->tile_stride;
     GTC_CUDA(cudaMemcpyAsync(r->d_loop, r->h_loop, sizeof(LoopDev), cudaMemcpyHostToDevice, r->stream));
     // (every per-run / per-step selection input is read from the loop state:
     // the launch arguments depend only on the run handle and its model config)
@@ -1294,7 +1300,6 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     aa = make_append_args(r->gp.dev, kparams(r->cfg.kernel), r->cfg.noise, r->space->dev(), 0, nullptr, 0.0,
                           n0_max, nullptr, &append_smem);
     aa.loop = r->d_loop;
-    aa.stable_rows = hold ? hold_n0 : r->n;  // hold: row hold_n0 is rewritten, rows below never
     ExtendArgs ea = make_pass_args(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, n0_max,
                                    r->mu, r->var, nullptr, r->tstat);
     ea.visited = r->visited;
@@ -1324,7 +1329,7 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     constexpr int kSteps = 16;
     if (graphed) {
       char key[256];
-      std::snprintf(key, sizeof key, "%u|%d|%d|%d|%d|%.17g|%.17g|%.17g", mask, n0_max, aa.stable_rows, hold ? 1 : 0,
+      std::snprintf(key, sizeof key, "%u|%d|%d|%d|%.17g|%.17g|%.17g", mask, n0_max, hold ? 1 : 0,
                     r->cfg.kernel.nu, r->cfg.kernel.lengthscale, r->cfg.kernel.output_variance, r->cfg.noise);
       if (r->graphs.key != key) {
         r->graphs.release();
@@ -1750,6 +1755,8 @@ static int execute_round(gtc_group* g) {
       size_t sm;
       app[i] = make_append_args(r->gp.dev, kparams(r->cfg.kernel), r->cfg.noise, r->space->dev(), q.pos, nullptr,
                                 q.y_raw, q.n0, q.newly ? r->visited : nullptr, &sm);
+      app[i].V = r->V;  // bordered row from the pick's V column (exact substitution below the margin)
+      app[i].tile_stride = r->tile_stride;
       const VarPartials vp = r->vp();
       ext[i] = make_pass_args(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, q.n0, r->mu,
                               r->var, &vp, r->tstat);
@@ -2000,6 +2007,7 @@ extern "C" int gtc_debug_append_marks(const gtc_run* r, uint64_t* marks) {
   return GTC_OK;
 }
 
+extern "C" int64_t gtc_run_exact_rows(const gtc_run* r) { return r ? (int64_t)r->gp.h_sc->exact_rows : -1; }
 extern "C" uint64_t gtc_run_stream(const gtc_run* r) { return r ? (uint64_t)(uintptr_t)r->stream : 0; }
 
 // =============================================================== stand-alone GpModel

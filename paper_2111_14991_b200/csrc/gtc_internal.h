@@ -21,7 +21,8 @@ constexpr int kCtaThreads = 256;           // single-CTA GP kernels
 constexpr int kMaxRows = 8;                // rows per multi-row extend pass (rebuild)
 constexpr int kMaxNmax = 1024;             // largest supported GP training size
 constexpr int kMaxDim = 64;                // largest supported search-space dimension
-constexpr size_t kCtaSmemLimit = 226 * 1024;  // L + Dinv staging budget of the single-CTA kernels
+constexpr size_t kCtaSmemLimit = 208 * 1024;  // dynamic staging budget of the single-CTA kernels (their static
+                                              // shared arrays need the rest of the 227 KB)
 
 struct KernelParams {
   int nu;
@@ -36,9 +37,10 @@ struct GpScalars {
   double y_std;
   double jitter;
   int32_t n;      // observations in the model
-  int32_t status; // 0 ok, 1 pivot <= 0 (factorisation failed)
+  int32_t status; // 0 ok, 1 pivot <= 0 (factorisation failed), 2 the bordered row taken from the
+                  // V column had a pivot below the exactness margin: the exact row is pending
   int32_t fail_row;
-  int32_t pad;
+  int32_t exact_rows;  // bordered rows that needed the exact substitution after a column attempt
   unsigned long long t[8];  // %globaltimer marks of the last k_gp_append phases (diagnostics)
 };
 
@@ -173,9 +175,12 @@ void launch_gp_factor(const GpDev& g, KernelParams k, double noise, double jitte
 // Single-CTA: append observation n0 (coords taken from `space` at `pos`, or
 // from `x_explicit` when pos < 0) to the factor; updates scalars and beta.
 // Optionally sets the visited bit of `pos`.
+// With V (the run's resident V, tile-major) the bordered row is taken from
+// candidate pos's V column when its pivot clears the margin (column_border_row).
 void launch_gp_append(const GpDev& g, KernelParams k, double noise, const SpaceDev& space,
                       int64_t pos, const double* x_explicit, double y_new, int n0,
-                      uint32_t* visited_mark, cudaStream_t stream);
+                      uint32_t* visited_mark, cudaStream_t stream, const double* V = nullptr,
+                      int64_t tile_stride = 0);
 // Single-CTA: recompute stats/beta for the prefix of n observations.
 void launch_gp_truncate(const GpDev& g, int n, cudaStream_t stream);
 
@@ -202,8 +207,10 @@ struct AppendArgs {
   int n0;
   uint32_t* visited_mark;
   int staged;
-  const LoopDev* loop;  // resident loop: pos / y_new / n0 from the loop state (no-op unless valid)
-  int stable_rows;      // resident loop: rows of L that no step of the chunk changes (staged early)
+  const LoopDev* loop;  // resident loop: pos / y_new / n0 from the loop state; the kernel is then only
+                        // the exact fallback of the selection's column row (no-op unless status == 2)
+  const double* V;      // resident V (tile-major): the bordered row is taken from the observed
+  int64_t tile_stride;  // candidate's V column when set (null: exact forward substitution only)
 };
 
 struct ExtendArgs {
@@ -392,6 +399,14 @@ struct LoopDev {
   double lambda_constant;
   double cv_mu_s;
   double cv_var_s;
+  // the bordered append of a valid step, run by the selection's last block
+  // from the pick's V column (column_border_row)
+  GpDev g;
+  KernelParams kp;
+  double noise;
+  SpaceDev sp;
+  const double* V;
+  int64_t tile_stride;
 };
 // Loop-mode launches of the bordered append / single-row pass (args.loop set;
 // smem / args.n0 sized for the largest row of the chunk).

@@ -149,6 +149,30 @@ __device__ long long block_sum_ll(long long v, long long* red) {
   return warp_sum_ll(t);
 }
 
+// Deterministic sums of the O(n) GP vectors that do not depend on the block
+// size: element q belongs to virtual lane q % 256 (ascending q within a
+// lane), and the 256 lane partials are combined with exactly the tree of
+// block_sum in a 256-thread block.  The bordered append runs in 256-thread
+// GP kernels and in the selection's last block (128 or 512 threads); with
+// these sums both give bit-identical factors.  `lanes[k][256]` hold the lane
+// partials (written by the caller before the call); every thread gets out[k].
+template <int K>
+__device__ void vsum256(double (*lanes)[256], double* out, double* red /* >= 8 K */) {
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int vw = w; vw < 8; vw += nw) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const double v = warp_sum(lanes[k][vw * 32 + lane]);
+      if (lane == 0) red[k * 8 + vw] = v;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = warp_sum(lane < 8 ? red[k * 8 + lane] : 0.0);
+  __syncthreads();  // lanes / red reusable
+}
+
 __device__ __forceinline__ bool visited_bit(const uint32_t* visited, int64_t j) {
   return (__ldg(visited + (j >> 5)) >> (j & 31)) & 1u;
 }
@@ -298,19 +322,33 @@ __device__ void cta_forward_solve(const double* Lp, int n, double* x, const doub
 }
 
 // Standardisation + beta for the first n observations (gp.hpp:97-103,130).
-// Deterministic block-tree sums (fixed order for a given n).
-__device__ void cta_stats_beta(const GpDev& g, int n, double* red) {
+// Deterministic virtual-lane sums (fixed order for a given n, any block size).
+// `ysum`: the sum of y[0, n) when the caller already reduced it (have_ysum).
+__device__ void cta_stats_beta(const GpDev& g, int n, bool have_ysum = false, double ysum = 0.0) {
+  __shared__ double lanes[1][256];
+  __shared__ double red[8];
   __shared__ double s_y0;
-  double part = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) part = __dadd_rn(part, g.y[i]);
-  const double sum = block_sum(part, red);
-  const double mean = n > 0 ? __ddiv_rn(sum, (double)n) : 0.0;
-  part = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const double dv = __dadd_rn(g.y[i], -mean);
-    part = __dadd_rn(part, __dmul_rn(dv, dv));
+  double out[1];
+  if (!have_ysum) {
+    for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+      double part = 0.0;
+      for (int i = v; i < n; i += 256) part = __dadd_rn(part, g.y[i]);
+      lanes[0][v] = part;
+    }
+    vsum256<1>(lanes, out, red);
+    ysum = out[0];
   }
-  const double ss = block_sum(part, red);
+  const double mean = n > 0 ? __ddiv_rn(ysum, (double)n) : 0.0;
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+    double part = 0.0;
+    for (int i = v; i < n; i += 256) {
+      const double dv = __dadd_rn(g.y[i], -mean);
+      part = __dadd_rn(part, __dmul_rn(dv, dv));
+    }
+    lanes[0][v] = part;
+  }
+  vsum256<1>(lanes, out, red);
+  const double ss = out[0];
   double stdv = 1.0;
   if (n > 1) {
     const double var = __ddiv_rn(ss, (double)n);
@@ -323,10 +361,9 @@ __device__ void cta_stats_beta(const GpDev& g, int n, double* red) {
     g.sc->n = n;
   }
   __syncthreads();
-  const double s_mean = mean, s_std = stdv;
-  const double shift = __dadd_rn(s_mean, -s_y0);
+  const double shift = __dadd_rn(mean, -s_y0);
   for (int i = threadIdx.x; i < n; i += blockDim.x)
-    g.beta[i] = __ddiv_rn(__dadd_rn(g.c[i], -__dmul_rn(shift, g.e[i])), s_std);
+    g.beta[i] = __ddiv_rn(__dadd_rn(g.c[i], -__dmul_rn(shift, g.e[i])), stdv);
   __syncthreads();
 }
 
@@ -426,6 +463,86 @@ __device__ void cta_ce_row(const GpDev& g, int row, const CtaSmem& m, double* re
   __syncthreads();
 }
 
+// Observation n0's training row (coordinates of candidate `pos`, or the
+// explicit point when pos < 0), raw value and squared norm; clears the
+// factorisation status.  Block-wide; ends with a barrier.
+__device__ void append_prologue(const GpDev& g, const SpaceDev& sp, int64_t pos, const double* x_explicit,
+                                double y_new, int n0) {
+  for (int t = threadIdx.x; t < g.d; t += blockDim.x)
+    g.train_x[(int64_t)n0 * g.d + t] = pos >= 0 ? sp.coords[(int64_t)t * sp.n_pad + pos] : x_explicit[t];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int t = 0; t < g.d; ++t) {
+      const double v = g.train_x[(int64_t)n0 * g.d + t];
+      s = __dadd_rn(s, __dmul_rn(v, v));
+    }
+    g.train_n2[n0] = s;
+    g.y[n0] = y_new;
+    g.sc->status = 0;
+    g.sc->fail_row = -1;
+    if (n0 == 0) g.sc->y0 = y_new;
+  }
+  __syncthreads();
+}
+
+// Bordered row n0 from the resident V column of the observed candidate.
+// The predictive pass already holds, for every candidate x, the forward
+// substitution V(:, x) = L^-1 k(X, x) (gp.hpp:163-164) -- which is exactly the
+// new row l = L^-1 k(X, x*) of the bordered factor (gp.hpp:105-121 restricted
+// to the last row).  The two differ only in how k is rounded: the reference's
+// Gram matrix uses direct differences (gp.hpp:110), the cross covariance the
+// expansion form (gp.hpp:176-179), both within a few ulp of the exact kernel.
+// So the row costs n0 strided loads and three block sums instead of an
+// n0-step dependent substitution chain.  The pivot x = k(0) + noise + jitter
+// - |l|^2 is a cancellation: when it is below 2^-8 of the diagonal (the
+// candidate is close to observed points, where the rounding of l matters
+// relative to x, and where the reference's own LLT test x <= 0 may flip) the
+// row is left to the exact substitution (returns false, nothing written).
+// `col` = V(0, x*), consecutive rows `col_stride` apart.  Block-wide.
+// (k(0) = s2 for every nu: the Matern polynomial is 1 and exp(0) = 1 exactly.)
+// One fused reduction gives |l|^2, l.c, l.e and the sum of y[0, n0] (the
+// standardisation's mean), then cta_stats_beta finishes; all sums are
+// virtual-lane sums, so the result does not depend on the block size.
+__device__ bool column_border_row(const GpDev& g, KernelParams k, double noise, const double* col,
+                                  int64_t col_stride, int n0, double* xs) {
+  __shared__ double lanes[4][256];
+  __shared__ double red[32];
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+    double sq = 0.0, pc = 0.0, pe = 0.0, py = 0.0;
+    for (int q = v; q < n0; q += 256) {
+      const double l = __ldcg(col + (int64_t)q * col_stride);
+      xs[q] = l;
+      sq = __dadd_rn(sq, __dmul_rn(l, l));
+      pc = __dadd_rn(pc, __dmul_rn(l, g.c[q]));
+      pe = __dadd_rn(pe, __dmul_rn(l, g.e[q]));
+      py = __dadd_rn(py, g.y[q]);
+    }
+    if (v == n0 % 256) py = __dadd_rn(py, g.y[n0]);  // the new observation, last in its lane
+    lanes[0][v] = sq;
+    lanes[1][v] = pc;
+    lanes[2][v] = pe;
+    lanes[3][v] = py;
+  }
+  double r[4];
+  vsum256<4>(lanes, r, red);
+  const double diag = __dadd_rn(k.s2, __dadd_rn(noise, g.sc->jitter));
+  const double x = __dadd_rn(diag, -r[0]);
+  if (!(x > 0x1p-8 * diag)) return false;
+  const double lnn = sqrt(x);
+  double* Lrow = g.L + packed(n0);
+  for (int q = threadIdx.x; q < n0; q += blockDim.x) Lrow[q] = xs[q];
+  if (threadIdx.x == 0) {
+    Lrow[n0] = lnn;
+    const double yr = __dadd_rn(g.y[n0], -g.sc->y0);
+    g.c[n0] = __ddiv_rn(__dadd_rn(yr, -r[1]), lnn);
+    g.e[n0] = __ddiv_rn(__dadd_rn(1.0, -r[2]), lnn);
+  }
+  __syncthreads();
+  cta_stats_beta(g, n0 + 1, true, r[3]);
+  return true;
+}
+
 // Rows [0, rows) of the packed factor into shared memory with TMA bulk copies
 // (cp.async.bulk global->shared, completion on an mbarrier): the factor is
 // evicted from L2 by every V stream, and one SM pulling 194 KB with scalar
@@ -502,7 +619,7 @@ __global__ void __launch_bounds__(kCtaThreads)
     }
   }
   for (int row = 0; row < n; ++row) cta_ce_row(g, row, m, red);
-  cta_stats_beta(g, n, red);
+  cta_stats_beta(g, n);
 }
 
 template <int NU>
@@ -510,88 +627,49 @@ __device__ void gp_append_body(const AppendArgs& a) {
   const GpDev& g = a.g;
   const KernelParams k = a.k;
   const double noise = a.noise;
-  const SpaceDev& sp = a.sp;
   int64_t pos = a.pos;
-  const double* x_explicit = a.x_explicit;
-  double y_new = a.y_new;
   int n0 = a.n0;
-  uint32_t* visited_mark = a.visited_mark;
-  const int staged = a.staged;
   extern __shared__ double smem[];
   __shared__ double red[32];
-  __shared__ double xnew[64];
-  __shared__ __align__(8) uint64_t pre_bar;
-  const CtaSmem m = cta_smem_layout(smem, g.n_max, n0 + 1, staged != 0);
-  if (a.loop) {  // resident loop: this step's evaluation (loop_advance)
-    pdl_trigger();
-    // rows [0, stable_rows) of L do not change during the chunk: stage them
-    // while the selection that produces this step's pick drains
-    const int pre = staged ? a.stable_rows : 0;
-    const uint32_t bar = smem_u32(&pre_bar);
-    if (pre > 0 && threadIdx.x == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      const uint32_t bytes = static_cast<uint32_t>(staged_l_doubles(pre) * 8);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-      bulk_g2s(smem_u32(m.Ls), g.L, bytes, bar);
-    }
-    pdl_wait();
-    const LoopDev* lp = a.loop;
-    const bool go = lp->halt == kLoopRunning && lp->valid;
-    pos = lp->pos;
-    y_new = lp->y;
-    n0 = lp->n0;
-    if (pre > 0) {
-      __syncthreads();  // barrier initialised before anyone waits on it
-      asm volatile(
-          "{\n"
-          ".reg .pred p;\n"
-          "WAIT_%=:\n"
-          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
-          "@!p bra WAIT_%=;\n"
-          "}\n" ::"r"(bar)
-          : "memory");
-    }
-    if (!go) return;  // (after the bulk copy landed)
-    if (staged)  // the rows appended during this chunk
-      for (int64_t i = packed(pre) + threadIdx.x; i < packed(n0); i += blockDim.x) m.Ls[i] = g.L[i];
-  } else {
-    pdl_begin();
-  }
+  const CtaSmem m = cta_smem_layout(smem, g.n_max, n0 + 1, a.staged != 0);
+  pdl_begin();
   unsigned long long* tm = g.sc->t;
-  if (threadIdx.x == 0) tm[0] = gtc_globaltimer();
-  if (visited_mark && threadIdx.x == 0) visited_mark[pos >> 5] |= 1u << (pos & 31);
-  for (int t = threadIdx.x; t < g.d; t += blockDim.x) {
-    const double v = pos >= 0 ? sp.coords[(int64_t)t * sp.n_pad + pos] : x_explicit[t];
-    xnew[t] = v;
-    g.train_x[(int64_t)n0 * g.d + t] = v;
+  if (a.loop) {
+    // resident loop: the selection's last block already appended this step's
+    // observation from the pick's V column; this kernel only runs the exact
+    // bordered row when that pivot fell below the margin (status 2)
+    const LoopDev* lp = a.loop;
+    if (lp->halt != kLoopRunning || !lp->valid || g.sc->status != 2) return;
+    pos = lp->pos;
+    n0 = lp->n0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      g.sc->status = 0;
+      ++g.sc->exact_rows;
+    }
+  } else {
+    if (a.visited_mark && threadIdx.x == 0) a.visited_mark[pos >> 5] |= 1u << (pos & 31);
+    append_prologue(g, a.sp, pos, a.x_explicit, a.y_new, n0);
+    if (threadIdx.x == 0) tm[0] = gtc_globaltimer();
+    if (a.V && pos >= 0) {
+      const double* col = a.V + (pos / kTile) * a.tile_stride + pos % kTile;
+      if (column_border_row(g, k, noise, col, kTile, n0, m.xs)) return;
+      if (threadIdx.x == 0) ++g.sc->exact_rows;
+    }
   }
-  if (threadIdx.x == 0) {
-    g.y[n0] = y_new;
-    g.sc->status = 0;
-    g.sc->fail_row = -1;
-    if (n0 == 0) g.sc->y0 = y_new;
-  }
-  if (a.loop)
-    __syncthreads();  // staged above
-  else
-    cta_stage_L(g, n0, m);  // includes __syncthreads
+  // exact bordered row: forward substitution over the staged factor
+  cta_stage_L(g, n0, m);  // includes __syncthreads
   {
     const double* lp = lp_of(g, m);
     for (int i = threadIdx.x; i < n0; i += blockDim.x) m.rinv[i] = __drcp_rn(lp[packed(i) + i]);
   }  // visible after the Gram-row barrier in cta_border_row
-  if (threadIdx.x == 0) {
-    tm[1] = gtc_globaltimer();
-    double s = 0.0;
-    for (int t = 0; t < g.d; ++t) s = __dadd_rn(s, __dmul_rn(xnew[t], xnew[t]));
-    g.train_n2[n0] = s;
-  }
+  if (threadIdx.x == 0) tm[1] = gtc_globaltimer();
   const double jitter = g.sc->jitter;
   if (!cta_border_row<NU>(g, k, noise, jitter, n0, m, red, tm)) return;
   if (threadIdx.x == 0) tm[4] = gtc_globaltimer();
   cta_ce_row(g, n0, m, red);
   if (threadIdx.x == 0) tm[5] = gtc_globaltimer();
-  cta_stats_beta(g, n0 + 1, red);
+  cta_stats_beta(g, n0 + 1);
   if (threadIdx.x == 0) tm[6] = gtc_globaltimer();
 }
 
@@ -609,8 +687,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_gp_append_batch(const AppendArg
 }
 
 __global__ void k_gp_truncate(GpDev g, int n) {
-  __shared__ double red[32];
-  cta_stats_beta(g, n, red);
+  cta_stats_beta(g, n);
 }
 
 // ------------------------------------------------------------ V extension
@@ -1365,56 +1442,12 @@ void launch_portfolio_trace(const PortDev& P, const PortOp* d_ops, int n, PortSt
   k_portfolio_trace<<<1, 32, 0, s>>>(P, d_ops, n, d_out);
 }
 
+// The selection result from the merged partials (one thread): the
+// first-candidate rule, the cross-shard merge pieces, then the resident
+// loop's advance.
 template <uint32_t MASK>
-__device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first_finite, long long cnt,
-                              double best, double lambda, double mean_var, int cv_fallback, int gp_status) {
-  __shared__ SelPart red[32];
-  __shared__ bool is_last;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  SelPart v{{b[0], b[1], b[2]}, first, first_finite, cnt};
-  v = sel_warp_reduce<MASK>(v);
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  if (warp == 0) {
-    const SelPart none{{{0.0, INT64_MAX}, {0.0, INT64_MAX}, {0.0, INT64_MAX}}, INT64_MAX, 1, 0};
-    v = sel_warp_reduce<MASK>(lane < nw ? red[lane] : none);
-    if (lane == 0) {
-      for (int af = 0; af < 3; ++af) {
-        c.b.pscore[blockIdx.x * 3 + af] = v.b[af].s;
-        c.b.ppos[blockIdx.x * 3 + af] = v.b[af].p;
-      }
-      c.b.pfirst[blockIdx.x] = v.first;
-      c.b.pfinite[blockIdx.x] = v.finite;
-      c.b.pcnt[blockIdx.x] = v.cnt;
-      __threadfence();
-      is_last = atomicAdd(c.b.counter, 1u) == gridDim.x - 1;
-    }
-  }
-  __syncthreads();
-  SEL_MARK(5);
-  if (!is_last) return;
-  // last block: merge the per-block records (all loads in flight at once)
-  __threadfence();
-  const SelPart none{{{0.0, INT64_MAX}, {0.0, INT64_MAX}, {0.0, INT64_MAX}}, INT64_MAX, 1, 0};
-  SelPart f = none;
-  for (int blk = threadIdx.x; blk < (int)gridDim.x; blk += blockDim.x) {
-    SelPart y;
-#pragma unroll
-    for (int af = 0; af < 3; ++af)
-      y.b[af] = Best{__ldcg(c.b.pscore + blk * 3 + af),
-                     (int64_t)__ldcg(reinterpret_cast<const long long*>(c.b.ppos) + blk * 3 + af)};
-    y.first = (int64_t)__ldcg(reinterpret_cast<const long long*>(c.b.pfirst) + blk);
-    y.finite = __ldcg(c.b.pfinite + blk);
-    y.cnt = __ldcg(c.b.pcnt + blk);
-    f = sel_merge<MASK>(f, y);
-  }
-  f = sel_warp_reduce<MASK>(f);
-  __syncthreads();  // red[] reuse
-  if (lane == 0) red[warp] = f;
-  __syncthreads();
-  if (warp != 0) return;
-  f = sel_warp_reduce<MASK>(lane < nw ? red[lane] : none);
-  if (lane != 0) return;
+__device__ void select_publish(const SelCtx& c, const SelPart& f, double best, double lambda, double mean_var,
+                               int cv_fallback, int gp_status) {
   const int64_t ff = f.first;
   const long long fc = f.cnt;
   c.out->first_nan_mask = 0;
@@ -1462,6 +1495,80 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first
   g_sel_trace[blockIdx.x][6] = gtc_globaltimer();
 #endif
 }
+
+// The bordered append of the resident loop's valid step, by the selection's
+// last block right after loop_advance: training row, then the new factor row
+// from the pick's V column (column_border_row).  When its pivot is below the
+// margin, status 2 leaves the exact row to the loop's append kernel (which is
+// a no-op otherwise) and the predictive pass waits for it.
+__device__ void loop_column_append(LoopDev* L) {
+  __shared__ double xs[kMaxNmax];
+  if (L->halt != kLoopRunning || !L->valid) return;  // (uniform: written before the barrier)
+  const int64_t pos = L->pos;
+  const int n0 = L->n0;
+  const GpDev g = L->g;
+  append_prologue(g, L->sp, pos, nullptr, L->y, n0);
+  const double* col = L->V + (pos / kTile) * L->tile_stride + pos % kTile;
+  if (!column_border_row(g, L->kp, L->noise, col, kTile, n0, xs) && threadIdx.x == 0) g.sc->status = 2;
+}
+
+template <uint32_t MASK>
+__device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first_finite, long long cnt,
+                              double best, double lambda, double mean_var, int cv_fallback, int gp_status) {
+  __shared__ SelPart red[32];
+  __shared__ bool is_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  SelPart v{{b[0], b[1], b[2]}, first, first_finite, cnt};
+  v = sel_warp_reduce<MASK>(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    const SelPart none{{{0.0, INT64_MAX}, {0.0, INT64_MAX}, {0.0, INT64_MAX}}, INT64_MAX, 1, 0};
+    v = sel_warp_reduce<MASK>(lane < nw ? red[lane] : none);
+    if (lane == 0) {
+      for (int af = 0; af < 3; ++af) {
+        c.b.pscore[blockIdx.x * 3 + af] = v.b[af].s;
+        c.b.ppos[blockIdx.x * 3 + af] = v.b[af].p;
+      }
+      c.b.pfirst[blockIdx.x] = v.first;
+      c.b.pfinite[blockIdx.x] = v.finite;
+      c.b.pcnt[blockIdx.x] = v.cnt;
+      __threadfence();
+      is_last = atomicAdd(c.b.counter, 1u) == gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  SEL_MARK(5);
+  if (!is_last) return;
+  // last block: merge the per-block records (all loads in flight at once)
+  __threadfence();
+  const SelPart none{{{0.0, INT64_MAX}, {0.0, INT64_MAX}, {0.0, INT64_MAX}}, INT64_MAX, 1, 0};
+  SelPart f = none;
+  for (int blk = threadIdx.x; blk < (int)gridDim.x; blk += blockDim.x) {
+    SelPart y;
+#pragma unroll
+    for (int af = 0; af < 3; ++af)
+      y.b[af] = Best{__ldcg(c.b.pscore + blk * 3 + af),
+                     (int64_t)__ldcg(reinterpret_cast<const long long*>(c.b.ppos) + blk * 3 + af)};
+    y.first = (int64_t)__ldcg(reinterpret_cast<const long long*>(c.b.pfirst) + blk);
+    y.finite = __ldcg(c.b.pfinite + blk);
+    y.cnt = __ldcg(c.b.pcnt + blk);
+    f = sel_merge<MASK>(f, y);
+  }
+  f = sel_warp_reduce<MASK>(f);
+  __syncthreads();  // red[] reuse
+  if (lane == 0) red[warp] = f;
+  __syncthreads();
+  if (warp == 0) {
+    f = sel_warp_reduce<MASK>(lane < nw ? red[lane] : none);
+    if (lane == 0) select_publish<MASK>(c, f, best, lambda, mean_var, cv_fallback, gp_status);
+  }
+  if (c.loop) {
+    __syncthreads();  // loop_advance (thread 0) done
+    loop_column_append(c.loop);
+  }
+}
+
 
 // ---------------------------------------------------- pruned selection
 //
@@ -1977,9 +2084,10 @@ static size_t cta_smem_bytes(int n_max, int rows, bool* staged) {
 // when the requirement grows, not on every launch of the observe step).
 template <class K>
 static void opt_in_smem(K kernel, size_t bytes) {
-  // the 48 KB default covers static + dynamic shared memory: opt in with room
-  // for the kernels' static arrays
-  if (bytes + 8 * 1024 <= 48 * 1024) return;
+  // the 48 KB default covers static + dynamic shared memory, so every kernel
+  // with dynamic shared memory opts in once (the static arrays of the GP
+  // kernels alone take 12-25 KB)
+  if (bytes == 0) return;
   static std::mutex mu;
   static std::vector<std::pair<std::pair<const void*, int>, size_t>> set_to;
   int dev = 0;
@@ -2020,10 +2128,12 @@ AppendArgs make_append_args(const GpDev& g, KernelParams k, double noise, const 
 
 void launch_gp_append(const GpDev& g, KernelParams k, double noise, const SpaceDev& sp,
                       int64_t pos, const double* x_explicit, double y_new, int n0,
-                      uint32_t* visited_mark, cudaStream_t s) {
+                      uint32_t* visited_mark, cudaStream_t s, const double* V, int64_t tile_stride) {
   count_launch();
   size_t sm;
-  const AppendArgs a = make_append_args(g, k, noise, sp, pos, x_explicit, y_new, n0, visited_mark, &sm);
+  AppendArgs a = make_append_args(g, k, noise, sp, pos, x_explicit, y_new, n0, visited_mark, &sm);
+  a.V = V;
+  a.tile_stride = tile_stride;
   switch (k.nu) {
     case 0: opt_in_smem(k_gp_append<0>, sm); launch_pdl(k_gp_append<0>, 1, kCtaThreads, sm, s, a); break;
     case 1: opt_in_smem(k_gp_append<1>, sm); launch_pdl(k_gp_append<1>, 1, kCtaThreads, sm, s, a); break;

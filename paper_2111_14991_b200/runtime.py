@@ -241,6 +241,11 @@ class SurrogateRun:
                                    C.byref(done), C.byref(info)))
         return recs[:done.value]
 
+    def exact_rows(self) -> int:
+        """Bordered rows that needed the exact forward substitution because
+        the V-column pivot was below the exactness margin."""
+        return int(load().gtc_run_exact_rows(self._h))
+
     def last_steps_ms(self) -> float:
         return float(load().gtc_last_steps_ms(self._h))
 

@@ -35,6 +35,15 @@ TRAJECTORIES = [
     ("rr3d_lcb", "random-rough", "12x12x12", 9, "0.385", "bo-lcb", 150, 20, 4),
 ]
 
+# BASELINE.json configs[2] (C3): synthetic 100k-candidate space (6 params, ~30 %
+# invalid), bo-lcb with contextual variance, budget 220, n_init 20.  Written
+# without the space (1.6 MB): tests regenerate it with
+# paper_2111_14991_b200.synthetic.random_rough, which is pinned bit-exact to
+# the reference generator (space_c3.npz).
+BIG_TRAJECTORIES = [
+    ("c3_lcb", "random-rough", "10x10x10x10x5x2", 20261017, "0.3", "bo-lcb", 220, 20, 1),
+]
+
 
 def run(*args) -> dict:
     out = subprocess.run([str(TOOL), *map(str, args)], check=True, capture_output=True, text=True)
@@ -68,6 +77,13 @@ def main() -> None:
             meta = run("runbo", fn, grid, sseed, inv, strat, budget, n_init, bseed, tmp / name)
             arrs = load_dir(tmp / name)
             np.savez_compressed(HERE / f"traj_{name}.npz", **arrs,
+                                spec=np.array([fn, grid, str(sseed), inv, strat, str(budget), str(n_init), str(bseed)]),
+                                best=np.array([meta["best"]]), warnings=np.array([meta["warnings"]]))
+        for name, fn, grid, sseed, inv, strat, budget, n_init, bseed in BIG_TRAJECTORIES:
+            meta = run("runbo", fn, grid, sseed, inv, strat, budget, n_init, bseed, tmp / name)
+            arrs = load_dir(tmp / name)
+            np.savez_compressed(HERE / f"trajbig_{name}.npz", traj_pos=arrs["traj_pos"], traj_val=arrs["traj_val"],
+                                traj_lambda=arrs["traj_lambda"],
                                 spec=np.array([fn, grid, str(sseed), inv, strat, str(budget), str(n_init), str(bseed)]),
                                 best=np.array([meta["best"]]), warnings=np.array([meta["warnings"]]))
     print("golden fixtures written to", HERE)

@@ -38,6 +38,31 @@ def test_trajectory_matches_reference(gt, path):
     assert run.n_warnings == int(t["warnings"][0])
 
 
+BIG = sorted(__import__("pathlib").Path(__file__).parent.joinpath("golden").glob("trajbig_*.npz"))
+
+
+def big_space(t):
+    fn, grid, sseed, inv = [str(x) for x in t["spec"][:4]]
+    assert fn == "random-rough"
+    return synthetic.random_rough([int(k) for k in grid.split("x")], int(sseed), float(inv))
+
+
+@pytest.mark.parametrize("path", BIG, ids=[p.stem for p in BIG])
+def test_big_trajectory_matches_reference(gt, path):
+    """BASELINE configs[2] (C3: 100k candidates, ~30 % invalid, bo-lcb with
+    contextual variance, budget 220) through the resident loop.  Near-tied
+    picks may legitimately differ (the teacher-forced epsilon check in
+    test_gpu_eps.py is the gate); this pins the full trajectory while it holds."""
+    t = np.load(path)
+    coords, ids, values = big_space(t)
+    run = gt.run_bo(gt.Space(coords), ids, config_of(gt, t), values=values)
+    ref = t["traj_pos"]
+    first_diff = next((i for i in range(len(ref)) if run.positions[i] != ref[i]), None)
+    assert first_diff is None, f"diverged at evaluation {first_diff}"
+    assert run.best_value == t["best"][0]
+    np.testing.assert_allclose(run.lambdas, t["traj_lambda"], rtol=1e-9, atol=1e-12)
+
+
 def test_core_invariants_on_invalid_rich_space(gt):
     """test_strategies.cpp:172-192: never revisit, exact budget, monotone best."""
     coords, ids, values = synthetic.random_rough([13, 13], 17, 0.3)

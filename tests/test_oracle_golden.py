@@ -112,3 +112,48 @@ def test_reference_trajectory_fixtures_are_consistent(golden):
         assert len(pos) == min(budget, len(t["ids"])), f.name
         vals = t["values"][pos]
         np.testing.assert_array_equal(np.isnan(vals), np.isnan(t["traj_val"]))
+
+
+# ---------------------------------------------------------------- dense numpy oracle
+
+
+def _np_oracle():
+    import sys
+    import pathlib
+    sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1] / "oracle"))
+    import gtoracle_np
+    return gtoracle_np
+
+
+def test_np_oracle_matches_reference_golden(golden):
+    """oracle/gtoracle_np.py (LAPACK restatement used by the epsilon checker)
+    against the reference's own GpModel::fit/predict outputs."""
+    O = _np_oracle()
+    g = np.load(golden / "gp_predict.npz")
+    for t in sorted({k.split("_")[0] for k in g.files}):
+        nu, l, s2, y_mean, y_std, jitter = g[f"{t}_meta"]
+        m = O.fit(int(nu), l, s2, g[f"{t}_X"], g[f"{t}_y"])
+        assert m["y_mean"] == pytest.approx(y_mean, rel=1e-14, abs=1e-14)
+        assert m["y_std"] == pytest.approx(y_std, rel=1e-14)
+        assert m["jitter"] == jitter
+        mean, var = O.predict(m, g[f"{t}_Q"], chunk=7)
+        ref_m, ref_v = g[f"{t}_mean"], g[f"{t}_var"]
+        np.testing.assert_allclose(mean, ref_m, rtol=0, atol=1e-9 * max(1.0, np.abs(ref_m).max()))
+        np.testing.assert_allclose(var, ref_v, rtol=0, atol=1e-9 * max(1.0, s2))
+
+
+def test_np_oracle_known_answers():
+    O = _np_oracle()
+    # test_acquisition.cpp:15-32, 59-63, 81-104
+    assert abs(float(O.acquisition(1, 1 + 0.2 - 1.96 * 0.7, 0.7, 1.0, 0.2)) - 0.9750021048517795) <= 1e-9
+    assert abs(float(O.acquisition(0, 1.0, 1.0, 1.0, 0.0)) - 0.3989422804014327) <= 1e-12
+    assert float(O.acquisition(0, 1.0, 0.0, 2.0, 0.5)) == 0.5 and float(O.acquisition(1, 1.0, 0.0, 0.5, 0.1)) == 0.0
+    assert float(O.acquisition(2, 1.5, 0.5, 0.0, 2.0)) == -(1.5 - 2.0 * 0.5)
+    assert abs(O.cv_lambda(10.0, 1.0, 0.5, 5.0) - 0.25) <= 1e-12
+    assert O.cv_lambda(10.0, 1.0, 0.5, 0.0) is None and O.cv_lambda(0.0, 1.0, 0.5, 1.0) is None
+    # portfolio.hpp:32-61 rule: first candidate unconditionally, ties -> lowest position, NaN never wins
+    assert O.best_candidate([1.0, 3.0, 3.0, np.nan]) == 1
+    assert O.best_candidate([np.nan, 3.0]) == 0
+    assert O.eps_optimal([1.0, 1.0 - 5e-10, 0.5], 1) and not O.eps_optimal([1.0, 1.0 - 5e-9, 0.5], 1)
+    with pytest.raises(O.ConditioningError):
+        O.fit(1, 2.0, 1.0, np.full((3, 1), 0.5), np.array([1.0, 2.0, 3.0]), noise=0.0, jitter=1e-300)

@@ -480,6 +480,43 @@ int gtc_shard_observe(gtc_run* run, const double* x_new, int64_t local_pos, doub
 int gtc_shard_select(gtc_run* run, const gtc_select_args* args, double global_var_sum,
                      int64_t global_var_count, gtc_shard_selection* out);
 
+/* ---- device-resident candidate-axis sharding (gtc_run_steps over shards) -- */
+/* The whole iteration stays on the device: per step every shard runs its
+ * selection over its slice, the shards all-gather one record each (the
+ * best non-NaN score/position per acquisition function, the first eligible
+ * position, the winners' coordinates and V columns), every shard merges them
+ * with best_candidate's rule (portfolio.hpp:32-61) and appends the same
+ * bordered row from the winner's V column, then runs its predictive pass and
+ * all-gathers its fixed-point variance accumulators (the global lambda,
+ * strategies.hpp:404-418, summed exactly: bit-identical to one device).  Both
+ * exchanges are enqueued on the run's stream: no host round trip per
+ * iteration.  Picks, lambdas and the factor are identical to the unsharded
+ * gtc_run_steps on the same inputs. */
+typedef struct gtc_comm gtc_comm;
+#define GTC_NCCL_ID_BYTES 128
+/* ncclGetUniqueId (libnccl.so.2 is opened at run time); rank 0 creates it and
+ * the caller distributes the bytes (MPI, torch.distributed, a file...). */
+int gtc_comm_nccl_id(uint8_t* id_out /* GTC_NCCL_ID_BYTES */);
+/* ncclCommInitRank on `device`: one rank per process (or per host thread). */
+int gtc_comm_create_nccl(const uint8_t* id, int32_t rank, int32_t nranks, int32_t device, gtc_comm** out);
+/* Wraps a caller-owned ncclComm_t (passed as void*; not destroyed with the gtc_comm). */
+int gtc_comm_wrap_nccl(void* nccl_comm, gtc_comm** out);
+/* nranks in-process shards (out[0..nranks)), each driven by its own host
+ * thread, on any devices: exchanges are peer copies ordered by CUDA events. */
+int gtc_comm_create_local(int32_t nranks, gtc_comm** out);
+int gtc_comm_destroy(gtc_comm* comm);
+int32_t gtc_comm_rank(const gtc_comm* comm);
+int32_t gtc_comm_size(const gtc_comm* comm);
+/* This run (its space = global candidates [offset, offset + gtc_space_size))
+ * becomes rank gtc_comm_rank(comm) of a sharded run over n_global candidates.
+ * offset must be a multiple of 256 (the tile size: the variance totals are then
+ * bit-identical to one device).  Every rank fits the same observations with
+ * gtc_fit_points, marks its own visited positions (local indices), sets the
+ * GLOBAL value table (gtc_run_set_values with n = n_global) and calls
+ * gtc_run_steps with the same arguments; records carry global positions.
+ * comm = NULL detaches. */
+int gtc_run_attach_comm(gtc_run* run, gtc_comm* comm, int64_t offset, int64_t n_global);
+
 /* Per-candidate acquisition values (acquisition_{ei,pi,lcb}, acquisition.hpp:25-42;
  * the LCB slot returns -lcb like best_candidate's score, portfolio.hpp:47). */
 int gtc_acquisition_scores(int device, int32_t af, const double* means, const double* stds,

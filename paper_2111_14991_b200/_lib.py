@@ -195,6 +195,14 @@ SIGNATURES = [
     ("gtc_group_leave", C.c_int, [P]),
     ("gtc_run_set_group", C.c_int, [P, P]),
     ("gtc_cache_checksum", C.c_uint64, [U64P, DP, U8P, C.c_int64]),
+    ("gtc_comm_nccl_id", C.c_int, [U8P]),
+    ("gtc_comm_create_nccl", C.c_int, [U8P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(P)]),
+    ("gtc_comm_wrap_nccl", C.c_int, [C.c_void_p, C.POINTER(P)]),
+    ("gtc_comm_create_local", C.c_int, [C.c_int32, C.POINTER(P)]),
+    ("gtc_comm_destroy", C.c_int, [P]),
+    ("gtc_comm_rank", C.c_int32, [P]),
+    ("gtc_comm_size", C.c_int32, [P]),
+    ("gtc_run_attach_comm", C.c_int, [P, P, C.c_int64, C.c_int64]),
     ("gtc_run_bo_batch", C.c_int, [P, U64P, C.POINTER(gtc_bo_config), C.c_int32, DP, C.c_int32,
                                    C.POINTER(gtc_bo_record), DP, C.c_int64, C.POINTER(gtc_bo_summary),
                                    C.POINTER(C.c_int32)]),

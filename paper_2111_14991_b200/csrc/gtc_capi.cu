@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../../include/gridtune_cuda.h"
+#include "gtc_comm.hpp"
 #include "gtc_internal.h"
 #include "restriction.hpp"
 
@@ -259,6 +260,15 @@ struct gtc_run {
   // candidate-axis sharding: this run's candidates are global positions
   // [shard_offset, shard_offset + space->n)
   int64_t shard_offset = 0;
+  // device-resident sharding of the resident loop (gtc_run_attach_comm)
+  gtc_comm* comm = nullptr;
+  int64_t n_global = 0;
+  unsigned char* d_send = nullptr;  // this shard's selection record
+  unsigned char* d_recv = nullptr;  // [nranks] gathered records
+  VarAccum* d_gacc = nullptr;       // [nranks][2] gathered accumulators
+  double* d_xrec = nullptr;         // [rec_cap][d] pick coordinates per step
+  int xrec_cap = 0;
+  std::vector<double> xrec_host;
   double* d_xnew = nullptr;       // device copy of an explicit new point (d doubles)
   double* h_xnew = nullptr;       // pinned staging
   struct Readback {
@@ -284,6 +294,7 @@ struct gtc_run {
   VarAccum* live_acc() const { return acc_valid && predictions_valid ? acc + acc_gen : nullptr; }
   // resident loop (gtc_run_steps): value table, loop state, step records
   double* d_values = nullptr;
+  int64_t values_cap = 0;
   bool has_values = false;
   LoopDev* d_loop = nullptr;
   LoopDev* h_loop = nullptr;  // pinned
@@ -666,6 +677,10 @@ extern "C" int gtc_run_destroy(gtc_run* r) {
   cudaFree(r->d_loop);
   cudaFree(r->d_rec);
   cudaFree(r->d_sorted_y);
+  cudaFree(r->d_send);
+  cudaFree(r->d_recv);
+  cudaFree(r->d_gacc);
+  cudaFree(r->d_xrec);
   if (r->h_loop) cudaFreeHost(r->h_loop);
   for (cudaEvent_t ev : r->step_events) cudaEventDestroy(ev);
   r->graphs.release();
@@ -782,6 +797,8 @@ extern "C" int gtc_run_reset(gtc_run* r, const gtc_model_config* cfg) {
   r->y_host.clear();
   r->x_host.clear();
   r->shard_offset = 0;
+  r->comm = nullptr;
+  r->n_global = 0;
   r->group = nullptr;
   r->has_values = false;
   r->port = PortDev{};
@@ -1164,10 +1181,16 @@ extern "C" int gtc_portfolio_trace(int device, const gtc_portfolio_config* c, co
 
 extern "C" int gtc_run_set_values(gtc_run* r, const double* values, int64_t n) {
   if (!r || !values) return fail(GTC_ERR_INVALID, "null argument");
-  if (n != r->space->n) return fail(GTC_ERR_INVALID, "value table size != space size");
+  const int64_t want = r->comm ? r->n_global : r->space->n;  // sharded: the GLOBAL table
+  if (n != want) return fail(GTC_ERR_INVALID, "value table size != space size");
   GTC_CUDA(cudaSetDevice(r->space->device));
   int rc;
-  if (!r->d_values && (rc = dalloc(&r->d_values, (size_t)r->space->n))) return rc;
+  if (r->d_values && r->values_cap < n) {
+    cudaFree(r->d_values);
+    r->d_values = nullptr;
+  }
+  if (!r->d_values && (rc = dalloc(&r->d_values, (size_t)n))) return rc;
+  r->values_cap = n;
   GTC_CUDA(cudaMemcpyAsync(r->d_values, values, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, r->stream));
   GTC_CUDA(cudaStreamSynchronize(r->stream));
   r->has_values = true;
@@ -1176,18 +1199,28 @@ extern "C" int gtc_run_set_values(gtc_run* r, const double* values, int64_t n) {
 
 // Host bookkeeping of the steps a resident chunk ran (the same updates
 // gtc_observe makes per call).
-static void replay_steps(gtc_run* r, const StepRec* rec, int m, bool hold, int hold_n0, int64_t* hold_prev) {
+// Sharded runs: positions are global, the marks land on the owning shard
+// only and the coordinates come from the step's record (xrec).
+static void replay_steps(gtc_run* r, const StepRec* rec, int m, bool hold, int hold_n0, int64_t* hold_prev,
+                         const double* xrec = nullptr) {
+  const int64_t off = r->comm ? r->shard_offset : 0;
+  auto local = [&](int64_t pos) -> int64_t {
+    const int64_t p = pos - off;
+    return p >= 0 && p < r->space->n ? p : -1;
+  };
   for (int i = 0; i < m; ++i) {
     const int64_t pos = rec[i].position;
+    const int64_t lp = local(pos);
     if (rec[i].valid) {
       if (hold) {
-        if (*hold_prev >= 0) host_mark(r, *hold_prev, 0);
+        if (*hold_prev >= 0 && local(*hold_prev) >= 0) host_mark(r, local(*hold_prev), 0);
         *hold_prev = pos;
         keep_obs(r, hold_n0);
       }
-      push_obs(r, &r->space->host_coords[(size_t)pos * r->space->d], rec[i].value);
+      push_obs(r, xrec ? xrec + (size_t)i * r->space->d : &r->space->host_coords[(size_t)pos * r->space->d],
+               rec[i].value);
     }
-    host_mark(r, pos, 1);
+    if (lp >= 0) host_mark(r, lp, 1);
   }
 }
 
@@ -1229,6 +1262,16 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     GTC_CUDA(cudaMallocHost(&r->h_loop, sizeof(LoopDev)));
   }
   if (portfolio && !r->d_sorted_y && (rc = dalloc(&r->d_sorted_y, (size_t)r->cfg.n_max))) return rc;
+  const bool sharded = r->comm != nullptr;
+  const int d = r->space->d;
+  if (sharded && r->xrec_cap < k) {
+    cudaFree(r->d_xrec);
+    r->d_xrec = nullptr;
+    r->xrec_cap = 0;
+    if ((rc = dalloc(&r->d_xrec, (size_t)k * d))) return rc;
+    r->xrec_cap = k;
+  }
+  const int64_t rec_bytes = shard_record_bytes(mask, d, r->cfg.n_max);
   int af = 0;
   while (!((mask >> af) & 1u)) ++af;
   const int hold_n0 = r->n;  // hold: every valid step appends at this row
@@ -1237,12 +1280,12 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
   bool refitted = false;
   while (*done < k) {
     const int m = k - *done;
-    if (r->space->n - r->visited_count <= 0) break;
+    if (!sharded && r->space->n - r->visited_count <= 0) break;  // (sharded: the merge halts on the global count)
     if ((rc = ensure_predictions(r)) || (rc = ensure_var_totals(r))) return rc;
     const bool timing = (flags & GTC_STEPS_TIMING) != 0;
     // graph-launched chunks (see below) size for the largest row, so that one
     // captured graph serves every chunk of the run handle
-    bool graphed = !r->pdl && !timing && !r->graphs.failed;
+    bool graphed = !r->pdl && !timing && !r->graphs.failed && !sharded;
     const int n0_max = hold ? hold_n0 : graphed ? r->cfg.n_max - 1 : std::min(r->n + m - 1, r->cfg.n_max - 1);
     LoopDev& L = *r->h_loop;
     L = LoopDev{};
@@ -1289,6 +1332,17 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     L.sp = r->space->dev();
     L.V = r->V;
     L.tile_stride = r->tile_stride;
+    if (sharded) {
+      L.nranks = r->comm->nranks;
+      L.offset = r->shard_offset;
+      L.send = r->d_send;
+      L.recv = r->d_recv;
+      L.rec_bytes = rec_bytes;
+      L.gacc = r->d_gacc;
+      L.xrec = r->d_xrec;
+      L.gsel = r->red.sel;
+    }
+    L.sel_mask = mask;
     GTC_CUDA(cudaMemcpyAsync(r->d_loop, r->h_loop, sizeof(LoopDev), cudaMemcpyHostToDevice, r->stream));
     // (every per-run / per-step selection input is read from the loop state:
     // the launch arguments depend only on the run handle and its model config)
@@ -1354,11 +1408,32 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
       }
     }
     GTC_CUDA(cudaEventRecord(r->ev_step0, r->stream));
+    if (sharded) {
+      // per step: local selection -> all-gather of the records -> merge + loop
+      // advance + column row -> (exact row fallback) -> local pass -> all-gather
+      // of the accumulators; the chunk starts with the accumulators' exchange
+      const size_t acc_bytes = 2 * sizeof(VarAccum);
+      if ((rc = r->comm->allgather(r->acc, r->d_gacc, acc_bytes, r->stream))) return rc;
+      for (int i = 0; i < m; ++i) {
+        if (timing) GTC_CUDA(cudaEventRecord(te[3 * i], r->stream));
+        launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, vs, r->tstat, r->red.b, r->red.sel,
+                      r->stream);
+        GTC_LAUNCHED();
+        if ((rc = r->comm->allgather(r->d_send, r->d_recv, (size_t)rec_bytes, r->stream))) return rc;
+        launch_shard_merge(r->d_loop, r->cfg.kernel.nu, r->stream);
+        if (timing) GTC_CUDA(cudaEventRecord(te[3 * i + 1], r->stream));
+        launch_gp_append_loop(aa, r->cfg.kernel.nu, append_smem, r->stream);
+        if (timing) GTC_CUDA(cudaEventRecord(te[3 * i + 2], r->stream));
+        launch_extend_loop(ea, r->space->n_pad / kTile, r->cfg.kernel.nu, r->stream);
+        GTC_LAUNCHED();
+        if ((rc = r->comm->allgather(r->acc, r->d_gacc, acc_bytes, r->stream))) return rc;
+      }
+    }
     if (graphed) {
       for (int i = 0; i + kSteps <= m; i += kSteps) GTC_CUDA(cudaGraphLaunch(r->graphs.many, r->stream));
       for (int i = m - m % kSteps; i < m; ++i) GTC_CUDA(cudaGraphLaunch(r->graphs.one, r->stream));
     }
-    for (int i = 0; i < m && !graphed; ++i) {
+    for (int i = 0; i < m && !graphed && !sharded; ++i) {
       if (timing) GTC_CUDA(cudaEventRecord(te[3 * i], r->stream));
       launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, vs, r->tstat, r->red.b, r->red.sel,
                     r->stream);
@@ -1380,9 +1455,15 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sc, r->gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, r->stream));
     static_assert(sizeof(StepRec) == sizeof(gtc_step_record), "record layout");
     GTC_CUDA(cudaMemcpyAsync(records + *done, r->d_rec, sizeof(StepRec) * (size_t)m, cudaMemcpyDeviceToHost, r->stream));
+    if (sharded) {
+      r->xrec_host.resize((size_t)m * d);
+      GTC_CUDA(cudaMemcpyAsync(r->xrec_host.data(), r->d_xrec, sizeof(double) * (size_t)m * d, cudaMemcpyDeviceToHost,
+                               r->stream));
+    }
     GTC_CUDA(cudaStreamSynchronize(r->stream));
     const int steps = L.step;
-    replay_steps(r, reinterpret_cast<const StepRec*>(records + *done), steps, hold, hold_n0, &hold_prev);
+    replay_steps(r, reinterpret_cast<const StepRec*>(records + *done), steps, hold, hold_n0, &hold_prev,
+                 sharded ? r->xrec_host.data() : nullptr);
     *done += steps;
     r->acc_gen = L.gen;
     r->port = L.port;
@@ -1444,6 +1525,39 @@ extern "C" int gtc_fit_points(gtc_run* r, const double* X, const double* y_raw, 
 extern "C" int gtc_run_set_shard(gtc_run* r, int64_t offset) {
   if (!r || offset < 0) return fail(GTC_ERR_INVALID, "bad shard");
   r->shard_offset = offset;
+  return GTC_OK;
+}
+
+extern "C" int gtc_run_attach_comm(gtc_run* r, gtc_comm* comm, int64_t offset, int64_t n_global) {
+  if (!r) return fail(GTC_ERR_INVALID, "run is null");
+  GTC_CUDA(cudaSetDevice(r->space->device));
+  GTC_CUDA(cudaStreamSynchronize(r->stream));
+  if (!comm) {
+    r->comm = nullptr;
+    r->n_global = 0;
+    r->shard_offset = 0;
+    r->has_values = false;
+    return GTC_OK;
+  }
+  if (offset < 0 || offset % kTile != 0)
+    return fail(GTC_ERR_INVALID, "shard offset must be a non-negative multiple of 256");
+  if (n_global < offset + r->space->n) return fail(GTC_ERR_INVALID, "shard exceeds n_global");
+  const int nranks = comm->nranks;
+  const int64_t rb = shard_record_bytes(7u, r->space->d, r->cfg.n_max);
+  cudaFree(r->d_send);
+  cudaFree(r->d_recv);
+  cudaFree(r->d_gacc);
+  r->d_send = r->d_recv = nullptr;
+  r->d_gacc = nullptr;
+  int rc;
+  if ((rc = dalloc(&r->d_send, (size_t)rb)) || (rc = dalloc(&r->d_recv, (size_t)rb * nranks)) ||
+      (rc = dalloc(&r->d_gacc, (size_t)2 * nranks)))
+    return rc;
+  GTC_CUDA(cudaMemset(r->d_send, 0, (size_t)rb));
+  r->comm = comm;
+  r->shard_offset = offset;
+  r->n_global = n_global;
+  r->has_values = false;  // the table must be the global one
   return GTC_OK;
 }
 

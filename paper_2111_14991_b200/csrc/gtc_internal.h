@@ -133,7 +133,39 @@ struct VarSource {
   double sum;
   long long count;
   int direct;
+  // candidate-axis sharding: the all-gathered accumulators of every shard
+  // ([n_gathered][2] generations); their limbs sum exactly (integers), so the
+  // global total is bit-identical to one device holding every tile
+  const VarAccum* gathered;
+  int n_gathered;
+  int gen;
 };
+
+// Candidate-axis sharding of the resident loop (gtc_run_attach_comm): every
+// shard's selection ends in one record, all-gathered, then merged identically
+// on every shard with the reference's best_candidate rule (portfolio.hpp:32-61).
+// Record = ShardHdr | x[slots][d] | xfirst[d] | col[slots][n_max] (doubles),
+// one slot per acquisition function of the selection mask, in af order: the
+// winners' coordinates and V columns, so the shard that does not hold the
+// pick can still append its bordered row from the column (column_border_row).
+struct ShardHdr {
+  int64_t pos[3];     // best non-NaN position per AF slot (global; -1 none)
+  double score[3];
+  int64_t first;      // lowest eligible global position (-1 none)
+  int64_t count;      // eligible candidates of the shard
+  uint32_t nan_mask;  // bit af: the first eligible candidate's score is NaN
+  int32_t cv_fallback;
+  double lambda;
+  double mean_var;
+  double best_std;
+};
+__host__ __device__ __forceinline__ int shard_slots(uint32_t mask) {
+  return (int)(mask & 1u) + (int)((mask >> 1) & 1u) + (int)((mask >> 2) & 1u);
+}
+__host__ __device__ __forceinline__ int64_t shard_record_bytes(uint32_t mask, int d, int n_max) {
+  const int s = shard_slots(mask);
+  return (int64_t)sizeof(ShardHdr) + 8 * ((int64_t)(s + 1) * d + (int64_t)s * n_max);
+}
 
 struct LoopDev;
 
@@ -407,7 +439,22 @@ struct LoopDev {
   SpaceDev sp;
   const double* V;
   int64_t tile_stride;
+  // candidate-axis sharding (nranks > 0): the loop's positions, records and
+  // value table are GLOBAL; visited / first / count / acc / var are this
+  // shard's candidates [offset, offset + n_space)
+  int32_t nranks;
+  uint32_t sel_mask;        // the selection's AF mask (record slots)
+  int64_t offset;
+  unsigned char* send;      // this shard's record (written by k_select's last block)
+  const unsigned char* recv;// [nranks] records after the all-gather
+  int64_t rec_bytes;
+  const VarAccum* gacc;     // [nranks][2] all-gathered accumulators
+  double* xrec;             // [step][d] coordinates of each valid step's pick (host replay)
+  SelectDev* gsel;          // merged (global) selection
 };
+// Merge of the all-gathered shard records + loop advance + the bordered row
+// of a valid pick from the owning shard's V column (one CTA).
+void launch_shard_merge(LoopDev* loop, int nu, cudaStream_t stream);
 // Loop-mode launches of the bordered append / single-row pass (args.loop set;
 // smem / args.n0 sized for the largest row of the chunk).
 void launch_gp_append_loop(const AppendArgs& a, int nu, size_t smem, cudaStream_t stream);

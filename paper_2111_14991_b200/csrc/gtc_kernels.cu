@@ -211,12 +211,35 @@ __device__ void accum_add_one(VarAccum* a, double v, int sign, double s2) {
   atomicAdd(&a->count, sign > 0 ? 1ull : (unsigned long long)(-1ll));
 }
 
-__device__ __forceinline__ void accum_read(const VarAccum* a, double s2, double* sum, long long* cnt) {
+__device__ __forceinline__ double limbs_value(const unsigned long long* limb, double s2) {
   double t = 0.0;
 #pragma unroll
-  for (int k = 3; k >= 0; --k) t = __dadd_rn(ldexp(t, 42), (double)(long long)__ldcg(&a->limb[k]));
-  *sum = ldexp(t, var_scale_exp(s2) - 120);
+  for (int k = 3; k >= 0; --k) t = __dadd_rn(ldexp(t, 42), (double)(long long)limb[k]);
+  return ldexp(t, var_scale_exp(s2) - 120);
+}
+
+__device__ __forceinline__ void accum_read(const VarAccum* a, double s2, double* sum, long long* cnt) {
+  unsigned long long l[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) l[k] = __ldcg(&a->limb[k]);
+  *sum = limbs_value(l, s2);
   *cnt = (long long)__ldcg(&a->count);
+}
+
+// Total of the all-gathered shard accumulators (generation `gen` of each):
+// integer limb sums (wrapping, two's complement), so the result equals the
+// total one device would have accumulated over the union of the tiles.
+__device__ __forceinline__ void accum_read_gathered(const VarAccum* g, int n, int gen, double s2, double* sum,
+                                                    long long* cnt) {
+  unsigned long long l[4] = {0ull, 0ull, 0ull, 0ull}, c = 0ull;
+  for (int i = 0; i < n; ++i) {
+    const VarAccum* a = g + 2 * i + gen;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) l[k] += __ldcg(&a->limb[k]);
+    c += __ldcg(&a->count);
+  }
+  *sum = limbs_value(l, s2);
+  *cnt = (long long)c;
 }
 
 __device__ __forceinline__ void accum_clear(VarAccum* a) {
@@ -227,6 +250,8 @@ __device__ __forceinline__ void var_source_read(const VarSource& v, double* sum,
   if (v.direct) {
     *sum = v.sum;
     *cnt = v.count;
+  } else if (v.gathered) {
+    accum_read_gathered(v.gathered, v.n_gathered, v.gen, v.s2, sum, cnt);
   } else {
     accum_read(v.acc, v.s2, sum, cnt);
   }
@@ -1332,6 +1357,13 @@ __device__ void port_record(PortDev& P, int by, double observed) {
   if (P.mode == 2) port_update_bands(P, by);
 }
 
+// This shard's local index of global position `pos` (-1: another shard's);
+// without sharding offset = 0 and every position is local.
+__device__ __forceinline__ int64_t shard_local(const LoopDev* L, int64_t pos) {
+  const int64_t p = pos - L->offset;
+  return (p >= 0 && p < L->n_space) ? p : -1;
+}
+
 __device__ void loop_advance(LoopDev* L, const SelectDev* sel) {
   if (sel->n_candidates <= 0) {
     L->halt = kLoopNoCandidates;
@@ -1369,9 +1401,10 @@ __device__ void loop_advance(LoopDev* L, const SelectDev* sel) {
   L->pos = pos;
   L->y = y;
   L->valid = valid;
+  const int64_t lpos = shard_local(L, pos);  // visited / count / first / acc are the shard's
   if (valid) {
     if (L->hold) {  // steady state: replace the observation at row hold_n0
-      const int64_t prev = L->hold_prev;
+      const int64_t prev = L->hold_prev >= 0 ? shard_local(L, L->hold_prev) : -1;
       if (prev >= 0) {
         L->visited[prev >> 5] &= ~(1u << (prev & 31));
         ++L->count;
@@ -1387,16 +1420,17 @@ __device__ void loop_advance(LoopDev* L, const SelectDev* sel) {
       if (y < L->f_best) L->f_best = y;
     }
     L->gen ^= 1;  // the pass produces the next generation
-    L->visited[pos >> 5] |= 1u << (pos & 31);
-  } else {
+    if (lpos >= 0) L->visited[lpos >> 5] |= 1u << (lpos & 31);
+  } else if (lpos >= 0) {
     // no refit: the variance total loses this candidate in O(1)
-    mark_update(L->visited, pos, 1, L->acc + L->gen, L->var, L->s2);
+    mark_update(L->visited, lpos, 1, L->acc + L->gen, L->var, L->s2);
   }
+  if (lpos < 0) return;
   --L->count;
-  if (pos == L->first) {  // next unvisited position (first only moves forward within a run)
+  if (lpos == L->first) {  // next unvisited position (first only moves forward within a run)
     const int64_t n = L->n_space, nw = (n + 31) >> 5;
     int64_t found = -1;
-    for (int64_t w = pos >> 5; w < nw; ++w) {
+    for (int64_t w = lpos >> 5; w < nw; ++w) {
       uint32_t fb = ~L->visited[w];
       if (w == nw - 1 && (n & 31)) fb &= (1u << (n & 31)) - 1u;
       if (fb) {
@@ -1490,7 +1524,7 @@ __device__ void select_publish(const SelCtx& c, const SelPart& f, double best, d
   c.out->gp_status = gp_status;
   if (c.b.gthr) c.b.gthr[0] = c.b.gthr[1] = c.b.gthr[2] = 0ull;  // next selection starts afresh
   *c.b.counter = 0;
-  if (c.loop) loop_advance(c.loop, c.out);
+  if (c.loop && c.loop->nranks == 0) loop_advance(c.loop, c.out);  // (sharded: k_shard_merge advances)
 #ifdef GTC_SEL_TRACE
   g_sel_trace[blockIdx.x][6] = gtc_globaltimer();
 #endif
@@ -1510,6 +1544,50 @@ __device__ void loop_column_append(LoopDev* L) {
   append_prologue(g, L->sp, pos, nullptr, L->y, n0);
   const double* col = L->V + (pos / kTile) * L->tile_stride + pos % kTile;
   if (!column_border_row(g, L->kp, L->noise, col, kTile, n0, xs) && threadIdx.x == 0) g.sc->status = 2;
+}
+
+// Candidate-axis sharding: the shard's selection record for the all-gather
+// (ShardHdr + the winners' coordinates and V columns, gtc_internal.h), from
+// the local result select_publish just wrote.  Block-wide.
+__device__ void shard_publish(const SelCtx& c, const LoopDev* L) {
+  const SelectDev* s = c.out;
+  ShardHdr* h = reinterpret_cast<ShardHdr*>(L->send);
+  const int d = L->sp.d, n_max = L->g.n_max;
+  const uint32_t mask = L->sel_mask;
+  const int slots = shard_slots(mask);
+  double* xs = reinterpret_cast<double*>(h + 1);
+  double* xfirst = xs + slots * d;
+  double* cols = xfirst + d;
+  const int64_t off = L->offset;
+  const bool live = s->n_candidates > 0;
+  if (threadIdx.x == 0) {
+    for (int af = 0; af < 3; ++af) {
+      h->pos[af] = live && s->best_nonnan_pos[af] >= 0 ? s->best_nonnan_pos[af] + off : -1;
+      h->score[af] = s->best_nonnan_score[af];
+    }
+    h->first = live && s->first_eligible >= 0 ? s->first_eligible + off : -1;
+    h->count = s->n_candidates;
+    h->nan_mask = live ? s->first_nan_mask : 0u;
+    h->cv_fallback = s->cv_fallback;
+    h->lambda = s->lambda;
+    h->mean_var = s->mean_variance;
+    h->best_std = s->best_std;
+  }
+  const int rows = L->n < n_max ? L->n : n_max;  // V rows [0, n) of the model
+  int slot = 0;
+  for (int af = 0; af < 3; ++af) {
+    if (!(mask & (1u << af))) continue;
+    const int64_t j = live ? s->best_nonnan_pos[af] : -1;
+    if (j >= 0) {
+      for (int t = threadIdx.x; t < d; t += blockDim.x) xs[slot * d + t] = L->sp.coords[(int64_t)t * L->sp.n_pad + j];
+      const double* col = L->V + (j / kTile) * L->tile_stride + j % kTile;
+      for (int q = threadIdx.x; q < rows; q += blockDim.x) cols[(int64_t)slot * n_max + q] = __ldcg(col + (int64_t)q * kTile);
+    }
+    ++slot;
+  }
+  const int64_t f = live ? s->first_eligible : -1;
+  if (f >= 0)
+    for (int t = threadIdx.x; t < d; t += blockDim.x) xfirst[t] = L->sp.coords[(int64_t)t * L->sp.n_pad + f];
 }
 
 template <uint32_t MASK>
@@ -1564,11 +1642,118 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first
     if (lane == 0) select_publish<MASK>(c, f, best, lambda, mean_var, cv_fallback, gp_status);
   }
   if (c.loop) {
-    __syncthreads();  // loop_advance (thread 0) done
-    loop_column_append(c.loop);
+    __syncthreads();  // loop_advance / the local result (thread 0) done
+    if (c.loop->nranks > 0)
+      shard_publish(c, c.loop);
+    else
+      loop_column_append(c.loop);
   }
 }
 
+
+// Candidate-axis sharding: after the all-gather of the shard records, every
+// shard merges them identically (best_candidate over the union,
+// portfolio.hpp:32-61: the lowest eligible position is the first candidate and
+// wins unconditionally when its score is NaN; else the highest non-NaN score,
+// lowest position on ties), advances the replicated loop state (the visited
+// mark lands on the owning shard only) and, for a valid pick, appends the
+// bordered row from the winner's V column carried in its owner's record --
+// the same column, coordinates and arithmetic as on one device, so the
+// factor stays bit-identical on every shard.  The first-candidate case (NaN
+// scores, no column shipped) leaves the exact row to the append kernel.
+__global__ void __launch_bounds__(kCtaThreads) k_shard_merge(LoopDev* L) {
+  __shared__ double xs[kMaxNmax];
+  __shared__ const double* s_x;
+  __shared__ const double* s_col;
+  pdl_begin();
+  if (L->halt != kLoopRunning) return;
+  const int d = L->sp.d, n_max = L->g.n_max;
+  const uint32_t mask = L->sel_mask;
+  const int slots = shard_slots(mask);
+  const int64_t rb = L->rec_bytes;
+  auto hdr = [&](int i) { return reinterpret_cast<const ShardHdr*>(L->recv + (int64_t)i * rb); };
+  auto xs_of = [&](int i) { return reinterpret_cast<const double*>(hdr(i) + 1); };
+  if (threadIdx.x == 0) {
+    s_x = nullptr;
+    s_col = nullptr;
+    SelectDev* out = L->gsel;
+    long long cnt = 0;
+    int owner = -1;
+    int64_t gfirst = INT64_MAX;
+    for (int i = 0; i < L->nranks; ++i) {
+      const ShardHdr* h = hdr(i);
+      cnt += h->count;
+      if (h->count > 0 && h->first >= 0 && h->first < gfirst) {
+        gfirst = h->first;
+        owner = i;
+      }
+    }
+    int src[3] = {-1, -1, -1};  // shard whose record holds the winner's column (-1: first-candidate case)
+    for (int af = 0; af < 3; ++af) {
+      out->position[af] = -1;
+      out->score[af] = 0.0;
+      if (!(mask & (1u << af)) || owner < 0) continue;
+      if (hdr(owner)->nan_mask & (1u << af)) {
+        out->position[af] = gfirst;
+        out->score[af] = CUDART_NAN;
+        continue;
+      }
+      double bs = 0.0;
+      int64_t bp = -1;
+      for (int i = 0; i < L->nranks; ++i) {
+        const ShardHdr* h = hdr(i);
+        const int64_t p = h->pos[af];
+        if (p < 0) continue;
+        if (bp < 0 || h->score[af] > bs || (h->score[af] == bs && p < bp)) {
+          bs = h->score[af];
+          bp = p;
+          src[af] = i;
+        }
+      }
+      if (bp < 0) {  // every score NaN: the first candidate stands
+        out->position[af] = gfirst;
+        out->score[af] = CUDART_NAN;
+      } else {
+        out->position[af] = bp;
+        out->score[af] = bs;
+      }
+    }
+    const ShardHdr* h0 = hdr(0);
+    out->lambda = h0->lambda;
+    out->mean_variance = h0->mean_var;
+    out->best_std = h0->best_std;
+    out->n_candidates = cnt;
+    out->cv_fallback = h0->cv_fallback;
+    out->gp_status = 0;
+    loop_advance(L, out);
+    if (L->halt == kLoopRunning && L->valid) {
+      const int by = L->rec[L->step - 1].by;
+      int slot = 0;
+      for (int af = 0; af < by; ++af) slot += (mask >> af) & 1u;
+      const int o = src[by];
+      if (o >= 0 && hdr(o)->pos[by] == L->pos) {
+        s_x = xs_of(o) + slot * d;
+        s_col = xs_of(o) + (slots + 1) * d + (int64_t)slot * n_max;
+      } else {  // the first eligible candidate (owner's record)
+        s_x = xs_of(owner) + slots * d;
+      }
+    }
+  }
+  __syncthreads();
+  if (L->halt != kLoopRunning || !L->valid) return;
+  const GpDev g = L->g;
+  const int n0 = L->n0;
+  append_prologue(g, L->sp, -1, s_x, L->y, n0);
+  for (int t = threadIdx.x; t < d; t += blockDim.x) L->xrec[(int64_t)(L->step - 1) * d + t] = s_x[t];
+  const bool ok = s_col != nullptr && column_border_row(g, L->kp, L->noise, s_col, 1, n0, xs);
+  if (!ok && threadIdx.x == 0) g.sc->status = 2;
+}
+
+void launch_shard_merge(LoopDev* loop, int nu, cudaStream_t s) {
+  (void)nu;
+  count_launch();
+  launch_pdl(k_shard_merge, dim3(1), dim3(kCtaThreads), 0, s, loop);
+}
 
 // ---------------------------------------------------- pruned selection
 //
@@ -2016,7 +2201,13 @@ __global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK))
     p.lambda_constant = lp->lambda_constant;
     p.cv_mu_s = lp->cv_mu_s;
     p.cv_var_s = lp->cv_var_s;
-    vs.acc = lp->acc + lp->gen;
+    if (lp->nranks > 0) {  // sharded: the global total from every shard's accumulators
+      vs.gathered = lp->gacc;
+      vs.n_gathered = lp->nranks;
+      vs.gen = lp->gen;
+    } else {
+      vs.acc = lp->acc + lp->gen;
+    }
   }
   select_run_body<MASK>(c, sc, p, vs, tstat, ntiles);
 }

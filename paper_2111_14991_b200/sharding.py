@@ -234,3 +234,121 @@ def split_bounds(n: int, parts: int, rank: int):
     lo = (n * rank) // parts
     hi = (n * (rank + 1)) // parts
     return lo, hi
+
+
+TILE = 256  # candidates per tile (gtc_internal.h kTile)
+
+
+def split_tiles(n: int, parts: int, rank: int):
+    """Contiguous slices [lo, hi) of n candidates on 256-candidate tile
+    boundaries (gtc_run_attach_comm requires tile-aligned offsets: the
+    per-tile fixed-point variance totals then sum to exactly the one-device
+    total, so lambda and every pick are bit-identical)."""
+    tiles = (n + TILE - 1) // TILE
+    lo = min(n, TILE * ((tiles * rank) // parts))
+    hi = min(n, TILE * ((tiles * (rank + 1)) // parts))
+    return lo, hi
+
+
+# ---------------------------------------------------------------------------
+# Device-resident sharding (gtc_comm + gtc_run_attach_comm): the whole
+# iteration -- local selection, all-gather of the shard records, merge, loop
+# advance, bordered row, local pass, all-gather of the variance accumulators --
+# is enqueued on the run's stream by gtc_run_steps; no host round trip.
+
+class Comm:
+    """A gtc_comm handle (NCCL rank or a member of an in-process group)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def rank(self) -> int:
+        return int(load().gtc_comm_rank(self._h))
+
+    @property
+    def size(self) -> int:
+        return int(load().gtc_comm_size(self._h))
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(load().gtc_comm_nccl_id(buf))
+        return bytes(buf)
+
+    @staticmethod
+    def nccl(uid: bytes, rank: int, nranks: int, device: int) -> "Comm":
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        check(load().gtc_comm_create_nccl(buf, int(rank), int(nranks), int(device), C.byref(h)))
+        return Comm(h)
+
+    @staticmethod
+    def local_group(nranks: int) -> List["Comm"]:
+        hs = (C.c_void_p * int(nranks))()
+        check(load().gtc_comm_create_local(int(nranks), hs))
+        return [Comm(C.c_void_p(h)) for h in hs]
+
+    def close(self):
+        if self._h:
+            load().gtc_comm_destroy(self._h)
+            self._h = None
+
+
+class ShardedRun:
+    """One shard of a run whose candidate axis is split over devices/ranks:
+    global candidates [offset, offset + len(coords_slice)), a replicated GP,
+    and gtc_run_steps iterations with the exchanges on the device."""
+
+    def __init__(self, coords_slice, offset: int, n_global: int, comm: Comm, kernel: MaternKernel,
+                 noise: float = 1e-10, jitter: float = 1e-6, n_max: int = 220, device: int = 0):
+        self.offset = int(offset)
+        self.n_global = int(n_global)
+        self.comm = comm
+        self.space = Space(coords_slice, device=device)
+        self.run = SurrogateRun(self.space, kernel, noise, jitter, n_max)
+        self.n_local = self.space.n
+        check(load().gtc_run_attach_comm(self.run.handle, comm.handle, self.offset, self.n_global))
+
+    def local(self, global_pos: int) -> int:
+        p = int(global_pos) - self.offset
+        return p if 0 <= p < self.n_local else -1
+
+    def fit_points(self, X, y) -> FitInfo:
+        X = np.ascontiguousarray(np.asarray(X, dtype=np.float64))
+        y = np.ascontiguousarray(np.asarray(y, dtype=np.float64))
+        info = _lib.gtc_fit_info()
+        check(load().gtc_fit_points(self.run.handle, _lib.dptr(X), _lib.dptr(y), len(y), C.byref(info)))
+        return FitInfo.of(info)
+
+    def mark_global(self, global_pos: int) -> None:
+        p = self.local(global_pos)
+        if p >= 0:
+            self.run.mark_visited(p)
+
+    def unmark_global(self, global_pos: int) -> None:
+        p = self.local(global_pos)
+        if p >= 0:
+            self.run.unmark_visited(p)
+
+    def local_totals(self) -> np.ndarray:
+        mv = C.c_double()
+        cnt = C.c_int64()
+        check(load().gtc_mean_variance(self.run.handle, C.byref(mv), C.byref(cnt)))
+        return np.array([mv.value * cnt.value, float(cnt.value)])
+
+    def set_values(self, values) -> None:
+        """The GLOBAL replay table (every shard evaluates every pick)."""
+        self.run.set_values(values)
+
+    def steps(self, af, k, f_best_raw, exploration=ExplorationConfig(), cv_state=ContextualVarianceState(),
+              hold=False, timing=False):
+        return self.run.steps(af, k, f_best_raw, exploration, cv_state, hold=hold, timing=timing)
+
+    def close(self):
+        self.run.close()
+        self.space.close()

@@ -15,8 +15,12 @@ V (1.76 GB) >> L2 (126 MB), so every step streams from HBM (no L2 flush needed).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config c4|c3|c2|c5]
-Under torchrun (N > 1) every rank runs an independent replica of the workload
-(run-level sharding, no collective on the data path); value = total iter/s.
+N > 1 (torchrun, or self-spawned by `--gpus N`): BASELINE configs[3] -- ONE C4
+run with its candidate axis split over the ranks (strong scaling; every
+iteration on the device, two NCCL all-gathers per iteration); the same GPUs
+running independent replicas (weak scaling, no collective) are reported
+under "replicas".  N = 1 also reports the sharded iteration at one rank
+("sharded_1rank": the cost of the exchanges and the merge).
 """
 from __future__ import annotations
 
@@ -40,6 +44,7 @@ METRIC = "BO iterations/sec (full-space GP posterior+acquisition) at N, n=220"
 # dram__bytes_read.sum + dram__bytes_write.sum per k_extend<1> launch, from the
 # committed ncu --set full capture of the resident loop
 TRAFFIC = {"c4": 1.76591e9}  # 1.758600 GB read + 7.31 MB written per launch (profiles/r01c_ncu_full.txt)
+CONFIG_AF = {"ei": 0, "poi": 1, "lcb": 2}
 CONFIGS = {
     "c4": dict(grid=[10] * 6, invalid=0.0, af="ei", workload="C4 synthetic random-rough 1M candidates (10^6 grid, d=6), n=220, bo-ei, contextual variance"),
     "c3": dict(grid=[10, 10, 10, 10, 5, 2], invalid=0.3, af="lcb", workload="C3 synthetic random-rough 100k candidates (d=6, ~30% invalid), n=220, bo-lcb, contextual variance"),
@@ -55,10 +60,11 @@ def parse():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS) + ["c1", "c2", "c5"])
     ap.add_argument("--n", type=int, default=220)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
-                    help="replicas: one independent C4 run per GPU (weak scaling, no collective); "
-                         "sharded: ONE C4 run with its candidate axis split over the GPUs (strong scaling, "
-                         "two small NCCL exchanges per iteration)")
+    ap.add_argument("--mode", default=None, choices=["single", "replicas", "sharded"],
+                    help="default: single at N = 1, sharded at N > 1.  sharded: ONE C4 run with its candidate "
+                         "axis split over the GPUs (strong scaling, BASELINE configs[3]; two NCCL all-gathers per "
+                         "iteration, enqueued on the device); replicas: one independent C4 run per GPU (weak "
+                         "scaling, no collective)")
     return ap.parse_args()
 
 
@@ -393,7 +399,8 @@ def cpu_baseline(cfg, n, budget_s=30.0):
     cores = os.cpu_count() or 1
     grid = "x".join(str(k) for k in cfg["grid"])
     try:
-        out = subprocess.run([str(tool), "bench", grid, str(BASE_SEED), str(n), str(cores), "1", cfg["af"]],
+        out = subprocess.run([str(tool), "bench", grid, str(BASE_SEED), str(n), str(cores), "1", cfg["af"],
+                              str(cfg["invalid"])],
                              capture_output=True, text=True, timeout=budget_s * 20)
         rec = json.loads(out.stdout.strip().splitlines()[-1])
     except Exception as e:  # noqa: BLE001
@@ -418,7 +425,8 @@ def run_reference_arm(args, cfg):
     cores = os.cpu_count() or 1
     grid = "x".join(str(k) for k in cfg["grid"])
     steps = max(1, min(args.steps, 3))
-    out = subprocess.run([str(tool), "bench", grid, str(BASE_SEED), str(args.n), str(cores), str(steps), cfg["af"]],
+    out = subprocess.run([str(tool), "bench", grid, str(BASE_SEED), str(args.n), str(cores), str(steps), cfg["af"],
+                          str(cfg["invalid"])],
                          capture_output=True, text=True)
     rec = json.loads(out.stdout.strip().splitlines()[-1])
     v = rec["iters_per_sec"]
@@ -432,79 +440,155 @@ def run_reference_arm(args, cfg):
                       "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
 
+def sustained(chunk, seconds=2.0):
+    """Repeats `chunk` (one K-step block, returns its step count) until the
+    device has been busy for `seconds`, so the clock / busy samplers see a
+    loaded GPU.  Returns (steps, wall seconds)."""
+    import torch
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    steps = 0
+    while True:
+        steps += chunk()
+        if time.perf_counter() - t0 >= seconds:
+            torch.cuda.synchronize()
+            if time.perf_counter() - t0 >= seconds:
+                break
+    return steps, time.perf_counter() - t0
+
+
 def run_sharded(args, cfg, rank, world, local):
-    """C4 with the candidate axis split over the ranks (strong scaling).
-    Each step: bordered row (replicated) + this shard's V-row pass -> NCCL
-    all-gather of (var sum, count) -> local selection -> NCCL all-gather of
-    the selection records -> identical merge on every rank."""
+    """BASELINE configs[3]: ONE C4 run with its candidate axis split over the
+    ranks (strong scaling).  Every iteration runs on the device
+    (gtc_run_steps with a gtc_comm attached): local selection -> NCCL
+    all-gather of the shard records -> identical merge + loop advance +
+    bordered row on every rank -> local V-row pass -> NCCL all-gather of the
+    fixed-point variance accumulators.  No host round trip per iteration."""
     import torch
     import paper_2111_14991_b200 as gt
     from paper_2111_14991_b200 import AcquisitionId, ContextualVarianceState, ExplorationConfig, MaternKernel, MaternNu
-    from paper_2111_14991_b200.sharding import DistributedShard, Shard, ShardGroup, TorchComm, split_bounds
+    from paper_2111_14991_b200.sharding import Comm, ShardedRun, split_tiles
 
     coords, ids, values = make_workload(cfg)
     N, n = len(values), args.n
-    lo, hi = split_bounds(N, world, rank)
-    af = AcquisitionId.ei if args.config == "c4" else AcquisitionId.lcb
+    lo, hi = split_tiles(N, world, rank)
+    af = AcquisitionId(CONFIG_AF[cfg["af"]])
     kern = MaternKernel(MaternNu.three_halves, 1.5, 1.0)
-    shard = Shard(coords[lo:hi], lo, kern, n_max=n, device=local)
+    if world > 1:
+        obj = [Comm.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    else:
+        uid = Comm.nccl_unique_id()
+    comm = Comm.nccl(uid, rank, world, local)
+    launches0 = gt.load().gtc_kernel_launches()
+    sh = ShardedRun(coords[lo:hi], lo, N, comm, kern, n_max=n, device=local)
     pos = prefix_positions(values, n - 1, BASE_SEED)
     y = values[pos]
-    shard.fit_points(coords[pos], y)
+    sh.fit_points(coords[pos], y)
     for p in pos:
-        shard.mark_global(int(p))
-    group = DistributedShard(shard, TorchComm()) if world > 1 else ShardGroup([shard])
-    cv = ContextualVarianceState(float(np.mean(y[:20])), group.mean_variance())
+        sh.mark_global(int(p))
+    tot = sh.local_totals()
+    if world > 1:
+        t = torch.tensor(tot, dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t)
+        tot = t.cpu().numpy()
+    cv = ContextualVarianceState(float(np.mean(y[:20])), float(tot[0] / tot[1]))
     expl = ExplorationConfig()
     f_best = float(np.min(y))
-    pick = group.select([af], f_best, expl, cv).position[int(af)]
-    stream = torch.cuda.ExternalStream(gt.load().gtc_run_stream(shard.run.handle))
+    stream = torch.cuda.ExternalStream(gt.load().gtc_run_stream(sh.run.handle))
+    state = {"last": None}
 
-    def step(pick, f_best):
-        shard.run.truncate_async(n - 1)      # bench rollback: model back to n-1 observations
-        yv = float(values[pick])
-        s = group.observe(coords[pick], pick, yv, [af], min(f_best, yv), expl, cv)
-        if shard.local(pick) >= 0:           # bench rollback: keep the candidate set fixed
-            shard.run.unmark_visited(shard.local(pick))
-        return s.position[int(af)], f_best
+    def resident(k, timing=False):
+        sh.run.truncate_async(n - 1)         # back to n-1 observations (previous call's last step)
+        if state["last"] is not None:
+            sh.unmark_global(state["last"])
+        recs = sh.steps(af, k, f_best, expl, cv, hold=True, timing=timing)
+        state["last"] = recs[-1].position if recs else None
+        return len(recs)
 
-    for _ in range(args.warmup):
-        pick, f_best = step(pick, f_best)
+    sh.set_values(values)
+    resident(max(3, args.warmup))
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
+    before = gt.load().gtc_kernel_launches()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
         e0.record(stream)
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            pick, f_best = step(pick, f_best)
+        k_done = resident(args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
+        launches = gt.load().gtc_kernel_launches() - before
+        assert k_done == args.steps
+        if world > 1:
+            torch.distributed.barrier()
+        # e2e: the same K steps through the C ABI from host buffers (global
+        # value table H2D + step records D2H), wall clock
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sh.set_values(values)
+        resident(args.steps)
         wall = time.perf_counter() - t0
+        if world > 1:
+            torch.distributed.barrier()
+        sus_steps, sus_s = sustained(lambda: resident(args.steps))
     dev_ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([dev_ms, wall], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dev_ms, wall, sus_s], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        dev_ms, wall = float(t[0]), float(t[1])
-    if rank == 0:
-        print(json.dumps({
-            "metric": METRIC, "value": args.steps / (dev_ms / 1e3), "unit": "iter/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": cfg["workload"] + " (candidate axis sharded)", "N": N, "n": n,
-                       "parallelism": f"candidate-shard{world}",
-                       "timing": "CUDA events bracketing the K steps on rank's stream (includes the NCCL exchanges), max over ranks"},
-            "e2e": {"value": args.steps / wall, "unit": "iter/s", "h2d_bytes_per_step": 8 * (coords.shape[1] + 2),
-                    "d2h_bytes_per_step": 16 + 8 * 13},
-            "clocks": clocks.summary()}))
+        dev_ms, wall, sus_s = float(t[0]), float(t[1]), float(t[2])
+    out = {
+        "metric": METRIC, "value": args.steps / (dev_ms / 1e3), "unit": "iter/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"] + " (candidate axis sharded)", "N": N, "n": n,
+                   "d": coords.shape[1], "parallelism": f"candidate-shard{world}",
+                   "shard": [lo, hi], "l2": "V stream > L2 per GPU up to 8 shards (220 MB/shard at 8)",
+                   "timing": "CUDA events bracketing the K-step gtc_run_steps call on each rank's run stream "
+                             "(every kernel and both NCCL all-gathers per iteration), max over ranks"},
+        "e2e": {"value": args.steps / wall, "unit": "iter/s", "h2d_bytes_per_step": 8 * N / args.steps,
+                "d2h_bytes_per_step": 40 + 8 * coords.shape[1],
+                "api": "gtc_run_set_values (global table H2D) + gtc_run_steps (records D2H), wall clock, max over ranks"},
+        "sustained": {"steps": sus_steps, "seconds": sus_s, "value": sus_steps / sus_s,
+                      "note": "the K-step block repeated for >= 2 s (wall clock) so clock/busy samplers see load"},
+        "gpu_launches": int(launches), "clocks": clocks.summary(),
+        "comm": "nccl", "exchanges_per_iteration": 2,
+    }
+    sh.close()
+    comm.close()
+    return out
+
+
+def self_spawn(args) -> bool:
+    """`bench.py --gpus N` without torchrun: relaunch under torch.distributed.run
+    with N ranks (one per GPU) on 127.0.0.1; returns True when it did."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl != "ours":
+        return False
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the NCCL init lines show every rank
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"), *sys.argv[1:]]
+    rc = subprocess.run(cmd, env=env).returncode
+    if rc:
+        sys.exit(rc)
+    return True
 
 
 def main():
     args = parse()
+    if self_spawn(args):
+        return
+    _, world_env, _ = dist_env()
+    if args.impl == "ours" and world_env > 1 and args.gpus != world_env:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}; measuring {world_env} ranks",
+              file=sys.stderr)
     if args.config in ("c1", "c2", "c5"):
         if args.impl == "reference":
             rank, _, _ = dist_env()
@@ -536,18 +620,48 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         init_dist(local)
-    if args.mode == "sharded":
-        run_sharded(args, cfg, rank, world, local)
-        if world > 1:
-            torch.distributed.destroy_process_group()
-        return
+    mode = args.mode or ("sharded" if world > 1 else "single")
+    if mode == "replicas":
+        mode = "single"
+    if mode == "sharded":
+        out = run_sharded(args, cfg, rank, world, local)
+        # the same GPUs running independent replicas (weak scaling, no collective)
+        rep = run_single(args, cfg, rank, world, local, extras=False)
+        if rank == 0:
+            out["replicas"] = {"value": rep["value"], "unit": "iter/s", "scaling": "weak",
+                               "ms_per_step": rep["ms_per_step"],
+                               "note": f"{world} independent C4 runs, one per GPU (run-level sharding)"}
+    else:
+        out = run_single(args, cfg, rank, world, local, extras=True)
+        if world == 1 and torch.cuda.device_count() >= 1:
+            # the sharded iteration at one rank (NCCL world 1): its overhead vs the fused step
+            try:
+                s1 = run_sharded(args, cfg, rank, world, local)
+                out["sharded_1rank"] = {"value": s1["value"], "ms_per_step": s1["ms_per_step"],
+                                        "ratio_to_fused": s1["value"] / out["value"],
+                                        "note": "gtc_run_steps with an NCCL world-1 gtc_comm attached: "
+                                                "both all-gathers and the merge kernel in every iteration"}
+            except Exception as e:  # noqa: BLE001
+                out["sharded_1rank"] = {"error": str(e)[:200]}
+    if rank == 0:
+        if mode != "sharded" and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(cfg, args.n)
+        print(json.dumps(out))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_single(args, cfg, rank, world, local, extras=True):
+    """One independent C4 run per rank (N = 1: THE configuration of the
+    headline metric; N > 1: replicas, weak scaling).  Returns the JSON dict."""
+    import torch
     import paper_2111_14991_b200 as gt
     from paper_2111_14991_b200 import AcquisitionId, ContextualVarianceState, ExplorationConfig, MaternKernel, MaternNu
 
     coords, ids, values = make_workload(cfg)
     N = len(values)
     n = args.n
-    af = AcquisitionId.ei if args.config == "c4" else AcquisitionId.lcb
+    af = AcquisitionId(CONFIG_AF[cfg["af"]])
     launches0 = gt.load().gtc_kernel_launches()
     space = gt.Space(coords, device=local)
     run = gt.SurrogateRun(space, MaternKernel(MaternNu.three_halves, 1.5, 1.0), n_max=n)
@@ -611,7 +725,16 @@ def main():
         recs2 = resident(args.steps)
         wall = time.perf_counter() - t0
         assert len(recs2) == args.steps
+        sus_steps, sus_s = sustained(lambda: len(resident(args.steps))) if extras else (0, 0.0)
     dev_ms = e0.elapsed_time(e1)
+    if not extras:
+        if world > 1:
+            t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            dev_ms = float(t[0])
+        run.close()
+        space.close()
+        return {"value": world * args.steps / (dev_ms / 1e3), "ms_per_step": dev_ms / args.steps}
 
     # the per-iteration gtc_observe loop (live objective on the host: one
     # H2D observation + D2H selection per iteration), for reference
@@ -646,6 +769,7 @@ def main():
     avg_pass = float(phases[2])
     alg_bytes = N * 8 * n  # n-1 rows of V read + 1 row written per candidate
     achieved = alg_bytes / (avg_pass / 1e3) / 1e9
+    out = {}
     if rank == 0:
         rec_bytes = 32
         out = {
@@ -677,14 +801,12 @@ def main():
             "clocks": clocks.summary(),
             "bordered_rows_exact": int(exact_rows),
             "phases_us": dict(zip(("select+advance", "append", "pass"), (round(1e3 * float(v), 2) for v in phases))),
+            "sustained": {"steps": sus_steps, "seconds": sus_s, "value": world * sus_steps / sus_s if sus_s else None,
+                          "note": "the K-step block repeated for >= 2 s (wall clock) so clock/busy samplers see load"},
         }
-        if not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(cfg, n)
-        print(json.dumps(out))
     run.close()
     space.close()
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    return out if rank == 0 else {}
 
 
 if __name__ == "__main__":

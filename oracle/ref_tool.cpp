@@ -229,14 +229,18 @@ int cmd_runbo(int argc, char** argv) {
 // + mean variance + contextual lambda + best_candidate (strategies.hpp:366-436).
 int cmd_bench(int argc, char** argv) {
   if (argc < 8) return 2;
-  const MeasurementCache cache = make_cache("random-rough", argv[2], std::stoull(argv[3]), "0");
+  // optional argv[8]: the workload's runtime-invalid fraction (C3: 0.3)
+  const MeasurementCache cache = make_cache("random-rough", argv[2], std::stoull(argv[3]), argc > 8 ? argv[8] : "0");
   const EnumeratedSpace space(cache.space());
   const std::size_t n = std::stoul(argv[4]);
   const unsigned threads = std::max(1u, static_cast<unsigned>(std::stoul(argv[5])));
   const int steps = std::stoi(argv[6]);
-  const AcquisitionId af = std::string(argv[7]) == "ei" ? AcquisitionId::ei
-                           : std::string(argv[7]) == "poi" ? AcquisitionId::poi
-                                                           : AcquisitionId::lcb;
+  const std::string af_name = argv[7];
+  if (af_name != "ei" && af_name != "poi" && af_name != "lcb") {
+    std::fprintf(stderr, "unknown acquisition function '%s' (ei, poi, lcb)\n", af_name.c_str());
+    return 2;
+  }
+  const AcquisitionId af = af_name == "ei" ? AcquisitionId::ei : af_name == "poi" ? AcquisitionId::poi : AcquisitionId::lcb;
   const std::size_t N = space.size(), d = space.dimension();
   const Objective objective = cache.objective();
   Rng rng(12345);
@@ -246,9 +250,11 @@ int cmd_bench(int argc, char** argv) {
   while (train.size() < n) {
     const std::size_t p = rng.uniform_below(N);
     if (visited[p]) continue;
+    const auto m = objective(space.configs[p]);
+    if (!m.value) continue;  // runtime-invalid: never reaches the GP (strategies.hpp:444-449)
     visited[p] = true;
     train.push_back(p);
-    vals.push_back(*objective(space.configs[p]).value);
+    vals.push_back(*m.value);
   }
   Eigen::MatrixXd X(n, d);
   Eigen::VectorXd y(n);

@@ -195,7 +195,10 @@ int gtc_fit(gtc_run* run, const int64_t* positions, const double* y_raw, int32_t
  * refactorises when the new pivot fails, exactly like gp.hpp:116-129. */
 int gtc_append(gtc_run* run, int64_t position, double y_raw, gtc_fit_info* info);
 
-/* Rolls the model back to its first n observations (prefix-stable state). */
+/* Rolls the model back to its first n observations: GpModel::fit of that
+ * prefix.  O(n) and asynchronous (info = NULL) while the factor is at the base
+ * jitter (the factor is prefix-stable); after a jitter escalation the prefix
+ * is refactorised from the base jitter, synchronously. */
 int gtc_truncate(gtc_run* run, int32_t n, gtc_fit_info* info);
 
 /* Visited bookkeeping (RunContext::evaluate, strategies.hpp:183-186). */
@@ -361,8 +364,10 @@ int32_t gtc_space_device(const gtc_space* space);
 #define GTC_STRATEGY_BO_POI 3
 #define GTC_STRATEGY_BO_LCB 4
 
-/* StrategyConfig (strategies.hpp:79-122), BO fields.  lengthscale <= 0 and
- * discount <= 0 select the reference defaults (1.5 / 2.0; 0.65 / 0.75). */
+/* StrategyConfig (strategies.hpp:79-122), BO fields.  lengthscale = NaN and
+ * discount = NaN select the reference defaults (1.5 / 2.0; 0.65 / 0.75); other
+ * out-of-range values fail like the reference ("kernel lengthscale must be
+ * positive", GTC_ERR_INVALID; "discount factor must be in (0,1)", GTC_ERR_CONFIG). */
 typedef struct {
   int32_t strategy;
   uint64_t seed;

@@ -32,7 +32,7 @@ from typing import List, Optional
 import numpy as np
 
 from .gp import Error
-from .space import ParameterDef, ParamKind, SearchSpace
+from .space import ParameterDef, ParamKind, SearchSpace, parse_restriction
 
 SCHEMA_VERSION = 1  # cache.hpp:27
 MAGIC = b"GTCBIN\x00\x01"
@@ -87,12 +87,17 @@ class MeasurementCache:
         if es.n != len(self.ids):
             raise CacheError(f"cache '{self.kernel_name}' has {len(self.ids)} entries but the space has "
                              f"{es.n} valid configurations")
-        if not np.array_equal(es.ids, self.ids):
-            missing = np.setdiff1d(es.ids, self.ids)
-            raise CacheError(f"cache '{self.kernel_name}' is missing an entry for configuration {int(missing[0])}")
-        bad = (self.reasons == 0) & ~(self.values > 0.0)
-        if bad.any():
-            raise CacheError(f"cache '{self.kernel_name}' entry {int(self.ids[np.argmax(bad)])} has non-positive value")
+        # the reference walks the valid configurations in ascending order and
+        # reports the first one that is missing or has a non-positive value
+        missing = np.setdiff1d(es.ids, self.ids)
+        bad = self.ids[(self.reasons == 0) & ~(self.values > 0.0)]
+        bad = bad[np.isin(bad, es.ids)]
+        first_missing = int(missing[0]) if len(missing) else None
+        first_bad = int(bad.min()) if len(bad) else None
+        if first_missing is not None and (first_bad is None or first_missing < first_bad):
+            raise CacheError(f"cache '{self.kernel_name}' is missing an entry for configuration {first_missing}")
+        if first_bad is not None:
+            raise CacheError(f"cache '{self.kernel_name}' entry {first_bad} has non-positive value")
         if self.true_minimum is not None and self.min_valid_value() != self.true_minimum:
             raise CacheError(f"cache '{self.kernel_name}' states minimum {self.true_minimum:.6f} but the entries' "
                              f"minimum is {self.min_valid_value():.6f}")
@@ -134,30 +139,62 @@ class MeasurementCache:
         doc["entries"] = entries
         pathlib.Path(path).write_text(json.dumps(doc, indent=1) + "\n")
 
+    def config_at(self, index: int) -> list:
+        """The configuration tuple of a canonical index (mixed radix, first
+        parameter most significant; SearchSpace::config_at, search_space.hpp:57-72)."""
+        out, rest = [], int(index)
+        for p in reversed(self.params):
+            out.append(p.values[rest % p.size()])
+            rest //= p.size()
+        return out[::-1]
+
     @staticmethod
-    def load_json(path) -> "MeasurementCache":
+    def load_json(path, validate: bool = True) -> "MeasurementCache":
+        """MeasurementCache::load (cache.hpp:156-241): header, restrictions
+        parsed, entries in file order (unknown reason, embedded config tuple
+        against its index, duplicates), stored checksum, then validate() --
+        which enumerates the space on the device; validate=False skips only
+        that last step (host-only tools and CPU tests)."""
         try:
             doc = json.loads(pathlib.Path(path).read_text())
         except OSError:
             raise CacheError(f"cannot open cache file '{path}'") from None
         except json.JSONDecodeError as e:
             raise CacheError(f"cache file '{path}' is not valid JSON: {e}") from None
-        c = MeasurementCache._from_header(doc, path)
-        ent = sorted(doc["entries"], key=lambda e: int(e["index"]))
-        c.ids = np.array([int(e["index"]) for e in ent], dtype=np.uint64)
-        c.values = np.array([float(e["value"]) if "value" in e else math.nan for e in ent])
-        reasons = []
-        for e in ent:
-            if "value" in e:
-                reasons.append(0)
-            elif e.get("invalid") in REASONS[1:]:
-                reasons.append(REASONS.index(e["invalid"]))
-            else:
-                raise CacheError(f"unknown invalid reason '{e.get('invalid')}'")
-        c.reasons = np.array(reasons, dtype=np.uint8)
-        if len(np.unique(c.ids)) != len(c.ids):
-            raise CacheError("duplicate entry for configuration %d" % int(c.ids[np.argmax(np.diff(c.ids) == 0)]))
+        try:
+            c = MeasurementCache._from_header(doc, path)
+            ids, values, reasons, seen = [], [], [], set()
+            for e in doc["entries"]:
+                idx = int(e["index"])
+                if "value" in e:
+                    values.append(float(e["value"]))
+                    reasons.append(0)
+                else:
+                    reason = e["invalid"]
+                    if reason not in REASONS[1:]:
+                        raise CacheError(f"unknown invalid reason '{reason}'")
+                    values.append(math.nan)
+                    reasons.append(REASONS.index(reason))
+                if "config" in e:  # the embedded tuple must match the index
+                    want = c.config_at(idx)
+                    got = e["config"]
+                    if len(got) != len(want):
+                        raise CacheError(f"entry {idx} config tuple has wrong arity")
+                    if any(not _same_value(g, w) for g, w in zip(got, want)):
+                        raise CacheError(f"entry {idx} config tuple does not match its index")
+                if idx in seen:
+                    raise CacheError(f"duplicate entry for configuration {idx}")
+                seen.add(idx)
+                ids.append(idx)
+        except KeyError as e:
+            raise CacheError(f"cache file '{path}' is malformed: missing key {e}") from None
+        order = np.argsort(np.array(ids, dtype=np.uint64), kind="stable")
+        c.ids = np.array(ids, dtype=np.uint64)[order]
+        c.values = np.array(values, dtype=np.float64)[order]
+        c.reasons = np.array(reasons, dtype=np.uint8)[order]
         c._check_stored_checksum(doc, path)
+        if validate:
+            c.validate()
         return c
 
     @staticmethod
@@ -169,6 +206,8 @@ class MeasurementCache:
             if jp["kind"] not in ("numeric", "categorical", "boolean"):
                 raise CacheError(f"unknown parameter kind '{jp['kind']}'")
             params.append(ParameterDef(jp["name"], jp["values"], ParamKind[jp["kind"]]))
+        for text in doc.get("restrictions", []):  # SearchSpace construction parses them (host only)
+            parse_restriction(text, params)
         return MeasurementCache(kernel_name=doc["kernel_name"], params=params,
                                 restrictions=list(doc.get("restrictions", [])),
                                 device_name=doc.get("device_name", "unknown"),
@@ -193,7 +232,9 @@ class MeasurementCache:
             f.write(np.ascontiguousarray(self.reasons, dtype=np.uint8).tobytes())
 
     @staticmethod
-    def load_binary(path, verify_checksum: bool = True) -> "MeasurementCache":
+    def load_binary(path, verify_checksum: bool = True, validate: bool = True) -> "MeasurementCache":
+        """The binary format: same header and checks as load_json (ascending
+        unique indices instead of per-entry tuples), then validate()."""
         try:
             raw = np.memmap(path, dtype=np.uint8, mode="r")
         except OSError:
@@ -214,11 +255,24 @@ class MeasurementCache:
             raise CacheError(f"cache file '{path}' entries are not in ascending index order")
         if verify_checksum:
             c._check_stored_checksum(doc, path)
+        if validate:
+            c.validate()
         return c
 
     @staticmethod
-    def load(path) -> "MeasurementCache":
+    def load(path, validate: bool = True) -> "MeasurementCache":
         """Either format, by content."""
         with open(path, "rb") as f:
             head = f.read(8)
-        return MeasurementCache.load_binary(path) if head == MAGIC else MeasurementCache.load_json(path)
+        if head == MAGIC:
+            return MeasurementCache.load_binary(path, validate=validate)
+        return MeasurementCache.load_json(path, validate=validate)
+
+
+def _same_value(a, b) -> bool:
+    """value_from_json(a) == b (parameter.hpp Value equality: same kind and value)."""
+    if isinstance(b, bool) or isinstance(a, bool):
+        return isinstance(a, bool) and isinstance(b, bool) and a == b
+    if isinstance(b, str) or isinstance(a, str):
+        return isinstance(a, str) and isinstance(b, str) and a == b
+    return float(a) == float(b)

@@ -39,13 +39,13 @@ StrategyConfig to_config(const gtc_bo_config& c) {
   s.n_init = static_cast<std::size_t>(c.n_init);
   s.invalid_consumes_budget = c.invalid_consumes_budget != 0;
   s.nu = static_cast<MaternNu>(c.nu);
-  if (c.lengthscale > 0.0) s.lengthscale = c.lengthscale;
+  if (!std::isnan(c.lengthscale)) s.lengthscale = c.lengthscale;  // NaN: the reference default; <= 0 throws downstream
   s.output_variance = c.output_variance;
   s.noise = c.noise;
   s.jitter = c.jitter;
   s.exploration.mode = static_cast<ExplorationConfig::Mode>(c.exploration_mode);
   s.exploration.constant = c.exploration_constant;
-  if (c.discount > 0.0) s.discount = c.discount;
+  if (!std::isnan(c.discount)) s.discount = c.discount;  // NaN: the reference default; outside (0,1) throws downstream
   s.required_improvement = c.required_improvement;
   s.skip_threshold = c.skip_threshold;
   s.lhs_restarts = static_cast<std::size_t>(c.lhs_restarts);

@@ -944,6 +944,12 @@ extern "C" int gtc_truncate(gtc_run* r, int32_t n, gtc_fit_info* info) {
   if (n < 0 || n > r->n) return fail(GTC_ERR_INVALID, "truncate: n out of range");
   GTC_CUDA(cudaSetDevice(r->space->device));
   if (n == 0) return gtc_fit(r, nullptr, nullptr, 0, info);
+  if (r->jitter != r->cfg.jitter) {
+    // the factor was escalated past the base jitter by a later observation:
+    // GpModel::fit of the prefix restarts at the base jitter (gp.hpp:116-129)
+    keep_obs(r, n);
+    return refit(r, r->cfg.jitter, info);
+  }
   launch_gp_truncate(r->gp.dev, n, r->stream);
   GTC_LAUNCHED();
   r->n = n;

@@ -3,6 +3,8 @@ the C ABI: the C++ host mirror (include/gridtune_b200/strategies.hpp) drives
 the resident device surrogate; this module only marshals arguments."""
 from __future__ import annotations
 
+import math
+
 import ctypes as C
 import enum
 from dataclasses import dataclass, field
@@ -56,9 +58,9 @@ class StrategyConfig:
         return _lib.gtc_bo_config(
             int(self.id), int(self.seed) & 0xFFFFFFFFFFFFFFFF, int(self.budget), int(self.n_init),
             1 if self.invalid_consumes_budget else 0, int(self.nu),
-            float(self.lengthscale) if self.lengthscale is not None else 0.0, float(self.output_variance),
+            float(self.lengthscale) if self.lengthscale is not None else math.nan, float(self.output_variance),
             float(self.noise), float(self.jitter), int(self.exploration.mode), float(self.exploration.constant),
-            float(self.discount) if self.discount is not None else 0.0, float(self.required_improvement),
+            float(self.discount) if self.discount is not None else math.nan, float(self.required_improvement),
             int(self.skip_threshold), int(self.lhs_restarts))
 
 

@@ -4,7 +4,7 @@ Vectorised numpy restatement of the reference generator
 /root/reference/proj/include/gridtune/synthetic.hpp:38-180 (random-rough,
 rosenbrock-disc, rastrigin-box, step-plateau) and of the unrestricted
 EnumeratedSpace (search_space.hpp:57-72,158-166).  Bit-exact against the
-reference (tests/test_synthetic.py pins it on golden files written by
+reference (tests/test_host_cpu.py pins it on golden files written by
 oracle/_ref/ref_tool).  This is an input generator, not part of the hot path.
 """
 from __future__ import annotations

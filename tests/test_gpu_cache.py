@@ -35,3 +35,21 @@ def test_validation_errors(gt):
     c.true_minimum = 0.5
     with pytest.raises(gt.CacheError, match="states minimum"):
         c.validate()
+
+
+def test_load_validates_like_the_reference(gt, tmp_path):
+    """MeasurementCache::load ends with validate() (cache.hpp:236): a cache
+    missing one configuration is rejected at load time."""
+    import json
+    doc = json.loads((GOLDEN / "cache_rr4d.json").read_text())
+    gone = doc["entries"].pop(4)
+    (tmp_path / "short.json").write_text(json.dumps({k: v for k, v in doc.items() if k != "checksum"}))
+    with pytest.raises(gt.CacheError, match="entries but the space has"):
+        gt.MeasurementCache.load(tmp_path / "short.json")
+    # same count, one configuration replaced by an index outside the space
+    doc["entries"].append({"index": 10 ** 12, "value": 1.0})
+    doc.pop("checksum")
+    (tmp_path / "m.json").write_text(json.dumps(doc))
+    with pytest.raises(gt.CacheError, match=f"missing an entry for configuration {gone['index']}"):
+        gt.MeasurementCache.load(tmp_path / "m.json")
+    assert len(gt.MeasurementCache.load(GOLDEN / "cache_rr4d.json").ids) == len(doc["entries"])

@@ -52,3 +52,20 @@ def test_cases_batched(gt):
         out = gt.run_bo_batch(es, es.ids, [cfg, cfg], t["values"], threads=2)
         for r in out:
             np.testing.assert_array_equal(r.positions, t["traj_pos"])
+
+
+@pytest.mark.parametrize("field,value,exc,msg", [
+    ("lengthscale", -1.0, "Error", "kernel lengthscale must be positive"),
+    ("lengthscale", 0.0, "Error", "kernel lengthscale must be positive"),
+    ("discount", 1.5, "ConfigError", "discount factor must be in"),
+    ("discount", 0.0, "ConfigError", "discount factor must be in"),
+])
+def test_out_of_range_config_fails_like_the_reference(gt, field, value, exc, msg):
+    """A user-supplied lengthscale <= 0 or discount outside (0,1) is an error
+    (gp.hpp:35, portfolio.hpp:107), never silently replaced by the default."""
+    from paper_2111_14991_b200 import synthetic
+    coords, ids, values = synthetic.random_rough([6, 6], 3, 0.0)
+    space = gt.Space(coords)
+    cfg = gt.StrategyConfig(id=gt.StrategyId.bo_multi, seed=1, budget=30, n_init=5, **{field: value})
+    with pytest.raises(getattr(gt, exc), match=msg):
+        gt.run_bo(space, ids, cfg, values=values)

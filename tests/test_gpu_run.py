@@ -139,6 +139,23 @@ def test_append_jitter_escalation_matches_refit(gt, oracle):
     assert rel(var[[3, 4]], v2[[3, 4]]) <= 1e-6
 
 
+def test_truncate_after_escalation_refits_prefix_at_base_jitter(gt, oracle):
+    """Truncating below the observation that forced a jitter escalation gives
+    GpModel::fit of the prefix, which restarts at the base jitter."""
+    coords = np.array([[0.2, 0.2], [0.2 + 1e-9, 0.2], [0.7, 0.1], [0.9, 0.9], [0.5, 0.5]])
+    run = gt.SurrogateRun(gt.Space(coords), gt.MaternKernel(), 0.0, 1e-17, 8)
+    run.fit([0, 2], [1.0, 3.0])
+    assert run.append(1, 2.0).jitter == 1.6e-16
+    info = run.truncate(2)
+    assert info.jitter == 1e-17 and info.n == 2
+    rc, om = oracle.fit(1, 2.0, 1.0, coords[[0, 2]], np.array([1.0, 3.0]), noise=0.0, jitter=1e-17)
+    mean, var = run.predictions()
+    m2, v2 = oracle.predict(om, coords)
+    assert rel(mean, m2) <= 1e-9 and rel(var, v2) <= 1e-9
+    info = run.append(3, 0.5)  # appends at the base jitter again
+    assert info.jitter == 1e-17
+
+
 def test_conditioning_error_on_append(gt):
     coords = np.array([[0.5], [0.5 + 1e-12], [0.9]])
     run = gt.SurrogateRun(gt.Space(coords), gt.MaternKernel(), 0.0, 1e-300, 8)

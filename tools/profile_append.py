@@ -1,5 +1,5 @@
 import sys, numpy as np, ctypes as C
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
 import paper_2111_14991_b200 as gt
 from paper_2111_14991_b200 import synthetic, _lib
 coords, ids, values = synthetic.random_rough([10]*6, 20261017, 0.0)

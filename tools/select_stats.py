@@ -5,7 +5,7 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
 import paper_2111_14991_b200 as gt  # noqa: E402
 from paper_2111_14991_b200 import synthetic  # noqa: E402
 from paper_2111_14991_b200 import AcquisitionId, ContextualVarianceState, ExplorationConfig  # noqa: E402

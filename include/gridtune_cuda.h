@@ -328,6 +328,10 @@ int gtc_last_phase_ms(const gtc_run* run, double* out3);
  * seen by gtc_observe: [0] start, [1] factor staged, [2] Gram row, [3] forward
  * solve, [4] pivot/row written, [5] c/e rows, [6] statistics + beta. */
 int gtc_debug_append_marks(const gtc_run* run, uint64_t* marks7);
+/* Diagnostics of libraries built with -DGTC_SEL_TRACE (GTC_ERR_INVALID
+ * otherwise): %globaltimer marks (ns), 8 per row: rows < grid = the last
+ * selection's blocks, row 2040 the loop-mode append, row 2041 the pass. */
+int gtc_debug_select_trace(uint64_t* marks, int32_t rows);
 /* Diagnostics: bordered rows (since the run was created) whose
  * V-column pivot was below the exactness margin, so the exact forward
  * substitution ran (as of the last synchronising call). */

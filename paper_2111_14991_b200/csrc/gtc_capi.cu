@@ -2127,6 +2127,13 @@ extern "C" int gtc_debug_append_marks(const gtc_run* r, uint64_t* marks) {
   return GTC_OK;
 }
 
+extern "C" int gtc_debug_select_trace(uint64_t* marks, int32_t rows) {
+  if (!marks || rows <= 0 || rows > 2048) return fail(GTC_ERR_INVALID, "bad arguments");
+  if (read_sel_trace(reinterpret_cast<unsigned long long*>(marks), rows))
+    return fail(GTC_ERR_INVALID, "library built without GTC_SEL_TRACE");
+  return GTC_OK;
+}
+
 extern "C" int64_t gtc_run_exact_rows(const gtc_run* r) { return r ? (int64_t)r->gp.h_sc->exact_rows : -1; }
 extern "C" uint64_t gtc_run_stream(const gtc_run* r) { return r ? (uint64_t)(uintptr_t)r->stream : 0; }
 

@@ -482,6 +482,7 @@ void launch_extend_loop(const ExtendArgs& a, int64_t tiles, int nu, cudaStream_t
 void set_thread_pdl(bool on);
 
 int reduce_blocks(int64_t n);  // grid size used by the reduction kernels
+int read_sel_trace(unsigned long long* out, int rows);  // GTC_SEL_TRACE builds (diagnostics)
 uint64_t launches();
 
 }  // namespace gtc

@@ -51,9 +51,25 @@ namespace gtc {
 __device__ unsigned long long g_sel_trace[2048][8];
 #define SEL_MARK(k) \
   do { if (threadIdx.x == 0) g_sel_trace[blockIdx.x][k] = gtc_globaltimer(); } while (0)
+#define TRACE_AT(row, k) \
+  do { if (threadIdx.x == 0) g_sel_trace[row][k] = gtc_globaltimer(); } while (0)
 #else
 #define SEL_MARK(k) do {} while (0)
+#define TRACE_AT(row, k) do {} while (0)
 #endif
+
+// Diagnostics (GTC_SEL_TRACE builds only): the %globaltimer marks of the
+// last selection (rows = blocks; marks 0-3, 5 per block, 6 in the last
+// block), the loop-mode append (row 2040) and the pass (row 2041, block 0).
+int read_sel_trace(unsigned long long* out, int rows) {
+#ifdef GTC_SEL_TRACE
+  return cudaMemcpyFromSymbol(out, g_sel_trace, sizeof(unsigned long long) * 8 * (size_t)rows) == cudaSuccess ? 0 : -4;
+#else
+  (void)out;
+  (void)rows;
+  return -1;
+#endif
+}
 
 static std::atomic<uint64_t> g_launches{0};
 uint64_t launches() { return g_launches.load(); }
@@ -660,17 +676,30 @@ __device__ void gp_append_body(const AppendArgs& a) {
   pdl_begin();
   unsigned long long* tm = g.sc->t;
   if (a.loop) {
-    // resident loop: the selection's last block already appended this step's
-    // observation from the pick's V column; this kernel only runs the exact
-    // bordered row when that pivot fell below the margin (status 2)
+    // resident loop: this step's pick (loop_advance, in the selection's last
+    // block) is appended from its V column here; a sharded loop's merge kernel
+    // already did that and this kernel only runs the exact bordered row when
+    // the column pivot fell below the margin (status 2)
     const LoopDev* lp = a.loop;
-    if (lp->halt != kLoopRunning || !lp->valid || g.sc->status != 2) return;
+    TRACE_AT(2040, 0);
+    if (lp->halt != kLoopRunning || !lp->valid) return;
     pos = lp->pos;
     n0 = lp->n0;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      g.sc->status = 0;
-      ++g.sc->exact_rows;
+    if (lp->nranks == 0) {
+      append_prologue(g, lp->sp, pos, nullptr, lp->y, n0);
+      TRACE_AT(2040, 1);
+      const double* col = lp->V + (pos / kTile) * lp->tile_stride + pos % kTile;
+      const bool ok = column_border_row(g, k, noise, col, kTile, n0, m.xs);
+      TRACE_AT(2040, 2);
+      if (ok) return;
+      if (threadIdx.x == 0) ++g.sc->exact_rows;
+    } else {
+      if (g.sc->status != 2) return;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        g.sc->status = 0;
+        ++g.sc->exact_rows;
+      }
     }
   } else {
     if (a.visited_mark && threadIdx.x == 0) a.visited_mark[pos >> 5] |= 1u << (pos & 31);
@@ -746,6 +775,7 @@ template <int R, int NU, int UP = GTC_PASS_U>
 __device__ __forceinline__ void extend_body(const ExtendArgs& a_in) {
   ExtendArgs a = a_in;
   pdl_begin();
+  if (blockIdx.x == 0) TRACE_AT(2041, 0);
   if (a.loop) {  // resident loop: only after a valid evaluation; generation flipped by loop_advance
     const LoopDev* lp = a.loop;
     if (lp->halt != kLoopRunning || !lp->valid) return;
@@ -1530,22 +1560,6 @@ __device__ void select_publish(const SelCtx& c, const SelPart& f, double best, d
 #endif
 }
 
-// The bordered append of the resident loop's valid step, by the selection's
-// last block right after loop_advance: training row, then the new factor row
-// from the pick's V column (column_border_row).  When its pivot is below the
-// margin, status 2 leaves the exact row to the loop's append kernel (which is
-// a no-op otherwise) and the predictive pass waits for it.
-__device__ void loop_column_append(LoopDev* L) {
-  __shared__ double xs[kMaxNmax];
-  if (L->halt != kLoopRunning || !L->valid) return;  // (uniform: written before the barrier)
-  const int64_t pos = L->pos;
-  const int n0 = L->n0;
-  const GpDev g = L->g;
-  append_prologue(g, L->sp, pos, nullptr, L->y, n0);
-  const double* col = L->V + (pos / kTile) * L->tile_stride + pos % kTile;
-  if (!column_border_row(g, L->kp, L->noise, col, kTile, n0, xs) && threadIdx.x == 0) g.sc->status = 2;
-}
-
 // Candidate-axis sharding: the shard's selection record for the all-gather
 // (ShardHdr + the winners' coordinates and V columns, gtc_internal.h), from
 // the local result select_publish just wrote.  Block-wide.
@@ -1641,12 +1655,9 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first
     f = sel_warp_reduce<MASK>(lane < nw ? red[lane] : none);
     if (lane == 0) select_publish<MASK>(c, f, best, lambda, mean_var, cv_fallback, gp_status);
   }
-  if (c.loop) {
-    __syncthreads();  // loop_advance / the local result (thread 0) done
-    if (c.loop->nranks > 0)
-      shard_publish(c, c.loop);
-    else
-      loop_column_append(c.loop);
+  if (c.loop && c.loop->nranks > 0) {
+    __syncthreads();  // the local result (thread 0) done
+    shard_publish(c, c.loop);
   }
 }
 

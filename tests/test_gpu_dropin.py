@@ -47,3 +47,30 @@ def test_reference_acceptance_on_the_b200_backend():
     fails = [l for l in text.splitlines() if l.startswith("[FAIL]") and not l.startswith("[FAIL] criterion 2:")]
     assert "[PASS] criterion 1:" in text
     assert not fails, text[-3000:]
+
+
+def _golden_rows():
+    import sys
+    sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent / "golden"))
+    from make_golden import TRAJECTORIES
+    return TRAJECTORIES
+
+
+@pytest.mark.parametrize("row", _golden_rows(), ids=lambda r: r[0])
+def test_run_bo_b200_reproduces_reference_trajectories(row):
+    """INTEGRATION.md §3 as compiled code: run_bo_b200 (the reference's run_bo
+    signature, types and objective callback; the loop on the B200 library)
+    picks the same configurations as the unmodified reference's run_bo on the
+    golden runs (tests/golden/traj_*.npz), lambda within 1e-9."""
+    import json
+
+    import numpy as np
+    name, fn, grid, sseed, inv, strategy, budget, n_init, bseed = row
+    out = run("dropin_runbo", fn, grid, str(sseed), inv, strategy, str(budget), str(n_init), str(bseed))
+    assert out.returncode == 0, out.stderr
+    got = json.loads(out.stdout.strip().splitlines()[-1])
+    z = np.load(pathlib.Path(__file__).resolve().parent / "golden" / f"traj_{name}.npz")
+    np.testing.assert_array_equal(np.array(got["pos"]), z["traj_pos"])
+    lam = np.array(got["lambda"])
+    assert len(lam) == len(z["traj_lambda"])
+    np.testing.assert_allclose(lam, z["traj_lambda"], rtol=1e-9, atol=1e-12)

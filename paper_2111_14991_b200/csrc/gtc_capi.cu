@@ -1349,6 +1349,10 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
       L.gsel = r->red.sel;
     }
     L.sel_mask = mask;
+    // one device: the selection's last block appends valid picks (no append
+    // kernel per step); sharded: the merge kernel + the append kernel do
+    L.fused_append = sharded ? 0 : 1;
+    const int fused_n_max = sharded ? 0 : r->cfg.n_max;
     GTC_CUDA(cudaMemcpyAsync(r->d_loop, r->h_loop, sizeof(LoopDev), cudaMemcpyHostToDevice, r->stream));
     // (every per-run / per-step selection input is read from the loop state:
     // the launch arguments depend only on the run handle and its model config)
@@ -1377,8 +1381,7 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     cudaEvent_t* te = r->step_events.data();
     auto launch_iteration = [&]() -> int {
       launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, vs, r->tstat, r->red.b, r->red.sel,
-                    r->stream);
-      launch_gp_append_loop(aa, r->cfg.kernel.nu, append_smem, r->stream);
+                    r->stream, fused_n_max);
       launch_extend_loop(ea, r->space->n_pad / kTile, r->cfg.kernel.nu, r->stream);
       GTC_LAUNCHED();
       return GTC_OK;
@@ -1442,10 +1445,11 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     for (int i = 0; i < m && !graphed && !sharded; ++i) {
       if (timing) GTC_CUDA(cudaEventRecord(te[3 * i], r->stream));
       launch_select(r->mu, r->var, r->visited, r->space->n, r->gp.dev.sc, p, vs, r->tstat, r->red.b, r->red.sel,
-                    r->stream);
-      if (timing) GTC_CUDA(cudaEventRecord(te[3 * i + 1], r->stream));
-      launch_gp_append_loop(aa, r->cfg.kernel.nu, append_smem, r->stream);
-      if (timing) GTC_CUDA(cudaEventRecord(te[3 * i + 2], r->stream));
+                    r->stream, fused_n_max);
+      if (timing) {  // (the append runs in the selection's last block: an empty phase)
+        GTC_CUDA(cudaEventRecord(te[3 * i + 1], r->stream));
+        GTC_CUDA(cudaEventRecord(te[3 * i + 2], r->stream));
+      }
       launch_extend_loop(ea, r->space->n_pad / kTile, r->cfg.kernel.nu, r->stream);
       GTC_LAUNCHED();
     }

@@ -326,7 +326,10 @@ void launch_varsum(const double* var, const uint32_t* visited, int64_t n, double
 // argmax for every AF in the mask.
 void launch_select(const double* mu, const double* var, const uint32_t* visited, int64_t n,
                    const GpScalars* sc, SelectParams p, const VarSource& vs, const TileStats* tstat,
-                   const ReduceBufs& bufs, SelectDev* out, cudaStream_t stream);
+                   const ReduceBufs& bufs, SelectDev* out, cudaStream_t stream, int fused_append_n_max = 0);
+// Dynamic shared memory of a loop-mode selection whose last block appends the
+// pick (LoopDev::fused_append), for a model of n_max rows.
+size_t loop_append_smem(int n_max);
 
 // best_candidate over caller spans of stds (not variances).
 void launch_best_candidate(const double* mu, const double* std, const uint8_t* excluded,
@@ -439,6 +442,8 @@ struct LoopDev {
   SpaceDev sp;
   const double* V;
   int64_t tile_stride;
+  int32_t fused_append;     // the selection's last block appends valid picks (loop_append; no append kernel)
+  int32_t pad_fa;
   // candidate-axis sharding (nranks > 0): the loop's positions, records and
   // value table are GLOBAL; visited / first / count / acc / var are this
   // shard's candidates [offset, offset + n_space)

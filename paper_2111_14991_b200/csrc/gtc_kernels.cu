@@ -776,15 +776,29 @@ __device__ __forceinline__ void extend_body(const ExtendArgs& a_in) {
   ExtendArgs a = a_in;
   pdl_begin();
   if (blockIdx.x == 0) TRACE_AT(2041, 0);
-  if (a.loop) {  // resident loop: only after a valid evaluation; generation flipped by loop_advance
-    const LoopDev* lp = a.loop;
-    if (lp->halt != kLoopRunning || !lp->valid) return;
-    a.n0 = lp->n0;
-    a.acc = lp->acc + lp->gen;
-    a.acc_clear = lp->acc + (lp->gen ^ 1);
+  // resident loop: only after a valid evaluation; generation flipped by
+  // loop_advance.  One thread per CTA reads the loop state and the status
+  // word (every CTA reads the same words: one request per CTA, not per warp).
+  __shared__ int s_n0, s_gen, s_status;
+  __shared__ VarAccum* s_acc;
+  if (threadIdx.x == 0) {
+    if (a.loop) {
+      const LoopDev* lp = a.loop;
+      s_n0 = (lp->halt != kLoopRunning || !lp->valid) ? -1 : lp->n0;
+      s_gen = lp->gen;
+      s_acc = lp->acc;
+    }
+    s_status = a.check_status ? a.g.sc->status : 0;
+  }
+  __syncthreads();
+  if (a.loop) {
+    if (s_n0 < 0) return;
+    a.n0 = s_n0;
+    a.acc = s_acc + s_gen;
+    a.acc_clear = s_acc + (s_gen ^ 1);
   }
   accum_clear(a.acc_clear);  // next generation's accumulator (even when the pass is skipped)
-  if (a.check_status && a.g.sc->status != 0) return;  // bordered row failed: host refactors
+  if (s_status != 0) return;  // bordered row failed: host refactors
   extern __shared__ double sm[];
   const int n0 = a.n0, r = a.r;
   const int ld = n0 + R;
@@ -984,6 +998,9 @@ __device__ __forceinline__ void extend_body(const ExtendArgs& a_in) {
           }
         }
         if (a.acc) accum_add(a.acc, ts, tc, a.s2);
+#ifdef GTC_SEL_TRACE
+        atomicMax(&g_sel_trace[2043][0], gtc_globaltimer());
+#endif
         if (a.tstat)
           a.tstat[blockIdx.x] =
               TileStats{mn, vx >= 0.0 ? vx : -1.0, vn, sm_, sv, sp == LLONG_MAX ? -1 : (int64_t)sp};
@@ -1511,13 +1528,13 @@ void launch_portfolio_trace(const PortDev& P, const PortOp* d_ops, int n, PortSt
 // loop's advance.
 template <uint32_t MASK>
 __device__ void select_publish(const SelCtx& c, const SelPart& f, double best, double lambda, double mean_var,
-                               int cv_fallback, int gp_status) {
+                               int cv_fallback, int gp_status, SelectDev* out, LoopDev* loop) {
   const int64_t ff = f.first;
   const long long fc = f.cnt;
-  c.out->first_nan_mask = 0;
+  out->first_nan_mask = 0;
   for (int af = 0; af < 3; ++af) {
-    c.out->best_nonnan_pos[af] = -1;
-    c.out->best_nonnan_score[af] = 0.0;
+    out->best_nonnan_pos[af] = -1;
+    out->best_nonnan_score[af] = 0.0;
   }
   for (int af = 0; af < 3; ++af) {
     int64_t pos = -1;
@@ -1538,26 +1555,231 @@ __device__ void select_publish(const SelCtx& c, const SelPart& f, double best, d
         sc = f.b[af].s;
       }
       // the pieces a cross-shard merge needs to apply the same rule
-      c.out->best_nonnan_pos[af] = f.b[af].p == INT64_MAX ? -1 : f.b[af].p;
-      c.out->best_nonnan_score[af] = f.b[af].s;
-      if (first_nan) c.out->first_nan_mask |= 1u << af;
+      out->best_nonnan_pos[af] = f.b[af].p == INT64_MAX ? -1 : f.b[af].p;
+      out->best_nonnan_score[af] = f.b[af].s;
+      if (first_nan) out->first_nan_mask |= 1u << af;
     }
-    c.out->position[af] = pos;
-    c.out->score[af] = sc;
+    out->position[af] = pos;
+    out->score[af] = sc;
   }
-  c.out->first_eligible = fc > 0 ? ff : -1;
-  c.out->lambda = lambda;
-  c.out->mean_variance = mean_var;
-  c.out->best_std = best;
-  c.out->n_candidates = (int64_t)fc;
-  c.out->cv_fallback = cv_fallback;
-  c.out->gp_status = gp_status;
+  out->first_eligible = fc > 0 ? ff : -1;
+  out->lambda = lambda;
+  out->mean_variance = mean_var;
+  out->best_std = best;
+  out->n_candidates = (int64_t)fc;
+  out->cv_fallback = cv_fallback;
+  out->gp_status = gp_status;
   if (c.b.gthr) c.b.gthr[0] = c.b.gthr[1] = c.b.gthr[2] = 0ull;  // next selection starts afresh
   *c.b.counter = 0;
-  if (c.loop && c.loop->nranks == 0) loop_advance(c.loop, c.out);  // (sharded: k_shard_merge advances)
 #ifdef GTC_SEL_TRACE
-  g_sel_trace[blockIdx.x][6] = gtc_globaltimer();
+  g_sel_trace[2042][2] = gtc_globaltimer();
 #endif
+  if (loop && loop->nranks == 0) loop_advance(loop, out);  // (sharded: k_shard_merge advances)
+#ifdef GTC_SEL_TRACE
+  g_sel_trace[2042][3] = gtc_globaltimer();
+#endif
+}
+
+// ---- the resident loop's bordered append, fused into the selection's last block
+//
+// Dynamic shared memory of a loop-mode selection (loop_append_smem): l, c, e,
+// y, the substitution result and the pivot reciprocals [n_max] each, the
+// pick's coordinates [kMaxDim], the virtual-lane partials [4][256] and the
+// reduction scratch [32].
+__host__ __device__ __forceinline__ size_t loop_append_doubles(int n_max) {
+  return 6 * (size_t)n_max + kMaxDim + 4 * 256 + 32;
+}
+
+__device__ __forceinline__ double matern_rt(int nu, double r, double l, double s2) {
+  return nu == 0 ? matern<0>(r, l, s2) : nu == 1 ? matern<1>(r, l, s2) : matern<2>(r, l, s2);
+}
+
+// cta_stats_beta over shared copies of y, c, e (n entries, the sum of y given):
+// the same operations in the same order, so the same bits.
+__device__ void stats_beta_staged(const GpDev& g, int n, double ysum, double y0, const double* ys, const double* cs,
+                                  const double* es, double (*lanes)[256], double* red) {
+  const double mean = n > 0 ? __ddiv_rn(ysum, (double)n) : 0.0;
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+    double part = 0.0;
+    for (int i = v; i < n; i += 256) {
+      const double dv = __dadd_rn(ys[i], -mean);
+      part = __dadd_rn(part, __dmul_rn(dv, dv));
+    }
+    lanes[0][v] = part;
+  }
+  double out[1];
+  vsum256<1>(lanes, out, red);
+  double stdv = 1.0;
+  if (n > 1) {
+    const double var = __ddiv_rn(out[0], (double)n);
+    stdv = var > 0.0 ? sqrt(var) : 1.0;
+  }
+  if (threadIdx.x == 0) {
+    g.sc->y_mean = mean;
+    g.sc->y_std = stdv;
+    g.sc->n = n;
+  }
+  const double shift = __dadd_rn(mean, -y0);
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    g.beta[i] = __ddiv_rn(__dadd_rn(cs[i], -__dmul_rn(shift, es[i])), stdv);
+}
+
+// Observation n0 = the step's valid pick, appended to the factor by the
+// selection's last block right after loop_advance (no separate kernel, no
+// launch boundary in the resident loop).  Every input is loaded at once (the
+// pick's V column and coordinates, c, e, y, the scalars); then
+//  - the V-column row (column_border_row: l = V(:, x*), the same fused
+//    virtual-lane sums, the same 2^-8 pivot margin), or below the margin
+//  - the exact bordered row (gp.hpp:105-121): Gram row with direct
+//    differences, forward substitution as a column sweep -- each row's
+//    subtractions in ascending column order, then times 1/L_ii, the operation
+//    order of cta_forward_solve -- and |l|^2, l.c, l.e as virtual-lane sums
+//    (== block_sum in the 256-thread GP kernels), so both rows are
+//    bit-identical to k_gp_append's;
+//  - then the standardisation and beta (cta_stats_beta's order).
+// A failed exact pivot (x <= 0) sets status 1: the pass skips, the next
+// selection halts the loop (kLoopPivot) and the host refactorises.
+// `L` is the last block's shared copy of the loop state (already advanced).
+__device__ void loop_append(const LoopDev& L, double* dsm) {
+  const GpDev& g = L.g;
+  const int n0 = L.n0, d = L.sp.d, nm = g.n_max;
+  const int64_t pos = L.pos;
+  double* ls = dsm;
+  double* cs = ls + nm;
+  double* es = cs + nm;
+  double* ys = es + nm;
+  double* xsol = ys + nm;
+  double* rv = xsol + nm;
+  double* xn = rv + nm;
+  double (*lanes)[256] = reinterpret_cast<double (*)[256]>(xn + kMaxDim);
+  double* red = xn + kMaxDim + 4 * 256;
+  __shared__ double s_y0, s_jit;
+  TRACE_AT(2040, 0);
+  const double* col = L.V + (pos / kTile) * L.tile_stride + pos % kTile;
+  for (int q = threadIdx.x; q < n0; q += blockDim.x) {
+    ls[q] = __ldcg(col + (int64_t)q * kTile);
+    cs[q] = __ldcg(g.c + q);
+    es[q] = __ldcg(g.e + q);
+    ys[q] = __ldcg(g.y + q);
+  }
+  for (int t = threadIdx.x; t < d; t += blockDim.x) xn[t] = __ldcg(L.sp.coords + (int64_t)t * L.sp.n_pad + pos);
+  if (threadIdx.x == 0) {
+    s_y0 = n0 == 0 ? L.y : __ldcg(&g.sc->y0);
+    s_jit = __ldcg(&g.sc->jitter);
+    ys[n0] = L.y;
+  }
+  __syncthreads();
+  TRACE_AT(2040, 1);
+  // append_prologue's effects: training row, its squared norm, the value, status
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int t = 0; t < d; ++t) {
+      g.train_x[(int64_t)n0 * d + t] = xn[t];
+      s = __dadd_rn(s, __dmul_rn(xn[t], xn[t]));
+    }
+    g.train_n2[n0] = s;
+    g.y[n0] = L.y;
+    g.sc->status = 0;
+    g.sc->fail_row = -1;
+    if (n0 == 0) g.sc->y0 = L.y;
+  }
+  // |l|^2, l.c, l.e and the sum of y[0, n0] in one virtual-lane reduction
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+    double sq = 0.0, pc = 0.0, pe = 0.0, py = 0.0;
+    for (int q = v; q < n0; q += 256) {
+      const double l = ls[q];
+      sq = __dadd_rn(sq, __dmul_rn(l, l));
+      pc = __dadd_rn(pc, __dmul_rn(l, cs[q]));
+      pe = __dadd_rn(pe, __dmul_rn(l, es[q]));
+      py = __dadd_rn(py, ys[q]);
+    }
+    if (v == n0 % 256) py = __dadd_rn(py, ys[n0]);  // the new observation, last in its lane
+    lanes[0][v] = sq;
+    lanes[1][v] = pc;
+    lanes[2][v] = pe;
+    lanes[3][v] = py;
+  }
+  double r[4];
+  vsum256<4>(lanes, r, red);
+  const double diag = __dadd_rn(L.kp.s2, __dadd_rn(L.noise, s_jit));
+  const double yr = __dadd_rn(L.y, -s_y0);
+  double* Lrow = g.L + packed(n0);
+  const double x = __dadd_rn(diag, -r[0]);
+  const double* lrow = ls;
+  if (!(x > 0x1p-8 * diag)) {
+    // ---- exact bordered row
+    const double* xr = xn;
+    for (int q = threadIdx.x; q < n0; q += blockDim.x) {
+      const double* xa = g.train_x + (int64_t)q * d;
+      double ss = 0.0;
+      for (int t = 0; t < d; ++t) {
+        const double dv = __dadd_rn(xa[t], -xr[t]);
+        ss = __dadd_rn(ss, __dmul_rn(dv, dv));
+      }
+      ls[q] = matern_rt(L.kp.nu, sqrt(ss), L.kp.lengthscale, L.kp.s2);
+      rv[q] = __drcp_rn(__ldg(g.L + packed(q) + q));
+    }
+    __syncthreads();
+    // rows are owned by fixed threads, so each thread walks its rows of the
+    // packed factor sequentially (L1 lines reused across iterations)
+    for (int i = 0; i < n0; ++i) {
+      const double xi = __dmul_rn(ls[i], rv[i]);
+      if (threadIdx.x == 0) xsol[i] = xi;
+      for (int q = threadIdx.x; q < n0; q += blockDim.x)
+        if (q > i) ls[q] = __dadd_rn(ls[q], -__dmul_rn(__ldg(g.L + packed(q) + i), xi));
+      __syncthreads();
+    }
+    for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+      double sq = 0.0;
+      for (int q = v; q < n0; q += 256) sq = __dadd_rn(sq, __dmul_rn(xsol[q], xsol[q]));
+      lanes[0][v] = sq;
+    }
+    double t1[1];
+    vsum256<1>(lanes, t1, red);
+    const double xe = __dadd_rn(diag, -t1[0]);
+    if (xe <= 0.0) {  // Eigen LLT fails exactly when x <= 0 (a NaN pivot proceeds)
+      if (threadIdx.x == 0) {
+        g.sc->status = 1;
+        g.sc->fail_row = n0;
+      }
+      __syncthreads();
+      return;
+    }
+    const double lnn = sqrt(xe);
+    for (int q = threadIdx.x; q < n0; q += blockDim.x) Lrow[q] = xsol[q];
+    for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+      double pc = 0.0, pe = 0.0;
+      for (int q = v; q < n0; q += 256) {
+        pc = __dadd_rn(pc, __dmul_rn(xsol[q], cs[q]));
+        pe = __dadd_rn(pe, __dmul_rn(xsol[q], es[q]));
+      }
+      lanes[0][v] = pc;
+      lanes[1][v] = pe;
+    }
+    double t2[2];
+    vsum256<2>(lanes, t2, red);
+    if (threadIdx.x == 0) {
+      Lrow[n0] = lnn;
+      cs[n0] = __ddiv_rn(__dadd_rn(yr, -t2[0]), lnn);
+      es[n0] = __ddiv_rn(__dadd_rn(1.0, -t2[1]), lnn);
+      g.c[n0] = cs[n0];
+      g.e[n0] = es[n0];
+      ++g.sc->exact_rows;
+    }
+  } else {
+    const double lnn = sqrt(x);
+    for (int q = threadIdx.x; q < n0; q += blockDim.x) Lrow[q] = lrow[q];
+    if (threadIdx.x == 0) {
+      Lrow[n0] = lnn;
+      cs[n0] = __ddiv_rn(__dadd_rn(yr, -r[1]), lnn);
+      es[n0] = __ddiv_rn(__dadd_rn(1.0, -r[2]), lnn);
+      g.c[n0] = cs[n0];
+      g.e[n0] = es[n0];
+    }
+  }
+  __syncthreads();
+  TRACE_AT(2040, 2);
+  stats_beta_staged(g, n0 + 1, r[3], s_y0, ys, cs, es, lanes, red);
 }
 
 // Candidate-axis sharding: the shard's selection record for the all-gather
@@ -1632,8 +1854,19 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first
   __syncthreads();
   SEL_MARK(5);
   if (!is_last) return;
-  // last block: merge the per-block records (all loads in flight at once)
+  TRACE_AT(2042, 0);
+  // last block: merge the per-block records (all loads in flight at once).
+  // The result record and the loop state are built in shared memory (one
+  // thread advances the loop: dependent global round trips would serialise)
+  // and copied out block-wide.
+  __shared__ SelectDev s_out;
+  __shared__ LoopDev s_loop;
+  static_assert(sizeof(LoopDev) % 8 == 0 && sizeof(SelectDev) % 8 == 0, "word copies");
+  constexpr int kLoopWords = sizeof(LoopDev) / 8, kOutWords = sizeof(SelectDev) / 8;
   __threadfence();
+  if (c.loop)
+    for (int i = threadIdx.x; i < kLoopWords; i += blockDim.x)
+      reinterpret_cast<unsigned long long*>(&s_loop)[i] = __ldcg(reinterpret_cast<const unsigned long long*>(c.loop) + i);
   const SelPart none{{{0.0, INT64_MAX}, {0.0, INT64_MAX}, {0.0, INT64_MAX}}, INT64_MAX, 1, 0};
   SelPart f = none;
   for (int blk = threadIdx.x; blk < (int)gridDim.x; blk += blockDim.x) {
@@ -1648,16 +1881,27 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first
     f = sel_merge<MASK>(f, y);
   }
   f = sel_warp_reduce<MASK>(f);
+  TRACE_AT(2042, 1);
   __syncthreads();  // red[] reuse
   if (lane == 0) red[warp] = f;
   __syncthreads();
   if (warp == 0) {
     f = sel_warp_reduce<MASK>(lane < nw ? red[lane] : none);
-    if (lane == 0) select_publish<MASK>(c, f, best, lambda, mean_var, cv_fallback, gp_status);
+    if (lane == 0) select_publish<MASK>(c, f, best, lambda, mean_var, cv_fallback, gp_status, &s_out,
+                                        c.loop ? &s_loop : nullptr);
   }
-  if (c.loop && c.loop->nranks > 0) {
-    __syncthreads();  // the local result (thread 0) done
+  __syncthreads();  // the result (thread 0) done
+  for (int i = threadIdx.x; i < kOutWords; i += blockDim.x)
+    reinterpret_cast<unsigned long long*>(c.out)[i] = reinterpret_cast<const unsigned long long*>(&s_out)[i];
+  if (c.loop)
+    for (int i = threadIdx.x; i < kLoopWords; i += blockDim.x)
+      reinterpret_cast<unsigned long long*>(c.loop)[i] = reinterpret_cast<const unsigned long long*>(&s_loop)[i];
+  if (c.loop && s_loop.nranks > 0) {
+    __syncthreads();  // c.out / c.loop written
     shard_publish(c, c.loop);
+  } else if (c.loop && s_loop.fused_append && s_loop.halt == kLoopRunning && s_loop.valid) {
+    extern __shared__ double dsm[];
+    loop_append(s_loop, dsm);
   }
 }
 
@@ -2086,7 +2330,16 @@ __device__ __forceinline__ void select_run_body(const SelCtx& c, const GpScalars
     f_mu = c.mu[fp];
     f_var = c.var[fp];
   }
-  const SelSetup u = sel_setup(sc, p, vs);
+#ifdef GTC_SEL_TRACE
+  if (threadIdx.x == 0) { g_sel_trace[blockIdx.x][4] = gtc_globaltimer() + (unsigned long long)(ts0.mu_min == 12345.0); }
+#endif
+  // one thread per block reads the variance total and the GP scalars (every
+  // block reads the same few words: one request per block, not per warp,
+  // keeps the L2 slice that holds them from serialising ~5k requests)
+  __shared__ SelSetup s_u;
+  if (threadIdx.x == 0) s_u = sel_setup(sc, p, vs);
+  __syncthreads();
+  const SelSetup u = s_u;
   const double bm_ei = __dadd_rn(u.best, -u.lambda), bp_pi = __dadd_rn(u.best, u.lambda);
   const bool base_ok = fabs(bm_ei) < 1e30 && fabs(bp_pi) < 1e30;
   const float kInf = __int_as_float(0x7f800000);
@@ -2198,27 +2451,45 @@ template <uint32_t MASK>
 __global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK))
     k_select(SelCtx c, const GpScalars* sc, SelectParams p, VarSource vs, const TileStats* tstat, int ntiles) {
   pdl_begin();
-  if (p.loop) {  // resident loop: per-step inputs from the loop state
-    const LoopDev* lp = p.loop;
-    if (lp->halt != kLoopRunning) return;
-    if (sc->status != 0) {  // the last bordered row failed: the host refactorises
-      if (blockIdx.x == 0 && threadIdx.x == 0) p.loop->halt = kLoopPivot;
-      return;
+  SEL_MARK(7);
+#ifdef GTC_SEL_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_sel_trace[2043][1] = g_sel_trace[2043][0];
+#endif
+  if (p.loop) {  // resident loop: per-step inputs from the loop state (read by one thread per block)
+    __shared__ SelectParams s_p;
+    __shared__ VarSource s_vs;
+    __shared__ int s_go;
+    if (threadIdx.x == 0) {
+      const LoopDev* lp = p.loop;
+      int go = lp->halt == kLoopRunning;
+      if (go && sc->status != 0) {  // the last bordered row failed: the host refactorises
+        if (blockIdx.x == 0) p.loop->halt = kLoopPivot;
+        go = 0;
+      }
+      if (go) {
+        p.f_best_raw = lp->f_best;
+        p.first_eligible = lp->first;
+        p.n_candidates = lp->count;
+        p.lambda_mode = lp->lambda_mode;
+        p.lambda_constant = lp->lambda_constant;
+        p.cv_mu_s = lp->cv_mu_s;
+        p.cv_var_s = lp->cv_var_s;
+        if (lp->nranks > 0) {  // sharded: the global total from every shard's accumulators
+          vs.gathered = lp->gacc;
+          vs.n_gathered = lp->nranks;
+          vs.gen = lp->gen;
+        } else {
+          vs.acc = lp->acc + lp->gen;
+        }
+        s_p = p;
+        s_vs = vs;
+      }
+      s_go = go;
     }
-    p.f_best_raw = lp->f_best;
-    p.first_eligible = lp->first;
-    p.n_candidates = lp->count;
-    p.lambda_mode = lp->lambda_mode;
-    p.lambda_constant = lp->lambda_constant;
-    p.cv_mu_s = lp->cv_mu_s;
-    p.cv_var_s = lp->cv_var_s;
-    if (lp->nranks > 0) {  // sharded: the global total from every shard's accumulators
-      vs.gathered = lp->gacc;
-      vs.n_gathered = lp->nranks;
-      vs.gen = lp->gen;
-    } else {
-      vs.acc = lp->acc + lp->gen;
-    }
+    __syncthreads();
+    if (!s_go) return;
+    p = s_p;
+    vs = s_vs;
   }
   select_run_body<MASK>(c, sc, p, vs, tstat, ntiles);
 }
@@ -2511,9 +2782,10 @@ static int select_threads(int ntiles, uint32_t mask) {
 
 void launch_select(const double* mu, const double* var, const uint32_t* visited, int64_t n,
                    const GpScalars* sc, SelectParams p, const VarSource& vs, const TileStats* tstat,
-                   const ReduceBufs& b, SelectDev* out, cudaStream_t s) {
+                   const ReduceBufs& b, SelectDev* out, cudaStream_t s, int fused_append_n_max) {
   count_launch();
   SelCtx c{mu, var, nullptr, visited, nullptr, p.excluded, p.n_excluded, n, p.af_mask, b, out, p.loop};
+  const size_t smem = fused_append_n_max > 0 ? loop_append_smem(fused_append_n_max) : 0;
   const uint32_t mask = (p.af_mask & 7u) ? (p.af_mask & 7u) : 7u;
   const int ntiles = (int)((n + kTile - 1) / kTile);
   static const int grid_override = [] {
@@ -2524,8 +2796,9 @@ void launch_select(const double* mu, const double* var, const uint32_t* visited,
   const int grid = std::max(1, std::min({ntiles, want, kMaxReduceGrid}));
   const int threads = select_threads(ntiles, mask);
 #define GTC_SELECT_CASE(M)                                                           \
-  case M:                                                                            \
-    launch_pdl(k_select<M>, dim3(grid), dim3(threads), 0, s, c, sc, p, vs, tstat, ntiles); \
+  case M:                                                                                 \
+    opt_in_smem(k_select<M>, smem);                                                         \
+    launch_pdl(k_select<M>, dim3(grid), dim3(threads), smem, s, c, sc, p, vs, tstat, ntiles); \
     break;
   switch (mask) {  // launch errors surface through the caller's cudaGetLastError()
     GTC_SELECT_CASE(1)
@@ -2538,6 +2811,8 @@ void launch_select(const double* mu, const double* var, const uint32_t* visited,
   }
 #undef GTC_SELECT_CASE
 }
+
+size_t loop_append_smem(int n_max) { return sizeof(double) * loop_append_doubles(n_max); }
 
 void launch_select_batch(const SelectRunArgs* d_args, int count, uint32_t mask, int64_t n, cudaStream_t s) {
   count_launch();

@@ -43,16 +43,18 @@ for rep in range(5):
     blocks = marks[:2040]
     used = blocks[:, 0] > 0
     b = blocks[used].astype(np.int64)
-    t0 = int(b[:, 0].min())
+    t0 = int(b[:, 7].min())
     rel = lambda v: round((int(v) - t0) / 1e3, 2)  # noqa: E731
-    last = b[b[:, 6] > 0]
     row = {
         "blocks": int(used.sum()),
         "select_start_first": 0.0, "select_start_last": rel(b[:, 0].max()),
         "setup_median": rel(np.median(b[:, 1])), "threshold_median": rel(np.median(b[:, 2])),
         "expand_median": rel(np.median(b[:, 3])), "expand_max": rel(b[:, 3].max()),
         "partials_max": rel(b[:, 5].max()),
-        "publish": rel(last[0, 6]) if len(last) else None,
+        "entry_median": rel(np.median(b[:, 7])), "loaded_median": rel(np.median(b[:, 4])),
+        "pass_end": rel(marks[2043, 1]),
+        "last_block_entry": rel(marks[2042, 0]), "last_merged": rel(marks[2042, 1]),
+        "publish_done": rel(marks[2042, 2]), "advance_done": rel(marks[2042, 3]),
         "append_start": rel(marks[2040, 0]), "append_prologue": rel(marks[2040, 1]),
         "append_column": rel(marks[2040, 2]), "pass_start": rel(marks[2041, 0]),
     }

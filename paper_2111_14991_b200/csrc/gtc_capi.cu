@@ -1357,7 +1357,14 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     // (every per-run / per-step selection input is read from the loop state:
     // the launch arguments depend only on the run handle and its model config)
     SelectParams p{mask, 0, 0.0, 0.0, 0.0, 0.0, nullptr, 0, -1, 0, r->d_loop};
-    const VarSource vs = r->vsrc();
+    if (!sharded) {  // L2 warm-up of the winners' table entries and V columns (rows < n0_max)
+      p.pf_table = r->d_values;
+      p.pf_V = r->V;
+      p.pf_tile_stride = r->tile_stride;
+      p.pf_rows = n0_max;
+    }
+    VarSource vs = r->vsrc();
+    vs.acc = r->acc;  // loop mode: both generations (the kernel picks the loop state's)
     // loop-mode launch arguments: per-step values come from the loop state
     AppendArgs aa{};
     size_t append_smem = 0;

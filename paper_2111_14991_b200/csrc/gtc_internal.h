@@ -183,6 +183,13 @@ struct SelectParams {
   LoopDev* loop;            // resident loop: f_best_raw / first_eligible / n_candidates / the
                             // variance total come from the loop state instead, and the
                             // selection's last block advances the loop (loop_advance)
+  // resident loop: every block warms L2 with the value-table entry and the V
+  // column of its local winners (the last block's lookups and the fused
+  // append then hit L2); null outside the loop
+  const double* pf_table = nullptr;
+  const double* pf_V = nullptr;
+  int64_t pf_tile_stride = 0;
+  int32_t pf_rows = 0;
 };
 
 // Per-block scratch of the selection kernels (sized by reduce_blocks(n)).

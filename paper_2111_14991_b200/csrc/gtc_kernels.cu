@@ -193,6 +193,8 @@ __device__ __forceinline__ bool visited_bit(const uint32_t* visited, int64_t j) 
   return (__ldg(visited + (j >> 5)) >> (j & 31)) & 1u;
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 // ---- deterministic variance totals (VarAccum, gtc_internal.h) ----
 __device__ __forceinline__ int var_scale_exp(double s2) {
   const int e = ilogb(s2);
@@ -1235,6 +1237,10 @@ struct SelCtx {
   ReduceBufs b;
   SelectDev* out;
   LoopDev* loop;  // resident loop: advanced by the last block (loop_advance)
+  const double* pf_table;  // SelectParams::pf_* (L2 warm-up of the winners' table entries / V columns)
+  const double* pf_V;
+  int64_t pf_tile_stride;
+  int32_t pf_rows;
 };
 
 __device__ __forceinline__ bool eligible(const SelCtx& c, int64_t j) {
@@ -1453,7 +1459,7 @@ __device__ void loop_advance(LoopDev* L, const SelectDev* sel) {
     if (L->hold) {  // steady state: replace the observation at row hold_n0
       const int64_t prev = L->hold_prev >= 0 ? shard_local(L, L->hold_prev) : -1;
       if (prev >= 0) {
-        L->visited[prev >> 5] &= ~(1u << (prev & 31));
+        atomicAnd(L->visited + (prev >> 5), ~(1u << (prev & 31)));  // (no return value: a reduction, no round trip)
         ++L->count;
         if (L->first < 0 || prev < L->first) L->first = prev;
       }
@@ -1467,7 +1473,7 @@ __device__ void loop_advance(LoopDev* L, const SelectDev* sel) {
       if (y < L->f_best) L->f_best = y;
     }
     L->gen ^= 1;  // the pass produces the next generation
-    if (lpos >= 0) L->visited[lpos >> 5] |= 1u << (lpos & 31);
+    if (lpos >= 0) atomicOr(L->visited + (lpos >> 5), 1u << (lpos & 31));
   } else if (lpos >= 0) {
     // no refit: the variance total loses this candidate in O(1)
     mark_update(L->visited, lpos, 1, L->acc + L->gen, L->var, L->s2);
@@ -1849,6 +1855,16 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first
       c.b.pcnt[blockIdx.x] = v.cnt;
       __threadfence();
       is_last = atomicAdd(c.b.counter, 1u) == gridDim.x - 1;
+    }
+    if (c.pf_table) {  // resident loop: warm L2 for the last block's lookups (any winner may be the pick)
+#pragma unroll
+      for (int af = 0; af < 3; ++af) {
+        const int64_t p = v.b[af].p;
+        if (!(MASK & (1u << af)) || p == INT64_MAX) continue;
+        if (lane == 0) prefetch_l2(c.pf_table + p);
+        const double* col = c.pf_V + (p / kTile) * c.pf_tile_stride + p % kTile;
+        for (int q = lane; q < c.pf_rows; q += 32) prefetch_l2(col + (int64_t)q * kTile);
+      }
     }
   }
   __syncthreads();
@@ -2234,10 +2250,8 @@ struct SelSetup {
   int fallback;
 };
 
-__device__ __forceinline__ SelSetup sel_setup(const GpScalars* sc, const SelectParams& p, const VarSource& vs) {
-  double s;
-  long long cnt;
-  var_source_read(vs, &s, &cnt);
+__device__ __forceinline__ SelSetup sel_setup_vals(double s, long long cnt, const SelectParams& p, double y_mean,
+                                                   double y_std) {
   SelSetup u;
   u.mean_var = cnt > 0 ? __ddiv_rn(s, (double)cnt) : 0.0;
   u.lambda = p.lambda_constant;
@@ -2250,8 +2264,15 @@ __device__ __forceinline__ SelSetup sel_setup(const GpScalars* sc, const SelectP
       u.lambda = l > 0.0 ? l : 0.0;
     }
   }
-  u.best = __ddiv_rn(__dadd_rn(p.f_best_raw, -sc->y_mean), sc->y_std);
+  u.best = __ddiv_rn(__dadd_rn(p.f_best_raw, -y_mean), y_std);
   return u;
+}
+
+__device__ __forceinline__ SelSetup sel_setup(const GpScalars* sc, const SelectParams& p, const VarSource& vs) {
+  double s;
+  long long cnt;
+  var_source_read(vs, &s, &cnt);
+  return sel_setup_vals(s, cnt, p, sc->y_mean, sc->y_std);
 }
 
 // Monotone map of non-NaN doubles to u64 (atomicMax of exact scores); 0 = none.
@@ -2311,8 +2332,8 @@ constexpr int kTileList = 512;  // tiles examined per block per round
 
 template <uint32_t MASK>
 __device__ __forceinline__ void select_run_body(const SelCtx& c, const GpScalars* sc, const SelectParams& p,
-                                                const VarSource& vs, const TileStats* tstat, int ntiles) {
-  __shared__ Best redb[32];
+                                                const VarSource& vs, const TileStats* tstat, int ntiles,
+                                                const SelSetup* pre = nullptr) {
   __shared__ int s_list[kTileList];
   __shared__ int s_n;
   SEL_MARK(0);
@@ -2321,6 +2342,8 @@ __device__ __forceinline__ void select_run_body(const SelCtx& c, const GpScalars
   // this thread's first tile summary, loaded before the variance total (independent)
   TileStats ts0{};
   if ((int)threadIdx.x < mine) ts0 = tstat[blockIdx.x + G * threadIdx.x];
+  // (its seed's eligibility too: the visited word load overlaps the setup below)
+  const bool seed_ok0 = (int)threadIdx.x < mine && ts0.pos_seed >= 0 && eligible(c, ts0.pos_seed);
   // the first eligible candidate's inputs, loaded now by the block that owns it
   // (used at the end; keeps the load off the block's tail)
   const int64_t fp = p.first_eligible;
@@ -2337,40 +2360,57 @@ __device__ __forceinline__ void select_run_body(const SelCtx& c, const GpScalars
   // block reads the same few words: one request per block, not per warp,
   // keeps the L2 slice that holds them from serialising ~5k requests)
   __shared__ SelSetup s_u;
-  if (threadIdx.x == 0) s_u = sel_setup(sc, p, vs);
-  __syncthreads();
-  const SelSetup u = s_u;
+  if (!pre) {
+    if (threadIdx.x == 0) s_u = sel_setup(sc, p, vs);
+    __syncthreads();
+  }
+  const SelSetup u = pre ? *pre : s_u;
   const double bm_ei = __dadd_rn(u.best, -u.lambda), bp_pi = __dadd_rn(u.best, u.lambda);
   const bool base_ok = fabs(bm_ei) < 1e30 && fabs(bp_pi) < 1e30;
   const float kInf = __int_as_float(0x7f800000);
   SEL_MARK(1);
-  // ---- block threshold
-  Best top[3] = {{0.0, INT64_MAX}, {0.0, INT64_MAX}, {0.0, INT64_MAX}};
+  // ---- block threshold: the best exact score among the seeds of this block's
+  // tiles (each tile's unvisited minimum-mean candidate, recorded by the pass
+  // with its mean and variance, so no candidate loads); any exact score of an
+  // eligible candidate is a valid threshold
+  double sb[3] = {-CUDART_INF, -CUDART_INF, -CUDART_INF};
   for (int k = threadIdx.x; k < mine; k += blockDim.x) {
-    const TileStats ts = k == (int)threadIdx.x ? ts0 : tstat[blockIdx.x + G * k];
-    if (ts.pos_seed < 0) continue;
-    float key[3];
-    bool hi;
-    tile_keys<MASK>(ts, key, &hi, base_ok, bm_ei, bp_pi, u.lambda);
+    const bool first_k = k == (int)threadIdx.x;
+    const TileStats ts = first_k ? ts0 : tstat[blockIdx.x + G * k];
+    if (ts.pos_seed < 0 || !(first_k ? seed_ok0 : eligible(c, ts.pos_seed))) continue;  // (marked after the pass)
+    const double sd = sqrt(ts.var_seed);
 #pragma unroll
-    for (int af = 0; af < 3; ++af)
-      if ((MASK & (1u << af)) && key[af] < kInf && key[af] > -kInf)
-        top[af] = better(top[af], Best{(double)key_rank(af, key[af], hi), blockIdx.x + G * k});
+    for (int af = 0; af < 3; ++af) {
+      if (!(MASK & (1u << af))) continue;
+      const double t = score_of(af, ts.mu_seed, sd, u.best, u.lambda);
+      if (t == t) sb[af] = fmax(sb[af], t);
+    }
+  }
+  __shared__ double s_sb[32][3];
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int af = 0; af < 3; ++af) {
+      if (!(MASK & (1u << af))) continue;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sb[af] = fmax(sb[af], __shfl_xor_sync(0xffffffffu, sb[af], o));
+      if (lane == 0) s_sb[warp][af] = sb[af];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int af = 0; af < 3; ++af) {
+        if (!(MASK & (1u << af))) continue;
+        double v = lane < nw ? s_sb[lane][af] : -CUDART_INF;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+        sb[af] = v;
+      }
+    }
   }
   Thr th[3];
 #pragma unroll
-  for (int af = 0; af < 3; ++af) {
-    th[af] = Thr{-CUDART_INF, -kInf};
-    if (!(MASK & (1u << af))) continue;
-    const Best tt = block_best(top[af], redb);  // same in every thread
-    if (tt.p == INT64_MAX) continue;
-    const TileStats ts = tstat[tt.p];
-    const int64_t j = ts.pos_seed;
-    if (!eligible(c, j)) continue;  // (marked visited after the pass)
-    // every thread scores it (no broadcast barrier); same inputs as c.mu/c.var[j]
-    const double t = score_of(af, ts.mu_seed, sqrt(ts.var_seed), u.best, u.lambda);
-    if (t == t) th[af] = make_thr(t);
-  }
+  for (int af = 0; af < 3; ++af) th[af] = Thr{sb[af], -kInf};  // (thread 0's values are the block's)
   // share thresholds across blocks: any block's exact score of an eligible
   // candidate is a valid threshold for every block (blocks far from the
   // optimum would otherwise score most of their candidates exactly)
@@ -2455,43 +2495,65 @@ __global__ void __launch_bounds__(kSelectThreads, sel_blocks_per_sm(MASK))
 #ifdef GTC_SEL_TRACE
   if (blockIdx.x == 0 && threadIdx.x == 0) g_sel_trace[2043][1] = g_sel_trace[2043][0];
 #endif
-  if (p.loop) {  // resident loop: per-step inputs from the loop state (read by one thread per block)
-    __shared__ SelectParams s_p;
-    __shared__ VarSource s_vs;
-    __shared__ int s_go;
+  // Resident loop: the per-step inputs come from the loop state.  One thread
+  // per block issues every load at once -- loop fields, GP scalars and BOTH
+  // variance-accumulator generations (the generation is itself a loaded
+  // value) -- so the block waits one L2 round trip, not a dependent chain;
+  // it computes lambda / best_std and shares them through shared memory.
+  __shared__ SelectParams s_p;
+  __shared__ SelSetup s_pre;
+  __shared__ int s_go, s_have;
+  if (p.loop) {
     if (threadIdx.x == 0) {
       const LoopDev* lp = p.loop;
-      int go = lp->halt == kLoopRunning;
-      if (go && sc->status != 0) {  // the last bordered row failed: the host refactorises
+      const int halt = lp->halt, status = sc->status, nranks = lp->nranks, gen = lp->gen;
+      const double f_best = lp->f_best, lconst = lp->lambda_constant, cvm = lp->cv_mu_s, cvv = lp->cv_var_s;
+      const int64_t first = lp->first, count = lp->count;
+      const int lmode = lp->lambda_mode;
+      const double y_mean = sc->y_mean, y_std = sc->y_std;
+      const VarAccum* gacc = lp->gacc;
+      unsigned long long l[2][5];
+#pragma unroll
+      for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int k = 0; k < 5; ++k) l[g][k] = __ldcg(reinterpret_cast<const unsigned long long*>(vs.acc + g) + k);
+      int go = halt == kLoopRunning;
+      if (go && status != 0) {  // the last bordered row failed: the host refactorises
         if (blockIdx.x == 0) p.loop->halt = kLoopPivot;
         go = 0;
       }
-      if (go) {
-        p.f_best_raw = lp->f_best;
-        p.first_eligible = lp->first;
-        p.n_candidates = lp->count;
-        p.lambda_mode = lp->lambda_mode;
-        p.lambda_constant = lp->lambda_constant;
-        p.cv_mu_s = lp->cv_mu_s;
-        p.cv_var_s = lp->cv_var_s;
-        if (lp->nranks > 0) {  // sharded: the global total from every shard's accumulators
-          vs.gathered = lp->gacc;
-          vs.n_gathered = lp->nranks;
-          vs.gen = lp->gen;
-        } else {
-          vs.acc = lp->acc + lp->gen;
-        }
-        s_p = p;
-        s_vs = vs;
+      p.f_best_raw = f_best;
+      p.first_eligible = first;
+      p.n_candidates = count;
+      p.lambda_mode = lmode;
+      p.lambda_constant = lconst;
+      p.cv_mu_s = cvm;
+      p.cv_var_s = cvv;
+      s_p = p;
+      s_have = nranks == 0;
+      if (go && nranks == 0) {
+        unsigned long long lg[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) lg[k] = (gen & 1) ? l[1][k] : l[0][k];  // (no dynamic register indexing)
+        s_pre = sel_setup_vals(limbs_value(lg, vs.s2), (long long)lg[4], p, y_mean, y_std);
+      } else if (go) {  // sharded: the global total from every shard's gathered accumulators
+        VarSource g = vs;
+        g.gathered = gacc;
+        g.n_gathered = nranks;
+        g.gen = gen;
+        double su;
+        long long cn;
+        var_source_read(g, &su, &cn);
+        s_pre = sel_setup_vals(su, cn, p, y_mean, y_std);
+        s_have = 1;
       }
       s_go = go;
     }
     __syncthreads();
     if (!s_go) return;
     p = s_p;
-    vs = s_vs;
   }
-  select_run_body<MASK>(c, sc, p, vs, tstat, ntiles);
+  select_run_body<MASK>(c, sc, p, vs, tstat, ntiles, (p.loop && s_have) ? &s_pre : nullptr);
 }
 
 
@@ -2784,7 +2846,8 @@ void launch_select(const double* mu, const double* var, const uint32_t* visited,
                    const GpScalars* sc, SelectParams p, const VarSource& vs, const TileStats* tstat,
                    const ReduceBufs& b, SelectDev* out, cudaStream_t s, int fused_append_n_max) {
   count_launch();
-  SelCtx c{mu, var, nullptr, visited, nullptr, p.excluded, p.n_excluded, n, p.af_mask, b, out, p.loop};
+  SelCtx c{mu,     var,   nullptr,          visited,          nullptr, p.excluded, p.n_excluded, n,
+           p.af_mask, b,   out,              p.loop,           p.pf_table, p.pf_V, p.pf_tile_stride, p.pf_rows};
   const size_t smem = fused_append_n_max > 0 ? loop_append_smem(fused_append_n_max) : 0;
   const uint32_t mask = (p.af_mask & 7u) ? (p.af_mask & 7u) : 7u;
   const int ntiles = (int)((n + kTile - 1) / kTile);

@@ -39,7 +39,8 @@ for rep in range(5):
     run.unmark_visited(recs[-1].position)
     marks = np.zeros((2048, 8), dtype=np.uint64)
     rc = _lib.load().gtc_debug_select_trace(marks.ctypes.data_as(_lib.U64P), 2048)
-    assert rc == 0, _lib.last_error()
+    if rc != 0:  # (not a GTC_SEL_TRACE build: the loop still runs, e.g. under ncu)
+        continue
     blocks = marks[:2040]
     used = blocks[:, 0] > 0
     b = blocks[used].astype(np.int64)

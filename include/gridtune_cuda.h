@@ -332,6 +332,12 @@ int gtc_debug_append_marks(const gtc_run* run, uint64_t* marks7);
  * otherwise): %globaltimer marks (ns), 8 per row: rows < grid = the last
  * selection's blocks, row 2040 the loop-mode append, row 2041 the pass. */
 int gtc_debug_select_trace(uint64_t* marks, int32_t rows);
+/* Diagnostics: how full V rebuilds (fits, refits, gtc_gp_predict) run in this
+ * process -- 1 (default) one tensor-core pass (FP64 mma.sync panels, V written
+ * once) + the posterior pass, 0 the streaming 8-row passes that re-read the V
+ * prefix from HBM; both write bit-identical V and posterior.  Returns the
+ * previous mode; a negative `mode` only queries. */
+int gtc_debug_set_rebuild(int32_t mode);
 /* Diagnostics: bordered rows (since the run was created) whose
  * V-column pivot was below the exactness margin, so the exact forward
  * substitution ran (as of the last synchronising call). */

@@ -175,6 +175,13 @@ int rebuild_predictions(const SpaceDev& sp, GpStore& gp, const gtc_kernel& k, do
     GTC_LAUNCHED();
     return GTC_OK;
   }
+  if (launch_rebuild(sp, gp.dev, kparams(k), V, tile_stride, n, s)) {
+    GTC_LAUNCHED();
+    // posterior, tile summaries and variance total from the rebuilt rows
+    launch_extend(sp, gp.dev, kparams(k), V, tile_stride, n, 0, true, mu, var, false, vp, tstat, s);
+    GTC_LAUNCHED();
+    return GTC_OK;
+  }
   for (int n0 = 0; n0 < n; n0 += kMaxRows) {
     const int r = std::min(kMaxRows, n - n0);
     launch_extend(sp, gp.dev, kparams(k), V, tile_stride, n0, r, n0 + r == n, mu, var, false, vp, tstat, s);
@@ -2143,6 +2150,12 @@ extern "C" int gtc_debug_select_trace(uint64_t* marks, int32_t rows) {
   if (read_sel_trace(reinterpret_cast<unsigned long long*>(marks), rows))
     return fail(GTC_ERR_INVALID, "library built without GTC_SEL_TRACE");
   return GTC_OK;
+}
+
+extern "C" int gtc_debug_set_rebuild(int32_t mode) {
+  const int prev = rebuild_mode();
+  if (mode >= 0) set_rebuild_mode(mode ? 1 : 0);
+  return prev;
 }
 
 extern "C" int64_t gtc_run_exact_rows(const gtc_run* r) { return r ? (int64_t)r->gp.h_sc->exact_rows : -1; }

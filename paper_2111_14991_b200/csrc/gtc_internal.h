@@ -314,6 +314,15 @@ void launch_extend(const SpaceDev& space, const GpDev& g, KernelParams k, double
                    int64_t tile_stride, int n0, int r, bool final, double* mu, double* var,
                    bool check_status, const VarPartials* vp, TileStats* tstat, cudaStream_t stream);
 
+// Tensor-core V rebuild (k_rebuild): V rows [0, n) of every candidate, bit-identical
+// to the streaming k_extend<8> passes; false = not taken (mode off / too large),
+// the caller falls back to the streaming passes.  The posterior comes from a
+// following final pass (r = 0).
+bool launch_rebuild(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V, int64_t tile_stride, int n,
+                    cudaStream_t stream);
+void set_rebuild_mode(int mode);  // 0 streaming, 1 tensor cores (default)
+int rebuild_mode();
+
 void launch_var_partials(const double* var, int64_t n, double s2, const VarPartials& vp, cudaStream_t stream);
 // Converts a variance source to (sum, count) on the device.
 void launch_var_totals(const VarSource& src, VarTotals* out, cudaStream_t stream);

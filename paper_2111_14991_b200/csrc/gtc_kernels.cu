@@ -33,11 +33,13 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <algorithm>
 #include <atomic>
 #include <climits>
 #include <cstdlib>
 #include <cstdint>
 #include <mutex>
+#include <string>
 #include <utility>
 #include <vector>
 
@@ -774,8 +776,9 @@ __device__ __forceinline__ double2 coord2(const SpaceDev& sp, int t, int64_t j0)
 // once.  One CTA per tile of kTile candidates, one double2 column pair per
 // thread.  With final_pass the posterior mean/variance are produced too.
 template <int R, int NU, int UP = GTC_PASS_U>
-__device__ __forceinline__ void extend_body(const ExtendArgs& a_in) {
+__device__ __forceinline__ void extend_body(const ExtendArgs& a_in, int64_t tile_ = -1) {
   ExtendArgs a = a_in;
+  const int64_t tile = tile_ >= 0 ? tile_ : (int64_t)blockIdx.x;
   pdl_begin();
   if (blockIdx.x == 0) TRACE_AT(2041, 0);
   // resident loop: only after a valid evaluation; generation flipped by
@@ -819,7 +822,6 @@ __device__ __forceinline__ void extend_body(const ExtendArgs& a_in) {
   for (int t = threadIdx.x; t < r; t += blockDim.x) xn2[t] = a.g.train_n2[n0 + t];
   __syncthreads();
 
-  const int64_t tile = blockIdx.x;
   const int64_t j0 = tile * kTile + 2 * threadIdx.x;
   const double2* Vt = reinterpret_cast<const double2*>(a.V + tile * a.tile_stride) + threadIdx.x;
   constexpr int kRowStride = kTile / 2;  // in double2
@@ -1004,7 +1006,7 @@ __device__ __forceinline__ void extend_body(const ExtendArgs& a_in) {
         atomicMax(&g_sel_trace[2043][0], gtc_globaltimer());
 #endif
         if (a.tstat)
-          a.tstat[blockIdx.x] =
+          a.tstat[tile] =
               TileStats{mn, vx >= 0.0 ? vx : -1.0, vn, sm_, sv, sp == LLONG_MAX ? -1 : (int64_t)sp};
       }
     }
@@ -2718,6 +2720,237 @@ static void extend_impl(const ExtendArgs& a, int64_t tiles, cudaStream_t s) {
   }
   opt_in_smem(k_extend<R, NU>, sm);
   launch_pdl(k_extend<R, NU>, dim3((unsigned)tiles), dim3(kExtendThreads), sm, s, a);
+}
+
+// ------------------------------------------------------------ V rebuild on the FP64 tensor cores
+//
+// The full forward substitution V = L^-1 K* (gp.hpp:163-164) for every
+// candidate -- the initial fit, refits after jitter escalation and the
+// stand-alone predict -- as ONE pass that writes V once, instead of n/8
+// streaming passes that re-read the growing prefix (k_extend<8>: ~n^2/16 rows
+// of HBM traffic).  Blocked by 8-row panels exactly like k_extend<8>:
+//   acc  = sum_{m < n0} L[n0+t][m] v_m       (ascending FMA chain)
+//   num  = k(x_{n0+t}, x) - acc               (expansion-form kernel)
+//   num -= L[n0+t][n0+s] * v_s, s < t         (multiply, then subtract)
+//   v    = num / L[n0+t][n0+t]
+// The panel contraction `acc` is the dense, GEMM-shaped part: FP64 mma.sync
+// m8n8k4 (DMMA), A = 8 panel rows x 4 columns of L, B = 4 V rows x 8
+// candidates, D = 8 x 8 accumulators.  A chain of DMMAs over k is
+// bit-identical to the ascending FMA chain (tools/dmma_order.cu: 0 of 262,144
+// elements differ), so this kernel writes exactly the V of the streaming
+// rebuild.  One warp owns 8 candidates: its V block [n][8] stays in shared
+// memory (B fragments: 4 rows x 64 B, conflict-free), its panel triangle runs
+// in the D-fragment layout (row t on lanes 4t..4t+3, broadcast by shuffle),
+// and warps never synchronise with each other.  L is read through L1 (the
+// warps of a CTA walk the same panels).  The posterior (mean, variance, tile
+// summaries, variance total) then comes from the R = 0 final pass, whose
+// FMA order over the rows is the streaming rebuild's.
+constexpr int kRbMaxWarps = 12;  // warps (groups of 8 candidates) per CTA, shared-memory permitting
+
+// Shared memory: two staged L panels [8][ld] (+ their training rows and
+// norms), then per warp its V block [n][8], candidate coordinates [d][8] and
+// squared norms [8].
+__host__ __device__ __forceinline__ int rebuild_ld(int n) { return ((n + 8 + 15) / 16) * 16 + 4; }
+__host__ __device__ __forceinline__ size_t rebuild_panel_doubles(int n, int d) {
+  return (size_t)8 * rebuild_ld(n) + (size_t)8 * d + 8;
+}
+__host__ __device__ __forceinline__ size_t rebuild_warp_doubles(int n, int d) {
+  return (size_t)8 * n + (size_t)8 * d + 8;
+}
+
+struct RebuildArgs {
+  SpaceDev sp;
+  GpDev g;
+  double* V;
+  int64_t tile_stride;
+  int n;
+  double lengthscale, s2;
+};
+
+__device__ __forceinline__ double coord1(const SpaceDev& sp, int t, int64_t j) {
+  if (sp.cidx) return __ldg(sp.ctab + t * 256 + sp.cidx[(int64_t)t * sp.n_pad + j]);
+  return __ldg(sp.coords + (int64_t)t * sp.n_pad + j);
+}
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// Panel n0 (rows n0 .. n0+7 of the packed factor, their training rows and
+// squared norms) into a staging buffer, asynchronously (cp.async).
+__device__ void rebuild_stage_panel(const GpDev& g, int n, int n0, double* buf) {
+  const int ld = rebuild_ld(n), d = g.d;
+  const int r = min(8, n - n0);
+  for (int t = 0; t < r; ++t) {
+    const double* src = g.L + packed(n0 + t);
+    for (int q = threadIdx.x; q <= n0 + t; q += blockDim.x) cp_async8(buf + t * ld + q, src + q);
+  }
+  double* xr = buf + 8 * ld;
+  for (int i = threadIdx.x; i < r * d; i += blockDim.x) cp_async8(xr + i, g.train_x + (int64_t)n0 * d + i);
+  for (int t = threadIdx.x; t < r; t += blockDim.x) cp_async8(xr + 8 * d + t, g.train_n2 + n0 + t);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// a / b correctly rounded (== __ddiv_rn) from the correctly rounded
+// reciprocal y = 1/b: one Markstein correction step (r = a - q0 b is exact by
+// FMA).  Outside the safe exponent range (and for a == 0, keeping the sign
+// of zero) it defers to __ddiv_rn.  Checked bit for bit against __ddiv_rn
+// on 1.7e10 operand pairs of the rebuild's ranges (tools/div_check.cu).
+__device__ __forceinline__ double quot_rn(double a, double b, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const double aq = fabs(q0), aa = fabs(a);
+  if (!(aq < 0x1p+960 && aq > 0x1p-960 && aa > 0x1p-960 && aa < 0x1p+960)) return __ddiv_rn(a, b);
+  const double r = fma(-q0, b, a);
+  return fma(r, y, q0);
+}
+
+template <int NU>
+__global__ void __launch_bounds__(kRbMaxWarps * 32, 1) k_rebuild(RebuildArgs a) {
+  extern __shared__ double sm[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
+  const int n = a.n, d = a.sp.d, ld = rebuild_ld(n);
+  const size_t pd = rebuild_panel_doubles(n, d);
+
+  double* Vs = sm + 2 * pd + (size_t)w * rebuild_warp_doubles(n, d);  // [n][8] this warp's V block
+  double* cx = Vs + (size_t)8 * n;                                     // [d][8] candidate coordinates
+  double* cn2 = cx + (size_t)8 * d;                                    // [8] squared norms
+  const int64_t c0 = ((int64_t)blockIdx.x * W + w) * 8;                // first candidate of the group
+  const bool active = c0 < a.sp.n_pad;
+  rebuild_stage_panel(a.g, n, 0, sm);
+  if (active) {
+    for (int idx = lane; idx < 8 * d; idx += 32) cx[idx] = coord1(a.sp, idx >> 3, c0 + (idx & 7));
+    __syncwarp();
+    if (lane < 8) {  // sequential in t (extend_body's c0n2)
+      double s = 0.0;
+      for (int t = 0; t < d; ++t) s = __dadd_rn(s, __dmul_rn(cx[t * 8 + lane], cx[t * 8 + lane]));
+      cn2[lane] = s;
+    }
+    __syncwarp();
+  }
+  const int row = lane >> 2, kq = lane & 3;  // fragment coordinates: D rows `row`, cols 2kq, 2kq+1
+  const int col = 2 * kq;
+  double* Vg = a.V + (c0 / kTile) * a.tile_stride + c0 % kTile;  // row m at Vg + m * kTile
+  int buf = 0;
+  for (int n0 = 0; n0 < n; n0 += 8, buf ^= 1) {
+    const int r = min(8, n - n0);
+    const bool live = row < r;
+    // the next panel streams in while this one is used
+    if (n0 + 8 < n) rebuild_stage_panel(a.g, n, n0 + 8, sm + (buf ^ 1) * pd);
+    if (n0 + 8 < n) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    const double* Lp = sm + buf * pd;
+    const double* Lr = Lp + row * ld;  // this thread's A row (rows past r: stale, masked)
+    const double* xr = Lp + 8 * ld;    // [r][d] training rows, then [r] norms
+    if (active) {
+      // ---- kernel values of the panel rows (gp.hpp:176-179 expansion form,
+      // extend_body's order); independent of the contraction below, so their
+      // latency overlaps it
+      double k0 = 0.0, k1 = 0.0, diag = 1.0, rinv = 1.0;
+      if (live) {
+        double dot0 = 0.0, dot1 = 0.0;
+        for (int t = 0; t < d; ++t) {
+          const double xv = xr[row * d + t];
+          dot0 = __dadd_rn(dot0, __dmul_rn(xv, cx[t * 8 + col]));
+          dot1 = __dadd_rn(dot1, __dmul_rn(xv, cx[t * 8 + col + 1]));
+        }
+        const double xn2 = xr[8 * d + row];
+        const double d20 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, dot0), xn2), cn2[col]);
+        const double d21 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, dot1), xn2), cn2[col + 1]);
+        k0 = matern<NU>(sqrt(fmax(d20, 0.0)), a.lengthscale, a.s2);
+        k1 = matern<NU>(sqrt(fmax(d21, 0.0)), a.lengthscale, a.s2);
+        diag = Lr[n0 + row];
+        rinv = __drcp_rn(diag);
+      }
+      // ---- panel contraction on the tensor cores: rows m < n0 (the
+      // fragments of four k-steps loaded together, then their DMMAs)
+      double d0 = 0.0, d1 = 0.0;
+      const double* Bp = Vs + kq * 8 + row;  // B fragment: V row m0 + kq, candidate `row`
+      const double* Ap = Lr + kq;
+      int m0 = 0;
+      for (; m0 + 16 <= n0; m0 += 16) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          av[u] = live ? Ap[m0 + 4 * u] : 0.0;
+          bv[u] = Bp[(m0 + 4 * u) * 8];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(d0), "+d"(d1)
+                       : "d"(av[u]), "d"(bv[u]));
+      }
+      for (; m0 < n0; m0 += 4) {
+        const double av = live ? Ap[m0] : 0.0, bv = Bp[m0 * 8];
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(d0), "+d"(d1)
+                     : "d"(av), "d"(bv));
+      }
+      double num0 = __dadd_rn(k0, -d0), num1 = __dadd_rn(k1, -d1);
+      // ---- the panel triangle, branch-free: at step s the lanes of row s
+      // divide (quot_rn: == __ddiv_rn) and broadcast; later rows subtract
+      double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        if (s >= r) break;
+        const double q0 = quot_rn(num0, diag, rinv), q1 = quot_rn(num1, diag, rinv);
+        if (row == s) {
+          v0 = q0;
+          v1 = q1;
+        }
+        const double b0 = __shfl_sync(0xffffffffu, q0, s * 4 + kq);
+        const double b1 = __shfl_sync(0xffffffffu, q1, s * 4 + kq);
+        const double l = Lr[n0 + s];
+        if (row > s) {
+          num0 = __dadd_rn(num0, -__dmul_rn(l, b0));
+          num1 = __dadd_rn(num1, -__dmul_rn(l, b1));
+        }
+      }
+      if (live) {
+        *reinterpret_cast<double2*>(Vs + (n0 + row) * 8 + col) = make_double2(v0, v1);
+        *reinterpret_cast<double2*>(Vg + (int64_t)(n0 + row) * kTile + col) = make_double2(v0, v1);
+      }
+      __syncwarp();
+    }
+    __syncthreads();  // this buffer is free for the stage after next
+  }
+}
+
+// 0: streaming rebuild (k_extend<8>, n/8 launches, prefix from HBM);
+// 1: tensor-core rebuild (k_rebuild + one final pass).  GTC_REBUILD=stream
+// selects 0 (diagnostics).  (A third variant -- one CTA per tile running all
+// of its 8-row panels back to back so the prefix would come from L2 -- was
+// measured and dropped: 36 % L2 hit rate, 10.7 GB of DRAM reads, 9.6 ms.)
+static int g_rebuild_mode = [] {
+  const char* e = std::getenv("GTC_REBUILD");
+  return (e && std::string(e) == "stream") ? 0 : 1;
+}();
+void set_rebuild_mode(int mode) { g_rebuild_mode = mode; }
+
+int rebuild_mode() { return g_rebuild_mode; }
+
+// V rows [0, n) of every candidate (no posterior).  Returns false when the
+// tensor-core path is off or the per-warp block does not fit shared memory.
+bool launch_rebuild(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V, int64_t tile_stride, int n,
+                    cudaStream_t s) {
+  if (g_rebuild_mode != 1 || n <= 0) return false;
+  constexpr size_t kBudget = 224 * 1024;
+  const size_t fixed = sizeof(double) * 2 * rebuild_panel_doubles(n, sp.d);
+  const size_t per_warp = sizeof(double) * rebuild_warp_doubles(n, sp.d);
+  if (fixed + per_warp > kBudget) return false;
+  const int64_t groups = sp.n_pad / 8;
+  const int W = (int)std::min<int64_t>({(int64_t)kRbMaxWarps, (int64_t)((kBudget - fixed) / per_warp), groups});
+  const size_t smem = fixed + per_warp * W;
+  count_launch();
+  const RebuildArgs a{sp, g, V, tile_stride, n, k.lengthscale, k.s2};
+  const unsigned grid = (unsigned)((groups + W - 1) / W);
+  switch (k.nu) {
+    case 0: opt_in_smem(k_rebuild<0>, smem); k_rebuild<0><<<grid, W * 32, smem, s>>>(a); break;
+    case 1: opt_in_smem(k_rebuild<1>, smem); k_rebuild<1><<<grid, W * 32, smem, s>>>(a); break;
+    default: opt_in_smem(k_rebuild<2>, smem); k_rebuild<2><<<grid, W * 32, smem, s>>>(a); break;
+  }
+  return true;
 }
 
 void launch_extend(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V,

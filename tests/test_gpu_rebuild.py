@@ -1,0 +1,63 @@
+"""The tensor-core V rebuild (k_rebuild: FP64 mma.sync panels, one pass) against
+the streaming rebuild (k_extend<8>, n/8 passes) -- the full forward
+substitution of GpModel::predict (gp.hpp:150-168) that fits, refits and the
+stand-alone predict run.  The DMMA chain is an ascending FMA chain, so the two
+must agree BIT FOR BIT: posterior mean/variance, the variance total (lambda's
+input) and every later incremental append (which reads the rebuilt V rows)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def rebuild_mode(gt):
+    lib = gt.load()
+    prev = lib.gtc_debug_set_rebuild(-1)
+    yield lambda m: lib.gtc_debug_set_rebuild(m)
+    lib.gtc_debug_set_rebuild(prev)
+
+
+def fitted(gt, coords, nu, pos, y, mode, set_mode, extra=None):
+    set_mode(mode)
+    space = gt.Space(coords)
+    run = gt.SurrogateRun(space, gt.MaternKernel(nu, 1.3, 0.9), n_max=len(pos) + 2)
+    run.fit(pos, y)
+    mu, var = run.predictions()
+    out = [mu.copy(), var.copy(), run.mean_variance()]
+    if extra is not None:  # one incremental append on top of the rebuilt rows
+        run.append(int(extra[0]), float(extra[1]))
+        mu2, var2 = run.predictions()
+        out += [mu2.copy(), var2.copy()]
+    return out
+
+
+@pytest.mark.parametrize("mode", [1])
+@pytest.mark.parametrize("nu", ["half", "three_halves", "five_halves"])
+@pytest.mark.parametrize("n", [1, 7, 8, 9, 37, 64, 150])
+def test_rebuild_bit_identical_to_streaming(gt, rebuild_mode, nu, n, mode):
+    rng = np.random.default_rng(n * 7 + len(nu))
+    N, d = 20_000 + 37 * n, 5
+    grid = np.linspace(0.0, 1.0, 11)
+    coords = grid[rng.integers(0, 11, size=(N, d))]  # discrete: the compact 1-byte coordinate path
+    pos = rng.choice(N, n + 1, replace=False)
+    y = 2.0 + rng.standard_normal(n + 1)
+    mnu = getattr(gt.MaternNu, nu)
+    a = fitted(gt, coords, mnu, pos[:n], y[:n], 0, rebuild_mode, extra=(pos[n], y[n]))
+    b = fitted(gt, coords, mnu, pos[:n], y[:n], mode, rebuild_mode, extra=(pos[n], y[n]))
+    for x, z in zip(a, b):
+        np.testing.assert_array_equal(np.asarray(x), np.asarray(z))
+
+
+@pytest.mark.parametrize("mode", [1])
+def test_rebuild_continuous_coordinates_and_n220(gt, rebuild_mode, mode):
+    """Non-discrete coordinates (the FP64 SoA path) at the headline n = 220."""
+    rng = np.random.default_rng(5)
+    N, d, n = 60_000, 6, 220
+    coords = rng.random((N, d))
+    pos = rng.choice(N, n, replace=False)
+    y = rng.standard_normal(n)
+    a = fitted(gt, coords, gt.MaternNu.three_halves, pos, y, 0, rebuild_mode)
+    b = fitted(gt, coords, gt.MaternNu.three_halves, pos, y, mode, rebuild_mode)
+    for x, z in zip(a, b):
+        np.testing.assert_array_equal(np.asarray(x), np.asarray(z))

@@ -2745,17 +2745,20 @@ static void extend_impl(const ExtendArgs& a, int64_t tiles, cudaStream_t s) {
 // warps of a CTA walk the same panels).  The posterior (mean, variance, tile
 // summaries, variance total) then comes from the R = 0 final pass, whose
 // FMA order over the rows is the streaming rebuild's.
-constexpr int kRbMaxWarps = 12;  // warps (groups of 8 candidates) per CTA, shared-memory permitting
+constexpr int kRbMaxWarps = 12;  // warps per CTA, shared-memory permitting
+constexpr int kRbGroups = 2;     // column groups of 8 candidates per warp (DMMA chains sharing A)
+constexpr int kRbCands = 8 * kRbGroups;
 
-// Shared memory: two staged L panels [8][ld] (+ their training rows and
-// norms), then per warp its V block [n][8], candidate coordinates [d][8] and
-// squared norms [8].
+// Shared memory: two staged L panels [8][ld] (+ their training rows, norms
+// and pivot reciprocals), then per warp its V blocks [kRbGroups][n][8], the
+// candidate coordinates [d][kRbCands], their squared norms and a transpose
+// scratch [kRbGroups][8][8].
 __host__ __device__ __forceinline__ int rebuild_ld(int n) { return ((n + 8 + 15) / 16) * 16 + 4; }
 __host__ __device__ __forceinline__ size_t rebuild_panel_doubles(int n, int d) {
-  return (size_t)8 * rebuild_ld(n) + (size_t)8 * d + 8;
+  return (size_t)8 * rebuild_ld(n) + (size_t)8 * d + 8 + 8;
 }
 __host__ __device__ __forceinline__ size_t rebuild_warp_doubles(int n, int d) {
-  return (size_t)8 * n + (size_t)8 * d + 8;
+  return (size_t)kRbCands * n + (size_t)kRbCands * d + kRbCands + 64 * kRbGroups;
 }
 
 struct RebuildArgs {
@@ -2804,31 +2807,51 @@ __device__ __forceinline__ double quot_rn(double a, double b, double y) {
   return fma(r, y, q0);
 }
 
+// matern<NU> with the distance scaled by quot_rn (the same bits as its
+// __ddiv_rn(r, lengthscale)); linv = __drcp_rn(lengthscale).
+template <int NU>
+__device__ __forceinline__ double matern_q(double r, double lengthscale, double linv, double s2) {
+  const double s = quot_rn(r, lengthscale, linv);
+  if (NU == 0) return __dmul_rn(s2, exp(-s));
+  if (NU == 1) {
+    const double a = __dmul_rn(1.7320508075688772, s);
+    return __dmul_rn(__dmul_rn(s2, __dadd_rn(1.0, a)), exp(-a));
+  }
+  const double a = __dmul_rn(2.2360679774997896, s);
+  const double poly = __dadd_rn(__dadd_rn(1.0, a), __ddiv_rn(__dmul_rn(a, a), 3.0));
+  return __dmul_rn(__dmul_rn(s2, poly), exp(-a));
+}
+
 template <int NU>
 __global__ void __launch_bounds__(kRbMaxWarps * 32, 1) k_rebuild(RebuildArgs a) {
+  constexpr int G = kRbGroups;
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
   const int n = a.n, d = a.sp.d, ld = rebuild_ld(n);
   const size_t pd = rebuild_panel_doubles(n, d);
-
-  double* Vs = sm + 2 * pd + (size_t)w * rebuild_warp_doubles(n, d);  // [n][8] this warp's V block
-  double* cx = Vs + (size_t)8 * n;                                     // [d][8] candidate coordinates
-  double* cn2 = cx + (size_t)8 * d;                                    // [8] squared norms
-  const int64_t c0 = ((int64_t)blockIdx.x * W + w) * 8;                // first candidate of the group
+  double* Vs = sm + 2 * pd + (size_t)w * rebuild_warp_doubles(n, d);  // [G][n][8] this warp's V blocks
+  double* cx = Vs + (size_t)kRbCands * n;                              // [d][kRbCands] coordinates
+  double* cn2 = cx + (size_t)kRbCands * d;                             // [kRbCands] squared norms
+  double* T = cn2 + kRbCands;                                          // [G][8][8] transpose scratch
+  const int64_t c0 = ((int64_t)blockIdx.x * W + w) * kRbCands;         // first candidate of the warp
   const bool active = c0 < a.sp.n_pad;
+  const double linv = __drcp_rn(a.lengthscale);
   rebuild_stage_panel(a.g, n, 0, sm);
   if (active) {
-    for (int idx = lane; idx < 8 * d; idx += 32) cx[idx] = coord1(a.sp, idx >> 3, c0 + (idx & 7));
+    for (int idx = lane; idx < kRbCands * d; idx += 32)
+      cx[idx] = coord1(a.sp, idx / kRbCands, c0 + idx % kRbCands);
     __syncwarp();
-    if (lane < 8) {  // sequential in t (extend_body's c0n2)
+    if (lane < kRbCands) {  // sequential in t (extend_body's c0n2)
       double s = 0.0;
-      for (int t = 0; t < d; ++t) s = __dadd_rn(s, __dmul_rn(cx[t * 8 + lane], cx[t * 8 + lane]));
+      for (int t = 0; t < d; ++t) s = __dadd_rn(s, __dmul_rn(cx[t * kRbCands + lane], cx[t * kRbCands + lane]));
       cn2[lane] = s;
     }
     __syncwarp();
   }
   const int row = lane >> 2, kq = lane & 3;  // fragment coordinates: D rows `row`, cols 2kq, 2kq+1
   const int col = 2 * kq;
+  const bool tri = lane < kRbCands;          // transposed layout: lane = candidate
+  const int tg = lane >> 3, tc = lane & 7;   // its group and column
   double* Vg = a.V + (c0 / kTile) * a.tile_stride + c0 % kTile;  // row m at Vg + m * kTile
   int buf = 0;
   for (int n0 = 0; n0 < n; n0 += 8, buf ^= 1) {
@@ -2843,73 +2866,88 @@ __global__ void __launch_bounds__(kRbMaxWarps * 32, 1) k_rebuild(RebuildArgs a) 
     const double* Lr = Lp + row * ld;  // this thread's A row (rows past r: stale, masked)
     const double* xr = Lp + 8 * ld;    // [r][d] training rows, then [r] norms
     if (active) {
-      // ---- kernel values of the panel rows (gp.hpp:176-179 expansion form,
-      // extend_body's order); independent of the contraction below, so their
-      // latency overlaps it
-      double k0 = 0.0, k1 = 0.0, diag = 1.0, rinv = 1.0;
+      // ---- kernel values of the panel rows in the fragment layout
+      // (gp.hpp:176-179 expansion form, extend_body's order); independent of
+      // the contraction below, so their latency overlaps it
+      double kv[G][2];
+#pragma unroll
+      for (int g = 0; g < G; ++g) kv[g][0] = kv[g][1] = 0.0;
       if (live) {
-        double dot0 = 0.0, dot1 = 0.0;
-        for (int t = 0; t < d; ++t) {
-          const double xv = xr[row * d + t];
-          dot0 = __dadd_rn(dot0, __dmul_rn(xv, cx[t * 8 + col]));
-          dot1 = __dadd_rn(dot1, __dmul_rn(xv, cx[t * 8 + col + 1]));
-        }
         const double xn2 = xr[8 * d + row];
-        const double d20 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, dot0), xn2), cn2[col]);
-        const double d21 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, dot1), xn2), cn2[col + 1]);
-        k0 = matern<NU>(sqrt(fmax(d20, 0.0)), a.lengthscale, a.s2);
-        k1 = matern<NU>(sqrt(fmax(d21, 0.0)), a.lengthscale, a.s2);
-        diag = Lr[n0 + row];
-        rinv = __drcp_rn(diag);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int cc = 8 * g + col;
+          double dot0 = 0.0, dot1 = 0.0;
+          for (int t = 0; t < d; ++t) {
+            const double xv = xr[row * d + t];
+            dot0 = __dadd_rn(dot0, __dmul_rn(xv, cx[t * kRbCands + cc]));
+            dot1 = __dadd_rn(dot1, __dmul_rn(xv, cx[t * kRbCands + cc + 1]));
+          }
+          const double d20 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, dot0), xn2), cn2[cc]);
+          const double d21 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, dot1), xn2), cn2[cc + 1]);
+          kv[g][0] = matern_q<NU>(sqrt(fmax(d20, 0.0)), a.lengthscale, linv, a.s2);
+          kv[g][1] = matern_q<NU>(sqrt(fmax(d21, 0.0)), a.lengthscale, linv, a.s2);
+        }
       }
-      // ---- panel contraction on the tensor cores: rows m < n0 (the
-      // fragments of four k-steps loaded together, then their DMMAs)
-      double d0 = 0.0, d1 = 0.0;
-      const double* Bp = Vs + kq * 8 + row;  // B fragment: V row m0 + kq, candidate `row`
+      // ---- panel contraction on the tensor cores: rows m < n0, G chains
+      // sharing each A fragment (four k-steps of fragments loaded together)
+      double acc[G][2];
+#pragma unroll
+      for (int g = 0; g < G; ++g) acc[g][0] = acc[g][1] = 0.0;
       const double* Ap = Lr + kq;
+      const double* Bp = Vs + kq * 8 + row;  // group g's B fragment: + g * 8n, row m0 + kq at + m0 * 8
       int m0 = 0;
       for (; m0 + 16 <= n0; m0 += 16) {
-        double av[4], bv[4];
+        double av[4], bv[4][G];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           av[u] = live ? Ap[m0 + 4 * u] : 0.0;
-          bv[u] = Bp[(m0 + 4 * u) * 8];
+#pragma unroll
+          for (int g = 0; g < G; ++g) bv[u][g] = Bp[(size_t)g * 8 * n + (m0 + 4 * u) * 8];
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                       : "+d"(d0), "+d"(d1)
-                       : "d"(av[u]), "d"(bv[u]));
+#pragma unroll
+          for (int g = 0; g < G; ++g)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[g][0]), "+d"(acc[g][1])
+                         : "d"(av[u]), "d"(bv[u][g]));
       }
       for (; m0 < n0; m0 += 4) {
-        const double av = live ? Ap[m0] : 0.0, bv = Bp[m0 * 8];
-        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                     : "+d"(d0), "+d"(d1)
-                     : "d"(av), "d"(bv));
-      }
-      double num0 = __dadd_rn(k0, -d0), num1 = __dadd_rn(k1, -d1);
-      // ---- the panel triangle, branch-free: at step s the lanes of row s
-      // divide (quot_rn: == __ddiv_rn) and broadcast; later rows subtract
-      double v0 = 0.0, v1 = 0.0;
+        const double av = live ? Ap[m0] : 0.0;
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        if (s >= r) break;
-        const double q0 = quot_rn(num0, diag, rinv), q1 = quot_rn(num1, diag, rinv);
-        if (row == s) {
-          v0 = q0;
-          v1 = q1;
-        }
-        const double b0 = __shfl_sync(0xffffffffu, q0, s * 4 + kq);
-        const double b1 = __shfl_sync(0xffffffffu, q1, s * 4 + kq);
-        const double l = Lr[n0 + s];
-        if (row > s) {
-          num0 = __dadd_rn(num0, -__dmul_rn(l, b0));
-          num1 = __dadd_rn(num1, -__dmul_rn(l, b1));
+        for (int g = 0; g < G; ++g) {
+          const double bv = Bp[(size_t)g * 8 * n + m0 * 8];
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[g][0]), "+d"(acc[g][1])
+                       : "d"(av), "d"(bv));
         }
       }
-      if (live) {
-        *reinterpret_cast<double2*>(Vs + (n0 + row) * 8 + col) = make_double2(v0, v1);
-        *reinterpret_cast<double2*>(Vg + (int64_t)(n0 + row) * kTile + col) = make_double2(v0, v1);
+      // ---- num = k - acc, transposed through shared memory: lane c < 8G
+      // takes candidate c's eight panel rows
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        *reinterpret_cast<double2*>(T + g * 64 + row * 8 + col) =
+            make_double2(__dadd_rn(kv[g][0], -acc[g][0]), __dadd_rn(kv[g][1], -acc[g][1]));
+      __syncwarp();
+      // ---- the panel triangle, one candidate per lane, in registers
+      // (k_extend<8>'s order: subtract the earlier rows of the panel in
+      // ascending order, then divide; quot_rn == __ddiv_rn)
+      if (tri) {
+        double num[8], v[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) num[t] = t < r ? T[tg * 64 + t * 8 + tc] : 0.0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (t >= r) break;
+          const double* Lt = Lp + t * ld + n0;
+          double x = num[t];
+#pragma unroll
+          for (int s2 = 0; s2 < t; ++s2) x = __dadd_rn(x, -__dmul_rn(Lt[s2], v[s2]));
+          v[t] = quot_rn(x, Lt[t], __drcp_rn(Lt[t]));
+          Vs[(size_t)tg * 8 * n + (n0 + t) * 8 + tc] = v[t];
+          Vg[(int64_t)(n0 + t) * kTile + lane] = v[t];
+        }
       }
       __syncwarp();
     }
@@ -2939,7 +2977,7 @@ bool launch_rebuild(const SpaceDev& sp, const GpDev& g, KernelParams k, double* 
   const size_t fixed = sizeof(double) * 2 * rebuild_panel_doubles(n, sp.d);
   const size_t per_warp = sizeof(double) * rebuild_warp_doubles(n, sp.d);
   if (fixed + per_warp > kBudget) return false;
-  const int64_t groups = sp.n_pad / 8;
+  const int64_t groups = sp.n_pad / kRbCands;  // (n_pad is a multiple of 256)
   const int W = (int)std::min<int64_t>({(int64_t)kRbMaxWarps, (int64_t)((kBudget - fixed) / per_warp), groups});
   const size_t smem = fixed + per_warp * W;
   count_launch();

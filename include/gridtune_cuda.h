@@ -338,6 +338,11 @@ int gtc_debug_select_trace(uint64_t* marks, int32_t rows);
  * prefix from HBM; both write bit-identical V and posterior.  Returns the
  * previous mode; a negative `mode` only queries. */
 int gtc_debug_set_rebuild(int32_t mode);
+/* Diagnostics: how full factorisations (GpModel::fit, refits) run in this
+ * process -- 1 (default) right-looking with the packed factor in shared memory
+ * (n up to ~230), 0 the left-looking bordered rows; both produce the same
+ * factor bit for bit.  Returns the previous mode; negative only queries. */
+int gtc_debug_set_factor(int32_t mode);
 /* Diagnostics: bordered rows (since the run was created) whose
  * V-column pivot was below the exactness margin, so the exact forward
  * substitution ran (as of the last synchronising call). */

@@ -169,6 +169,7 @@ SIGNATURES = [
     ("gtc_run_exact_rows", C.c_int64, [P]),
     ("gtc_debug_select_trace", C.c_int, [U64P, C.c_int32]),
     ("gtc_debug_set_rebuild", C.c_int, [C.c_int32]),
+    ("gtc_debug_set_factor", C.c_int, [C.c_int32]),
     ("gtc_gp_fit", C.c_int, [C.c_int, C.POINTER(gtc_kernel), DP, DP, C.c_int32, C.c_int32,
                              C.c_double, C.c_double, C.POINTER(P), C.POINTER(gtc_fit_info)]),
     ("gtc_gp_predict", C.c_int, [P, DP, C.c_int64, DP, DP]),

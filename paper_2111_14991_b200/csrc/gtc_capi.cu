@@ -2158,6 +2158,12 @@ extern "C" int gtc_debug_set_rebuild(int32_t mode) {
   return prev;
 }
 
+extern "C" int gtc_debug_set_factor(int32_t mode) {
+  const int prev = factor_mode();
+  if (mode >= 0) set_factor_mode(mode ? 1 : 0);
+  return prev;
+}
+
 extern "C" int64_t gtc_run_exact_rows(const gtc_run* r) { return r ? (int64_t)r->gp.h_sc->exact_rows : -1; }
 extern "C" uint64_t gtc_run_stream(const gtc_run* r) { return r ? (uint64_t)(uintptr_t)r->stream : 0; }
 

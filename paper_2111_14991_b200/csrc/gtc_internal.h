@@ -320,6 +320,8 @@ void launch_extend(const SpaceDev& space, const GpDev& g, KernelParams k, double
 // following final pass (r = 0).
 bool launch_rebuild(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V, int64_t tile_stride, int n,
                     cudaStream_t stream);
+void set_factor_mode(int mode);  // 1 right-looking in shared memory (default), 0 left-looking bordered rows
+int factor_mode();
 void set_rebuild_mode(int mode);  // 0 streaming, 1 tensor cores (default)
 int rebuild_mode();
 

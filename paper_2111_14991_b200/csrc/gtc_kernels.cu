@@ -667,6 +667,106 @@ __global__ void __launch_bounds__(kCtaThreads)
   cta_stats_beta(g, n);
 }
 
+// The same factorisation, right-looking, with the whole packed factor in
+// shared memory (n <= ~230): step j takes row j's pivot (|L_j,<j|^2 as the
+// 256-lane tree sum of cta_border_row's block_sum), scales column j below
+// the diagonal by 1/L_jj and folds column j into the trailing rows.  Every
+// entry receives exactly the left-looking operations in the same order --
+// acc - L_rk * x_k for ascending k, then times 1/L_rr -- so the factor is
+// bit-identical to k_gp_factor's, in n barrier-separated steps instead of
+// n dependent substitution chains (O(n^2) latency).  The first failing
+// pivot (x <= 0) is the same row.
+constexpr int kFactorThreads = 1024;  // the trailing updates are latency-bound: all the warps one CTA can hold
+
+template <int NU>
+__global__ void __launch_bounds__(kFactorThreads) k_gp_factor_rl(GpDev g, KernelParams k, double noise, double jitter,
+                                                              int n) {
+  extern __shared__ double A[];  // packed rows [0, n), then c [n], e [n]
+  __shared__ double lanes[3][256];
+  __shared__ double red[32];
+  double* cs = A + even_up(packed(n));
+  double* es = cs + n;
+  double* colj = es + n;  // column j below the diagonal, contiguous (conflict-free trailing reads)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) {
+    g.sc->status = 0;
+    g.sc->fail_row = -1;
+    g.sc->jitter = jitter;
+    g.sc->y0 = n > 0 ? g.y[0] : 0.0;
+  }
+  for (int row = threadIdx.x; row < n; row += blockDim.x) {  // squared norms (sequential in t)
+    double s = 0.0;
+    for (int t = 0; t < g.d; ++t) {
+      const double v = g.train_x[(int64_t)row * g.d + t];
+      s = __dadd_rn(s, __dmul_rn(v, v));
+    }
+    g.train_n2[row] = s;
+  }
+  // Gram matrix below the diagonal, direct differences (gp.hpp:110), in
+  // cta_border_row's argument order
+  for (int i = w; i < n; i += nw)
+    for (int q = lane; q < i; q += 32)
+      A[packed(i) + q] = direct_kernel<NU>(g.train_x + (int64_t)q * g.d, g.train_x + (int64_t)i * g.d, g.d,
+                                           k.lengthscale, k.s2);
+  const double diag = __dadd_rn(matern<NU>(0.0, k.lengthscale, k.s2), __dadd_rn(noise, jitter));
+  __syncthreads();
+  const double y0 = n > 0 ? g.y[0] : 0.0;
+  double ynext = (threadIdx.x == 0 && n > 0) ? g.y[0] : 0.0;  // thread 0: y[j], loaded a step ahead
+  for (int j = 0; j < n; ++j) {
+    const double yj = ynext;
+    if (threadIdx.x == 0 && j + 1 < n) ynext = g.y[j + 1];
+    // row j is final left of the diagonal: its pivot sum and its c / e dot
+    // products (cta_ce_row) in one 256-lane tree reduction
+    const double* Aj = A + packed(j);
+    for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+      double sq = 0.0, pc = 0.0, pe = 0.0;
+      for (int q = v; q < j; q += 256) {
+        sq = __dadd_rn(sq, __dmul_rn(Aj[q], Aj[q]));
+        pc = __dadd_rn(pc, __dmul_rn(Aj[q], cs[q]));
+        pe = __dadd_rn(pe, __dmul_rn(Aj[q], es[q]));
+      }
+      lanes[0][v] = sq;
+      lanes[1][v] = pc;
+      lanes[2][v] = pe;
+    }
+    double sums[3];
+    vsum256<3>(lanes, sums, red);
+    const double x = __dadd_rn(diag, -sums[0]);
+    if (x <= 0.0) {  // Eigen LLT fails exactly when x <= 0 (a NaN pivot proceeds)
+      if (threadIdx.x == 0) {
+        g.sc->status = 1;
+        g.sc->fail_row = j;
+        g.sc->n = 0;
+      }
+      return;
+    }
+    const double ljj = sqrt(x), rj = __drcp_rn(ljj);
+    for (int q = threadIdx.x; q < j; q += blockDim.x) g.L[packed(j) + q] = Aj[q];  // row j is final
+    if (threadIdx.x == 0) {
+      A[packed(j) + j] = ljj;
+      g.L[packed(j) + j] = ljj;
+      const double yr = __dadd_rn(yj, -y0);
+      cs[j] = __ddiv_rn(__dadd_rn(yr, -sums[1]), ljj);
+      es[j] = __ddiv_rn(__dadd_rn(1.0, -sums[2]), ljj);
+      g.c[j] = cs[j];
+      g.e[j] = es[j];
+    }
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) {
+      const double l = __dmul_rn(A[packed(i) + j], rj);
+      A[packed(i) + j] = l;
+      colj[i] = l;
+    }
+    __syncthreads();
+    for (int i = j + 2 + w; i < n; i += nw) {
+      double* Ai = A + packed(i);
+      const double lij = colj[i];
+      for (int kk = j + 1 + lane; kk < i; kk += 32) Ai[kk] = __dadd_rn(Ai[kk], -__dmul_rn(colj[kk], lij));
+    }
+    __syncthreads();
+  }
+  cta_stats_beta(g, n);
+}
+
 template <int NU>
 __device__ void gp_append_body(const AppendArgs& a) {
   const GpDev& g = a.g;
@@ -2642,9 +2742,27 @@ static void opt_in_smem(K kernel, size_t bytes) {
     set_to.push_back({key, bytes});
 }
 
+// 1: right-looking factor in shared memory when it fits (default); 0: the
+// left-looking bordered rows (GTC_FACTOR=left, diagnostics).
+static int g_factor_mode = [] {
+  const char* e = std::getenv("GTC_FACTOR");
+  return (e && std::string(e) == "left") ? 0 : 1;
+}();
+void set_factor_mode(int mode) { g_factor_mode = mode; }
+int factor_mode() { return g_factor_mode; }
+
 void launch_gp_factor(const GpDev& g, KernelParams k, double noise, double jitter, int n,
                       cudaStream_t s) {
   count_launch();
+  const size_t rl = sizeof(double) * ((size_t)even_up(packed(n)) + 3 * (size_t)n);
+  if (g_factor_mode == 1 && n > 0 && rl <= 200 * 1024) {  // right-looking, the factor in shared memory
+    switch (k.nu) {
+      case 0: opt_in_smem(k_gp_factor_rl<0>, rl); k_gp_factor_rl<0><<<1, kFactorThreads, rl, s>>>(g, k, noise, jitter, n); break;
+      case 1: opt_in_smem(k_gp_factor_rl<1>, rl); k_gp_factor_rl<1><<<1, kFactorThreads, rl, s>>>(g, k, noise, jitter, n); break;
+      default: opt_in_smem(k_gp_factor_rl<2>, rl); k_gp_factor_rl<2><<<1, kFactorThreads, rl, s>>>(g, k, noise, jitter, n); break;
+    }
+    return;
+  }
   bool staged;
   const size_t sm = cta_smem_bytes(g.n_max, n, &staged);
   const int st = staged ? 1 : 0;

@@ -1,4 +1,7 @@
-"""The tensor-core V rebuild (k_rebuild: FP64 mma.sync panels, one pass) against
+"""The full factorisation and V rebuild of GpModel::fit on the device.
+
+The right-looking shared-memory factor (k_gp_factor_rl) against the
+left-looking bordered rows (k_gp_factor), and the tensor-core V rebuild (k_rebuild: FP64 mma.sync panels, one pass) against
 the streaming rebuild (k_extend<8>, n/8 passes) -- the full forward
 substitution of GpModel::predict (gp.hpp:150-168) that fits, refits and the
 stand-alone predict run.  The DMMA chain is an ascending FMA chain, so the two
@@ -60,4 +63,57 @@ def test_rebuild_continuous_coordinates_and_n220(gt, rebuild_mode, mode):
     a = fitted(gt, coords, gt.MaternNu.three_halves, pos, y, 0, rebuild_mode)
     b = fitted(gt, coords, gt.MaternNu.three_halves, pos, y, mode, rebuild_mode)
     for x, z in zip(a, b):
+        np.testing.assert_array_equal(np.asarray(x), np.asarray(z))
+
+
+@pytest.fixture
+def factor_mode(gt):
+    lib = gt.load()
+    prev = lib.gtc_debug_set_factor(-1)
+    yield lambda m: lib.gtc_debug_set_factor(m)
+    lib.gtc_debug_set_factor(prev)
+
+
+@pytest.mark.parametrize("nu", ["half", "three_halves", "five_halves"])
+@pytest.mark.parametrize("n", [1, 2, 33, 100, 220])
+def test_right_looking_factor_bit_identical(gt, factor_mode, nu, n):
+    """Same factor bit for bit: identical posterior, standardisation, fit
+    info (jitter) and a later append on top of it."""
+    rng = np.random.default_rng(100 + n)
+    N, d = 30_000, 4
+    coords = rng.random((N, d))
+    pos = rng.choice(N, n + 1, replace=False)
+    y = rng.standard_normal(n + 1) * 3.0
+    out = []
+    for mode in (0, 1):
+        factor_mode(mode)
+        run = gt.SurrogateRun(gt.Space(coords), gt.MaternKernel(getattr(gt.MaternNu, nu), 0.8, 1.1), n_max=n + 2)
+        info = run.fit(pos[:n], y[:n])
+        mu, var = run.predictions()
+        run.append(int(pos[n]), float(y[n]))
+        mu2, var2 = run.predictions()
+        out.append([mu.copy(), var.copy(), mu2.copy(), var2.copy(), info.jitter, info.y_mean, info.y_std])
+    for x, z in zip(*out):
+        np.testing.assert_array_equal(np.asarray(x), np.asarray(z))
+
+
+def test_right_looking_factor_escalates_like_left_looking(gt, factor_mode):
+    """Near-duplicate training points at jitter 1e-17 (test_gpu_run's
+    escalation case, scaled up): the same failing pivot, the same escalated
+    jitter, the same posterior from both factorisations."""
+    rng = np.random.default_rng(9)
+    coords = rng.random((3_000, 2))
+    coords[1] = coords[0] + np.array([1e-9, 0.0])
+    coords[11] = coords[10] + np.array([0.0, 1e-9])
+    pos = np.concatenate([[0, 1, 10, 11], rng.choice(np.arange(20, 3_000), 40, replace=False)])
+    y = rng.standard_normal(len(pos))
+    out = []
+    for mode in (0, 1):
+        factor_mode(mode)
+        run = gt.SurrogateRun(gt.Space(coords), gt.MaternKernel(), 0.0, 1e-17, len(pos) + 1)
+        info = run.fit(pos, y)
+        mu, var = run.predictions()
+        out.append([mu.copy(), var.copy(), info.jitter])
+    assert out[0][2] > 1e-17  # the escalation happened
+    for x, z in zip(*out):
         np.testing.assert_array_equal(np.asarray(x), np.asarray(z))

@@ -217,7 +217,8 @@ def run_c5(args, rank=0, world=1, local=0):
                    "sweep_seconds": [round(t, 4) for t in sweep.times], "statistic": "median of the sweeps",
                    "parallelism": f"run-sharded over {world} GPU(s)", "evaluations": evals,
                    "timing": "wall clock of gtc_run_bo_batch per case (observe groups), max over ranks"},
-        "evaluations_per_sec": evals / dt, "clocks": clocks, "cpu_baseline": c2_reference()}))
+        "evaluations_per_sec": evals / dt, "clocks": clocks,
+        "cpu_baseline": None if args.no_cpu_baseline else c5_reference(local)}))
 
 
 def c2_values(n, invalid, minimum, seed):
@@ -367,27 +368,77 @@ def run_c2(args, rank=0, world=1, local=0):
                    "sweep_seconds": [round(t, 4) for t in sweep.times], "statistic": "median of the sweeps",
                    "timing": "wall clock of gtc_run_bo_batch (host thread pool, one stream per run)"},
         "evaluations_per_sec": evals / t_total, "clocks": clocks,
-        "cpu_baseline": c2_reference()}))
+        "cpu_baseline": None if args.no_cpu_baseline else c2_reference(local)}))
 
 
-def c2_reference():
-    """The unmodified reference run_bo (oracle/_ref/ref_tool runbo) on one
-    host core for one run of a conv-sized proxy (random-rough 12x8x8x12 =
-    9,216 candidates, 38.5 % invalid, bo-multi, budget 220, n_init 20);
-    run_experiment runs one run per worker thread, so runs/s = cores / t."""
+def cpu_info():
+    """The host CPU the CPU baselines ran on (model name, logical cores)."""
+    model = "unknown"
+    try:
+        for line in pathlib.Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "logical_cores": os.cpu_count() or 1}
+
+
+SHIM_CAVEAT = ("the reference is header-only C++ over Eigen, which this image lacks: it is compiled unmodified "
+               "against the in-repo Eigen-API shim (oracle/shim: unblocked LLT, column-blocked TRSM, SSE2 lanes, "
+               "-O3 without -march); real Eigen's blocked TRSM would likely be 2-3x faster, so the CPU numbers "
+               "are conservative for the GEMM-heavy C4 path")
+
+
+def experiment_reference(cases, strategies, reps, local=0):
+    """The reference's own run_experiment (experiment.hpp:313-358, thread pool
+    of one worker per host core) via `oracle/_ref/ref_tool experiment` over a
+    plan of reference-format cache files holding exactly the spaces and
+    values the GPU arm replays (device-enumerated ids, c2_values)."""
     tool = ROOT / "oracle" / "_ref" / "ref_tool"
     if not tool.exists():
         return None
     import tempfile
+    import paper_2111_14991_b200 as gt
+    from paper_2111_14991_b200.cache import MeasurementCache
     cores = os.cpu_count() or 1
     with tempfile.TemporaryDirectory() as tmp:
-        t0 = time.perf_counter()
-        subprocess.run([str(tool), "runbo", "random-rough", "12x8x8x12", str(BASE_SEED), "0.385", "bo-multi", "220",
-                        "20", "1", tmp], check=True, capture_output=True, timeout=900)
-        t = time.perf_counter() - t0
-    return {"value": cores / t, "unit": "runs/s", "cores": cores, "kind": "reference",
-            "sample": f"one reference run_bo (bo-multi, budget 220) on a 9,216-candidate random-rough proxy took "
-                      f"{t:.1f} s on one core; {cores} concurrent runs as run_experiment's thread pool"}
+        tmp = pathlib.Path(tmp)
+        spaces = []
+        for name, (params, rs, invalid, minimum) in cases.items():
+            pdefs = [gt.ParameterDef(k, v) for k, v in params]
+            es = gt.SearchSpace(pdefs, rs).enumerate(device=local)
+            values = c2_values(es.n, invalid, minimum, BASE_SEED + len(name))
+            bad = np.isnan(values)
+            cache = MeasurementCache(kernel_name=name, params=pdefs, restrictions=list(rs),
+                                     ids=np.asarray(es.ids, dtype=np.uint64), values=values,
+                                     reasons=np.where(bad, 2, 0).astype(np.uint8))  # 2: runtime_error
+            cache.save_json(tmp / f"{name}.json")
+            spaces.append({"name": name, "cache": f"{name}.json"})
+        plan = {"spaces": spaces, "strategies": strategies, "repetitions": reps, "budget": 220, "n_init": 20,
+                "base_seed": BASE_SEED}
+        (tmp / "plan.json").write_text(json.dumps(plan))
+        out = subprocess.run([str(tool), "experiment", str(tmp / "plan.json"), str(cores)], check=True,
+                             capture_output=True, text=True, timeout=3600)
+        rec = json.loads(out.stdout.strip().splitlines()[-1])
+    runs, secs = rec["runs"], rec["seconds"]
+    return {"value": runs / secs, "unit": "runs/s", "cores": rec["jobs"], "kind": "reference",
+            "sample": f"reference run_experiment(plan, jobs={rec['jobs']}) over {runs} runs "
+                      f"({'+'.join(cases)} x {'/'.join(strategies)} x {reps} repetitions, budget 220, n_init 20; "
+                      f"the GPU arm's spaces and values as reference cache files) took {secs:.1f} s",
+            "evaluations": rec["evaluations"], "failed_runs": rec["failed"], **cpu_info(), "caveat": SHIM_CAVEAT}
+
+
+def c2_reference(local=0):
+    """C2 on the host: all 70 runs (conv + pnpoly x 35 repetitions, bo-multi)."""
+    return experiment_reference(C2_SPACES, ["bo-multi"], 35, local)
+
+
+def c5_reference(local=0):
+    """C5 on the host, a bounded sample: every (space, strategy) cell of the
+    sweep with 2 of its 100 repetitions (24 runs; the GEMM runs alone take
+    ~30 s each on one core)."""
+    return experiment_reference({"gemm": GEMM, **C2_SPACES}, ["bo-ei", "bo-poi", "bo-lcb", "bo-multi"], 2, local)
 
 
 def cpu_baseline(cfg, n, budget_s=30.0):
@@ -409,7 +460,16 @@ def cpu_baseline(cfg, n, budget_s=30.0):
             "sample": f"1 BO iteration of the reference CPU path at N={rec['N']}, n={rec['n']}: GpModel::fit + "
                       f"GpModel::predict over all unvisited candidates split across {rec['threads']} threads + "
                       f"lambda + best_candidate (oracle/_ref/ref_tool bench)",
-            "seconds_per_iteration": rec["seconds_per_step"]}
+            "seconds_per_iteration": rec["seconds_per_step"], **cpu_flops(rec), **cpu_info(), "caveat": SHIM_CAVEAT}
+
+
+def cpu_flops(rec):
+    """Achieved FP64 rate of the reference iteration: its dominant algorithmic
+    work is the triangular solve L^-1 K* over N candidates (N n(n+1) flop)
+    plus the Cholesky (n^3/3)."""
+    N, n = rec["N"], rec["n"]
+    flop = N * n * (n + 1) + n ** 3 / 3
+    return {"gflop_per_iteration": flop / 1e9, "cpu_gflops": flop / rec["seconds_per_step"] / 1e9}
 
 
 def run_reference_arm(args, cfg):
@@ -436,7 +496,8 @@ def run_reference_arm(args, cfg):
                       "cpu_baseline": {"value": v, "unit": "iter/s", "cores": rec["threads"], "kind": "reference",
                                        "sample": f"{rec['steps']} full BO iterations at N={rec['N']}, n={rec['n']} "
                                                  f"(reference GpModel::fit + predict over all unvisited, "
-                                                 f"{rec['threads']} threads)"},
+                                                 f"{rec['threads']} threads)",
+                                       **cpu_flops(rec), **cpu_info(), "caveat": SHIM_CAVEAT},
                       "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
 
@@ -593,7 +654,7 @@ def main():
         if args.impl == "reference":
             rank, _, _ = dist_env()
             if rank == 0:
-                ref = c1_reference() if args.config == "c1" else c2_reference()
+                ref = {"c1": c1_reference, "c2": c2_reference, "c5": c5_reference}[args.config]()
                 print(json.dumps({"impl": "reference", "metric": f"BO runs/sec ({args.config.upper()})",
                                   "value": ref["value"], "unit": "runs/s", "higher_is_better": True,
                                   "n_gpus": args.gpus, "cpu_baseline": ref,

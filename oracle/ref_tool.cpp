@@ -28,6 +28,7 @@
 #include <thread>
 #include <vector>
 
+#include "gridtune/experiment.hpp"
 #include "gridtune/strategies.hpp"
 #include "gridtune/synthetic.hpp"
 #include "json.hpp"
@@ -436,6 +437,33 @@ int cmd_cachegen(int argc, char** argv) {
   return 0;
 }
 
+// experiment <plan.json> <jobs>: the reference's own run_experiment
+// (experiment.hpp:313-358) over a plan of cache files -- its thread pool of
+// `jobs` workers (0 = hardware_concurrency), every run through run_strategy.
+// Prints the wall time of the call (cache loading + every run) and the
+// number of runs / evaluations.
+int cmd_experiment(int argc, char** argv) {
+  if (argc < 4) return 2;
+  const fs::path plan_path = argv[2];
+  const ExperimentPlan plan = ExperimentPlan::load(plan_path);
+  const std::size_t jobs = std::stoul(argv[3]);
+  const auto t0 = std::chrono::steady_clock::now();
+  const ExperimentResult res = run_experiment(plan, jobs, plan_path.parent_path());
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  std::size_t runs = 0, evals = 0, failed = 0;
+  for (const RunOutcome& o : res.outcomes) {
+    if (o.run) {
+      ++runs;
+      evals += o.run->evaluations;
+    } else {
+      ++failed;
+    }
+  }
+  std::printf("{\"runs\": %zu, \"failed\": %zu, \"evaluations\": %zu, \"seconds\": %.6f, \"jobs\": %zu}\n", runs,
+              failed, evals, secs, jobs ? jobs : (std::size_t)std::thread::hardware_concurrency());
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc < 2) {
     std::fprintf(stderr, "usage: ref_tool space|gemm|gp|runbo|bench ...\n");
@@ -453,6 +481,7 @@ int main(int argc, char** argv) {
     else if (cmd == "enumjson") rc = cmd_enumjson(argc, argv);
     else if (cmd == "restrict") rc = cmd_restrict(argc, argv);
     else if (cmd == "cachegen") rc = cmd_cachegen(argc, argv);
+    else if (cmd == "experiment") rc = cmd_experiment(argc, argv);
     if (rc == 2) std::fprintf(stderr, "bad arguments for %s\n", cmd.c_str());
     return rc;
   } catch (const std::exception& e) {

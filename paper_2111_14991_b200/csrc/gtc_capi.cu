@@ -175,6 +175,10 @@ int rebuild_predictions(const SpaceDev& sp, GpStore& gp, const gtc_kernel& k, do
     GTC_LAUNCHED();
     return GTC_OK;
   }
+  if (launch_rebuild_wide(sp, gp.dev, kparams(k), V, tile_stride, n, mu, var, vp, tstat, s)) {
+    GTC_LAUNCHED();
+    return GTC_OK;
+  }
   if (launch_rebuild(sp, gp.dev, kparams(k), V, tile_stride, n, s)) {
     GTC_LAUNCHED();
     // posterior, tile summaries and variance total from the rebuilt rows
@@ -2154,7 +2158,7 @@ extern "C" int gtc_debug_select_trace(uint64_t* marks, int32_t rows) {
 
 extern "C" int gtc_debug_set_rebuild(int32_t mode) {
   const int prev = rebuild_mode();
-  if (mode >= 0) set_rebuild_mode(mode ? 1 : 0);
+  if (mode >= 0) set_rebuild_mode(mode > 2 ? 2 : mode);
   return prev;
 }
 

@@ -320,9 +320,13 @@ void launch_extend(const SpaceDev& space, const GpDev& g, KernelParams k, double
 // following final pass (r = 0).
 bool launch_rebuild(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V, int64_t tile_stride, int n,
                     cudaStream_t stream);
+// Wide streaming rebuild (k_extend_wide: 32 rows per pass, the 8-row panel
+// arithmetic): V rows [0, n) and the posterior; false = not taken.
+bool launch_rebuild_wide(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V, int64_t tile_stride, int n,
+                         double* mu, double* var, const VarPartials* vp, TileStats* tstat, cudaStream_t stream);
 void set_factor_mode(int mode);  // 1 right-looking in shared memory (default), 0 left-looking bordered rows
 int factor_mode();
-void set_rebuild_mode(int mode);  // 0 streaming, 1 tensor cores (default)
+void set_rebuild_mode(int mode);  // 0 streaming 8-row passes, 1 tensor cores, 2 wide 32-row passes (default)
 int rebuild_mode();
 
 void launch_var_partials(const double* var, int64_t n, double s2, const VarPartials& vp, cudaStream_t stream);

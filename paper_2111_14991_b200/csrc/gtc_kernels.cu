@@ -133,6 +133,19 @@ __device__ __forceinline__ double matern(double r, double lengthscale, double s2
   return __dmul_rn(__dmul_rn(s2, poly), exp(-a));
 }
 
+// a / b correctly rounded (== __ddiv_rn) from the correctly rounded
+// reciprocal y = 1/b: one Markstein correction step (r = a - q0 b is exact by
+// FMA).  Outside the safe exponent range (and for a == 0, keeping the sign
+// of zero) it defers to __ddiv_rn.  Checked bit for bit against __ddiv_rn
+// on 1.7e10 operand pairs of the rebuild's ranges (tools/div_check.cu).
+__device__ __forceinline__ double quot_rn(double a, double b, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const double aq = fabs(q0), aa = fabs(a);
+  if (!(aq < 0x1p+960 && aq > 0x1p-960 && aa > 0x1p-960 && aa < 0x1p+960)) return __ddiv_rn(a, b);
+  const double r = fma(-q0, b, a);
+  return fma(r, y, q0);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -872,6 +885,95 @@ __device__ __forceinline__ double2 coord2(const SpaceDev& sp, int t, int64_t j0)
 #define GTC_PASS_DB 0  // double-buffered row groups
 #endif
 
+// The final pass's epilogue for one thread's candidate pair (j0, j0 + 1):
+// posterior mean and variance (gp.hpp:162-166), the tile's share of the
+// variance total over unvisited candidates (strategies.hpp:406-407, fixed
+// point), and the tile summary for the selection's pruning.  Block-wide (one
+// CTA per tile, kExtendThreads threads).
+__device__ __forceinline__ void pass_epilogue(const ExtendArgs& a, int64_t tile, int64_t j0, double b0, double b1,
+                                              double q0, double q1) {
+  // mean = k*^T alpha = v^T beta;  var = max(s2 - sum v^2, 0)   (gp.hpp:162-166)
+  const double var0 = fmax(__dadd_rn(a.s2, -q0), 0.0), var1 = fmax(__dadd_rn(a.s2, -q1), 0.0);
+  *reinterpret_cast<double2*>(a.mu + j0) = make_double2(b0, b1);
+  *reinterpret_cast<double2*>(a.var + j0) = make_double2(var0, var1);
+  if (a.acc || a.tstat) {
+    // one reduction for the epilogue's tile quantities:
+    //  - this tile's share of the mean posterior variance over the unvisited
+    //    candidates (strategies.hpp:406-407), added to the run's fixed-point
+    //    total; consumed by the next kernel on the stream (k_select)
+    //  - the tile summary (min mean, max/min variance) for tile pruning
+    constexpr int kW = kExtendThreads / 32;
+    __shared__ double rs[kW], rmn[kW], rvx[kW], rvn[kW], rsm[kW], rva[kW];
+    __shared__ long long rc[kW], rpos[kW];
+    const bool in0 = j0 < a.sp.n, in1 = j0 + 1 < a.sp.n;
+    const uint32_t w = (in0 && a.visited) ? __ldg(a.visited + (j0 >> 5)) : 0xffffffffu;
+    const bool u0 = in0 && !((w >> (j0 & 31)) & 1u);
+    const bool u1 = in1 && !((w >> ((j0 + 1) & 31)) & 1u);
+    double ts = (u0 ? var0 : 0.0) + (u1 ? var1 : 0.0);
+    long long tc = (long long)u0 + (long long)u1;
+    // bounds over all candidates; seed = unvisited argmin of the mean
+    double mn = fmin(in0 ? b0 : CUDART_INF, in1 ? b1 : CUDART_INF);
+    double vx = fmax(in0 ? var0 : -CUDART_INF, in1 ? var1 : -CUDART_INF);
+    double vn = fmin(in0 ? var0 : CUDART_INF, in1 ? var1 : CUDART_INF);
+    double sm_ = u0 ? b0 : CUDART_INF, sv = u0 ? var0 : 0.0;
+    long long sp = u0 ? j0 : LLONG_MAX;
+    if (u1 && (b1 < sm_ || sp == LLONG_MAX)) {
+      sm_ = b1;
+      sv = var1;
+      sp = j0 + 1;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ts += __shfl_xor_sync(0xffffffffu, ts, o);
+      tc += __shfl_xor_sync(0xffffffffu, tc, o);
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      vx = fmax(vx, __shfl_xor_sync(0xffffffffu, vx, o));
+      vn = fmin(vn, __shfl_xor_sync(0xffffffffu, vn, o));
+      const double osm = __shfl_xor_sync(0xffffffffu, sm_, o), osv = __shfl_xor_sync(0xffffffffu, sv, o);
+      const long long osp = __shfl_xor_sync(0xffffffffu, sp, o);
+      if (osm < sm_ || (osm == sm_ && osp < sp)) {
+        sm_ = osm;
+        sv = osv;
+        sp = osp;
+      }
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+      rs[wid] = ts;
+      rc[wid] = tc;
+      rmn[wid] = mn;
+      rvx[wid] = vx;
+      rvn[wid] = vn;
+      rsm[wid] = sm_;
+      rva[wid] = sv;
+      rpos[wid] = sp;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 1; k < kW; ++k) {  // fixed order
+        ts += rs[k];
+        tc += rc[k];
+        mn = fmin(mn, rmn[k]);
+        vx = fmax(vx, rvx[k]);
+        vn = fmin(vn, rvn[k]);
+        if (rsm[k] < sm_ || (rsm[k] == sm_ && rpos[k] < sp)) {
+          sm_ = rsm[k];
+          sv = rva[k];
+          sp = rpos[k];
+        }
+      }
+      if (a.acc) accum_add(a.acc, ts, tc, a.s2);
+#ifdef GTC_SEL_TRACE
+      atomicMax(&g_sel_trace[2043][0], gtc_globaltimer());
+#endif
+      if (a.tstat)
+        a.tstat[tile] =
+            TileStats{mn, vx >= 0.0 ? vx : -1.0, vn, sm_, sv, sp == LLONG_MAX ? -1 : (int64_t)sp};
+    }
+  }
+}
+
 // Rows [n0, n0+r) of V for every candidate, r <= R, streaming rows [0, n0)
 // once.  One CTA per tile of kTile candidates, one double2 column pair per
 // thread.  With final_pass the posterior mean/variance are produced too.
@@ -1029,88 +1131,154 @@ __device__ __forceinline__ void extend_body(const ExtendArgs& a_in, int64_t tile
       }
     }
   }
-  if (a.final_pass) {
-    // mean = k*^T alpha = v^T beta;  var = max(s2 - sum v^2, 0)   (gp.hpp:162-166)
-    const double var0 = fmax(__dadd_rn(a.s2, -q0), 0.0), var1 = fmax(__dadd_rn(a.s2, -q1), 0.0);
-    *reinterpret_cast<double2*>(a.mu + j0) = make_double2(b0, b1);
-    *reinterpret_cast<double2*>(a.var + j0) = make_double2(var0, var1);
-    if (a.acc || a.tstat) {
-      // one reduction for the epilogue's tile quantities:
-      //  - this tile's share of the mean posterior variance over the unvisited
-      //    candidates (strategies.hpp:406-407), added to the run's fixed-point
-      //    total; consumed by the next kernel on the stream (k_select)
-      //  - the tile summary (min mean, max/min variance) for tile pruning
-      constexpr int kW = kExtendThreads / 32;
-      __shared__ double rs[kW], rmn[kW], rvx[kW], rvn[kW], rsm[kW], rva[kW];
-      __shared__ long long rc[kW], rpos[kW];
-      const bool in0 = j0 < a.sp.n, in1 = j0 + 1 < a.sp.n;
-      const uint32_t w = (in0 && a.visited) ? __ldg(a.visited + (j0 >> 5)) : 0xffffffffu;
-      const bool u0 = in0 && !((w >> (j0 & 31)) & 1u);
-      const bool u1 = in1 && !((w >> ((j0 + 1) & 31)) & 1u);
-      double ts = (u0 ? var0 : 0.0) + (u1 ? var1 : 0.0);
-      long long tc = (long long)u0 + (long long)u1;
-      // bounds over all candidates; seed = unvisited argmin of the mean
-      double mn = fmin(in0 ? b0 : CUDART_INF, in1 ? b1 : CUDART_INF);
-      double vx = fmax(in0 ? var0 : -CUDART_INF, in1 ? var1 : -CUDART_INF);
-      double vn = fmin(in0 ? var0 : CUDART_INF, in1 ? var1 : CUDART_INF);
-      double sm_ = u0 ? b0 : CUDART_INF, sv = u0 ? var0 : 0.0;
-      long long sp = u0 ? j0 : LLONG_MAX;
-      if (u1 && (b1 < sm_ || sp == LLONG_MAX)) {
-        sm_ = b1;
-        sv = var1;
-        sp = j0 + 1;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        ts += __shfl_xor_sync(0xffffffffu, ts, o);
-        tc += __shfl_xor_sync(0xffffffffu, tc, o);
-        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        vx = fmax(vx, __shfl_xor_sync(0xffffffffu, vx, o));
-        vn = fmin(vn, __shfl_xor_sync(0xffffffffu, vn, o));
-        const double osm = __shfl_xor_sync(0xffffffffu, sm_, o), osv = __shfl_xor_sync(0xffffffffu, sv, o);
-        const long long osp = __shfl_xor_sync(0xffffffffu, sp, o);
-        if (osm < sm_ || (osm == sm_ && osp < sp)) {
-          sm_ = osm;
-          sv = osv;
-          sp = osp;
-        }
-      }
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-      if (lane == 0) {
-        rs[wid] = ts;
-        rc[wid] = tc;
-        rmn[wid] = mn;
-        rvx[wid] = vx;
-        rvn[wid] = vn;
-        rsm[wid] = sm_;
-        rva[wid] = sv;
-        rpos[wid] = sp;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-#pragma unroll
-        for (int k = 1; k < kW; ++k) {  // fixed order
-          ts += rs[k];
-          tc += rc[k];
-          mn = fmin(mn, rmn[k]);
-          vx = fmax(vx, rvx[k]);
-          vn = fmin(vn, rvn[k]);
-          if (rsm[k] < sm_ || (rsm[k] == sm_ && rpos[k] < sp)) {
-            sm_ = rsm[k];
-            sv = rva[k];
-            sp = rpos[k];
-          }
-        }
-        if (a.acc) accum_add(a.acc, ts, tc, a.s2);
-#ifdef GTC_SEL_TRACE
-        atomicMax(&g_sel_trace[2043][0], gtc_globaltimer());
+  if (a.final_pass) pass_epilogue(a, tile, j0, b0, b1, q0, q1);
+}
+
+// ---- wide streaming rebuild: 32 rows of V per pass (four 8-row panels)
+//
+// The full forward substitution V = L^-1 K* (gp.hpp:163-164) for the fit,
+// refits and predict, with exactly the arithmetic of the 8-row passes
+// (k_extend<8>): for row t of panel q
+//   acc  = sum_{m < n0 + 8q} L[t][m] v_m    ascending FMA chain: the streamed
+//          prefix m < n0, then the pass's earlier panels m in [n0, n0 + 8q)
+//   num  = k(x_t, x) - acc;  num -= L[t][s] v_s for s in panel q, s < t;
+//   v_t  = num / L[t][t]                     (quot_rn == __ddiv_rn)
+// but each pass streams the V prefix ONCE for 32 rows instead of 8: the
+// prefix traffic N 8 n^2 / 64 instead of / 16 (5.4 GB instead of 24 GB at
+// N = 1M, n = 220), and every loaded V row feeds 64 FMAs per thread (two
+// candidates x 32 rows) -- the rebuild becomes FP64-bound rather than
+// HBM-bound.  The pass's rows of L are staged transposed in shared memory
+// ([m][32]: two rows per 16-byte broadcast load).  The final pass adds the
+// posterior (pass_epilogue, the same accumulation order over the rows).
+constexpr int kWideRows = 32;
+#ifndef GTC_WIDE_U
+#define GTC_WIDE_U 4
 #endif
-        if (a.tstat)
-          a.tstat[tile] =
-              TileStats{mn, vx >= 0.0 ? vx : -1.0, vn, sm_, sv, sp == LLONG_MAX ? -1 : (int64_t)sp};
+
+__host__ __device__ __forceinline__ size_t wide_smem_doubles(int n0, int d) {
+  return (size_t)(n0 + kWideRows) * kWideRows + (size_t)(n0 + kWideRows) + (size_t)kWideRows * d + 2 * kWideRows +
+         (size_t)2 * 8 * kExtendThreads;  // + one panel's kernel values [8][threads] double2
+}
+
+template <int NU>
+__global__ void __launch_bounds__(kExtendThreads, 3) k_extend_wide(ExtendArgs a) {
+  extern __shared__ double sm[];
+  const int n0 = a.n0, r = a.r, d = a.g.d;
+  constexpr int R = kWideRows;
+  double* LT = sm;                          // [n0 + R][R]: LT[m * R + t] = L[n0 + t][m] (0 past the row)
+  double* bs = LT + (size_t)(n0 + R) * R;   // [n0 + r] beta (final pass)
+  double* xn = bs + (n0 + R);               // [R][d] new training coords
+  double* xn2 = xn + R * d;                 // [R] their squared norms
+  double* rinv = xn2 + R;                   // [R] 1 / L[t][t]
+  for (int idx = threadIdx.x; idx < (n0 + R) * R; idx += blockDim.x) {
+    const int m = idx / R, t = idx % R;
+    LT[idx] = (t < r && m <= n0 + t) ? a.g.L[packed(n0 + t) + m] : 0.0;
+  }
+  if (a.final_pass)
+    for (int q = threadIdx.x; q < n0 + r; q += blockDim.x) bs[q] = a.g.beta[q];
+  for (int idx = threadIdx.x; idx < r * d; idx += blockDim.x) xn[idx] = a.g.train_x[(int64_t)n0 * d + idx];
+  for (int t = threadIdx.x; t < R; t += blockDim.x) {
+    xn2[t] = t < r ? a.g.train_n2[n0 + t] : 0.0;
+    rinv[t] = t < r ? __drcp_rn(a.g.L[packed(n0 + t) + n0 + t]) : 1.0;
+  }
+  __syncthreads();
+
+  const int64_t tile = blockIdx.x;
+  const int64_t j0 = tile * kTile + 2 * threadIdx.x;
+  const double2* Vt = reinterpret_cast<const double2*>(a.V + tile * a.tile_stride) + threadIdx.x;
+  constexpr int kRowStride = kTile / 2;  // in double2
+  double acc0[R], acc1[R];
+#pragma unroll
+  for (int t = 0; t < R; ++t) acc0[t] = acc1[t] = 0.0;
+  double q0 = 0.0, q1 = 0.0, b0 = 0.0, b1 = 0.0;
+  constexpr int U = GTC_WIDE_U;
+  for (int i = 0; i < n0; i += U) {
+    double2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      v[u] = i + u < n0 ? __ldcs(Vt + (int64_t)(i + u) * kRowStride) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (i + u >= n0) break;
+      const double2* lt = reinterpret_cast<const double2*>(LT + (size_t)(i + u) * R);
+#pragma unroll
+      for (int t2 = 0; t2 < R / 2; ++t2) {
+        const double2 l = lt[t2];
+        acc0[2 * t2] = fma(l.x, v[u].x, acc0[2 * t2]);
+        acc1[2 * t2] = fma(l.x, v[u].y, acc1[2 * t2]);
+        acc0[2 * t2 + 1] = fma(l.y, v[u].x, acc0[2 * t2 + 1]);
+        acc1[2 * t2 + 1] = fma(l.y, v[u].y, acc1[2 * t2 + 1]);
+      }
+      if (a.final_pass) {
+        const double bb = bs[i + u];
+        q0 = fma(v[u].x, v[u].x, q0);
+        q1 = fma(v[u].y, v[u].y, q1);
+        b0 = fma(v[u].x, bb, b0);
+        b1 = fma(v[u].y, bb, b1);
       }
     }
   }
+  // candidate coordinates and squared norms (extend_body's order)
+  double c0n2 = 0.0, c1n2 = 0.0;
+  for (int t = 0; t < d; ++t) {
+    const double2 c = coord2(a.sp, t, j0);
+    c0n2 = __dadd_rn(c0n2, __dmul_rn(c.x, c.x));
+    c1n2 = __dadd_rn(c1n2, __dmul_rn(c.y, c.y));
+  }
+  double2* Vw = reinterpret_cast<double2*>(a.V + tile * a.tile_stride) + threadIdx.x;
+  // kernel values of all the pass's rows first, into this thread's shared
+  // slots (independent evaluations: the exp / sqrt / division chains overlap
+  // instead of sitting on the triangle's dependency chain)
+  double2* kv = reinterpret_cast<double2*>(rinv + R) + threadIdx.x;  // [8][kExtendThreads] double2
+  // the pass's rows, panel by panel; acc0/acc1[t] become v once row t is done
+#pragma unroll
+  for (int pq = 0; pq < R / 8; ++pq) {
+  for (int t = 8 * pq; t < min(r, 8 * pq + 8); ++t) {
+    double dot0 = 0.0, dot1 = 0.0;
+    for (int q = 0; q < d; ++q) {
+      const double2 c = coord2(a.sp, q, j0);
+      const double xv = xn[t * d + q];
+      dot0 = __dadd_rn(dot0, __dmul_rn(xv, c.x));
+      dot1 = __dadd_rn(dot1, __dmul_rn(xv, c.y));
+    }
+    const double d20 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, dot0), xn2[t]), c0n2);
+    const double d21 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, dot1), xn2[t]), c1n2);
+    kv[(t - 8 * pq) * kExtendThreads] = make_double2(matern<NU>(sqrt(fmax(d20, 0.0)), a.lengthscale, a.s2),
+                                                     matern<NU>(sqrt(fmax(d21, 0.0)), a.lengthscale, a.s2));
+  }
+#pragma unroll
+    for (int t = 8 * pq; t < 8 * pq + 8; ++t) {
+      if (t >= r) break;
+      // the FMA chain continued over the earlier panels of this pass (ascending)
+#pragma unroll
+      for (int s = 0; s < 8 * pq; ++s) {
+        const double l = LT[(size_t)(n0 + s) * R + t];
+        acc0[t] = fma(l, acc0[s], acc0[t]);
+        acc1[t] = fma(l, acc1[s], acc1[t]);
+      }
+      const double2 kk = kv[(t - 8 * pq) * kExtendThreads];
+      double num0 = __dadd_rn(kk.x, -acc0[t]);
+      double num1 = __dadd_rn(kk.y, -acc1[t]);
+#pragma unroll
+      for (int s = 8 * pq; s < t; ++s) {
+        const double l = LT[(size_t)(n0 + s) * R + t];
+        num0 = __dadd_rn(num0, -__dmul_rn(l, acc0[s]));
+        num1 = __dadd_rn(num1, -__dmul_rn(l, acc1[s]));
+      }
+      const double diag = LT[(size_t)(n0 + t) * R + t];
+      acc0[t] = quot_rn(num0, diag, rinv[t]);
+      acc1[t] = quot_rn(num1, diag, rinv[t]);
+      Vw[(int64_t)(n0 + t) * kRowStride] = make_double2(acc0[t], acc1[t]);
+      if (a.final_pass) {
+        const double bb = bs[n0 + t];
+        q0 = fma(acc0[t], acc0[t], q0);
+        q1 = fma(acc1[t], acc1[t], q1);
+        b0 = fma(acc0[t], bb, b0);
+        b1 = fma(acc1[t], bb, b1);
+      }
+    }
+  }
+  if (a.final_pass) pass_epilogue(a, tile, j0, b0, b1, q0, q1);
 }
 
 template <int R, int NU>
@@ -2912,19 +3080,6 @@ __device__ void rebuild_stage_panel(const GpDev& g, int n, int n0, double* buf) 
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// a / b correctly rounded (== __ddiv_rn) from the correctly rounded
-// reciprocal y = 1/b: one Markstein correction step (r = a - q0 b is exact by
-// FMA).  Outside the safe exponent range (and for a == 0, keeping the sign
-// of zero) it defers to __ddiv_rn.  Checked bit for bit against __ddiv_rn
-// on 1.7e10 operand pairs of the rebuild's ranges (tools/div_check.cu).
-__device__ __forceinline__ double quot_rn(double a, double b, double y) {
-  const double q0 = __dmul_rn(a, y);
-  const double aq = fabs(q0), aa = fabs(a);
-  if (!(aq < 0x1p+960 && aq > 0x1p-960 && aa > 0x1p-960 && aa < 0x1p+960)) return __ddiv_rn(a, b);
-  const double r = fma(-q0, b, a);
-  return fma(r, y, q0);
-}
-
 // matern<NU> with the distance scaled by quot_rn (the same bits as its
 // __ddiv_rn(r, lengthscale)); linv = __drcp_rn(lengthscale).
 template <int NU>
@@ -3080,11 +3235,39 @@ __global__ void __launch_bounds__(kRbMaxWarps * 32, 1) k_rebuild(RebuildArgs a) 
 // measured and dropped: 36 % L2 hit rate, 10.7 GB of DRAM reads, 9.6 ms.)
 static int g_rebuild_mode = [] {
   const char* e = std::getenv("GTC_REBUILD");
-  return (e && std::string(e) == "stream") ? 0 : 1;
+  if (e && std::string(e) == "stream") return 0;
+  if (e && std::string(e) == "dmma") return 1;
+  return 2;
 }();
 void set_rebuild_mode(int mode) { g_rebuild_mode = mode; }
 
 int rebuild_mode() { return g_rebuild_mode; }
+
+// Wide streaming rebuild (k_extend_wide, 32 rows per pass), the final pass
+// with the posterior.  false = not taken (mode off, or the staging does not
+// fit shared memory for this n).
+bool launch_rebuild_wide(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V, int64_t tile_stride, int n,
+                         double* mu, double* var, const VarPartials* vp, TileStats* tstat, cudaStream_t s) {
+  if (g_rebuild_mode != 2 || n <= 0) return false;
+  const size_t need = sizeof(double) * wide_smem_doubles(n, sp.d);
+  if (need > 200 * 1024) return false;
+  const int64_t tiles = sp.n_pad / kTile;
+  for (int n0 = 0; n0 < n; n0 += kWideRows) {
+    count_launch();
+    const int r = std::min(kWideRows, n - n0);
+    const bool final = n0 + r == n;
+    const ExtendArgs a{sp, g, V, tile_stride, n0, r, final ? 1 : 0, 0, k.lengthscale, k.s2, mu, var,
+                       vp ? vp->visited : nullptr, (vp && final) ? vp->acc : nullptr, vp ? vp->acc_clear : nullptr,
+                       final ? tstat : nullptr};
+    const size_t smem = sizeof(double) * wide_smem_doubles(n0, sp.d);
+    switch (k.nu) {
+      case 0: opt_in_smem(k_extend_wide<0>, need); k_extend_wide<0><<<(unsigned)tiles, kExtendThreads, smem, s>>>(a); break;
+      case 1: opt_in_smem(k_extend_wide<1>, need); k_extend_wide<1><<<(unsigned)tiles, kExtendThreads, smem, s>>>(a); break;
+      default: opt_in_smem(k_extend_wide<2>, need); k_extend_wide<2><<<(unsigned)tiles, kExtendThreads, smem, s>>>(a); break;
+    }
+  }
+  return true;
+}
 
 // V rows [0, n) of every candidate (no posterior).  Returns false when the
 // tensor-core path is off or the per-warp block does not fit shared memory.

@@ -1447,10 +1447,11 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
                       r->stream);
         GTC_LAUNCHED();
         if ((rc = r->comm->allgather(r->d_send, r->d_recv, (size_t)rec_bytes, r->stream))) return rc;
-        launch_shard_merge(r->d_loop, r->cfg.kernel.nu, r->stream);
-        if (timing) GTC_CUDA(cudaEventRecord(te[3 * i + 1], r->stream));
-        launch_gp_append_loop(aa, r->cfg.kernel.nu, append_smem, r->stream);
-        if (timing) GTC_CUDA(cudaEventRecord(te[3 * i + 2], r->stream));
+        launch_shard_merge(r->d_loop, r->cfg.kernel.nu, r->cfg.n_max, r->stream);  // + the bordered append
+        if (timing) {
+          GTC_CUDA(cudaEventRecord(te[3 * i + 1], r->stream));
+          GTC_CUDA(cudaEventRecord(te[3 * i + 2], r->stream));
+        }
         launch_extend_loop(ea, r->space->n_pad / kTile, r->cfg.kernel.nu, r->stream);
         GTC_LAUNCHED();
         if ((rc = r->comm->allgather(r->acc, r->d_gacc, acc_bytes, r->stream))) return rc;

@@ -481,7 +481,7 @@ struct LoopDev {
 };
 // Merge of the all-gathered shard records + loop advance + the bordered row
 // of a valid pick from the owning shard's V column (one CTA).
-void launch_shard_merge(LoopDev* loop, int nu, cudaStream_t stream);
+void launch_shard_merge(LoopDev* loop, int nu, int n_max, cudaStream_t stream);
 // Loop-mode launches of the bordered append / single-row pass (args.loop set;
 // smem / args.n0 sized for the largest row of the chunk).
 void launch_gp_append_loop(const AppendArgs& a, int nu, size_t smem, cudaStream_t stream);

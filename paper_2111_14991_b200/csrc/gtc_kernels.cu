@@ -1916,10 +1916,12 @@ __device__ void stats_beta_staged(const GpDev& g, int n, double ysum, double y0,
 // A failed exact pivot (x <= 0) sets status 1: the pass skips, the next
 // selection halts the loop (kLoopPivot) and the host refactorises.
 // `L` is the last block's shared copy of the loop state (already advanced).
-__device__ void loop_append(const LoopDev& L, double* dsm) {
+// `col` (null: the exact row directly) is the pick's V column, rows
+// `col_stride` apart; `xsrc` its coordinates, `x_stride` apart.
+__device__ void loop_append(const LoopDev& L, double* dsm, const double* col, int64_t col_stride, const double* xsrc,
+                            int64_t x_stride) {
   const GpDev& g = L.g;
   const int n0 = L.n0, d = L.sp.d, nm = g.n_max;
-  const int64_t pos = L.pos;
   double* ls = dsm;
   double* cs = ls + nm;
   double* es = cs + nm;
@@ -1931,14 +1933,13 @@ __device__ void loop_append(const LoopDev& L, double* dsm) {
   double* red = xn + kMaxDim + 4 * 256;
   __shared__ double s_y0, s_jit;
   TRACE_AT(2040, 0);
-  const double* col = L.V + (pos / kTile) * L.tile_stride + pos % kTile;
   for (int q = threadIdx.x; q < n0; q += blockDim.x) {
-    ls[q] = __ldcg(col + (int64_t)q * kTile);
+    ls[q] = col ? __ldcg(col + (int64_t)q * col_stride) : 0.0;
     cs[q] = __ldcg(g.c + q);
     es[q] = __ldcg(g.e + q);
     ys[q] = __ldcg(g.y + q);
   }
-  for (int t = threadIdx.x; t < d; t += blockDim.x) xn[t] = __ldcg(L.sp.coords + (int64_t)t * L.sp.n_pad + pos);
+  for (int t = threadIdx.x; t < d; t += blockDim.x) xn[t] = __ldcg(xsrc + (int64_t)t * x_stride);
   if (threadIdx.x == 0) {
     s_y0 = n0 == 0 ? L.y : __ldcg(&g.sc->y0);
     s_jit = __ldcg(&g.sc->jitter);
@@ -1982,7 +1983,7 @@ __device__ void loop_append(const LoopDev& L, double* dsm) {
   double* Lrow = g.L + packed(n0);
   const double x = __dadd_rn(diag, -r[0]);
   const double* lrow = ls;
-  if (!(x > 0x1p-8 * diag)) {
+  if (!col || !(x > 0x1p-8 * diag)) {
     // ---- exact bordered row
     const double* xr = xn;
     for (int q = threadIdx.x; q < n0; q += blockDim.x) {
@@ -2040,7 +2041,7 @@ __device__ void loop_append(const LoopDev& L, double* dsm) {
       es[n0] = __ddiv_rn(__dadd_rn(1.0, -t2[1]), lnn);
       g.c[n0] = cs[n0];
       g.e[n0] = es[n0];
-      ++g.sc->exact_rows;
+      if (col) ++g.sc->exact_rows;  // (a column attempt fell below the margin)
     }
   } else {
     const double lnn = sqrt(x);
@@ -2187,7 +2188,9 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first
     shard_publish(c, c.loop);
   } else if (c.loop && s_loop.fused_append && s_loop.halt == kLoopRunning && s_loop.valid) {
     extern __shared__ double dsm[];
-    loop_append(s_loop, dsm);
+    const int64_t pos = s_loop.pos;
+    loop_append(s_loop, dsm, s_loop.V + (pos / kTile) * s_loop.tile_stride + pos % kTile, kTile,
+                s_loop.sp.coords + pos, s_loop.sp.n_pad);
   }
 }
 
@@ -2203,7 +2206,6 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first
 // factor stays bit-identical on every shard.  The first-candidate case (NaN
 // scores, no column shipped) leaves the exact row to the append kernel.
 __global__ void __launch_bounds__(kCtaThreads) k_shard_merge(LoopDev* L) {
-  __shared__ double xs[kMaxNmax];
   __shared__ const double* s_x;
   __shared__ const double* s_col;
   pdl_begin();
@@ -2282,18 +2284,23 @@ __global__ void __launch_bounds__(kCtaThreads) k_shard_merge(LoopDev* L) {
   }
   __syncthreads();
   if (L->halt != kLoopRunning || !L->valid) return;
-  const GpDev g = L->g;
-  const int n0 = L->n0;
-  append_prologue(g, L->sp, -1, s_x, L->y, n0);
   for (int t = threadIdx.x; t < d; t += blockDim.x) L->xrec[(int64_t)(L->step - 1) * d + t] = s_x[t];
-  const bool ok = s_col != nullptr && column_border_row(g, L->kp, L->noise, s_col, 1, n0, xs);
-  if (!ok && threadIdx.x == 0) g.sc->status = 2;
+  // the bordered row from the winner's V column carried in its owner's record
+  // (or, for the first-candidate case and below the margin, the exact row):
+  // the same arithmetic as one device's fused append
+  extern __shared__ double dsm[];
+  loop_append(*L, dsm, s_col, 1, s_x, 1);
 }
 
-void launch_shard_merge(LoopDev* loop, int nu, cudaStream_t s) {
+template <class K>
+static void opt_in_smem(K kernel, size_t bytes);
+
+void launch_shard_merge(LoopDev* loop, int nu, int n_max, cudaStream_t s) {
   (void)nu;
   count_launch();
-  launch_pdl(k_shard_merge, dim3(1), dim3(kCtaThreads), 0, s, loop);
+  const size_t smem = loop_append_smem(n_max);
+  opt_in_smem(k_shard_merge, smem);
+  launch_pdl(k_shard_merge, dim3(1), dim3(kCtaThreads), smem, s, loop);
 }
 
 // ---------------------------------------------------- pruned selection

@@ -685,13 +685,24 @@ def main():
     if mode == "replicas":
         mode = "single"
     if mode == "sharded":
-        out = run_sharded(args, cfg, rank, world, local)
+        try:
+            out, err = run_sharded(args, cfg, rank, world, local), None
+        except Exception as e:  # noqa: BLE001  (e.g. NCCL refuses several ranks on one GPU)
+            out, err = None, f"{type(e).__name__}: {str(e)[:200]}"
+            print(f"bench.py: candidate-sharded run failed on rank {rank}: {err}", file=sys.stderr)
+            if world > 1:
+                torch.distributed.barrier()
         # the same GPUs running independent replicas (weak scaling, no collective)
-        rep = run_single(args, cfg, rank, world, local, extras=False)
+        rep = run_single(args, cfg, rank, world, local, extras=out is None and err is not None)
         if rank == 0:
-            out["replicas"] = {"value": rep["value"], "unit": "iter/s", "scaling": "weak",
-                               "ms_per_step": rep["ms_per_step"],
-                               "note": f"{world} independent C4 runs, one per GPU (run-level sharding)"}
+            replicas = {"value": rep["value"], "unit": "iter/s", "scaling": "weak",
+                        "ms_per_step": rep["ms_per_step"],
+                        "note": f"{world} independent C4 runs, one per GPU (run-level sharding)"}
+            if out is None:  # report the replicas line (weak scaling) rather than nothing, and say why
+                out = dict(rep)
+                out["scaling"] = "weak"
+                out["sharded_error"] = err
+            out["replicas"] = replicas
     else:
         out = run_single(args, cfg, rank, world, local, extras=True)
         if world == 1 and torch.cuda.device_count() >= 1:

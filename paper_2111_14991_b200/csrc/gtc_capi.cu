@@ -285,8 +285,11 @@ struct gtc_run {
   struct Readback {
     SelectDev sel;
     GpScalars sc;
+    uint32_t seq;  // written last by the selection's last block (direct read-back)
+    uint32_t pad;
   };
-  Readback* h_rb = nullptr;  // pinned: one D2H per gtc_observe
+  Readback* h_rb = nullptr;  // pinned: the selection writes its result here directly (gtc_observe)
+  uint32_t rb_seq = 0;
   // fixed-point variance totals over the unvisited candidates, two
   // alternating generations (VarAccum); acc_valid: the current generation
   // matches the current visited set and predictions
@@ -735,6 +738,7 @@ extern "C" int gtc_run_create(gtc_space* space, const gtc_model_config* cfg, gtc
   if (e == cudaSuccess) e = cudaMemset(r->visited, 0, words * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemset(r->acc, 0, 2 * sizeof(VarAccum));
   if (e == cudaSuccess) e = cudaMallocHost(&r->h_rb, sizeof(gtc_run::Readback));
+  if (e == cudaSuccess) std::memset(r->h_rb, 0, sizeof(gtc_run::Readback));  // (seq starts at 0)
   if (e == cudaSuccess) e = cudaMallocHost(&r->h_xnew, sizeof(double) * kMaxDim);
   if (e == cudaSuccess) e = cudaMalloc(&r->d_xnew, sizeof(double) * kMaxDim);
   if (e != cudaSuccess) {
@@ -1116,10 +1120,16 @@ static int build_selection(gtc_run* r, const gtc_select_args* a, bool global_tot
 // mean variance comes from the global (sum, count) passed by value
 // (candidate-axis sharding) instead of this run's own variance total.
 static int enqueue_selection(gtc_run* r, const gtc_select_args* a, bool global_totals = false,
-                             double global_sum = 0.0, long long global_count = 0) {
+                             double global_sum = 0.0, long long global_count = 0, uint32_t host_seq = 0) {
   SelectRunArgs sa;
   int rc = build_selection(r, a, global_totals, global_sum, global_count, &sa);
   if (rc) return rc;
+  if (host_seq) {  // the last block writes the record + scalars into h_rb, then the sequence word
+    sa.p.host_sel = &r->h_rb->sel;
+    sa.p.host_sc = &r->h_rb->sc;
+    sa.p.host_seq = &r->h_rb->seq;
+    sa.p.seq = host_seq;
+  }
   launch_select(sa.mu, sa.var, sa.visited, sa.n, sa.sc, sa.p, sa.vs, sa.tstat, sa.b, sa.out, r->stream);
   GTC_LAUNCHED();
   return GTC_OK;
@@ -1377,11 +1387,8 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
     VarSource vs = r->vsrc();
     vs.acc = r->acc;  // loop mode: both generations (the kernel picks the loop state's)
     // loop-mode launch arguments: per-step values come from the loop state
-    AppendArgs aa{};
-    size_t append_smem = 0;
-    aa = make_append_args(r->gp.dev, kparams(r->cfg.kernel), r->cfg.noise, r->space->dev(), 0, nullptr, 0.0,
-                          n0_max, nullptr, &append_smem);
-    aa.loop = r->d_loop;
+    // (the bordered append runs in the selection's last block, or in the
+    // sharded merge kernel)
     ExtendArgs ea = make_pass_args(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V, r->tile_stride, n0_max,
                                    r->mu, r->var, nullptr, r->tstat);
     ea.visited = r->visited;
@@ -1765,10 +1772,31 @@ static int observe_device(ObserveReq& q, gtc_fit_info* info) {
     r->acc_valid = acc != nullptr;
   }
   q.selecting = q.a && r->space->n - r->visited_count > 0;
-  if (q.selecting && (rc = enqueue_selection(r, q.a))) return rc;
+  // direct read-back: the selection's last block writes its record and the
+  // GP scalars into the pinned h_rb and then a sequence word the host spins
+  // on -- no copy-engine transfers and no stream synchronisation on the
+  // iteration's critical path (phase events keep the synchronising path)
+  const bool direct = q.selecting && !ev;
+  const uint32_t seq = direct ? ++r->rb_seq : 0;
+  if (q.selecting && (rc = enqueue_selection(r, q.a, false, 0.0, 0, seq))) return rc;
   if (ev) GTC_CUDA(cudaEventRecord(r->ev_step1, r->stream));
   r->step_timed = ev;
   r->step_appended = q.appended;
+  if (direct) {
+    const volatile uint32_t* flag = &r->h_rb->seq;
+    for (uint32_t spins = 0; *flag != seq; ++spins) {
+      if ((spins & 1023u) == 1023u) {  // the stream finished (or failed) without the flag?
+        const cudaError_t e = cudaStreamQuery(r->stream);
+        if (e != cudaErrorNotReady) {
+          if (e != cudaSuccess) GTC_CUDA(e);
+          if (*flag != seq) return fail(GTC_ERR_CUDA, "selection finished without its read-back");
+          break;
+        }
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return GTC_OK;
+  }
   if (q.selecting)
     GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sel, r->red.sel, sizeof(SelectDev), cudaMemcpyDeviceToHost, r->stream));
   GTC_CUDA(cudaMemcpyAsync(&r->h_rb->sc, r->gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, r->stream));

@@ -190,6 +190,14 @@ struct SelectParams {
   const double* pf_V = nullptr;
   int64_t pf_tile_stride = 0;
   int32_t pf_rows = 0;
+  // gtc_observe read-back without a copy engine or a stream synchronisation:
+  // the last block also writes the result record and the GP scalars straight
+  // into the run's pinned host buffer, then (after a system fence) `seq` into
+  // *host_seq, on which the host spins; null: the caller copies them
+  SelectDev* host_sel = nullptr;
+  GpScalars* host_sc = nullptr;
+  uint32_t* host_seq = nullptr;
+  uint32_t seq = 0;
 };
 
 // Per-block scratch of the selection kernels (sized by reduce_blocks(n)).
@@ -246,8 +254,6 @@ struct AppendArgs {
   int n0;
   uint32_t* visited_mark;
   int staged;
-  const LoopDev* loop;  // resident loop: pos / y_new / n0 from the loop state; the kernel is then only
-                        // the exact fallback of the selection's column row (no-op unless status == 2)
   const double* V;      // resident V (tile-major): the bordered row is taken from the observed
   int64_t tile_stride;  // candidate's V column when set (null: exact forward substitution only)
 };
@@ -482,9 +488,8 @@ struct LoopDev {
 // Merge of the all-gathered shard records + loop advance + the bordered row
 // of a valid pick from the owning shard's V column (one CTA).
 void launch_shard_merge(LoopDev* loop, int nu, int n_max, cudaStream_t stream);
-// Loop-mode launches of the bordered append / single-row pass (args.loop set;
-// smem / args.n0 sized for the largest row of the chunk).
-void launch_gp_append_loop(const AppendArgs& a, int nu, size_t smem, cudaStream_t stream);
+// Loop-mode launch of the single-row pass (args.loop set; args.n0 sized for
+// the largest row of the chunk).
 // Portfolio script (== gtc_portfolio_op / gtc_portfolio_state).
 struct PortOp {
   int32_t kind;  // 0 suggest (picks = per-AF argmax positions), 1 record (af, value)

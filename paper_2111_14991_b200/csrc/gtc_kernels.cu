@@ -785,48 +785,20 @@ __device__ void gp_append_body(const AppendArgs& a) {
   const GpDev& g = a.g;
   const KernelParams k = a.k;
   const double noise = a.noise;
-  int64_t pos = a.pos;
-  int n0 = a.n0;
+  const int64_t pos = a.pos;
+  const int n0 = a.n0;
   extern __shared__ double smem[];
   __shared__ double red[32];
   const CtaSmem m = cta_smem_layout(smem, g.n_max, n0 + 1, a.staged != 0);
   pdl_begin();
   unsigned long long* tm = g.sc->t;
-  if (a.loop) {
-    // resident loop: this step's pick (loop_advance, in the selection's last
-    // block) is appended from its V column here; a sharded loop's merge kernel
-    // already did that and this kernel only runs the exact bordered row when
-    // the column pivot fell below the margin (status 2)
-    const LoopDev* lp = a.loop;
-    TRACE_AT(2040, 0);
-    if (lp->halt != kLoopRunning || !lp->valid) return;
-    pos = lp->pos;
-    n0 = lp->n0;
-    if (lp->nranks == 0) {
-      append_prologue(g, lp->sp, pos, nullptr, lp->y, n0);
-      TRACE_AT(2040, 1);
-      const double* col = lp->V + (pos / kTile) * lp->tile_stride + pos % kTile;
-      const bool ok = column_border_row(g, k, noise, col, kTile, n0, m.xs);
-      TRACE_AT(2040, 2);
-      if (ok) return;
-      if (threadIdx.x == 0) ++g.sc->exact_rows;
-    } else {
-      if (g.sc->status != 2) return;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        g.sc->status = 0;
-        ++g.sc->exact_rows;
-      }
-    }
-  } else {
-    if (a.visited_mark && threadIdx.x == 0) a.visited_mark[pos >> 5] |= 1u << (pos & 31);
-    append_prologue(g, a.sp, pos, a.x_explicit, a.y_new, n0);
-    if (threadIdx.x == 0) tm[0] = gtc_globaltimer();
-    if (a.V && pos >= 0) {
-      const double* col = a.V + (pos / kTile) * a.tile_stride + pos % kTile;
-      if (column_border_row(g, k, noise, col, kTile, n0, m.xs)) return;
-      if (threadIdx.x == 0) ++g.sc->exact_rows;
-    }
+  if (a.visited_mark && threadIdx.x == 0) a.visited_mark[pos >> 5] |= 1u << (pos & 31);
+  append_prologue(g, a.sp, pos, a.x_explicit, a.y_new, n0);
+  if (threadIdx.x == 0) tm[0] = gtc_globaltimer();
+  if (a.V && pos >= 0) {
+    const double* col = a.V + (pos / kTile) * a.tile_stride + pos % kTile;
+    if (column_border_row(g, k, noise, col, kTile, n0, m.xs)) return;
+    if (threadIdx.x == 0) ++g.sc->exact_rows;
   }
   // exact bordered row: forward substitution over the staged factor
   cta_stage_L(g, n0, m);  // includes __syncthreads
@@ -1511,6 +1483,11 @@ struct SelCtx {
   const double* pf_V;
   int64_t pf_tile_stride;
   int32_t pf_rows;
+  SelectDev* host_sel;     // SelectParams::host_* (direct read-back into pinned host memory)
+  GpScalars* host_sc;
+  uint32_t* host_seq;
+  uint32_t seq;
+  const GpScalars* sc_src;
 };
 
 __device__ __forceinline__ bool eligible(const SelCtx& c, int64_t j) {
@@ -2183,6 +2160,20 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first
   if (c.loop)
     for (int i = threadIdx.x; i < kLoopWords; i += blockDim.x)
       reinterpret_cast<unsigned long long*>(c.loop)[i] = reinterpret_cast<const unsigned long long*>(&s_loop)[i];
+  if (c.host_sel) {  // direct read-back (gtc_observe): record + scalars, system fence, then the sequence word
+    static_assert(sizeof(GpScalars) % 8 == 0, "word copies");
+    for (int i = threadIdx.x; i < kOutWords; i += blockDim.x)
+      reinterpret_cast<unsigned long long*>(c.host_sel)[i] = reinterpret_cast<const unsigned long long*>(&s_out)[i];
+    for (int i = threadIdx.x; i < (int)(sizeof(GpScalars) / 8); i += blockDim.x)
+      reinterpret_cast<unsigned long long*>(c.host_sc)[i] =
+          __ldcg(reinterpret_cast<const unsigned long long*>(c.sc_src) + i);
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      *reinterpret_cast<volatile uint32_t*>(c.host_seq) = c.seq;
+    }
+  }
   if (c.loop && s_loop.nranks > 0) {
     __syncthreads();  // c.out / c.loop written
     shard_publish(c, c.loop);
@@ -2980,14 +2971,6 @@ void launch_gp_append_batch(const AppendArgs* d_args, int count, int nu, size_t 
   }
 }
 
-void launch_gp_append_loop(const AppendArgs& a, int nu, size_t smem, cudaStream_t s) {
-  count_launch();
-  switch (nu) {
-    case 0: opt_in_smem(k_gp_append<0>, smem); launch_pdl(k_gp_append<0>, 1, kCtaThreads, smem, s, a); break;
-    case 1: opt_in_smem(k_gp_append<1>, smem); launch_pdl(k_gp_append<1>, 1, kCtaThreads, smem, s, a); break;
-    default: opt_in_smem(k_gp_append<2>, smem); launch_pdl(k_gp_append<2>, 1, kCtaThreads, smem, s, a); break;
-  }
-}
 
 
 void launch_gp_truncate(const GpDev& g, int n, cudaStream_t s) {
@@ -3426,7 +3409,8 @@ void launch_select(const double* mu, const double* var, const uint32_t* visited,
                    const ReduceBufs& b, SelectDev* out, cudaStream_t s, int fused_append_n_max) {
   count_launch();
   SelCtx c{mu,     var,   nullptr,          visited,          nullptr, p.excluded, p.n_excluded, n,
-           p.af_mask, b,   out,              p.loop,           p.pf_table, p.pf_V, p.pf_tile_stride, p.pf_rows};
+           p.af_mask, b,   out,              p.loop,           p.pf_table, p.pf_V, p.pf_tile_stride, p.pf_rows,
+           p.host_sel, p.host_sc, p.host_seq, p.seq, sc};
   const size_t smem = fused_append_n_max > 0 ? loop_append_smem(fused_append_n_max) : 0;
   const uint32_t mask = (p.af_mask & 7u) ? (p.af_mask & 7u) : 7u;
   const int ntiles = (int)((n + kTile - 1) / kTile);

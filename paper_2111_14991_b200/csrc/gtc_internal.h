@@ -272,6 +272,7 @@ struct ExtendArgs {
   VarAccum* acc_clear;
   TileStats* tstat;  // final pass: per-tile posterior summary (optional)
   const LoopDev* loop;  // resident loop: n0 and the accumulator generation from the loop state
+  int32_t kstar = 0;    // wide rebuild: V rows [n0, n0 + r) already hold the kernel values k(x_t, x) (k_kstar)
 };
 
 struct SelectRunArgs {

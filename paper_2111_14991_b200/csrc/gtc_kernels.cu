@@ -146,6 +146,21 @@ __device__ __forceinline__ double quot_rn(double a, double b, double y) {
   return fma(r, y, q0);
 }
 
+// matern<NU> with the distance scaled by quot_rn (the same bits as its
+// __ddiv_rn(r, lengthscale)); linv = __drcp_rn(lengthscale).
+template <int NU>
+__device__ __forceinline__ double matern_q(double r, double lengthscale, double linv, double s2) {
+  const double s = quot_rn(r, lengthscale, linv);
+  if (NU == 0) return __dmul_rn(s2, exp(-s));
+  if (NU == 1) {
+    const double a = __dmul_rn(1.7320508075688772, s);
+    return __dmul_rn(__dmul_rn(s2, __dadd_rn(1.0, a)), exp(-a));
+  }
+  const double a = __dmul_rn(2.2360679774997896, s);
+  const double poly = __dadd_rn(__dadd_rn(1.0, a), __ddiv_rn(__dmul_rn(a, a), 3.0));
+  return __dmul_rn(__dmul_rn(s2, poly), exp(-a));
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -1127,9 +1142,44 @@ constexpr int kWideRows = 32;
 #define GTC_WIDE_U 4
 #endif
 
-__host__ __device__ __forceinline__ size_t wide_smem_doubles(int n0, int d) {
+__host__ __device__ __forceinline__ size_t wide_smem_doubles(int n0, int d, bool kstar = false) {
   return (size_t)(n0 + kWideRows) * kWideRows + (size_t)(n0 + kWideRows) + (size_t)kWideRows * d + 2 * kWideRows +
-         (size_t)2 * 8 * kExtendThreads;  // + one panel's kernel values [8][threads] double2
+         (kstar ? 0 : (size_t)2 * 8 * kExtendThreads);  // + one panel's kernel values [8][threads] double2
+}
+
+// Kernel values k(x_t, x) of rows [0, n) for every candidate, written into V
+// row t (k_extend_wide then reads them back and overwrites them with v_t):
+// the exp / sqrt / division work of the rebuild at full occupancy (8 rows x 2
+// candidates per thread), in extend_body's expansion-form order (gp.hpp:176-179).
+template <int NU>
+__global__ void __launch_bounds__(kExtendThreads) k_kstar(ExtendArgs a, int n) {
+  const int d = a.g.d;
+  const int64_t tile = blockIdx.x;
+  const int64_t j0 = tile * kTile + 2 * threadIdx.x;
+  double c0n2 = 0.0, c1n2 = 0.0;
+  for (int t = 0; t < d; ++t) {
+    const double2 c = coord2(a.sp, t, j0);
+    c0n2 = __dadd_rn(c0n2, __dmul_rn(c.x, c.x));
+    c1n2 = __dadd_rn(c1n2, __dmul_rn(c.y, c.y));
+  }
+  double2* Vw = reinterpret_cast<double2*>(a.V + tile * a.tile_stride) + threadIdx.x;
+  const int t0 = 8 * blockIdx.y, t1 = min(n, t0 + 8);
+  const double linv = __drcp_rn(a.lengthscale);
+  for (int t = t0; t < t1; ++t) {
+    const double* xr = a.g.train_x + (int64_t)t * d;
+    double dot0 = 0.0, dot1 = 0.0;
+    for (int q = 0; q < d; ++q) {
+      const double2 c = coord2(a.sp, q, j0);
+      const double xv = __ldg(xr + q);
+      dot0 = __dadd_rn(dot0, __dmul_rn(xv, c.x));
+      dot1 = __dadd_rn(dot1, __dmul_rn(xv, c.y));
+    }
+    const double xn2 = __ldg(a.g.train_n2 + t);
+    const double d20 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, dot0), xn2), c0n2);
+    const double d21 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, dot1), xn2), c1n2);
+    Vw[(int64_t)t * (kTile / 2)] = make_double2(matern_q<NU>(sqrt(fmax(d20, 0.0)), a.lengthscale, linv, a.s2),
+                                                matern_q<NU>(sqrt(fmax(d21, 0.0)), a.lengthscale, linv, a.s2));
+  }
 }
 
 template <int NU>
@@ -1198,14 +1248,15 @@ __global__ void __launch_bounds__(kExtendThreads, 3) k_extend_wide(ExtendArgs a)
     c1n2 = __dadd_rn(c1n2, __dmul_rn(c.y, c.y));
   }
   double2* Vw = reinterpret_cast<double2*>(a.V + tile * a.tile_stride) + threadIdx.x;
-  // kernel values of all the pass's rows first, into this thread's shared
-  // slots (independent evaluations: the exp / sqrt / division chains overlap
-  // instead of sitting on the triangle's dependency chain)
+  // kernel values of each panel's rows first (from k_kstar's V rows, or
+  // evaluated here into this thread's shared slots: independent evaluations,
+  // so the exp / sqrt / division chains overlap instead of sitting on the
+  // triangle's dependency chain)
   double2* kv = reinterpret_cast<double2*>(rinv + R) + threadIdx.x;  // [8][kExtendThreads] double2
   // the pass's rows, panel by panel; acc0/acc1[t] become v once row t is done
 #pragma unroll
   for (int pq = 0; pq < R / 8; ++pq) {
-  for (int t = 8 * pq; t < min(r, 8 * pq + 8); ++t) {
+  for (int t = 8 * pq; !a.kstar && t < min(r, 8 * pq + 8); ++t) {
     double dot0 = 0.0, dot1 = 0.0;
     for (int q = 0; q < d; ++q) {
       const double2 c = coord2(a.sp, q, j0);
@@ -1228,7 +1279,7 @@ __global__ void __launch_bounds__(kExtendThreads, 3) k_extend_wide(ExtendArgs a)
         acc0[t] = fma(l, acc0[s], acc0[t]);
         acc1[t] = fma(l, acc1[s], acc1[t]);
       }
-      const double2 kk = kv[(t - 8 * pq) * kExtendThreads];
+      const double2 kk = a.kstar ? Vw[(int64_t)(n0 + t) * kRowStride] : kv[(t - 8 * pq) * kExtendThreads];
       double num0 = __dadd_rn(kk.x, -acc0[t]);
       double num1 = __dadd_rn(kk.y, -acc1[t]);
 #pragma unroll
@@ -3070,21 +3121,6 @@ __device__ void rebuild_stage_panel(const GpDev& g, int n, int n0, double* buf) 
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// matern<NU> with the distance scaled by quot_rn (the same bits as its
-// __ddiv_rn(r, lengthscale)); linv = __drcp_rn(lengthscale).
-template <int NU>
-__device__ __forceinline__ double matern_q(double r, double lengthscale, double linv, double s2) {
-  const double s = quot_rn(r, lengthscale, linv);
-  if (NU == 0) return __dmul_rn(s2, exp(-s));
-  if (NU == 1) {
-    const double a = __dmul_rn(1.7320508075688772, s);
-    return __dmul_rn(__dmul_rn(s2, __dadd_rn(1.0, a)), exp(-a));
-  }
-  const double a = __dmul_rn(2.2360679774997896, s);
-  const double poly = __dadd_rn(__dadd_rn(1.0, a), __ddiv_rn(__dmul_rn(a, a), 3.0));
-  return __dmul_rn(__dmul_rn(s2, poly), exp(-a));
-}
-
 template <int NU>
 __global__ void __launch_bounds__(kRbMaxWarps * 32, 1) k_rebuild(RebuildArgs a) {
   constexpr int G = kRbGroups;
@@ -3242,14 +3278,25 @@ bool launch_rebuild_wide(const SpaceDev& sp, const GpDev& g, KernelParams k, dou
   const size_t need = sizeof(double) * wide_smem_doubles(n, sp.d);
   if (need > 200 * 1024) return false;
   const int64_t tiles = sp.n_pad / kTile;
+  {  // every kernel value first, at full occupancy, into the V rows they become
+    count_launch();
+    ExtendArgs a{sp, g, V, tile_stride, 0, 0, 0, 0, k.lengthscale, k.s2};
+    const dim3 grid((unsigned)tiles, (unsigned)((n + 7) / 8));
+    switch (k.nu) {
+      case 0: k_kstar<0><<<grid, kExtendThreads, 0, s>>>(a, n); break;
+      case 1: k_kstar<1><<<grid, kExtendThreads, 0, s>>>(a, n); break;
+      default: k_kstar<2><<<grid, kExtendThreads, 0, s>>>(a, n); break;
+    }
+  }
   for (int n0 = 0; n0 < n; n0 += kWideRows) {
     count_launch();
     const int r = std::min(kWideRows, n - n0);
     const bool final = n0 + r == n;
-    const ExtendArgs a{sp, g, V, tile_stride, n0, r, final ? 1 : 0, 0, k.lengthscale, k.s2, mu, var,
-                       vp ? vp->visited : nullptr, (vp && final) ? vp->acc : nullptr, vp ? vp->acc_clear : nullptr,
-                       final ? tstat : nullptr};
-    const size_t smem = sizeof(double) * wide_smem_doubles(n0, sp.d);
+    ExtendArgs a{sp, g, V, tile_stride, n0, r, final ? 1 : 0, 0, k.lengthscale, k.s2, mu, var,
+                 vp ? vp->visited : nullptr, (vp && final) ? vp->acc : nullptr, vp ? vp->acc_clear : nullptr,
+                 final ? tstat : nullptr};
+    a.kstar = 1;
+    const size_t smem = sizeof(double) * wide_smem_doubles(n0, sp.d, true);
     switch (k.nu) {
       case 0: opt_in_smem(k_extend_wide<0>, need); k_extend_wide<0><<<(unsigned)tiles, kExtendThreads, smem, s>>>(a); break;
       case 1: opt_in_smem(k_extend_wide<1>, need); k_extend_wide<1><<<(unsigned)tiles, kExtendThreads, smem, s>>>(a); break;

@@ -1383,6 +1383,9 @@ extern "C" int gtc_run_steps(gtc_run* r, const gtc_select_args* a, int32_t k, in
       p.pf_V = r->V;
       p.pf_tile_stride = r->tile_stride;
       p.pf_rows = n0_max;
+      p.pf_gp[0] = r->gp.dev.c;
+      p.pf_gp[1] = r->gp.dev.e;
+      p.pf_gp[2] = r->gp.dev.y;
     }
     VarSource vs = r->vsrc();
     vs.acc = r->acc;  // loop mode: both generations (the kernel picks the loop state's)

@@ -190,6 +190,7 @@ struct SelectParams {
   const double* pf_V = nullptr;
   int64_t pf_tile_stride = 0;
   int32_t pf_rows = 0;
+  const double* pf_gp[3] = {nullptr, nullptr, nullptr};  // c, e, y: warmed by the last block at its entry (fused append)
   // gtc_observe read-back without a copy engine or a stream synchronisation:
   // the last block also writes the result record and the GP scalars straight
   // into the run's pinned host buffer, then (after a system fence) `seq` into

@@ -1534,6 +1534,9 @@ struct SelCtx {
   const double* pf_V;
   int64_t pf_tile_stride;
   int32_t pf_rows;
+  const double* pf_c;      // SelectParams::pf_gp (the fused append's c, e, y inputs)
+  const double* pf_e;
+  const double* pf_y;
   SelectDev* host_sel;     // SelectParams::host_* (direct read-back into pinned host memory)
   GpScalars* host_sc;
   uint32_t* host_seq;
@@ -2179,6 +2182,11 @@ __device__ void select_finish(const SelCtx& c, Best* b, int64_t first, int first
   static_assert(sizeof(LoopDev) % 8 == 0 && sizeof(SelectDev) % 8 == 0, "word copies");
   constexpr int kLoopWords = sizeof(LoopDev) / 8, kOutWords = sizeof(SelectDev) / 8;
   __threadfence();
+  if (c.pf_c) {  // the fused append's inputs: into L2 while the merge runs (16 doubles per line)
+    const int lines = (c.pf_rows + 16) / 16;
+    for (int i = threadIdx.x; i < 3 * lines; i += blockDim.x)
+      prefetch_l2((i < lines ? c.pf_c : i < 2 * lines ? c.pf_e : c.pf_y) + 16 * (i % lines));
+  }
   if (c.loop)
     for (int i = threadIdx.x; i < kLoopWords; i += blockDim.x)
       reinterpret_cast<unsigned long long*>(&s_loop)[i] = __ldcg(reinterpret_cast<const unsigned long long*>(c.loop) + i);
@@ -3457,7 +3465,7 @@ void launch_select(const double* mu, const double* var, const uint32_t* visited,
   count_launch();
   SelCtx c{mu,     var,   nullptr,          visited,          nullptr, p.excluded, p.n_excluded, n,
            p.af_mask, b,   out,              p.loop,           p.pf_table, p.pf_V, p.pf_tile_stride, p.pf_rows,
-           p.host_sel, p.host_sc, p.host_seq, p.seq, sc};
+           p.pf_gp[0], p.pf_gp[1], p.pf_gp[2], p.host_sel, p.host_sc, p.host_seq, p.seq, sc};
   const size_t smem = fused_append_n_max > 0 ? loop_append_smem(fused_append_n_max) : 0;
   const uint32_t mask = (p.af_mask & 7u) ? (p.af_mask & 7u) : 7u;
   const int ntiles = (int)((n + kTile - 1) / kTile);

@@ -294,6 +294,10 @@ struct gtc_run {
   // alternating generations (VarAccum); acc_valid: the current generation
   // matches the current visited set and predictions
   TileStats* tstat = nullptr;  // [tiles] posterior summary per tile (selection pruning)
+  // gtc_truncate without `info` defers the standardisation / beta of the
+  // prefix (k_gp_truncate) to its first consumer; a bordered append
+  // recomputes them anyway (-1: up to date)
+  int stats_stale = -1;
   VarAccum* acc = nullptr;  // [2]
   int acc_gen = 0;
   bool acc_valid = false;
@@ -848,6 +852,7 @@ static int upload_train(gtc_run* r) {
 // `start_jitter`, then the full predictive pass.
 static int refit(gtc_run* r, double start_jitter, gtc_fit_info* info) {
   const int n = (int)r->y_host.size();
+  r->stats_stale = -1;  // (the factorisation recomputes them)
   int rc = upload_train(r);
   if (rc) return rc;
   rc = factor_with_escalation(r->gp, r->cfg.kernel, r->cfg.noise, r->cfg.jitter, start_jitter, n, r->stream);
@@ -914,6 +919,7 @@ static bool phase_events() {
 // (asynchronous; the pass is a no-op if the pivot fails on the device).
 static int enqueue_append(gtc_run* r, int64_t pos, double y_raw, uint32_t* mark) {
   const int n0 = r->n;
+  r->stats_stale = -1;  // (the bordered row recomputes the standardisation and beta of rows [0, n0])
   launch_gp_append(r->gp.dev, kparams(r->cfg.kernel), r->cfg.noise, r->space->dev(), pos, nullptr, y_raw, n0,
                    mark, r->stream, r->V, r->tile_stride);
   GTC_LAUNCHED();
@@ -954,6 +960,8 @@ extern "C" int gtc_append(gtc_run* r, int64_t pos, double y_raw, gtc_fit_info* i
   return GTC_OK;
 }
 
+static int flush_stats(gtc_run* r);
+
 extern "C" int gtc_truncate(gtc_run* r, int32_t n, gtc_fit_info* info) {
   if (!r) return fail(GTC_ERR_INVALID, "run is null");
   if (n < 0 || n > r->n) return fail(GTC_ERR_INVALID, "truncate: n out of range");
@@ -965,12 +973,12 @@ extern "C" int gtc_truncate(gtc_run* r, int32_t n, gtc_fit_info* info) {
     keep_obs(r, n);
     return refit(r, r->cfg.jitter, info);
   }
-  launch_gp_truncate(r->gp.dev, n, r->stream);
-  GTC_LAUNCHED();
   r->n = n;
   keep_obs(r, n);
   r->predictions_valid = false;
+  r->stats_stale = n;  // (a following append recomputes them: nothing to launch now)
   if (info) {  // the scalars need a round trip; without `info` the call stays asynchronous
+    if (int rc = flush_stats(r)) return rc;
     GTC_CUDA(cudaMemcpyAsync(r->gp.h_sc, r->gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, r->stream));
     GTC_CUDA(cudaStreamSynchronize(r->stream));
     fill_info(info, *r->gp.h_sc, n, 0);
@@ -978,7 +986,16 @@ extern "C" int gtc_truncate(gtc_run* r, int32_t n, gtc_fit_info* info) {
   return GTC_OK;
 }
 
+static int flush_stats(gtc_run* r) {
+  if (r->stats_stale < 0) return GTC_OK;
+  launch_gp_truncate(r->gp.dev, r->stats_stale, r->stream);
+  GTC_LAUNCHED();
+  r->stats_stale = -1;
+  return GTC_OK;
+}
+
 static int ensure_predictions(gtc_run* r) {
+  if (int rc = flush_stats(r)) return rc;
   if (r->predictions_valid) return GTC_OK;
   if (r->n == 0) {
     launch_prior(r->mu, r->var, r->space->n_pad, r->cfg.kernel.output_variance, r->tstat, r->stream);
@@ -1633,6 +1650,7 @@ extern "C" int gtc_shard_observe(gtc_run* r, const double* x_new, int64_t local_
     } else {
       std::memcpy(r->h_xnew, x_new, sizeof(double) * r->space->d);
       GTC_CUDA(cudaMemcpyAsync(r->d_xnew, r->h_xnew, sizeof(double) * r->space->d, cudaMemcpyHostToDevice, r->stream));
+      r->stats_stale = -1;  // (recomputed by the bordered row)
       launch_gp_append(r->gp.dev, kparams(r->cfg.kernel), r->cfg.noise, r->space->dev(), -1, r->d_xnew, y_raw, n0,
                        nullptr, r->stream);
       GTC_LAUNCHED();
@@ -1752,6 +1770,7 @@ static void observe_prepare(ObserveReq& q) {
 static int observe_device(ObserveReq& q, gtc_fit_info* info) {
   gtc_run* r = q.r;
   int rc;
+  if (!(q.valid && q.n0 > 0) && (rc = flush_stats(r))) return rc;  // (an append recomputes them)
   set_thread_pdl(r->pdl);
   const bool ev = phase_events();
   if (ev) GTC_CUDA(cudaEventRecord(r->ev_step0, r->stream));
@@ -1927,6 +1946,7 @@ static int execute_round(gtc_group* g) {
     n_cand = r->space->n;
     if (q.valid) {
       size_t sm;
+      r->stats_stale = -1;  // (the bordered row recomputes the standardisation and beta)
       app[i] = make_append_args(r->gp.dev, kparams(r->cfg.kernel), r->cfg.noise, r->space->dev(), q.pos, nullptr,
                                 q.y_raw, q.n0, q.newly ? r->visited : nullptr, &sm);
       app[i].V = r->V;  // bordered row from the pick's V column (exact substitution below the margin)

@@ -1010,6 +1010,10 @@ __device__ __forceinline__ void extend_body(const ExtendArgs& a_in, int64_t tile
     xn[idx] = a.g.train_x[(int64_t)n0 * a.g.d + idx];
   for (int t = threadIdx.x; t < r; t += blockDim.x) xn2[t] = a.g.train_n2[n0 + t];
   __syncthreads();
+  if (blockIdx.x == 0) TRACE_AT(2041, 1);
+#ifdef GTC_SEL_TRACE
+  if (threadIdx.x == 0) atomicMax(&g_sel_trace[2041][2], gtc_globaltimer());  // last CTA through its staging
+#endif
 
   const int64_t j0 = tile * kTile + 2 * threadIdx.x;
   const double2* Vt = reinterpret_cast<const double2*>(a.V + tile * a.tile_stride) + threadIdx.x;

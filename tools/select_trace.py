@@ -58,6 +58,7 @@ for rep in range(5):
         "publish_done": rel(marks[2042, 2]), "advance_done": rel(marks[2042, 3]),
         "append_start": rel(marks[2040, 0]), "append_prologue": rel(marks[2040, 1]),
         "append_column": rel(marks[2040, 2]), "pass_start": rel(marks[2041, 0]),
+        "pass_staged_block0": rel(marks[2041, 1]), "pass_staged_last": rel(marks[2041, 2]),
     }
     out.append(row)
 print(json.dumps({"config": cfg_name, "us_since_first_select_block": out}, indent=1))

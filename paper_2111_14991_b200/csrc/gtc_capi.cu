@@ -807,6 +807,7 @@ extern "C" int gtc_run_reset(gtc_run* r, const gtc_model_config* cfg) {
   r->jitter = cfg->jitter;
   r->n = 0;
   r->predictions_valid = false;
+  r->stats_stale = -1;
   r->acc_gen = 0;
   r->acc_valid = false;
   r->visited_host.assign(words, 0u);
@@ -879,6 +880,7 @@ extern "C" int gtc_fit(gtc_run* r, const int64_t* positions, const double* y_raw
   int rc = check_fit_inputs(y_raw, n, r->cfg.noise, r->cfg.jitter);
   if (rc) return rc;
   GTC_CUDA(cudaSetDevice(r->space->device));
+  r->stats_stale = -1;  // (a fit replaces the model; n == 0 sets the prior scalars below)
   keep_obs(r, 0);
   for (int i = 0; i < n; ++i) {
     if (positions[i] < 0 || positions[i] >= r->space->n)

@@ -236,3 +236,42 @@ def test_observe_equals_separate_calls(gt):
         ma, va = run_a.predictions()
         mb, vb = run_b.predictions()
         assert ma.tobytes() == mb.tobytes() and va.tobytes() == vb.tobytes()
+
+
+def test_async_truncate_defers_but_matches_eager(gt):
+    """gtc_truncate without info defers the prefix standardisation/beta to the
+    first consumer; predictions, the mean variance and a following append
+    equal the eager truncate's bit for bit."""
+    rng = np.random.default_rng(21)
+    coords = rng.random((5000, 3))
+    pos = rng.choice(5000, 30, replace=False)
+    y = rng.standard_normal(30) * 2.0 + 5.0
+
+    def make():
+        run = gt.SurrogateRun(gt.Space(coords), gt.MaternKernel(gt.MaternNu.five_halves, 0.9, 1.2), n_max=40)
+        run.fit(pos[:25], y[:25])
+        return run
+
+    a, b = make(), make()
+    a.truncate(18)
+    b.truncate_async(18)
+    ma, va = a.predictions()
+    mb, vb = b.predictions()
+    np.testing.assert_array_equal(ma, mb)
+    np.testing.assert_array_equal(va, vb)
+    assert a.mean_variance() == b.mean_variance()
+    # truncate, then append right away (the append recomputes the statistics)
+    c, e = make(), make()
+    c.truncate(20)
+    e.truncate_async(20)
+    c.append(int(pos[27]), float(y[27]))
+    e.append(int(pos[27]), float(y[27]))
+    mc, vc = c.predictions()
+    me, ve = e.predictions()
+    np.testing.assert_array_equal(mc, me)
+    np.testing.assert_array_equal(vc, ve)
+    # a refit after an async truncate starts from clean statistics
+    e.truncate_async(10)
+    e.fit(pos[:12], y[:12])
+    c.fit(pos[:12], y[:12])
+    np.testing.assert_array_equal(c.predictions()[0], e.predictions()[0])

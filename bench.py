@@ -337,15 +337,17 @@ def run_c1(args, rank=0, world=1, local=0):
     if rank != 0:
         return
     dt = float(np.sum(ts))
+    med = float(np.median(ts))  # (single runs see rare host-side stalls of 30-100 ms: the median is the statistic)
     print(json.dumps({
-        "metric": "BO runs/sec (C1: GEMM simulation mode, bo-ei, budget 220, one run at a time)", "value": k / dt,
-        "unit": "runs/s", "n_gpus": 1, "steps": k, "warmup": max(3, args.warmup), "ms_per_step": 1e3 * dt / k,
+        "metric": "BO runs/sec (C1: GEMM simulation mode, bo-ei, budget 220, one run at a time)", "value": 1.0 / med,
+        "unit": "runs/s", "n_gpus": 1, "steps": k, "warmup": max(3, args.warmup), "ms_per_step": 1e3 * med,
+        "mean_runs_per_s": k / dt, "statistic": "median run time over the runs (mean in mean_runs_per_s)",
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic measurements over the device-enumerated GEMM space (17,956 of 82,944 configurations)",
         "config": {"workload": "C1 GEMM, bo-ei, contextual variance, n_init 20, budget 220", "runs": k,
                    "timing": "wall clock of gtc_run_bo_table per run (initial design, fit, 200 resident iterations, "
                              "records D2H)", "median_ms": 1e3 * float(np.median(ts))},
-        "e2e": {"value": k / dt, "unit": "runs/s", "h2d_bytes_per_step": 8 * es.n, "d2h_bytes_per_step": 32 * 200},
+        "e2e": {"value": 1.0 / med, "unit": "runs/s", "h2d_bytes_per_step": 8 * es.n, "d2h_bytes_per_step": 32 * 200},
         "evaluations": int(run.evaluations), "clocks": clocks.summary(),
         "cpu_baseline": None if args.no_cpu_baseline else c1_reference()}))
 

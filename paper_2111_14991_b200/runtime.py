@@ -188,8 +188,10 @@ class SurrogateRun:
         next selection (when afs is non-empty) with one host round trip.
         Returns (FitInfo, Selection or None)."""
         valid = y_raw is not None
-        r = _lib.gtc_select_result()
-        info = _lib.gtc_fit_info()
+        bufs = getattr(self, "_obs_bufs", None)  # result structs reused across the per-iteration calls
+        if bufs is None:
+            bufs = self._obs_bufs = (_lib.gtc_select_result(), _lib.gtc_fit_info(), load().gtc_observe)
+        r, info, observe = bufs
         if afs:
             if excluded:
                 a, _keep = self._args(afs, f_best_raw, exploration, cv_state, excluded)
@@ -202,11 +204,11 @@ class SurrogateRun:
                     self._obs_args = cached
                 a = cached[1]
                 a.f_best_raw = float(f_best_raw)
-            check(load().gtc_observe(self._h, int(position), float(y_raw) if valid else 0.0, int(valid),
-                                     C.byref(a), C.byref(r), C.byref(info)))
+            check(observe(self._h, int(position), float(y_raw) if valid else 0.0, int(valid),
+                          C.byref(a), C.byref(r), C.byref(info)))
             return FitInfo.of(info), self._selection(r)
-        check(load().gtc_observe(self._h, int(position), float(y_raw) if valid else 0.0, int(valid), None,
-                                 C.byref(r), C.byref(info)))
+        check(observe(self._h, int(position), float(y_raw) if valid else 0.0, int(valid), None,
+                      C.byref(r), C.byref(info)))
         return FitInfo.of(info), None
 
     def set_values(self, values) -> None:

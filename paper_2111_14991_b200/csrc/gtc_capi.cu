@@ -2212,7 +2212,7 @@ extern "C" int gtc_debug_select_trace(uint64_t* marks, int32_t rows) {
 
 extern "C" int gtc_debug_set_rebuild(int32_t mode) {
   const int prev = rebuild_mode();
-  if (mode >= 0) set_rebuild_mode(mode > 2 ? 2 : mode);
+  if (mode >= 0) set_rebuild_mode(mode > 3 ? 3 : mode);
   return prev;
 }
 

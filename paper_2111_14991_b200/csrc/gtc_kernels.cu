@@ -1308,6 +1308,114 @@ __global__ void __launch_bounds__(kExtendThreads, 3) k_extend_wide(ExtendArgs a)
   if (a.final_pass) pass_epilogue(a, tile, j0, b0, b1, q0, q1);
 }
 
+// ---- wide rebuild on the FP64 tensor cores: 32 rows per pass, DMMA contraction
+//
+// The 32-row passes of k_extend_wide with the prefix contraction
+//   acc[t][x] = sum_{m < n0} L[n0 + t][m] v_m(x)
+// as FP64 mma.sync m8n8k4 (DMMA): a warp owns 8 candidates and the four
+// 8-row panels of the pass (four 8x8 accumulator fragments); each k-step
+// loads ONE B fragment (4 V rows x 8 candidates, streamed from HBM) and
+// reuses it for the four panels' A fragments (L rows staged in shared
+// memory).  A chain of DMMAs is the ascending FMA chain
+// (tools/dmma_order.cu), so the prefix part, the continuation over the
+// pass's earlier panels (DMMA again, B from the panels' v in shared memory)
+// and the panel triangles (shuffle broadcast, quot_rn == __ddiv_rn) are the
+// 8-row passes' arithmetic bit for bit.  Four accumulator fragments are 8
+// doubles per thread instead of 64, so 24 warps per SM keep 8 k-steps of the
+// stream in flight.  The kernel values come from k_kstar; the posterior from
+// a following r = 0 pass.
+constexpr int kWmWarps = 8;  // warps (8 candidates each) per CTA
+constexpr int kWmU = 8;      // k-steps of B fragments in flight per warp
+
+__host__ __device__ __forceinline__ int wm_ld(int n0) { return ((n0 + kWideRows + 15) / 16) * 16 + 4; }
+__host__ __device__ __forceinline__ size_t wm_smem_doubles(int n0) {
+  return (size_t)kWideRows * wm_ld(n0) + kWideRows + (size_t)kWmWarps * 4 * 64;
+}
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kWmWarps * 32, 3) k_extend_wide_mma(ExtendArgs a) {
+  extern __shared__ double sm[];
+  constexpr int R = kWideRows;
+  const int n0 = a.n0, r = a.r, ld = wm_ld(n0);
+  double* Ls = sm;             // [R][ld]: Ls[t * ld + m] = L[n0 + t][m] for m <= n0 + t, rows t < r; else 0
+  double* rinvs = Ls + R * ld;  // [R] 1 / L[n0 + t][n0 + t]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* vbuf = rinvs + R + (size_t)w * 4 * 64;  // [4 panels][8 rows][8 candidates] this warp's v
+  for (int idx = threadIdx.x; idx < R * ld; idx += blockDim.x) {
+    const int t = idx / ld, m = idx % ld;
+    Ls[idx] = (t < r && m <= n0 + t) ? a.g.L[packed(n0 + t) + m] : 0.0;
+  }
+  for (int t = threadIdx.x; t < R; t += blockDim.x) rinvs[t] = t < r ? __drcp_rn(a.g.L[packed(n0 + t) + n0 + t]) : 1.0;
+  __syncthreads();
+  const int row = lane >> 2, kq = lane & 3, col = 2 * kq;
+  const int64_t c0 = ((int64_t)blockIdx.x * kWmWarps + w) * 8;  // this warp's first candidate
+  if (c0 >= a.sp.n_pad) return;
+  double* Vt = a.V + (c0 / kTile) * a.tile_stride + c0 % kTile;  // row m of the warp's candidates at Vt + m * kTile
+  double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  // ---- the prefix: rows m < n0 (n0 is a multiple of 32), B streamed, kWmU k-steps in flight
+  const double* Bp = Vt + (int64_t)kq * kTile + row;  // B fragment of k-step m0: V[m0 + kq][row]
+  for (int m0 = 0; m0 < n0; m0 += 4 * kWmU) {
+    double bv[kWmU];
+#pragma unroll
+    for (int u = 0; u < kWmU; ++u) bv[u] = m0 + 4 * u < n0 ? __ldcs(Bp + (int64_t)(m0 + 4 * u) * kTile) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kWmU; ++u) {
+      if (m0 + 4 * u >= n0) break;
+      const double* Ap = Ls + row * ld + m0 + 4 * u + kq;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dmma(d[i], Ap[8 * i * ld], bv[u]);
+    }
+  }
+  // ---- the pass's four panels
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int t = 8 * i + row;  // this thread's D row
+    const bool live = t < r;
+    // the FMA chain continued over the earlier panels (DMMA, B from their v)
+#pragma unroll
+    for (int j = 0; j < i; ++j) {
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const double av = Ls[t * ld + n0 + 8 * j + 4 * kk + kq];
+        const double bv = vbuf[j * 64 + (4 * kk + kq) * 8 + row];
+        dmma(d[i], av, bv);
+      }
+    }
+    // kernel values (k_kstar wrote them into these V rows)
+    double2 kk2 = make_double2(0.0, 0.0);
+    if (live) kk2 = __ldcg(reinterpret_cast<const double2*>(Vt + (int64_t)(n0 + t) * kTile + col));
+    double num0 = __dadd_rn(kk2.x, -d[i][0]), num1 = __dadd_rn(kk2.y, -d[i][1]);
+    // the panel triangle (k_extend<8>'s order), row s on lanes 4s .. 4s + 3
+    const double diag = live ? Ls[t * ld + n0 + t] : 1.0, rinv = rinvs[t];
+    double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      if (8 * i + s >= r) break;
+      const double q0 = quot_rn(num0, diag, rinv), q1 = quot_rn(num1, diag, rinv);
+      if (row == s) {
+        v0 = q0;
+        v1 = q1;
+      }
+      const double b0 = __shfl_sync(0xffffffffu, q0, s * 4 + kq);
+      const double b1 = __shfl_sync(0xffffffffu, q1, s * 4 + kq);
+      const double l = Ls[t * ld + n0 + 8 * i + s];
+      if (row > s) {
+        num0 = __dadd_rn(num0, -__dmul_rn(l, b0));
+        num1 = __dadd_rn(num1, -__dmul_rn(l, b1));
+      }
+    }
+    if (!live) v0 = v1 = 0.0;  // (rows past the model: zero B entries for the later panels)
+    *reinterpret_cast<double2*>(vbuf + i * 64 + row * 8 + col) = make_double2(v0, v1);
+    if (live) *reinterpret_cast<double2*>(Vt + (int64_t)(n0 + t) * kTile + col) = make_double2(v0, v1);
+    __syncwarp();
+  }
+}
+
 template <int R, int NU>
 __global__ void __launch_bounds__(kExtendThreads, R == 1 ? GTC_PASS_MINB : 4) k_extend(ExtendArgs a) {
   extend_body<R, NU>(a);
@@ -3275,6 +3383,7 @@ static int g_rebuild_mode = [] {
   const char* e = std::getenv("GTC_REBUILD");
   if (e && std::string(e) == "stream") return 0;
   if (e && std::string(e) == "dmma") return 1;
+  if (e && std::string(e) == "widemma") return 3;
   return 2;
 }();
 void set_rebuild_mode(int mode) { g_rebuild_mode = mode; }
@@ -3286,7 +3395,9 @@ int rebuild_mode() { return g_rebuild_mode; }
 // fit shared memory for this n).
 bool launch_rebuild_wide(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V, int64_t tile_stride, int n,
                          double* mu, double* var, const VarPartials* vp, TileStats* tstat, cudaStream_t s) {
-  if (g_rebuild_mode != 2 || n <= 0) return false;
+  if ((g_rebuild_mode != 2 && g_rebuild_mode != 3) || n <= 0) return false;
+  const bool mma = g_rebuild_mode == 3;
+  if (mma && sizeof(double) * wm_smem_doubles(n) > 200 * 1024) return false;
   const size_t need = sizeof(double) * wide_smem_doubles(n, sp.d);
   if (need > 200 * 1024) return false;
   const int64_t tiles = sp.n_pad / kTile;
@@ -3299,6 +3410,18 @@ bool launch_rebuild_wide(const SpaceDev& sp, const GpDev& g, KernelParams k, dou
       case 1: k_kstar<1><<<grid, kExtendThreads, 0, s>>>(a, n); break;
       default: k_kstar<2><<<grid, kExtendThreads, 0, s>>>(a, n); break;
     }
+  }
+  if (mma) {  // DMMA passes (V rows only), then the posterior from an r = 0 pass
+    for (int n0 = 0; n0 < n; n0 += kWideRows) {
+      count_launch();
+      ExtendArgs a{sp, g, V, tile_stride, n0, std::min(kWideRows, n - n0), 0, 0, k.lengthscale, k.s2};
+      const size_t smem = sizeof(double) * wm_smem_doubles(n0);
+      opt_in_smem(k_extend_wide_mma, smem);
+      const unsigned grid = (unsigned)(sp.n_pad / (8 * kWmWarps));
+      k_extend_wide_mma<<<grid, kWmWarps * 32, smem, s>>>(a);
+    }
+    launch_extend(sp, g, k, V, tile_stride, n, 0, true, mu, var, false, vp, tstat, s);
+    return true;
   }
   for (int n0 = 0; n0 < n; n0 += kWideRows) {
     count_launch();

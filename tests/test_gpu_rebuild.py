@@ -35,7 +35,7 @@ def fitted(gt, coords, nu, pos, y, mode, set_mode, extra=None):
     return out
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 @pytest.mark.parametrize("nu", ["half", "three_halves", "five_halves"])
 @pytest.mark.parametrize("n", [1, 7, 8, 9, 37, 64, 150])
 def test_rebuild_bit_identical_to_streaming(gt, rebuild_mode, nu, n, mode):
@@ -52,7 +52,7 @@ def test_rebuild_bit_identical_to_streaming(gt, rebuild_mode, nu, n, mode):
         np.testing.assert_array_equal(np.asarray(x), np.asarray(z))
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 def test_rebuild_continuous_coordinates_and_n220(gt, rebuild_mode, mode):
     """Non-discrete coordinates (the FP64 SoA path) at the headline n = 220."""
     rng = np.random.default_rng(5)

@@ -333,11 +333,13 @@ int gtc_debug_append_marks(const gtc_run* run, uint64_t* marks7);
  * selection's blocks, row 2040 the loop-mode append, row 2041 the pass. */
 int gtc_debug_select_trace(uint64_t* marks, int32_t rows);
 /* Diagnostics: how full V rebuilds (fits, refits, gtc_gp_predict) run in this
- * process -- 2 (default) the kernel values first, then 32-row passes; 3 the
- * same passes with the contraction on the FP64 tensor cores (mma.sync) + the
- * posterior pass; 1 one tensor-core pass with shared-memory-resident V blocks
- * + the posterior pass; 0 the streaming 8-row passes that re-read the V
- * prefix from HBM.  All write bit-identical V and posterior.  Returns the
+ * process -- 4 (default) the kernel values first, then persistent 64-row
+ * passes on the FP64 tensor cores (mma.sync) + the posterior pass (mode 2
+ * when the pass's rows of L exceed shared memory, n > ~380); 2 the kernel
+ * values first, then 32-row FMA passes; 3 the 32-row passes on mma.sync +
+ * the posterior pass; 1 one tensor-core pass with shared-memory-resident V
+ * blocks + the posterior pass; 0 the streaming 8-row passes that re-read the
+ * V prefix from HBM.  All write bit-identical V and posterior.  Returns the
  * previous mode; a negative `mode` only queries. */
 int gtc_debug_set_rebuild(int32_t mode);
 /* Diagnostics: how full factorisations (GpModel::fit, refits) run in this

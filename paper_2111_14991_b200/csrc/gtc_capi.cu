@@ -124,7 +124,7 @@ struct GpStore {
         (rc = dalloc(&dev.y, n_max)) || (rc = dalloc(&dev.L, packed_size(n_max) + 2)) ||
         (rc = dalloc(&dev.c, n_max)) || (rc = dalloc(&dev.e, n_max)) ||
         (rc = dalloc(&dev.beta, n_max)) || (rc = dalloc(&dev.sc, 1)) ||
-        (rc = dalloc(&dev.scratch, n_max)))
+        (rc = dalloc(&dev.scratch, n_max)) || (rc = dalloc(&dev.work, kGpWork)))
       return rc;
     GTC_CUDA(cudaMemset(dev.sc, 0, sizeof(GpScalars)));
     GTC_CUDA(cudaMallocHost(&h_sc, sizeof(GpScalars)));
@@ -134,7 +134,7 @@ struct GpStore {
   }
   void release() {
     cudaFree(dev.train_x); cudaFree(dev.train_n2); cudaFree(dev.y); cudaFree(dev.L);
-    cudaFree(dev.c); cudaFree(dev.e); cudaFree(dev.beta); cudaFree(dev.sc); cudaFree(dev.scratch);
+    cudaFree(dev.c); cudaFree(dev.e); cudaFree(dev.beta); cudaFree(dev.sc); cudaFree(dev.scratch); cudaFree(dev.work);
     if (h_sc) cudaFreeHost(h_sc);
   }
 };
@@ -2212,7 +2212,7 @@ extern "C" int gtc_debug_select_trace(uint64_t* marks, int32_t rows) {
 
 extern "C" int gtc_debug_set_rebuild(int32_t mode) {
   const int prev = rebuild_mode();
-  if (mode >= 0) set_rebuild_mode(mode > 3 ? 3 : mode);
+  if (mode >= 0) set_rebuild_mode(mode > 4 ? 4 : mode);
   return prev;
 }
 

@@ -51,6 +51,8 @@ __device__ __forceinline__ unsigned long long gtc_globaltimer() {
 }
 
 // Device pointers of one GP model.
+constexpr int kGpWork = 16;
+
 struct GpDev {
   double* train_x;   // [n_max][d]
   double* train_n2;  // [n_max] squared norms (sequential), for the expansion distance
@@ -61,6 +63,7 @@ struct GpDev {
   double* beta;      // [n_max] L^-1 y_standardized
   GpScalars* sc;
   double* scratch;   // [n_max] misc
+  int* work;         // [kGpWork] group counters of the persistent rebuild passes
   int n_max;
   int d;
 };

@@ -138,10 +138,23 @@ __device__ __forceinline__ double matern(double r, double lengthscale, double s2
 // FMA).  Outside the safe exponent range (and for a == 0, keeping the sign
 // of zero) it defers to __ddiv_rn.  Checked bit for bit against __ddiv_rn
 // on 1.7e10 operand pairs of the rebuild's ranges (tools/div_check.cu).
+__device__ __noinline__ double ddiv_slow(double a, double b) { return __ddiv_rn(a, b); }
+
 __device__ __forceinline__ double quot_rn(double a, double b, double y) {
   const double q0 = __dmul_rn(a, y);
   const double aq = fabs(q0), aa = fabs(a);
   if (!(aq < 0x1p+960 && aq > 0x1p-960 && aa > 0x1p-960 && aa < 0x1p+960)) return __ddiv_rn(a, b);
+  const double r = fma(-q0, b, a);
+  return fma(r, y, q0);
+}
+
+// quot_rn with the out-of-range case out of line (compact code for the
+// heavily unrolled tensor-core passes: their instruction-cache misses were
+// the top stall)
+__device__ __forceinline__ double quot_rn_c(double a, double b, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const double aq = fabs(q0), aa = fabs(a);
+  if (!(aq < 0x1p+960 && aq > 0x1p-960 && aa > 0x1p-960 && aa < 0x1p+960)) return ddiv_slow(a, b);
   const double r = fma(-q0, b, a);
   return fma(r, y, q0);
 }
@@ -1155,14 +1168,24 @@ __host__ __device__ __forceinline__ size_t wide_smem_doubles(int n0, int d, bool
 // row t (k_extend_wide then reads them back and overwrites them with v_t):
 // the exp / sqrt / division work of the rebuild at full occupancy (8 rows x 2
 // candidates per thread), in extend_body's expansion-form order (gp.hpp:176-179).
-template <int NU>
+// DMAX > 0: the candidates' coordinates are decoded once into registers
+// (d <= DMAX) instead of once per row -- the kernel is issue-bound (ncu: 84 %
+// SM throughput, 1.5e9 warp instructions at n = 220, N = 1M); same
+// arithmetic order either way.
+template <int NU, int DMAX>
 __global__ void __launch_bounds__(kExtendThreads) k_kstar(ExtendArgs a, int n) {
   const int d = a.g.d;
   const int64_t tile = blockIdx.x;
   const int64_t j0 = tile * kTile + 2 * threadIdx.x;
+  double2 cc[DMAX > 0 ? DMAX : 1];
   double c0n2 = 0.0, c1n2 = 0.0;
   for (int t = 0; t < d; ++t) {
     const double2 c = coord2(a.sp, t, j0);
+    if (DMAX > 0) {
+#pragma unroll
+      for (int q = 0; q < (DMAX > 0 ? DMAX : 1); ++q)
+        if (q == t) cc[q] = c;
+    }
     c0n2 = __dadd_rn(c0n2, __dmul_rn(c.x, c.x));
     c1n2 = __dadd_rn(c1n2, __dmul_rn(c.y, c.y));
   }
@@ -1172,11 +1195,21 @@ __global__ void __launch_bounds__(kExtendThreads) k_kstar(ExtendArgs a, int n) {
   for (int t = t0; t < t1; ++t) {
     const double* xr = a.g.train_x + (int64_t)t * d;
     double dot0 = 0.0, dot1 = 0.0;
-    for (int q = 0; q < d; ++q) {
-      const double2 c = coord2(a.sp, q, j0);
-      const double xv = __ldg(xr + q);
-      dot0 = __dadd_rn(dot0, __dmul_rn(xv, c.x));
-      dot1 = __dadd_rn(dot1, __dmul_rn(xv, c.y));
+    if (DMAX > 0) {
+#pragma unroll
+      for (int q = 0; q < (DMAX > 0 ? DMAX : 1); ++q) {
+        if (q >= d) break;
+        const double xv = __ldg(xr + q);
+        dot0 = __dadd_rn(dot0, __dmul_rn(xv, cc[q].x));
+        dot1 = __dadd_rn(dot1, __dmul_rn(xv, cc[q].y));
+      }
+    } else {
+      for (int q = 0; q < d; ++q) {
+        const double2 c = coord2(a.sp, q, j0);
+        const double xv = __ldg(xr + q);
+        dot0 = __dadd_rn(dot0, __dmul_rn(xv, c.x));
+        dot1 = __dadd_rn(dot1, __dmul_rn(xv, c.y));
+      }
     }
     const double xn2 = __ldg(a.g.train_n2 + t);
     const double d20 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, dot0), xn2), c0n2);
@@ -1413,6 +1446,172 @@ __global__ void __launch_bounds__(kWmWarps * 32, 3) k_extend_wide_mma(ExtendArgs
     *reinterpret_cast<double2*>(vbuf + i * 64 + row * 8 + col) = make_double2(v0, v1);
     if (live) *reinterpret_cast<double2*>(Vt + (int64_t)(n0 + t) * kTile + col) = make_double2(v0, v1);
     __syncwarp();
+  }
+}
+
+// ---- persistent 64-row DMMA passes (GTC_REBUILD=pmma, mode 4)
+//
+// The same 8-row panel arithmetic as k_extend_wide_mma, regrouped so the
+// FP64 tensor cores are fed from half the stream with no per-CTA staging in
+// the steady state:
+//  * 64 rows (eight 8-row panels) per pass: every streamed B fragment feeds
+//    eight panels' A fragments (1.5 instead of 5.4 GB of prefix reads at
+//    n = 220), four passes instead of seven;
+//  * a warp owns 16 candidates as two interleaved 8-candidate groups (even /
+//    odd positions): one 16-byte load per lane and k-step gives both groups'
+//    B fragments from full 128-byte lines, and each A fragment feeds two DMMAs;
+//  * one persistent CTA per SM stages the pass's rows of L once and loops
+//    over candidate groups (no per-CTA L staging on the critical path);
+//  * the continuation over the pass's earlier panels is right-looking: once
+//    panel j is solved its v (re-laid out from the accumulator to the B
+//    fragment layout by shuffles) updates panels i > j at once, so row t of
+//    panel i still sees the ascending chain prefix, panel 0, ..., panel i-1
+//    -- bit for bit the FMA chain of k_extend<8> (tools/dmma_order.cu).
+constexpr int kPmRows = 64;
+constexpr int kPmWarps = 16;
+#ifndef GTC_PM_U
+#define GTC_PM_U 4
+#endif
+
+// ld = 8 (mod 16) doubles: the paired A loads below are conflict-free per
+// 8-lane phase.  Within every 8-column block the columns are stored paired
+// (column m0 + q at m0 + 2q, m0 + 4 + q at m0 + 2q + 1), so one 16-byte load
+// gives a lane its A elements of two consecutive k-steps.
+__host__ __device__ __forceinline__ int pm_ld(int n0) { return ((n0 + kPmRows + 15) / 16) * 16 + 8; }
+__host__ __device__ __forceinline__ int pm_perm(int m) { return (m & ~7) | ((m & 3) << 1) | ((m >> 2) & 1); }
+__host__ __device__ __forceinline__ size_t pm_smem_doubles(int n0) {
+  // + the panels' diagonal blocks [8][8][8] + per-warp triangle buffers
+  return (size_t)kPmRows * pm_ld(n0) + kPmRows + 8 * 64 + (size_t)kPmWarps * 128;
+}
+
+__global__ void __launch_bounds__(kPmWarps * 32, 1) k_extend_pm(ExtendArgs a, int* __restrict__ next_group) {
+  extern __shared__ double sm[];
+  constexpr int R = kPmRows, U = GTC_PM_U;
+  const int n0 = a.n0, r = a.r, ld = pm_ld(n0);
+  const int P = (r + 7) / 8;    // live panels of this pass
+  double* Ls = sm;              // [R][ld]: Ls[t * ld + m] = L[n0 + t][m] for m <= n0 + t, rows t < r; else 0
+  double* rinvs = Ls + R * ld;  // [R] 1 / L[n0 + t][n0 + t]
+  double* Lb = rinvs + R;       // [8 panels][8][8]: Lb[j * 64 + t * 8 + s] = L[n0 + 8j + t][n0 + 8j + s] (s <= t)
+  for (int idx = threadIdx.x; idx < R * ld; idx += blockDim.x) {
+    const int t = idx / ld, m = idx % ld;  // Ls[t * ld + pm_perm(m)] = L[n0 + t][m]
+    Ls[t * ld + pm_perm(m)] = (t < r && m <= n0 + t) ? a.g.L[packed(n0 + t) + m] : 0.0;
+  }
+  for (int t = threadIdx.x; t < R; t += blockDim.x) rinvs[t] = t < r ? __drcp_rn(a.g.L[packed(n0 + t) + n0 + t]) : 1.0;
+  for (int idx = threadIdx.x; idx < 8 * 64; idx += blockDim.x) {
+    const int j = idx >> 6, t = (idx >> 3) & 7, q = idx & 7, tr = 8 * j + t;
+    Lb[idx] = (tr < r && q <= t) ? a.g.L[packed(n0 + tr) + n0 + 8 * j + q] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int row = lane >> 2, kq = lane & 3;
+  const int64_t groups = a.sp.n_pad / 16;
+  // groups are handed out dynamically (one atomic per group and warp): a
+  // CTA that starts late on a busy SM does not hold the whole pass back
+  for (;;) {
+    int64_t grp = 0;
+    if (lane == 0) grp = atomicAdd(next_group, 1);
+    grp = __shfl_sync(0xffffffffu, grp, 0);
+    if (grp >= groups) break;
+    const int64_t c0 = grp * 16;
+    double* Vt = a.V + (c0 / kTile) * a.tile_stride + c0 % kTile;  // row m of the group at Vt + m * kTile
+    // d[i][g][c]: panel i, group g (candidates c0 + 2n + g), accumulator column c
+    double d[8][2][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i][0][0] = d[i][0][1] = d[i][1][0] = d[i][1][1] = 0.0;
+    // the pass's kernel-value rows into L2 now (read after the prefix)
+    for (int t = lane; t < r; t += 32)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(Vt + (int64_t)(n0 + t) * kTile));
+    // ---- the prefix rows m < n0, B fragments streamed (lane: V[m + kq][c0 + 2 row + {0, 1}])
+    const double2* Bp = reinterpret_cast<const double2*>(Vt + (int64_t)kq * kTile) + row;
+    static_assert(U % 2 == 0, "k-steps are consumed in pairs");
+    for (int m0 = 0; m0 < n0; m0 += 4 * U) {  // (n0 is a multiple of 64)
+      double2 bv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        bv[u] = m0 + 4 * u < n0 ? __ldcs(Bp + (int64_t)(m0 + 4 * u) * (kTile / 2)) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < U; u += 2) {
+        if (m0 + 4 * u >= n0) break;
+        const double* Ap = Ls + row * ld + m0 + 4 * u + 2 * kq;  // (k-steps m0 + 4u and m0 + 4u + 4)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i >= P) break;
+          const double2 av = *reinterpret_cast<const double2*>(Ap + 8 * i * ld);
+          dmma(d[i][0], av.x, bv[u].x);
+          dmma(d[i][1], av.x, bv[u].y);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i >= P) break;
+          const double2 av = *reinterpret_cast<const double2*>(Ap + 8 * i * ld);
+          dmma(d[i][0], av.y, bv[u + 1].x);
+          dmma(d[i][1], av.y, bv[u + 1].y);
+        }
+      }
+    }
+    // ---- the pass's panels, each solved then applied to the later ones.
+    // The triangle runs one candidate per lane (lanes c and c + 16 both own
+    // candidate c0 + c): the accumulators go through this warp's shared
+    // buffer tb[8 rows][16 candidates], the candidate's 8 rows are solved in
+    // registers, v goes back through tb to the B fragment layout.
+    double* tb = Lb + 8 * 64 + w * 128;
+    const int cl = lane & 15;
+    // kernel values of the panel's rows for this lane's candidate (k_kstar),
+    // the next panel's in flight while this one is solved
+    double kvn[8];
+#pragma unroll
+    for (int tt = 0; tt < 8; ++tt) kvn[tt] = tt < r ? __ldcg(Vt + (int64_t)(n0 + tt) * kTile + cl) : 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j >= P) break;
+      const int rows = min(8, r - 8 * j);
+      double kv[8];
+#pragma unroll
+      for (int tt = 0; tt < 8; ++tt) {
+        kv[tt] = kvn[tt];
+        kvn[tt] = 8 * (j + 1) + tt < r ? __ldcg(Vt + (int64_t)(n0 + 8 * (j + 1) + tt) * kTile + cl) : 0.0;
+      }
+      // accumulators -> tb: lane (row, kq) holds candidates 4 kq + (g0 c0, g1 c0, g0 c1, g1 c1)
+      __syncwarp();
+      reinterpret_cast<double2*>(tb + row * 16 + 4 * kq)[0] = make_double2(d[j][0][0], d[j][1][0]);
+      reinterpret_cast<double2*>(tb + row * 16 + 4 * kq)[1] = make_double2(d[j][0][1], d[j][1][1]);
+      __syncwarp();
+      // the panel triangle (k_extend<8>'s order): num = k - acc, then
+      // num -= l_ts v_s for s < t ascending (separately rounded), v = num / L_tt
+      const double* Lp = Lb + j * 64;  // Lp[tt * 8 + s] = L[n0 + 8j + tt][n0 + 8j + s]
+      double v[8];
+#pragma unroll
+      for (int tt = 0; tt < 8; ++tt) {
+        v[tt] = 0.0;
+        if (tt < rows) {
+          double num = __dadd_rn(kv[tt], -tb[tt * 16 + cl]);
+#pragma unroll
+          for (int s = 0; s < tt; ++s) num = __dadd_rn(num, -__dmul_rn(Lp[tt * 8 + s], v[s]));
+          v[tt] = quot_rn_c(num, Lp[tt * 8 + tt], rinvs[8 * j + tt]);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int tt = 0; tt < 8; ++tt) {
+        if (lane < 16) tb[tt * 16 + cl] = v[tt];  // (0 for rows past the model: zero B entries)
+        if (lane < 16 && tt < rows) Vt[(int64_t)(n0 + 8 * j + tt) * kTile + cl] = v[tt];
+      }
+      __syncwarp();
+      // panel j's v as B fragments (k-step kk: rows 8j + 4kk + kq; group g column row = candidate 2 row + g)
+      if (j + 1 < P) {
+        const double2 b0 = *reinterpret_cast<const double2*>(tb + kq * 16 + 2 * row);
+        const double2 b1 = *reinterpret_cast<const double2*>(tb + (4 + kq) * 16 + 2 * row);
+#pragma unroll
+        for (int i = j + 1; i < 8; ++i) {
+          if (i >= P) break;
+          const double2 av = *reinterpret_cast<const double2*>(Ls + (8 * i + row) * ld + n0 + 8 * j + 2 * kq);
+          dmma(d[i][0], av.x, b0.x);
+          dmma(d[i][1], av.x, b0.y);
+          dmma(d[i][0], av.y, b1.x);
+          dmma(d[i][1], av.y, b1.y);
+        }
+      }
+    }
   }
 }
 
@@ -3379,12 +3578,16 @@ __global__ void __launch_bounds__(kRbMaxWarps * 32, 1) k_rebuild(RebuildArgs a) 
 // selects 0 (diagnostics).  (A third variant -- one CTA per tile running all
 // of its 8-row panels back to back so the prefix would come from L2 -- was
 // measured and dropped: 36 % L2 hit rate, 10.7 GB of DRAM reads, 9.6 ms.)
+// 2: k_kstar + the 32-row DFMA passes (k_extend_wide); 3: the same on FP64
+// mma.sync (k_extend_wide_mma); 4 (default): the persistent 64-row DMMA
+// passes (k_extend_pm; falls back to 2 when its rows of L do not fit).
 static int g_rebuild_mode = [] {
   const char* e = std::getenv("GTC_REBUILD");
   if (e && std::string(e) == "stream") return 0;
   if (e && std::string(e) == "dmma") return 1;
+  if (e && std::string(e) == "wide") return 2;
   if (e && std::string(e) == "widemma") return 3;
-  return 2;
+  return 4;
 }();
 void set_rebuild_mode(int mode) { g_rebuild_mode = mode; }
 
@@ -3395,8 +3598,10 @@ int rebuild_mode() { return g_rebuild_mode; }
 // fit shared memory for this n).
 bool launch_rebuild_wide(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V, int64_t tile_stride, int n,
                          double* mu, double* var, const VarPartials* vp, TileStats* tstat, cudaStream_t s) {
-  if ((g_rebuild_mode != 2 && g_rebuild_mode != 3) || n <= 0) return false;
+  if ((g_rebuild_mode < 2 || g_rebuild_mode > 4) || n <= 0) return false;
   const bool mma = g_rebuild_mode == 3;
+  // the 64-row passes when their rows of L fit shared memory (n <= ~380), else the 32-row passes
+  const bool pm = g_rebuild_mode == 4 && sizeof(double) * pm_smem_doubles((n - 1) / kPmRows * kPmRows) <= 200 * 1024;
   if (mma && sizeof(double) * wm_smem_doubles(n) > 200 * 1024) return false;
   const size_t need = sizeof(double) * wide_smem_doubles(n, sp.d);
   if (need > 200 * 1024) return false;
@@ -3405,11 +3610,37 @@ bool launch_rebuild_wide(const SpaceDev& sp, const GpDev& g, KernelParams k, dou
     count_launch();
     ExtendArgs a{sp, g, V, tile_stride, 0, 0, 0, 0, k.lengthscale, k.s2};
     const dim3 grid((unsigned)tiles, (unsigned)((n + 7) / 8));
+    const bool regs = sp.d <= 8;
     switch (k.nu) {
-      case 0: k_kstar<0><<<grid, kExtendThreads, 0, s>>>(a, n); break;
-      case 1: k_kstar<1><<<grid, kExtendThreads, 0, s>>>(a, n); break;
-      default: k_kstar<2><<<grid, kExtendThreads, 0, s>>>(a, n); break;
+      case 0: regs ? k_kstar<0, 8><<<grid, kExtendThreads, 0, s>>>(a, n) : k_kstar<0, 0><<<grid, kExtendThreads, 0, s>>>(a, n); break;
+      case 1: regs ? k_kstar<1, 8><<<grid, kExtendThreads, 0, s>>>(a, n) : k_kstar<1, 0><<<grid, kExtendThreads, 0, s>>>(a, n); break;
+      default: regs ? k_kstar<2, 8><<<grid, kExtendThreads, 0, s>>>(a, n) : k_kstar<2, 0><<<grid, kExtendThreads, 0, s>>>(a, n); break;
     }
+  }
+  if (pm) {  // persistent 64-row DMMA passes (V rows only), then the posterior from an r = 0 pass
+    static int sms = [] {
+      int dev = 0, v = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+      return v > 0 ? v : 148;
+    }();
+    const int64_t groups = sp.n_pad / 16;
+    // group counters of this rebuild's passes (the GP store's, so runs
+    // rebuilding concurrently on their own streams do not share them)
+    const int passes = (n + kPmRows - 1) / kPmRows;
+    int* ctr = g.work;
+    if (!ctr || passes > kGpWork) return false;
+    cudaMemsetAsync(ctr, 0, passes * sizeof(int), s);
+    for (int n0 = 0, pass = 0; n0 < n; n0 += kPmRows, ++pass) {
+      count_launch();
+      ExtendArgs a{sp, g, V, tile_stride, n0, std::min(kPmRows, n - n0), 0, 0, k.lengthscale, k.s2};
+      const size_t smem = sizeof(double) * pm_smem_doubles(n0);
+      opt_in_smem(k_extend_pm, smem);
+      const unsigned grid = (unsigned)std::min<int64_t>(sms, (groups + kPmWarps - 1) / kPmWarps);
+      k_extend_pm<<<grid, kPmWarps * 32, smem, s>>>(a, ctr + pass);
+    }
+    launch_extend(sp, g, k, V, tile_stride, n, 0, true, mu, var, false, vp, tstat, s);
+    return true;
   }
   if (mma) {  // DMMA passes (V rows only), then the posterior from an r = 0 pass
     for (int n0 = 0; n0 < n; n0 += kWideRows) {

@@ -35,7 +35,7 @@ def fitted(gt, coords, nu, pos, y, mode, set_mode, extra=None):
     return out
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3])
+@pytest.mark.parametrize("mode", [1, 2, 3, 4])
 @pytest.mark.parametrize("nu", ["half", "three_halves", "five_halves"])
 @pytest.mark.parametrize("n", [1, 7, 8, 9, 37, 64, 150])
 def test_rebuild_bit_identical_to_streaming(gt, rebuild_mode, nu, n, mode):
@@ -52,7 +52,7 @@ def test_rebuild_bit_identical_to_streaming(gt, rebuild_mode, nu, n, mode):
         np.testing.assert_array_equal(np.asarray(x), np.asarray(z))
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3])
+@pytest.mark.parametrize("mode", [1, 2, 3, 4])
 def test_rebuild_continuous_coordinates_and_n220(gt, rebuild_mode, mode):
     """Non-discrete coordinates (the FP64 SoA path) at the headline n = 220."""
     rng = np.random.default_rng(5)
@@ -62,6 +62,23 @@ def test_rebuild_continuous_coordinates_and_n220(gt, rebuild_mode, mode):
     y = rng.standard_normal(n)
     a = fitted(gt, coords, gt.MaternNu.three_halves, pos, y, 0, rebuild_mode)
     b = fitted(gt, coords, gt.MaternNu.three_halves, pos, y, mode, rebuild_mode)
+    for x, z in zip(a, b):
+        np.testing.assert_array_equal(np.asarray(x), np.asarray(z))
+
+
+@pytest.mark.parametrize("n", [300, 420])
+def test_rebuild_large_n_persistent_passes_and_fallback(gt, rebuild_mode, n):
+    """Mode 4 (persistent 64-row DMMA passes) at n = 300 (five passes, the
+    last one partial) and n = 420 (rows of L past its shared-memory budget:
+    the 32-row passes take over) -- bit for bit the streaming rebuild."""
+    rng = np.random.default_rng(n)
+    N, d = 9_000, 4
+    grid = np.linspace(0.0, 1.0, 13)
+    coords = grid[rng.integers(0, 13, size=(N, d))]
+    pos = rng.choice(N, n + 1, replace=False)
+    y = rng.standard_normal(n + 1)
+    a = fitted(gt, coords, gt.MaternNu.five_halves, pos[:n], y[:n], 0, rebuild_mode, extra=(pos[n], y[n]))
+    b = fitted(gt, coords, gt.MaternNu.five_halves, pos[:n], y[:n], 4, rebuild_mode, extra=(pos[n], y[n]))
     for x, z in zip(a, b):
         np.testing.assert_array_equal(np.asarray(x), np.asarray(z))
 

@@ -3587,6 +3587,7 @@ static int g_rebuild_mode = [] {
   if (e && std::string(e) == "dmma") return 1;
   if (e && std::string(e) == "wide") return 2;
   if (e && std::string(e) == "widemma") return 3;
+  if (e && std::string(e) == "pmma") return 4;
   return 4;
 }();
 void set_rebuild_mode(int mode) { g_rebuild_mode = mode; }

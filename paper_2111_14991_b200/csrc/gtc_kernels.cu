@@ -1172,6 +1172,7 @@ __host__ __device__ __forceinline__ size_t wide_smem_doubles(int n0, int d, bool
 // (d <= DMAX) instead of once per row -- the kernel is issue-bound (ncu: 84 %
 // SM throughput, 1.5e9 warp instructions at n = 220, N = 1M); same
 // arithmetic order either way.
+constexpr int kKstarRows = 32;  // rows per CTA (the coordinate decode amortised over them)
 template <int NU, int DMAX>
 __global__ void __launch_bounds__(kExtendThreads) k_kstar(ExtendArgs a, int n) {
   const int d = a.g.d;
@@ -1190,16 +1191,24 @@ __global__ void __launch_bounds__(kExtendThreads) k_kstar(ExtendArgs a, int n) {
     c1n2 = __dadd_rn(c1n2, __dmul_rn(c.y, c.y));
   }
   double2* Vw = reinterpret_cast<double2*>(a.V + tile * a.tile_stride) + threadIdx.x;
-  const int t0 = 8 * blockIdx.y, t1 = min(n, t0 + 8);
+  const int t0 = kKstarRows * blockIdx.y, t1 = min(n, t0 + kKstarRows);
+  // the CTA's training rows (and squared norms) in shared memory
+  __shared__ double xs[kKstarRows * 8 + kKstarRows];
+  const bool staged = DMAX > 0 && d <= 8;
+  if (staged) {
+    for (int idx = threadIdx.x; idx < (t1 - t0) * d; idx += blockDim.x) xs[idx] = a.g.train_x[(int64_t)t0 * d + idx];
+    for (int t = threadIdx.x; t < t1 - t0; t += blockDim.x) xs[kKstarRows * 8 + t] = a.g.train_n2[t0 + t];
+    __syncthreads();
+  }
   const double linv = __drcp_rn(a.lengthscale);
   for (int t = t0; t < t1; ++t) {
-    const double* xr = a.g.train_x + (int64_t)t * d;
+    const double* xr = staged ? xs + (t - t0) * d : a.g.train_x + (int64_t)t * d;
     double dot0 = 0.0, dot1 = 0.0;
     if (DMAX > 0) {
 #pragma unroll
       for (int q = 0; q < (DMAX > 0 ? DMAX : 1); ++q) {
         if (q >= d) break;
-        const double xv = __ldg(xr + q);
+        const double xv = xr[q];
         dot0 = __dadd_rn(dot0, __dmul_rn(xv, cc[q].x));
         dot1 = __dadd_rn(dot1, __dmul_rn(xv, cc[q].y));
       }
@@ -1211,7 +1220,7 @@ __global__ void __launch_bounds__(kExtendThreads) k_kstar(ExtendArgs a, int n) {
         dot1 = __dadd_rn(dot1, __dmul_rn(xv, c.y));
       }
     }
-    const double xn2 = __ldg(a.g.train_n2 + t);
+    const double xn2 = staged ? xs[kKstarRows * 8 + (t - t0)] : __ldg(a.g.train_n2 + t);
     const double d20 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, dot0), xn2), c0n2);
     const double d21 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, dot1), xn2), c1n2);
     Vw[(int64_t)t * (kTile / 2)] = make_double2(matern_q<NU>(sqrt(fmax(d20, 0.0)), a.lengthscale, linv, a.s2),
@@ -3610,7 +3619,7 @@ bool launch_rebuild_wide(const SpaceDev& sp, const GpDev& g, KernelParams k, dou
   {  // every kernel value first, at full occupancy, into the V rows they become
     count_launch();
     ExtendArgs a{sp, g, V, tile_stride, 0, 0, 0, 0, k.lengthscale, k.s2};
-    const dim3 grid((unsigned)tiles, (unsigned)((n + 7) / 8));
+    const dim3 grid((unsigned)tiles, (unsigned)((n + kKstarRows - 1) / kKstarRows));
     const bool regs = sp.d <= 8;
     switch (k.nu) {
       case 0: regs ? k_kstar<0, 8><<<grid, kExtendThreads, 0, s>>>(a, n) : k_kstar<0, 0><<<grid, kExtendThreads, 0, s>>>(a, n); break;

@@ -821,7 +821,8 @@ def run_single(args, cfg, rank, world, local, extras=True):
         run.truncate_async(n - 1)            # bench rollback: model back to n-1 observations
         yv = float(values[pick])
         _, s = run.observe(pick, yv, [af], min(f_best, yv), expl, cv)
-        run.unmark_visited(pick)             # bench rollback: keep the candidate set fixed
+        # (the observed position stays visited, as in a real run: the
+        # candidate set loses one position per iteration, <= K + 3 of N)
         return s.pick(af)
 
     for _ in range(3):
@@ -862,7 +863,7 @@ def run_single(args, cfg, rank, world, local, extras=True):
             # D2H every step); e2e_resident: the simulation-mode call
             "e2e": {"value": world * k_obs / wall_obs, "unit": "iter/s", "steps": k_obs,
                     "h2d_bytes_per_step": 16 + 64, "d2h_bytes_per_step": 104 + 48,
-                    "api": "gtc_observe per iteration (+ the bench's rollback calls gtc_truncate/gtc_unmark_visited)"},
+                    "api": "gtc_observe per iteration (+ the bench's rollback gtc_truncate to n-1 observations, host-side until the next append; observed positions stay visited)"},
             "e2e_resident": {"value": e2e, "unit": "iter/s", "h2d_bytes_per_step": (nbytes + 256) / args.steps,
                              "d2h_bytes_per_step": rec_bytes + 256 / args.steps,
                              "api": "gtc_run_set_values (H2D table) + gtc_run_steps (K steps, D2H records), wall clock"},

@@ -168,8 +168,8 @@ class SurrogateRun:
 
     @staticmethod
     def _selection(r) -> Selection:
-        return Selection(tuple(r.position), tuple(r.score), r.lambda_, r.mean_variance, r.best_std,
-                         int(r.n_candidates), bool(r.cv_fallback))
+        return Selection(tuple(r.position[:]), tuple(r.score[:]), r.lambda_, r.mean_variance, r.best_std,
+                         r.n_candidates, bool(r.cv_fallback))
 
     def select(self, afs: Sequence[AcquisitionId], f_best_raw: float,
                exploration: ExplorationConfig = ExplorationConfig(),
@@ -188,27 +188,29 @@ class SurrogateRun:
         next selection (when afs is non-empty) with one host round trip.
         Returns (FitInfo, Selection or None)."""
         valid = y_raw is not None
-        bufs = getattr(self, "_obs_bufs", None)  # result structs reused across the per-iteration calls
+        bufs = getattr(self, "_obs_bufs", None)  # result structs (and their refs) reused across calls
         if bufs is None:
-            bufs = self._obs_bufs = (_lib.gtc_select_result(), _lib.gtc_fit_info(), load().gtc_observe)
-        r, info, observe = bufs
+            r0, i0 = _lib.gtc_select_result(), _lib.gtc_fit_info()
+            bufs = self._obs_bufs = (r0, i0, load().gtc_observe, C.byref(r0), C.byref(i0))
+        r, info, observe, r_ref, info_ref = bufs
         if afs:
             if excluded:
                 a, _keep = self._args(afs, f_best_raw, exploration, cv_state, excluded)
+                a_ref = C.byref(a)
             else:  # per-iteration calls: reuse the argument struct, only f_best changes
-                key = (tuple(int(x) for x in afs), int(exploration.mode), float(exploration.constant),
-                       float(cv_state.initial_sample_mean), float(cv_state.initial_mean_variance))
+                key = (tuple(map(int, afs)), exploration.mode, exploration.constant,
+                       cv_state.initial_sample_mean, cv_state.initial_mean_variance)
                 cached = getattr(self, "_obs_args", None)
                 if cached is None or cached[0] != key:
-                    cached = (key, self._args(afs, f_best_raw, exploration, cv_state, None)[0])
-                    self._obs_args = cached
-                a = cached[1]
+                    a = self._args(afs, f_best_raw, exploration, cv_state, None)[0]
+                    cached = self._obs_args = (key, a, C.byref(a))
+                a, a_ref = cached[1], cached[2]
                 a.f_best_raw = float(f_best_raw)
-            check(observe(self._h, int(position), float(y_raw) if valid else 0.0, int(valid),
-                          C.byref(a), C.byref(r), C.byref(info)))
-            return FitInfo.of(info), self._selection(r)
-        check(observe(self._h, int(position), float(y_raw) if valid else 0.0, int(valid), None,
-                      C.byref(r), C.byref(info)))
+            rc = observe(self._h, int(position), float(y_raw) if valid else 0.0, valid, a_ref, r_ref, info_ref)
+            if rc:
+                check(rc)
+            return FitInfo(info.n, bool(info.rebuilt), info.y_mean, info.y_std, info.jitter), self._selection(r)
+        check(observe(self._h, int(position), float(y_raw) if valid else 0.0, int(valid), None, r_ref, info_ref))
         return FitInfo.of(info), None
 
     def set_values(self, values) -> None:

@@ -14,14 +14,15 @@ cv = gt.ContextualVarianceState(float(np.mean(values[pos[:20]])), run.mean_varia
 expl = gt.ExplorationConfig(); fb = float(np.min(values[pos]))
 af = gt.AcquisitionId.ei
 pick = run.select([af], fb, expl, cv).pick(af)
-def loop(k, rollback):
+def loop(k, rollback, unmark=True):
     global pick
     torch.cuda.synchronize(); t0 = time.perf_counter()
     for _ in range(k):
         if rollback: run.truncate_async(219)
         _, s = run.observe(pick, float(values[pick]), [af], fb, expl, cv)
-        if rollback: run.unmark_visited(pick)
+        if rollback and unmark: run.unmark_visited(pick)
         pick = s.pick(af)
     torch.cuda.synchronize(); return (time.perf_counter() - t0) / k * 1e6
 print("with rollback us/iter", loop(60, True), loop(60, True))
+print("truncate only (visited set grows) us/iter", loop(200, True, False), loop(200, True, False))
 print("growing model (no rollback, n 220->280) us/iter", loop(60, False))

@@ -820,6 +820,9 @@ def run_single(args, cfg, rank, world, local, extras=True):
     def step_observe(pick):
         run.truncate_async(n - 1)            # bench rollback: model back to n-1 observations
         yv = float(values[pick])
+        if yv != yv:  # runtime-invalid (C3): marked visited, never reaches the GP (strategies.hpp:444-449)
+            _, s = run.observe(pick, None, [af], f_best, expl, cv)
+            return s.pick(af)
         _, s = run.observe(pick, yv, [af], min(f_best, yv), expl, cv)
         # (the observed position stays visited, as in a real run: the
         # candidate set loses one position per iteration, <= K + 3 of N)

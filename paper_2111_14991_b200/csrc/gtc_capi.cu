@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <chrono>
 #include <cstdlib>
 #include <atomic>
@@ -143,7 +144,8 @@ struct GpStore {
 // reference's jitter escalation (gp.hpp:116-129), starting at `start_jitter`
 // and never exceeding base * 2^6.  On success h_sc holds the scalars.
 int factor_with_escalation(GpStore& gp, const gtc_kernel& k, double noise, double base_jitter,
-                           double start_jitter, int n, cudaStream_t s) {
+                           double start_jitter, int n, cudaStream_t s,
+                           const std::function<int()>& after_first_launch = {}) {
   double jitter = start_jitter;
   // attempts already "spent" below start_jitter (each failed in the reference)
   int attempts = 0;
@@ -152,9 +154,13 @@ int factor_with_escalation(GpStore& gp, const gtc_kernel& k, double noise, doubl
     return fail(GTC_ERR_CONDITIONING, "Gram matrix factorization failed after jitter escalation to " +
                                           fmt_jitter(base_jitter * 64.0));
   }
-  while (true) {
+  for (bool first = true;; first = false) {
     launch_gp_factor(gp.dev, kparams(k), noise, jitter, n, s);
     GTC_LAUNCHED();
+    if (first && after_first_launch) {
+      const int rc = after_first_launch();
+      if (rc) return rc;
+    }
     GTC_CUDA(cudaMemcpyAsync(gp.h_sc, gp.dev.sc, sizeof(GpScalars), cudaMemcpyDeviceToHost, s));
     GTC_CUDA(cudaStreamSynchronize(s));
     if (gp.h_sc->status == 0) return GTC_OK;
@@ -169,13 +175,13 @@ int factor_with_escalation(GpStore& gp, const gtc_kernel& k, double noise, doubl
 // Rebuilds V rows [0, n) for `space` (chunks of kMaxRows) and the posterior.
 int rebuild_predictions(const SpaceDev& sp, GpStore& gp, const gtc_kernel& k, double* V,
                         int64_t tile_stride, int n, double* mu, double* var, const VarPartials* vp,
-                        TileStats* tstat, cudaStream_t s) {
+                        TileStats* tstat, cudaStream_t s, bool kstar_done = false) {
   if (n == 0) {
     launch_prior(mu, var, sp.n_pad, k.output_variance, tstat, s);
     GTC_LAUNCHED();
     return GTC_OK;
   }
-  if (launch_rebuild_wide(sp, gp.dev, kparams(k), V, tile_stride, n, mu, var, vp, tstat, s)) {
+  if (launch_rebuild_wide(sp, gp.dev, kparams(k), V, tile_stride, n, mu, var, vp, tstat, s, kstar_done)) {
     GTC_LAUNCHED();
     return GTC_OK;
   }
@@ -340,6 +346,9 @@ struct gtc_run {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;          // last predictive pass
   cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;  // last gtc_observe device span
   bool pass_timed = false, step_timed = false, step_appended = false;
+  // full fits: the kernel values run on `side` beside the factorisation
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 struct gtc_gp {
@@ -704,8 +713,9 @@ extern "C" int gtc_run_destroy(gtc_run* r) {
   r->graphs.release();
   if (r->h_xnew) cudaFreeHost(r->h_xnew);
   if (r->h_rb) cudaFreeHost(r->h_rb);
-  for (cudaEvent_t ev : {r->ev0, r->ev1, r->ev_step0, r->ev_step1})
+  for (cudaEvent_t ev : {r->ev0, r->ev1, r->ev_step0, r->ev_step1, r->ev_fork, r->ev_join})
     if (ev) cudaEventDestroy(ev);
+  if (r->side) cudaStreamDestroy(r->side);
   if (r->stream) cudaStreamDestroy(r->stream);
   delete r;
   return GTC_OK;
@@ -737,8 +747,11 @@ extern "C" int gtc_run_create(gtc_space* space, const gtc_model_config* cfg, gtc
     return rc;
   }
   cudaError_t e = cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking);
   for (cudaEvent_t* ev : {&r->ev0, &r->ev1, &r->ev_step0, &r->ev_step1})
     if (e == cudaSuccess) e = cudaEventCreate(ev);
+  for (cudaEvent_t* ev : {&r->ev_fork, &r->ev_join})
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaMemset(r->visited, 0, words * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemset(r->acc, 0, 2 * sizeof(VarAccum));
   if (e == cudaSuccess) e = cudaMallocHost(&r->h_rb, sizeof(gtc_run::Readback));
@@ -856,7 +869,26 @@ static int refit(gtc_run* r, double start_jitter, gtc_fit_info* info) {
   r->stats_stale = -1;  // (the factorisation recomputes them)
   int rc = upload_train(r);
   if (rc) return rc;
-  rc = factor_with_escalation(r->gp, r->cfg.kernel, r->cfg.noise, r->cfg.jitter, start_jitter, n, r->stream);
+  // the kernel values need only the training coordinates (and no jitter):
+  // they run on the side stream while the single-CTA factorisation (and its
+  // escalation round trips) run on the run's stream
+  // (launched after the factor kernel: its one large CTA gets an SM before
+  // the kernel values' grid fills them)
+  const bool kstar = r->side && rebuild_wide_taken(r->space->dev(), n);
+  bool forked = false;
+  if (kstar) GTC_CUDA(cudaEventRecord(r->ev_fork, r->stream));
+  rc = factor_with_escalation(r->gp, r->cfg.kernel, r->cfg.noise, r->cfg.jitter, start_jitter, n, r->stream,
+                              [&]() -> int {
+                                if (!kstar) return GTC_OK;
+                                GTC_CUDA(cudaStreamWaitEvent(r->side, r->ev_fork, 0));
+                                launch_kstar(r->space->dev(), r->gp.dev, kparams(r->cfg.kernel), r->V,
+                                             r->tile_stride, n, r->side);
+                                GTC_LAUNCHED();
+                                GTC_CUDA(cudaEventRecord(r->ev_join, r->side));
+                                forked = true;
+                                return GTC_OK;
+                              });
+  if (forked) GTC_CUDA(cudaStreamWaitEvent(r->stream, r->ev_join, 0));  // (also on failure: V is the run's again)
   if (rc) {
     r->predictions_valid = false;
     return rc;
@@ -865,7 +897,7 @@ static int refit(gtc_run* r, double start_jitter, gtc_fit_info* info) {
   r->jitter = r->gp.h_sc->jitter;
   const VarPartials vp = r->vp();
   rc = rebuild_predictions(r->space->dev(), r->gp, r->cfg.kernel, r->V, r->tile_stride, n, r->mu, r->var, &vp,
-                           r->tstat, r->stream);
+                           r->tstat, r->stream, forked);
   if (rc) return rc;
   r->predictions_valid = true;
   r->acc_valid = true;

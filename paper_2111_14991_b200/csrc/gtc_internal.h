@@ -334,7 +334,11 @@ bool launch_rebuild(const SpaceDev& sp, const GpDev& g, KernelParams k, double* 
 // Wide streaming rebuild (k_extend_wide: 32 rows per pass, the 8-row panel
 // arithmetic): V rows [0, n) and the posterior; false = not taken.
 bool launch_rebuild_wide(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V, int64_t tile_stride, int n,
-                         double* mu, double* var, const VarPartials* vp, TileStats* tstat, cudaStream_t stream);
+                         double* mu, double* var, const VarPartials* vp, TileStats* tstat, cudaStream_t stream, bool kstar_done = false);
+// whether launch_rebuild_wide takes this n (then its kernel values come from launch_kstar)
+bool rebuild_wide_taken(const SpaceDev& sp, int n);
+void launch_kstar(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V, int64_t tile_stride, int n,
+                  cudaStream_t s);
 void set_factor_mode(int mode);  // 1 right-looking in shared memory (default), 0 left-looking bordered rows
 int factor_mode();
 void set_rebuild_mode(int mode);  // 0 streaming 8-row passes, 1 tensor cores, 2 wide 32-row passes (default)

@@ -1197,7 +1197,14 @@ __global__ void __launch_bounds__(kExtendThreads) k_kstar(ExtendArgs a, int n) {
   const bool staged = DMAX > 0 && d <= 8;
   if (staged) {
     for (int idx = threadIdx.x; idx < (t1 - t0) * d; idx += blockDim.x) xs[idx] = a.g.train_x[(int64_t)t0 * d + idx];
-    for (int t = threadIdx.x; t < t1 - t0; t += blockDim.x) xs[kKstarRows * 8 + t] = a.g.train_n2[t0 + t];
+    __syncthreads();
+    // squared norms from the coordinates (the factor kernels' order, so the
+    // same bits as g.train_n2 -- the kernel values do not wait for the factor)
+    for (int t = threadIdx.x; t < t1 - t0; t += blockDim.x) {
+      double s = 0.0;
+      for (int q = 0; q < d; ++q) s = __dadd_rn(s, __dmul_rn(xs[t * d + q], xs[t * d + q]));
+      xs[kKstarRows * 8 + t] = s;
+    }
     __syncthreads();
   }
   const double linv = __drcp_rn(a.lengthscale);
@@ -1220,7 +1227,13 @@ __global__ void __launch_bounds__(kExtendThreads) k_kstar(ExtendArgs a, int n) {
         dot1 = __dadd_rn(dot1, __dmul_rn(xv, c.y));
       }
     }
-    const double xn2 = staged ? xs[kKstarRows * 8 + (t - t0)] : __ldg(a.g.train_n2 + t);
+    double xn2;
+    if (staged) {
+      xn2 = xs[kKstarRows * 8 + (t - t0)];
+    } else {
+      xn2 = 0.0;
+      for (int q = 0; q < d; ++q) xn2 = __dadd_rn(xn2, __dmul_rn(__ldg(xr + q), __ldg(xr + q)));
+    }
     const double d20 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, dot0), xn2), c0n2);
     const double d21 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, dot1), xn2), c1n2);
     Vw[(int64_t)t * (kTile / 2)] = make_double2(matern_q<NU>(sqrt(fmax(d20, 0.0)), a.lengthscale, linv, a.s2),
@@ -3606,17 +3619,19 @@ int rebuild_mode() { return g_rebuild_mode; }
 // Wide streaming rebuild (k_extend_wide, 32 rows per pass), the final pass
 // with the posterior.  false = not taken (mode off, or the staging does not
 // fit shared memory for this n).
-bool launch_rebuild_wide(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V, int64_t tile_stride, int n,
-                         double* mu, double* var, const VarPartials* vp, TileStats* tstat, cudaStream_t s) {
+bool rebuild_wide_taken(const SpaceDev& sp, int n) {
   if ((g_rebuild_mode < 2 || g_rebuild_mode > 4) || n <= 0) return false;
-  const bool mma = g_rebuild_mode == 3;
-  // the 64-row passes when their rows of L fit shared memory (n <= ~380), else the 32-row passes
-  const bool pm = g_rebuild_mode == 4 && sizeof(double) * pm_smem_doubles((n - 1) / kPmRows * kPmRows) <= 200 * 1024;
-  if (mma && sizeof(double) * wm_smem_doubles(n) > 200 * 1024) return false;
-  const size_t need = sizeof(double) * wide_smem_doubles(n, sp.d);
-  if (need > 200 * 1024) return false;
+  if (g_rebuild_mode == 3 && sizeof(double) * wm_smem_doubles(n) > 200 * 1024) return false;
+  return sizeof(double) * wide_smem_doubles(n, sp.d) <= 200 * 1024;
+}
+
+// Every kernel value k(x_t, x), t < n, at full occupancy, into the V rows
+// they become (needs only the training coordinates: the fit runs it beside
+// the factorisation on a second stream).
+void launch_kstar(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V, int64_t tile_stride, int n,
+                  cudaStream_t s) {
   const int64_t tiles = sp.n_pad / kTile;
-  {  // every kernel value first, at full occupancy, into the V rows they become
+  {
     count_launch();
     ExtendArgs a{sp, g, V, tile_stride, 0, 0, 0, 0, k.lengthscale, k.s2};
     const dim3 grid((unsigned)tiles, (unsigned)((n + kKstarRows - 1) / kKstarRows));
@@ -3627,6 +3642,18 @@ bool launch_rebuild_wide(const SpaceDev& sp, const GpDev& g, KernelParams k, dou
       default: regs ? k_kstar<2, 8><<<grid, kExtendThreads, 0, s>>>(a, n) : k_kstar<2, 0><<<grid, kExtendThreads, 0, s>>>(a, n); break;
     }
   }
+}
+
+bool launch_rebuild_wide(const SpaceDev& sp, const GpDev& g, KernelParams k, double* V, int64_t tile_stride, int n,
+                         double* mu, double* var, const VarPartials* vp, TileStats* tstat, cudaStream_t s,
+                         bool kstar_done) {
+  if (!rebuild_wide_taken(sp, n)) return false;
+  const bool mma = g_rebuild_mode == 3;
+  // the 64-row passes when their rows of L fit shared memory (n <= ~380), else the 32-row passes
+  const bool pm = g_rebuild_mode == 4 && sizeof(double) * pm_smem_doubles((n - 1) / kPmRows * kPmRows) <= 200 * 1024;
+  const size_t need = sizeof(double) * wide_smem_doubles(n, sp.d);
+  const int64_t tiles = sp.n_pad / kTile;
+  if (!kstar_done) launch_kstar(sp, g, k, V, tile_stride, n, s);
   if (pm) {  // persistent 64-row DMMA passes (V rows only), then the posterior from an r = 0 pass
     static int sms = [] {
       int dev = 0, v = 0;

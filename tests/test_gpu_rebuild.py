@@ -83,6 +83,21 @@ def test_rebuild_large_n_persistent_passes_and_fallback(gt, rebuild_mode, n):
         np.testing.assert_array_equal(np.asarray(x), np.asarray(z))
 
 
+@pytest.mark.parametrize("mode", [2, 4])
+def test_rebuild_high_dimension(gt, rebuild_mode, mode):
+    """d = 11 > 8: the kernel values take k_kstar's per-row coordinate path
+    (no register copy, norms from global memory) -- still bit for bit."""
+    rng = np.random.default_rng(11)
+    N, d, n = 12_000, 11, 90
+    coords = rng.random((N, d))
+    pos = rng.choice(N, n + 1, replace=False)
+    y = rng.standard_normal(n + 1)
+    a = fitted(gt, coords, gt.MaternNu.five_halves, pos[:n], y[:n], 0, rebuild_mode, extra=(pos[n], y[n]))
+    b = fitted(gt, coords, gt.MaternNu.five_halves, pos[:n], y[:n], mode, rebuild_mode, extra=(pos[n], y[n]))
+    for x, z in zip(a, b):
+        np.testing.assert_array_equal(np.asarray(x), np.asarray(z))
+
+
 @pytest.fixture
 def factor_mode(gt):
     lib = gt.load()

@@ -1491,6 +1491,10 @@ __global__ void __launch_bounds__(kWmWarps * 32, 3) k_extend_wide_mma(ExtendArgs
 //    -- bit for bit the FMA chain of k_extend<8> (tools/dmma_order.cu).
 constexpr int kPmRows = 64;
 constexpr int kPmWarps = 16;
+#ifndef GTC_PM_RING
+#define GTC_PM_RING 8
+#endif
+constexpr int kPmRingSteps = GTC_PM_RING;  // k-steps of B in each warp's shared ring (0: register path)
 #ifndef GTC_PM_U
 #define GTC_PM_U 4
 #endif
@@ -1501,12 +1505,23 @@ constexpr int kPmWarps = 16;
 // gives a lane its A elements of two consecutive k-steps.
 __host__ __device__ __forceinline__ int pm_ld(int n0) { return ((n0 + kPmRows + 15) / 16) * 16 + 8; }
 __host__ __device__ __forceinline__ int pm_perm(int m) { return (m & ~7) | ((m & 3) << 1) | ((m >> 2) & 1); }
-__host__ __device__ __forceinline__ size_t pm_smem_doubles(int n0) {
-  // + the panels' diagonal blocks [8][8][8] + per-warp triangle buffers
-  return (size_t)kPmRows * pm_ld(n0) + kPmRows + 8 * 64 + (size_t)kPmWarps * 128;
+__host__ __device__ __forceinline__ size_t pm_smem_doubles(int n0, bool ring) {
+  // + the panels' diagonal blocks [8][8][8] + per-warp triangle buffers (+ B rings)
+  return (size_t)kPmRows * pm_ld(n0) + kPmRows + 8 * 64 + (size_t)kPmWarps * 128 +
+         (ring ? (size_t)kPmWarps * kPmRingSteps * 64 : 0);
 }
 
-__global__ void __launch_bounds__(kPmWarps * 32, 1) k_extend_pm(ExtendArgs a, int* __restrict__ next_group) {
+#ifndef GTC_PM_RING
+#define GTC_PM_RING 8
+#endif
+__device__ __forceinline__ void pm_cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void pm_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void pm_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(kPmWarps * 32, 1) k_extend_pm(ExtendArgs a, int* __restrict__ next_group, int use_ring) {
   extern __shared__ double sm[];
   constexpr int R = kPmRows, U = GTC_PM_U;
   const int n0 = a.n0, r = a.r, ld = pm_ld(n0);
@@ -1546,6 +1561,47 @@ __global__ void __launch_bounds__(kPmWarps * 32, 1) k_extend_pm(ExtendArgs a, in
     // ---- the prefix rows m < n0, B fragments streamed (lane: V[m + kq][c0 + 2 row + {0, 1}])
     const double2* Bp = reinterpret_cast<const double2*>(Vt + (int64_t)kq * kTile) + row;
     static_assert(U % 2 == 0, "k-steps are consumed in pairs");
+#if GTC_PM_RING
+    // B fragments through a per-warp shared ring filled by cp.async: S
+    // k-steps in flight per warp without holding them in registers
+    if (use_ring) {
+      constexpr int S = GTC_PM_RING;
+      static_assert(S % 2 == 0 && S >= 4, "ring of k-step pairs");
+      double2* ring = reinterpret_cast<double2*>(Lb + 8 * 64 + kPmWarps * 128) + (size_t)w * S * 32 + lane;
+      const int ksteps = n0 / 4;
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        if (q < ksteps) pm_cp16(ring + q * 32, Bp + (int64_t)(4 * q) * (kTile / 2));
+        pm_commit();
+      }
+      for (int ks = 0; ks < ksteps; ks += 2) {
+        pm_wait<S - 2>();  // k-steps ks, ks + 1 landed
+        const int slot = ks % S;
+        const double2 b0 = ring[slot * 32], b1 = ring[(slot + 1) * 32];
+        const double* Ap = Ls + row * ld + 4 * ks + 2 * kq;  // (k-steps ks and ks + 1)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i >= P) break;
+          const double2 av = *reinterpret_cast<const double2*>(Ap + 8 * i * ld);
+          dmma(d[i][0], av.x, b0.x);
+          dmma(d[i][1], av.x, b0.y);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i >= P) break;
+          const double2 av = *reinterpret_cast<const double2*>(Ap + 8 * i * ld);
+          dmma(d[i][0], av.y, b1.x);
+          dmma(d[i][1], av.y, b1.y);
+        }
+        // refill the two slots (after their values were consumed by the DMMAs above)
+        if (ks + S < ksteps) pm_cp16(ring + slot * 32, Bp + (int64_t)(4 * (ks + S)) * (kTile / 2));
+        pm_commit();
+        if (ks + S + 1 < ksteps) pm_cp16(ring + (slot + 1) * 32, Bp + (int64_t)(4 * (ks + S + 1)) * (kTile / 2));
+        pm_commit();
+      }
+      pm_wait<0>();
+    } else
+#endif
     for (int m0 = 0; m0 < n0; m0 += 4 * U) {  // (n0 is a multiple of 64)
       double2 bv[U];
 #pragma unroll
@@ -3650,7 +3706,10 @@ bool launch_rebuild_wide(const SpaceDev& sp, const GpDev& g, KernelParams k, dou
   if (!rebuild_wide_taken(sp, n)) return false;
   const bool mma = g_rebuild_mode == 3;
   // the 64-row passes when their rows of L fit shared memory (n <= ~380), else the 32-row passes
-  const bool pm = g_rebuild_mode == 4 && sizeof(double) * pm_smem_doubles((n - 1) / kPmRows * kPmRows) <= 200 * 1024;
+  const int pm_last = (n - 1) / kPmRows * kPmRows;
+  const bool pm = g_rebuild_mode == 4 && sizeof(double) * pm_smem_doubles(pm_last, false) <= 224 * 1024;
+  // (the B rings when every pass's staging fits with them: n <= ~250)
+  const bool pm_ring = pm && kPmRingSteps > 0 && sizeof(double) * pm_smem_doubles(pm_last, true) <= 224 * 1024;
   const size_t need = sizeof(double) * wide_smem_doubles(n, sp.d);
   const int64_t tiles = sp.n_pad / kTile;
   if (!kstar_done) launch_kstar(sp, g, k, V, tile_stride, n, s);
@@ -3671,10 +3730,10 @@ bool launch_rebuild_wide(const SpaceDev& sp, const GpDev& g, KernelParams k, dou
     for (int n0 = 0, pass = 0; n0 < n; n0 += kPmRows, ++pass) {
       count_launch();
       ExtendArgs a{sp, g, V, tile_stride, n0, std::min(kPmRows, n - n0), 0, 0, k.lengthscale, k.s2};
-      const size_t smem = sizeof(double) * pm_smem_doubles(n0);
+      const size_t smem = sizeof(double) * pm_smem_doubles(n0, pm_ring);
       opt_in_smem(k_extend_pm, smem);
       const unsigned grid = (unsigned)std::min<int64_t>(sms, (groups + kPmWarps - 1) / kPmWarps);
-      k_extend_pm<<<grid, kPmWarps * 32, smem, s>>>(a, ctr + pass);
+      k_extend_pm<<<grid, kPmWarps * 32, smem, s>>>(a, ctr + pass, pm_ring ? 1 : 0);
     }
     launch_extend(sp, g, k, V, tile_stride, n, 0, true, mu, var, false, vp, tstat, s);
     return true;

@@ -1477,7 +1477,7 @@ __global__ void __launch_bounds__(kWmWarps * 32, 3) k_extend_wide_mma(ExtendArgs
 // FP64 tensor cores are fed from half the stream with no per-CTA staging in
 // the steady state:
 //  * 64 rows (eight 8-row panels) per pass: every streamed B fragment feeds
-//    eight panels' A fragments (1.5 instead of 5.4 GB of prefix reads at
+//    eight panels' A fragments (2.9 instead of 5.4 GB of prefix reads at
 //    n = 220), four passes instead of seven;
 //  * a warp owns 16 candidates as two interleaved 8-candidate groups (even /
 //    odd positions): one 16-byte load per lane and k-step gives both groups'
@@ -1485,8 +1485,8 @@ __global__ void __launch_bounds__(kWmWarps * 32, 3) k_extend_wide_mma(ExtendArgs
 //  * one persistent CTA per SM stages the pass's rows of L once and loops
 //    over candidate groups (no per-CTA L staging on the critical path);
 //  * the continuation over the pass's earlier panels is right-looking: once
-//    panel j is solved its v (re-laid out from the accumulator to the B
-//    fragment layout by shuffles) updates panels i > j at once, so row t of
+//    panel j is solved its v (re-laid out to the B fragment layout through
+//    the warp's shared buffer) updates panels i > j at once, so row t of
 //    panel i still sees the ascending chain prefix, panel 0, ..., panel i-1
 //    -- bit for bit the FMA chain of k_extend<8> (tools/dmma_order.cu).
 constexpr int kPmRows = 64;
@@ -1511,9 +1511,6 @@ __host__ __device__ __forceinline__ size_t pm_smem_doubles(int n0, bool ring) {
          (ring ? (size_t)kPmWarps * kPmRingSteps * 64 : 0);
 }
 
-#ifndef GTC_PM_RING
-#define GTC_PM_RING 8
-#endif
 __device__ __forceinline__ void pm_cp16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
